@@ -1,0 +1,94 @@
+"""KATs of /root/reference/proj/tests/nystrom_test.cpp (Gaussian sketch rows)."""
+import numpy as np
+import pytest
+
+from support import (logspace_spectrum, min_eigenvalue, nystrom_definitional, random_psd,
+                     sym_eigenvalues)
+
+
+def test_zero_matrix_yields_exactly_zero_eigenvalues(impl):  # nystrom_test.cpp:12-20
+    approx = impl.randomized_nystrom(impl.DenseOperator(np.zeros((10, 10))), 3, impl.Rng(1))
+    assert approx.lam.shape == (3,)
+    assert np.array_equal(approx.lam, np.zeros(3))
+    assert approx.lambda_min == 0.0
+
+
+def test_rank_deficient_matrix_is_reconstructed(impl):  # :22-29
+    d = np.diag([1.0, 1, 0, 0])
+    approx = impl.randomized_nystrom(impl.DenseOperator(d), 3, impl.Rng(2))
+    assert np.linalg.norm(approx.materialize() - d) < 1e-8
+
+
+def test_stable_pipeline_matches_definitional_oracle(impl):  # :31-45
+    a = random_psd(impl, impl.Rng(3), 20, 1e2)
+    approx = impl.randomized_nystrom(impl.DenseOperator(a), 6, impl.Rng(42))
+    omega = impl.Rng(42).gaussian_matrix(20, 6)
+    assert np.linalg.norm(approx.materialize() - nystrom_definitional(a, omega)) < 1e-8 * np.linalg.norm(a)
+
+
+def test_out_of_range_sketch_sizes_rejected(impl):  # :47-55
+    op = impl.DenseOperator(np.eye(5))
+    rng = impl.Rng(4)
+    with pytest.raises(ValueError):
+        impl.randomized_nystrom(op, 0, rng)
+    with pytest.raises(ValueError):
+        impl.randomized_nystrom(op, 6, rng)
+    full = impl.randomized_nystrom(op, 5, rng)
+    assert np.linalg.norm(full.materialize() - np.eye(5)) < 1e-10
+
+
+def test_extend_sketch_grows_without_touching_old_columns(impl):  # :136-154
+    a = random_psd(impl, impl.Rng(10), 15)
+    op = impl.DenseOperator(a)
+    draw = impl.Rng(11)
+    pair = impl.make_empty_sketch(15)
+    with pytest.raises(ValueError):
+        impl.extend_sketch(pair, op, 0, draw)
+    pair = impl.extend_sketch(pair, op, 4, draw)
+    om4, y4 = pair.arrays(15)
+    pair = impl.extend_sketch(pair, op, 3, draw)
+    om, y = pair.arrays(15)
+    assert pair.size() == 7
+    assert np.array_equal(om[:, :4], om4) and np.array_equal(y[:, :4], y4)
+    assert np.abs(om.T @ om - np.eye(7)).max() < 1e-10
+    for j in range(7):
+        assert np.linalg.norm(y[:, j] - a @ om[:, j]) < 1e-12 * max(1.0, np.linalg.norm(y[:, j]))
+
+
+def test_extending_a_sketch_replays_the_oneshot_run(impl):  # :156-171
+    a = random_psd(impl, impl.Rng(12), 40, 1e2)
+    op = impl.DenseOperator(a)
+    grow = impl.Rng(2024)
+    pair = impl.extend_sketch(impl.make_empty_sketch(40), op, 5, grow)
+    pair = impl.extend_sketch(pair, op, 7, grow)
+    extended = impl.nystrom_from_sketch(pair)
+    oneshot = impl.randomized_nystrom(op, 12, impl.Rng(2024))
+    assert np.linalg.norm(extended.materialize() - oneshot.materialize()) < 1e-8 * np.linalg.norm(a)
+
+
+def test_loewner_order_and_majorization(impl):  # :223-246
+    rng = impl.Rng(14)
+    for _ in range(10):
+        n = 20 + rng.integer(81)
+        a = random_psd(impl, rng, n)
+        lam = sym_eigenvalues(a)
+        ell = 3 + rng.integer(n // 2)
+        approx = impl.randomized_nystrom(impl.DenseOperator(a), ell, rng)
+        tol = 1e-8 * lam[0]
+        assert min_eigenvalue(a - approx.materialize()) > -tol
+        assert np.all(approx.lam <= lam[: ell] + tol)
+        assert np.abs(approx.u.T @ approx.u - np.eye(ell)).max() < 1e-10
+        assert approx.shift_used > 0.0
+        assert np.all(np.diff(approx.lam) <= 0)
+
+
+def test_stable_pipeline_survives_sixteen_decades(impl):  # :265-282
+    n, ell = 30, 10
+    op = impl.synthesize_operator(logspace_spectrum(n, 0.0, -16.0), 23)
+    a = op.apply_block(np.eye(n))
+    approx = impl.randomized_nystrom(op, ell, impl.Rng(77))
+    ahat = approx.materialize()
+    assert np.all(np.isfinite(ahat))
+    assert min_eigenvalue(ahat) > -1e-14
+    omega = impl.Rng(77).gaussian_matrix(n, ell)
+    assert np.linalg.norm(ahat - nystrom_definitional(a, omega)) < 1e-6 * np.linalg.norm(a)
