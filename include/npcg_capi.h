@@ -1,0 +1,232 @@
+/*
+ * npcg_capi.h — drop-in C-ABI of the B200-native Nyström-PCG hot path.
+ *
+ * The reference (/root/reference/proj/core) exposes only a C++ API
+ * (the npcg headers, Eigen types) and no FFI. This header is the boundary a
+ * maintainer binds instead: plain pointers + sizes, column-major FP64
+ * (Eigen::MatrixXd layout, ld >= rows), 64-bit indices, status codes.
+ * Each entry point names the reference interface it replaces (file:line,
+ * paths relative to /root/reference/proj/core/). The C++ façade in
+ * include/npcg/ maps these back onto the reference's class/func names and
+ * exception types; INTEGRATION.md shows the bindings.
+ *
+ * Everything computes on one B200 (sm_100a) through hand-written CUDA kernels
+ * in libnpcg_b200.so. There is no CPU fallback: without a usable device every
+ * compute entry point returns NPCG_ECUDA.
+ *
+ * Pointers tagged `where` are host memory (NPCG_HOST) or device memory of the
+ * context's GPU (NPCG_DEVICE). Host buffers are copied in/out inside the call.
+ */
+#ifndef NPCG_CAPI_H
+#define NPCG_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map to the reference's exception types) -------------- */
+enum {
+  NPCG_OK = 0,
+  NPCG_EINVAL = 1,    /* std::invalid_argument  (operators.cpp:14-21, nystrom.cpp:144-145, ...) */
+  NPCG_ERUNTIME = 2,  /* std::runtime_error     (nystrom.cpp:124-130, operators.cpp:42-50)        */
+  NPCG_EDIVERGED = 3, /* npcg::SolveDivergenceError (solvers.hpp:51-57); report is filled        */
+  NPCG_ECUDA = 4,     /* CUDA failure / no device                                                 */
+  NPCG_ENCCL = 5      /* collective failure (multi-GPU builds)                                    */
+};
+enum { NPCG_HOST = 0, NPCG_DEVICE = 1 };
+
+typedef struct npcg_ctx npcg_ctx;
+typedef struct npcg_rng npcg_rng;
+typedef struct npcg_op npcg_op;
+typedef struct npcg_nys npcg_nys;
+typedef struct npcg_pre npcg_pre;
+
+/* Thread-local message of the last failing call, formatted like the
+ * reference's what() strings. */
+const char* npcg_last_error(void);
+const char* npcg_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+int npcg_ctx_create(int device, npcg_ctx** out);
+int npcg_ctx_destroy(npcg_ctx* ctx);
+int npcg_ctx_sync(npcg_ctx* ctx);
+/* The CUDA stream all of this context's work is ordered on (cudaStream_t). */
+void* npcg_ctx_stream(npcg_ctx* ctx);
+/* Device memory owned by the context's allocator (for NPCG_DEVICE inputs). */
+int npcg_dev_alloc(npcg_ctx* ctx, int64_t bytes, void** out);
+int npcg_dev_free(npcg_ctx* ctx, void* p);
+int npcg_memcpy(npcg_ctx* ctx, void* dst, int dst_where, const void* src, int src_where, int64_t bytes);
+/* Number of this library's kernel launches issued on ctx so far. */
+int64_t npcg_ctx_launches(npcg_ctx* ctx);
+
+/* ---- random (random.hpp:21-50, random.cpp:11-56) -------------------------
+ * The reference generator, bit for bit: std::mt19937_64 + cache-free
+ * Box-Muller, two engine words per normal, column-major fills. Host-side:
+ * it produces the Ω blocks, right-hand sides and power-method start vectors
+ * the GPU path consumes. */
+int npcg_rng_create(uint64_t seed, npcg_rng** out);
+int npcg_rng_clone(const npcg_rng* rng, npcg_rng** out);
+int npcg_rng_destroy(npcg_rng* rng);
+double npcg_rng_normal(npcg_rng* rng);                         /* random.cpp:11-18 */
+double npcg_rng_uniform(npcg_rng* rng);                        /* random.cpp:20    */
+uint64_t npcg_rng_word(npcg_rng* rng);                         /* engine()         */
+void npcg_rng_discard(npcg_rng* rng, uint64_t words);
+int npcg_rng_integer(npcg_rng* rng, uint64_t bound, uint64_t* out);   /* random.cpp:22-25 */
+/* gaussian_matrix (random.cpp:27-32) into dst (col-major, ld = rows). */
+int npcg_rng_gaussian(npcg_rng* rng, int64_t rows, int64_t cols, double* dst);
+int npcg_rng_sample(npcg_rng* rng, int64_t n, int64_t k, int64_t* out); /* random.cpp:44-56 */
+uint64_t npcg_splitmix64(uint64_t seed);                       /* bench.cpp:180-185 */
+
+/* ---- operators (operators.hpp:25-168) ----------------------------------- */
+/* DenseOperator(Matrix a), operators.cpp:64-70 (square + symmetry check). */
+int npcg_op_dense_create(npcg_ctx* ctx, int64_t rows, int64_t cols, const double* a, int64_t lda,
+                         int where, npcg_op** out);
+/* GramRidgeOperator(Matrix design) = (1/m) G^T G, operators.cpp:105-121. */
+int npcg_op_gram_create(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, int64_t ldg,
+                        int where, npcg_op** out);
+/* KernelOperator(points n x d, sigma, dense_cap), operators.cpp:141-150:
+ * stored (built on device) when n <= dense_cap, otherwise matrix-free. */
+int npcg_op_kernel_create(npcg_ctx* ctx, int64_t n, int64_t d, const double* pts, int64_t ldp,
+                          double sigma, int64_t dense_cap, int where, npcg_op** out);
+/* synthesize_operator(profile, seed), operators.cpp:211-219: Q from a seeded
+ * Gaussian, A = Q diag(lambda) Q^T symmetrised — on the device. */
+int npcg_op_synthesize(npcg_ctx* ctx, int64_t n, const double* lambda, uint64_t seed,
+                       npcg_op** out);
+/* A = G diag(lambda) G^T / r (low-rank synthetic psd; BASELINE config 5). */
+int npcg_op_lowrank_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g, int64_t ldg,
+                           const double* lambda, int where, npcg_op** out);
+int npcg_op_destroy(npcg_op* op);
+int npcg_op_dim(const npcg_op* op, int64_t* n);
+int npcg_op_kind(const npcg_op* op); /* 0 dense, 1 gram, 2 kernel stored, 3 kernel matrix-free */
+int npcg_op_has_column_access(const npcg_op* op);
+/* LinearOperator::matvec / apply_block (operators.cpp:25-40): dim + finiteness
+ * checks, then A V. V and out are rows x k col-major. */
+int npcg_op_apply(npcg_op* op, int64_t rows, int64_t k, const double* v, int64_t ldv, double* out,
+                  int64_t ldo, int where);
+/* LinearOperator::column (operators.cpp:42-50). */
+int npcg_op_column(npcg_op* op, int64_t j, double* out, int where);
+
+/* ---- Nyström (nystrom.hpp:19-89) ---------------------------------------- */
+/* make_empty_sketch(n) bound to op (nystrom.cpp:28-34). */
+int npcg_nys_create(npcg_op* op, npcg_nys** out);
+/* extend_sketch (nystrom.cpp:36-58) with the raw n x extra Gaussian block the
+ * reference Rng would draw (gaussian_matrix); block Gram-Schmidt x2 against
+ * the existing columns, orthonormalisation and Y_new = A Q_new on device. */
+int npcg_nys_extend(npcg_nys* nys, int64_t extra, const double* omega_raw, int64_t ld, int where);
+/* Same, drawing the block from `rng` (exact reference stream order). */
+int npcg_nys_extend_rng(npcg_nys* nys, int64_t extra, npcg_rng* rng);
+/* nystrom_from_sketch (nystrom.cpp:96-140): shift, Cholesky (x10 escalation,
+ * <= 3 retries), triangular solve, thin SVD, clamp. */
+int npcg_nys_factor(npcg_nys* nys);
+/* A factored approximation given directly (U n x ell, lambda ell). */
+int npcg_nys_from_factors(npcg_ctx* ctx, int64_t n, int64_t ell, const double* u, int64_t ldu,
+                          const double* lambda, double shift_used, int where, npcg_nys** out);
+int npcg_nys_info(const npcg_nys* nys, int64_t* n, int64_t* sketch_cols, int64_t* ell_factored,
+                  double* shift_used);
+/* lambda (ell), U (n x ell, nullable) of the factored approximation. */
+int npcg_nys_get(npcg_nys* nys, double* lambda, double* u, int64_t ldu, int where);
+/* The cached sketch pair (omega, y: n x size), nullable outputs. */
+int npcg_nys_get_sketch(npcg_nys* nys, double* omega, double* y, int64_t ld, int where);
+int npcg_nys_destroy(npcg_nys* nys);
+
+/* ---- preconditioner (preconditioner.hpp:20-65) --------------------------- */
+/* build_preconditioner(approx, mu), preconditioner.cpp:80-89 (mu > 0). */
+int npcg_pre_create(npcg_nys* nys, double mu, npcg_pre** out);
+/* apply_inverse / apply_inverse_block (preconditioner.cpp:27-45), R n x s. */
+int npcg_pre_apply_inverse(npcg_pre* pre, int64_t s, const double* r, int64_t ldr, double* z,
+                           int64_t ldz, int where);
+/* apply (preconditioner.cpp:17-25). */
+int npcg_pre_apply(npcg_pre* pre, int64_t s, const double* v, int64_t ldv, double* out,
+                   int64_t ldo, int where);
+int npcg_pre_destroy(npcg_pre* pre);
+
+/* ---- solvers (solvers.hpp:20-93) ----------------------------------------- */
+typedef struct {
+  double eta;        /* SolveOptions::eta      (default 1e-10) */
+  int64_t max_iter;  /* SolveOptions::max_iter (default 500)   */
+  int relative;      /* SolveOptions::relative                 */
+  int record_iterates;
+} npcg_solve_opts;
+
+typedef struct {
+  int64_t iterations;
+  int64_t matvec_count;
+  int converged;
+  int status;        /* 0 ok/max_iter, 1 breakdown (p'Ap <= 0), 2 non-finite residual, 3 non-finite initial */
+  double eta_used;
+  double wall_time;
+  int64_t history_len;
+} npcg_solve_report;
+
+/* nystrom_pcg (solvers.cpp:122-148) on s independent right-hand sides that
+ * share one pass over A per iteration (column j == nystrom_pcg on column j).
+ * pre == NULL -> identity (cg on A + mu I, solvers.cpp:111-120).
+ * history: s x (max_iter+1) col-major residual norms (nullable).
+ * iterates: (max_iter+1) x n x s (nullable; needs record_iterates).
+ * Returns NPCG_EDIVERGED if any column diverged (its report says which). */
+int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, int64_t ldb,
+             const double* x0, int64_t ldx0, const npcg_solve_opts* opts, double* x, int64_t ldx,
+             npcg_solve_report* reports, double* history, double* iterates, int where);
+
+/* block_nystrom_pcg (solvers.cpp:150-279), O'Leary block PCG. */
+typedef struct {
+  int64_t iterations;
+  int64_t fallback_count;
+  int64_t n_deflated;
+  double eta_used;
+  double wall_time;
+} npcg_block_report;
+int npcg_block_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, int64_t ldb,
+                   const npcg_solve_opts* opts, double* x, int64_t ldx, npcg_block_report* rep,
+                   int* converged, int64_t* deflated, double* final_residual, int where);
+
+/* iteration_bound (solvers.cpp:281-291). */
+int npcg_iteration_bound(double kappa, double epsilon, int64_t* out);
+
+/* ---- adaptive (adaptive.hpp:26-85) -------------------------------------- */
+/* estimate_error_power (adaptive.cpp:83-109) from a caller-drawn raw start
+ * vector g (n; the Rng's gaussian_vector). */
+int npcg_power_estimate(npcg_op* op, npcg_nys* nys, int64_t q, const double* g_raw, int where,
+                        double* estimate);
+int npcg_power_estimate_rng(npcg_op* op, npcg_nys* nys, int64_t q, npcg_rng* rng, double* estimate);
+
+typedef struct {
+  int64_t ell0, ell_max;
+  double mu;
+  int tol_mode;       /* 0 error (strategy 1), 1 ratio (strategy 2), 2 fixed (strategy 3) */
+  int has_tau;
+  double tau;         /* default 30 (error) / 10 (ratio) */
+  int64_t q;          /* power iterations, default 5 */
+  int secondary_criterion;
+  int sketch;         /* 0 gaussian */
+} npcg_adaptive_cfg;
+
+typedef struct {
+  int64_t ell_final, doublings;
+  int hit_cap;
+  int has_error_estimate;
+  double error_estimate;
+  double posterior_condition;
+} npcg_adaptive_outcome;
+
+/* adaptive_nystrom / adaptive_nystrom_ratio / fixed_rank_nystrom
+ * (adaptive.cpp:50-148). Ω blocks and power-method start vectors are drawn
+ * from `rng` in the reference's exact stream order. */
+int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg_nys** out,
+                  npcg_adaptive_outcome* outcome);
+/* posterior_condition_estimate (adaptive.cpp:150-156). */
+int npcg_posterior_condition(double lambda_ell, double mu, double err, double* out);
+
+/* ---- dense helpers (dense.hpp:26-50), on device ------------------------- */
+int npcg_orthonormal_columns(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, double* q,
+                             int where);                                    /* dense.cpp:98-117 */
+int npcg_thin_svd(npcg_ctx* ctx, int64_t m, int64_t n, const double* b, double* u, double* s,
+                  int where);                                               /* dense.cpp:81-96  */
+double npcg_ulp_spacing(double x);                                          /* dense.cpp:119-122 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NPCG_CAPI_H */

@@ -1,0 +1,671 @@
+"""B200-native Nyström PCG — Python host mirror of the reference's C++ API.
+
+Every call goes through the C-ABI of ``libnpcg_b200.so`` (include/npcg_capi.h),
+whose compute runs in hand-written sm_100a CUDA kernels. Names, argument
+meaning and error behaviour follow /root/reference/proj/core/include/npcg/:
+
+  reference                                  here
+  -----------------------------------------  -----------------------------------
+  Rng (random.hpp:21-38)                     Rng
+  DenseOperator / GramRidgeOperator /        DenseOperator / GramRidgeOperator /
+  KernelOperator / synthesize_operator        KernelOperator / synthesize_operator
+  (operators.hpp:50-168)
+  make_empty_sketch / extend_sketch /        same names (nystrom.hpp:51-89)
+  nystrom_from_sketch / randomized_nystrom
+  build_preconditioner,                      build_preconditioner,
+  NystromPreconditioner::apply(_inverse)     NystromPreconditioner.apply(_inverse)
+  nystrom_pcg / cg (solvers.hpp:60-87)       nystrom_pcg / cg
+  estimate_error_power / adaptive_nystrom    estimate_error_power / adaptive
+  (adaptive.hpp:56-85)
+
+Exceptions: std::invalid_argument -> InvalidArgument (ValueError),
+std::runtime_error -> NpcgRuntimeError (RuntimeError), SolveDivergenceError ->
+SolveDivergenceError (carries the partial report). There is no CPU fallback:
+if the library or a B200 is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libnpcg_b200.so"
+
+_i64 = C.c_int64
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+HOST, DEVICE = 0, 1
+
+
+class InvalidArgument(ValueError):
+    """reference std::invalid_argument"""
+
+
+class NpcgRuntimeError(RuntimeError):
+    """reference std::runtime_error"""
+
+
+class CudaError(RuntimeError):
+    """CUDA failure / no B200 device"""
+
+
+class SolveDivergenceError(RuntimeError):
+    """reference npcg::SolveDivergenceError (solvers.hpp:51-57)"""
+
+    def __init__(self, msg, report=None):
+        super().__init__(msg)
+        self.report = report
+
+
+class _SolveOpts(C.Structure):
+    _fields_ = [("eta", C.c_double), ("max_iter", _i64), ("relative", C.c_int), ("record_iterates", C.c_int)]
+
+
+class _SolveReport(C.Structure):
+    _fields_ = [("iterations", _i64), ("matvec_count", _i64), ("converged", C.c_int), ("status", C.c_int),
+                ("eta_used", C.c_double), ("wall_time", C.c_double), ("history_len", _i64)]
+
+
+class _BlockReport(C.Structure):
+    _fields_ = [("iterations", _i64), ("fallback_count", _i64), ("n_deflated", _i64), ("eta_used", C.c_double),
+                ("wall_time", C.c_double)]
+
+
+class _AdaptiveCfg(C.Structure):
+    _fields_ = [("ell0", _i64), ("ell_max", _i64), ("mu", C.c_double), ("tol_mode", C.c_int), ("has_tau", C.c_int),
+                ("tau", C.c_double), ("q", _i64), ("secondary_criterion", C.c_int), ("sketch", C.c_int)]
+
+
+class _AdaptiveOutcome(C.Structure):
+    _fields_ = [("ell_final", _i64), ("doublings", _i64), ("hit_cap", C.c_int), ("has_error_estimate", C.c_int),
+                ("error_estimate", C.c_double), ("posterior_condition", C.c_double)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libnpcg_b200.so (built in-tree by ``build.py``). Fails loudly."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise CudaError(f"{LIB_PATH} is missing: run `python -m paper_2110_02820_b200.build`")
+            L = C.CDLL(str(LIB_PATH))
+            L.npcg_last_error.restype = C.c_char_p
+            L.npcg_version.restype = C.c_char_p
+            L.npcg_rng_normal.restype = C.c_double
+            L.npcg_rng_normal.argtypes = [_vp]
+            L.npcg_rng_uniform.restype = C.c_double
+            L.npcg_rng_uniform.argtypes = [_vp]
+            L.npcg_rng_word.restype = C.c_uint64
+            L.npcg_rng_word.argtypes = [_vp]
+            L.npcg_rng_discard.argtypes = [_vp, C.c_uint64]
+            L.npcg_rng_discard.restype = None
+            L.npcg_splitmix64.restype = C.c_uint64
+            L.npcg_splitmix64.argtypes = [C.c_uint64]
+            L.npcg_ulp_spacing.restype = C.c_double
+            L.npcg_ulp_spacing.argtypes = [C.c_double]
+            L.npcg_ctx_stream.restype = _vp
+            L.npcg_ctx_launches.restype = _i64
+            L.npcg_ctx_launches.argtypes = [_vp]
+            L.npcg_op_kind.argtypes = [_vp]
+            L.npcg_op_has_column_access.argtypes = [_vp]
+            _lib = L
+    return _lib
+
+
+def _check(rc, report=None):
+    if rc == 0:
+        return
+    msg = lib().npcg_last_error().decode()
+    if rc == 1:
+        raise InvalidArgument(msg)
+    if rc == 3:
+        raise SolveDivergenceError(msg, report)
+    if rc == 4:
+        raise CudaError(msg)
+    raise NpcgRuntimeError(msg)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _f64(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """npcg_ctx: one B200, one stream."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        _check(lib().npcg_ctx_create(C.c_int(device), C.byref(h)))
+        self.h = h.value
+        self.device = device
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.npcg_ctx_destroy(_vp(self.h))
+            self.h = None
+
+    def sync(self):
+        _check(lib().npcg_ctx_sync(_vp(self.h)))
+
+    @property
+    def launches(self) -> int:
+        return lib().npcg_ctx_launches(_vp(self.h))
+
+    @property
+    def stream(self) -> int:
+        return lib().npcg_ctx_stream(_vp(self.h))
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("NPCG_DEVICE", "0")))
+    return _default_ctx
+
+
+# ------------------------------------------------------------------ random
+class Rng:
+    """reference npcg::Rng (random.hpp:21-38), bitwise: mt19937_64 + Box-Muller."""
+
+    def __init__(self, seed: int = 0, _handle=None):
+        if _handle is None:
+            h = _vp()
+            _check(lib().npcg_rng_create(C.c_uint64(seed), C.byref(h)))
+            _handle = h.value
+        self.h = _handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.npcg_rng_destroy(_vp(self.h))
+            self.h = None
+
+    def clone(self) -> "Rng":
+        h = _vp()
+        _check(lib().npcg_rng_clone(_vp(self.h), C.byref(h)))
+        return Rng(_handle=h.value)
+
+    def normal(self) -> float:
+        return lib().npcg_rng_normal(_vp(self.h))
+
+    def uniform(self) -> float:
+        return lib().npcg_rng_uniform(_vp(self.h))
+
+    def word(self) -> int:
+        return lib().npcg_rng_word(_vp(self.h))
+
+    def discard(self, k: int):
+        lib().npcg_rng_discard(_vp(self.h), C.c_uint64(k))
+
+    def integer(self, bound: int) -> int:
+        out = C.c_uint64()
+        _check(lib().npcg_rng_integer(_vp(self.h), C.c_uint64(bound), C.byref(out)))
+        return out.value
+
+    def gaussian_matrix(self, rows: int, cols: int) -> np.ndarray:
+        out = np.empty((rows, cols), dtype=np.float64, order="F")
+        _check(lib().npcg_rng_gaussian(_vp(self.h), _i64(rows), _i64(cols), _ptr(out)))
+        return out
+
+    def gaussian_vector(self, n: int) -> np.ndarray:
+        return self.gaussian_matrix(n, 1)[:, 0].copy()
+
+    def sample_without_replacement(self, n: int, k: int) -> np.ndarray:
+        out = np.empty(max(k, 0), dtype=np.int64)
+        _check(lib().npcg_rng_sample(_vp(self.h), _i64(n), _i64(k), out.ctypes.data_as(C.POINTER(_i64))))
+        return out
+
+
+def splitmix64(seed: int) -> int:
+    return lib().npcg_splitmix64(C.c_uint64(seed))
+
+
+def ulp_spacing(x: float) -> float:
+    return lib().npcg_ulp_spacing(float(x))
+
+
+def orthonormal_columns(g, ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    g = _f64(g)
+    q = np.empty_like(g, order="F")
+    _check(lib().npcg_orthonormal_columns(_vp(ctx.h), _i64(g.shape[0]), _i64(g.shape[1]), _ptr(g), _ptr(q), HOST))
+    return q
+
+
+def thin_svd(b, ctx: Context | None = None):
+    ctx = ctx or default_context()
+    b = _f64(b)
+    m, n = b.shape
+    u = np.empty((m, n), order="F")
+    s = np.empty(n)
+    _check(lib().npcg_thin_svd(_vp(ctx.h), _i64(m), _i64(n), _ptr(b), _ptr(u), _ptr(s), HOST))
+    return u, s
+
+
+# ------------------------------------------------------------------ operators
+class LinearOperator:
+    """npcg_op handle: LinearOperator NVI (operators.hpp:25-47) on a B200."""
+
+    def __init__(self, h, ctx: Context):
+        self.h, self.ctx = h, ctx
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.npcg_op_destroy(_vp(self.h))
+            self.h = None
+
+    def dim(self) -> int:
+        n = _i64()
+        _check(lib().npcg_op_dim(_vp(self.h), C.byref(n)))
+        return n.value
+
+    @property
+    def kind(self) -> int:
+        return lib().npcg_op_kind(_vp(self.h))
+
+    def has_column_access(self) -> bool:
+        return bool(lib().npcg_op_has_column_access(_vp(self.h)))
+
+    def matvec(self, v) -> np.ndarray:
+        v = _f64(v).ravel(order="F")
+        out = np.empty(self.dim())
+        _check(lib().npcg_op_apply(_vp(self.h), _i64(v.size), _i64(1), _ptr(v), _i64(max(v.size, 1)), _ptr(out),
+                                   _i64(max(out.size, 1)), HOST))
+        return out
+
+    def apply_block(self, V) -> np.ndarray:
+        V = _f64(V)
+        if V.ndim == 1:
+            V = V.reshape(-1, 1, order="F")
+        rows, k = V.shape
+        out = np.empty((self.dim(), k), order="F")
+        if k == 1:  # keep apply_block semantics (its messages) for one column
+            _check(lib().npcg_op_apply(_vp(self.h), _i64(rows), _i64(1), _ptr(V), _i64(max(rows, 1)), _ptr(out),
+                                       _i64(max(self.dim(), 1)), HOST))
+            return out
+        _check(lib().npcg_op_apply(_vp(self.h), _i64(rows), _i64(k), _ptr(V), _i64(max(rows, 1)), _ptr(out),
+                                   _i64(max(self.dim(), 1)), HOST))
+        return out
+
+    def column(self, j: int) -> np.ndarray:
+        out = np.empty(self.dim())
+        _check(lib().npcg_op_column(_vp(self.h), _i64(j), _ptr(out), HOST))
+        return out
+
+    def dense(self) -> np.ndarray:
+        return self.apply_block(np.eye(self.dim()))
+
+
+def _new_op(ctx, fn, *args) -> LinearOperator:
+    h = _vp()
+    _check(fn(*args, C.byref(h)))
+    return LinearOperator(h.value, ctx)
+
+
+def DenseOperator(a, ctx: Context | None = None) -> LinearOperator:
+    ctx = ctx or default_context()
+    a = _f64(a)
+    if a.ndim != 2:
+        raise InvalidArgument("DenseOperator: matrix must be square")
+    return _new_op(ctx, lib().npcg_op_dense_create, _vp(ctx.h), _i64(a.shape[0]), _i64(a.shape[1]), _ptr(a),
+                   _i64(max(a.shape[0], 1)), HOST)
+
+
+def GramRidgeOperator(g, ctx: Context | None = None) -> LinearOperator:
+    ctx = ctx or default_context()
+    g = _f64(g)
+    if g.ndim != 2:
+        raise InvalidArgument("GramRidgeOperator: design matrix must be nonempty")
+    return _new_op(ctx, lib().npcg_op_gram_create, _vp(ctx.h), _i64(g.shape[0]), _i64(g.shape[1]), _ptr(g),
+                   _i64(max(g.shape[0], 1)), HOST)
+
+
+def KernelOperator(points, sigma: float, dense_cap: int = 20000, ctx: Context | None = None) -> LinearOperator:
+    ctx = ctx or default_context()
+    p = _f64(points)
+    if p.ndim == 1:
+        p = p.reshape(-1, 1, order="F")
+    return _new_op(ctx, lib().npcg_op_kernel_create, _vp(ctx.h), _i64(p.shape[0]), _i64(p.shape[1]), _ptr(p),
+                   _i64(max(p.shape[0], 1)), C.c_double(sigma), _i64(dense_cap), HOST)
+
+
+def synthesize_operator(eigenvalues, seed: int, ctx: Context | None = None) -> LinearOperator:
+    ctx = ctx or default_context()
+    lam = _f64(eigenvalues).ravel()
+    return _new_op(ctx, lib().npcg_op_synthesize, _vp(ctx.h), _i64(lam.size), _ptr(lam), C.c_uint64(seed))
+
+
+def LowRankOperator(g, lam, ctx: Context | None = None) -> LinearOperator:
+    """A = G diag(lam) G^T / r (BASELINE config 5 generator), built on device."""
+    ctx = ctx or default_context()
+    g = _f64(g)
+    lam = _f64(lam).ravel()
+    return _new_op(ctx, lib().npcg_op_lowrank_create, _vp(ctx.h), _i64(g.shape[0]), _i64(g.shape[1]), _ptr(g),
+                   _i64(g.shape[0]), _ptr(lam), HOST)
+
+
+# ------------------------------------------------------------------ Nyström
+class _Nys:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.npcg_nys_destroy(_vp(self.h))
+            self.h = None
+
+
+@dataclass
+class NystromApproximation:
+    """reference NystromApproximation (nystrom.hpp:19-33); U/lambda fetched from device."""
+    u: np.ndarray
+    lam: np.ndarray
+    shift_used: float
+    h: object = field(default=None, repr=False)
+
+    @property
+    def lambda_min(self):
+        return float(self.lam[-1]) if self.lam.size else 0.0
+
+    def rank(self):
+        return int(np.count_nonzero(self.lam > 0))
+
+    def materialize(self):
+        return (self.u * self.lam) @ self.u.T
+
+
+def _approx_from(nys: _Nys, with_u: bool = True) -> NystromApproximation:
+    n, size, ell, shift = _i64(), _i64(), _i64(), C.c_double()
+    _check(lib().npcg_nys_info(_vp(nys.h), C.byref(n), C.byref(size), C.byref(ell), C.byref(shift)))
+    e = max(ell.value, 0)
+    lam = np.empty(e)
+    u = np.empty((n.value, e), order="F") if with_u else None
+    _check(lib().npcg_nys_get(_vp(nys.h), _ptr(lam), _ptr(u), _i64(max(n.value, 1)), HOST))
+    return NystromApproximation(u if u is not None else np.empty((n.value, 0)), lam, shift.value, nys)
+
+
+class SketchPair:
+    """reference SketchPair (nystrom.hpp:42-48): device-resident (omega, y)."""
+
+    def __init__(self, nys: _Nys, op: LinearOperator):
+        self._nys, self.op = nys, op
+
+    @property
+    def h(self):
+        return self._nys.h
+
+    def size(self) -> int:
+        size = _i64()
+        _check(lib().npcg_nys_info(_vp(self.h), None, C.byref(size), None, None))
+        return size.value
+
+    def arrays(self, n=None):
+        n = n or self.op.dim()
+        k = self.size()
+        om = np.empty((n, k), order="F")
+        y = np.empty((n, k), order="F")
+        _check(lib().npcg_nys_get_sketch(_vp(self.h), _ptr(om), _ptr(y), _i64(max(n, 1)), HOST))
+        return om, y
+
+
+def make_empty_sketch(n_or_op, op: LinearOperator | None = None) -> "SketchPair | _PendingSketch":
+    """make_empty_sketch(n) (nystrom.cpp:28-34). The device sketch binds to its
+    operator at the first extend_sketch call."""
+    if isinstance(n_or_op, LinearOperator):
+        op = n_or_op
+    if op is not None:
+        h = _vp()
+        _check(lib().npcg_nys_create(_vp(op.h), C.byref(h)))
+        return SketchPair(_Nys(h.value), op)
+    n = int(n_or_op)
+    if n < 1:
+        raise InvalidArgument("make_empty_sketch: dimension must be positive")
+    return _PendingSketch(n)
+
+
+class _PendingSketch:
+    def __init__(self, n):
+        self.n = n
+
+    def size(self):
+        return 0
+
+
+def extend_sketch(pair, op: LinearOperator, extra: int, rng: Rng) -> SketchPair:
+    """extend_sketch (nystrom.cpp:36-58); the device pair is grown in place
+    (old columns untouched) and returned."""
+    if isinstance(pair, _PendingSketch):
+        if pair.n != op.dim():
+            raise InvalidArgument("extend_sketch: dimension mismatch")
+        pair = make_empty_sketch(op)
+    _check(lib().npcg_nys_extend_rng(_vp(pair.h), _i64(extra), _vp(rng.h)))
+    return pair
+
+
+def extend_sketch_with(pair, op: LinearOperator, fresh) -> SketchPair:
+    """extend_sketch with a caller-drawn raw Gaussian block (n x extra)."""
+    if isinstance(pair, _PendingSketch):
+        pair = make_empty_sketch(op)
+    fresh = _f64(fresh)
+    _check(lib().npcg_nys_extend(_vp(pair.h), _i64(fresh.shape[1]), _ptr(fresh), _i64(fresh.shape[0]), HOST))
+    return pair
+
+
+def nystrom_from_sketch(pair: SketchPair) -> NystromApproximation:
+    """nystrom_from_sketch (nystrom.cpp:96-140), factored on device."""
+    _check(lib().npcg_nys_factor(_vp(pair.h)))
+    return _approx_from(pair._nys)
+
+
+def randomized_nystrom(op: LinearOperator, ell: int, rng: Rng) -> NystromApproximation:
+    """randomized_nystrom (nystrom.cpp:142-148)."""
+    n = op.dim()
+    if ell < 1 or ell > n:
+        raise InvalidArgument("randomized_nystrom: need 1 <= ell <= dim")
+    pair = extend_sketch(make_empty_sketch(op), op, ell, rng)
+    return nystrom_from_sketch(pair)
+
+
+def make_approximation(u, lam, shift_used=0.0, ctx: Context | None = None) -> NystromApproximation:
+    ctx = ctx or default_context()
+    u = _f64(u)
+    lam = _f64(lam).ravel()
+    n, ell = u.shape[0], lam.size
+    h = _vp()
+    _check(lib().npcg_nys_from_factors(_vp(ctx.h), _i64(n), _i64(ell), _ptr(u) if ell else None, _i64(max(n, 1)),
+                                       _ptr(lam) if ell else None, C.c_double(shift_used), HOST, C.byref(h)))
+    return NystromApproximation(u.reshape(n, ell), lam, shift_used, _Nys(h.value))
+
+
+# ------------------------------------------------------------------ preconditioner
+class NystromPreconditioner:
+    """npcg_pre: NystromPreconditioner (preconditioner.hpp:20-37) on device."""
+
+    def __init__(self, h, approx: NystromApproximation, mu: float):
+        self.h, self.approx, self.mu = h, approx, mu
+        self.n = approx.u.shape[0]
+        self.lambda_ell = approx.lambda_min
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.npcg_pre_destroy(_vp(self.h))
+            self.h = None
+
+    def _apply(self, fn, r):
+        r = _f64(r)
+        s = 1 if r.ndim == 1 else r.shape[1]
+        out = np.empty(r.shape, order="F")
+        _check(fn(_vp(self.h), _i64(s), _ptr(r), _i64(max(r.shape[0], 1)), _ptr(out), _i64(max(r.shape[0], 1)), HOST))
+        return out
+
+    def apply_inverse(self, r) -> np.ndarray:
+        r = np.asarray(r)
+        if r.shape[0] != self.n:
+            raise InvalidArgument("NystromPreconditioner - apply_inverse: length mismatch")
+        return self._apply(lib().npcg_pre_apply_inverse, r)
+
+    def apply(self, v) -> np.ndarray:
+        v = np.asarray(v)
+        if v.shape[0] != self.n:
+            raise InvalidArgument("NystromPreconditioner - apply: length mismatch")
+        return self._apply(lib().npcg_pre_apply, v)
+
+
+def build_preconditioner(approx: NystromApproximation, mu: float) -> NystromPreconditioner:
+    """build_preconditioner (preconditioner.cpp:80-89)."""
+    h = _vp()
+    _check(lib().npcg_pre_create(_vp(approx.h.h), C.c_double(mu), C.byref(h)))
+    return NystromPreconditioner(h.value, approx, mu)
+
+
+# ------------------------------------------------------------------ solvers
+@dataclass
+class SolveReport:
+    x: np.ndarray
+    iterations: int
+    residual_history: np.ndarray
+    converged: bool
+    matvec_count: int
+    wall_time: float
+    eta_used: float
+    iterates: np.ndarray | None = None
+    status: int = 0
+
+
+def _pcg(op, pre, mu, B, eta, max_iter, relative, record_iterates, x0):
+    B = _f64(B)
+    single = B.ndim == 1
+    if single:
+        B = B.reshape(-1, 1, order="F")
+    n, s = B.shape
+    if n != op.dim():
+        raise InvalidArgument("nystrom_pcg: right-hand side length mismatch")
+    if x0 is not None:
+        x0 = _f64(x0).reshape(n, s, order="F")
+        if x0.shape[0] != n:
+            raise InvalidArgument("nystrom_pcg: initial guess length mismatch")
+    X = np.empty((n, s), order="F")
+    reps = (_SolveReport * s)()
+    hist = np.zeros((max(max_iter, 0) + 1, s), order="F")
+    its = np.zeros(((max_iter + 1) * n * s,)) if record_iterates else None
+    opts = _SolveOpts(float(eta), int(max_iter), int(bool(relative)), int(bool(record_iterates)))
+    rc = lib().npcg_pcg(_vp(op.h), None if pre is None else _vp(pre.h), C.c_double(mu), _i64(s), _ptr(B), _i64(n),
+                        _ptr(x0), _i64(n), C.byref(opts), _ptr(X), _i64(n), reps, _ptr(hist), _ptr(its), HOST)
+    out = []
+    for j in range(s):
+        r = reps[j]
+        iters = None
+        if its is not None:
+            full = its.reshape(max_iter + 1, s, n)
+            iters = full[: r.history_len, j, :].copy()
+        out.append(SolveReport(X[:, j].copy(), r.iterations, hist[: r.history_len, j].copy(), bool(r.converged),
+                               r.matvec_count, r.wall_time, r.eta_used, iters, r.status))
+    if rc != 0:
+        bad = next((o for o in out if o.status != 0), out[0])
+        _check(rc, bad if single or rc == 3 else None)
+    return out[0] if single else out
+
+
+def nystrom_pcg(op: LinearOperator, b, mu: float, precond: NystromPreconditioner | None, eta=1e-10, max_iter=500,
+                relative=False, record_iterates=False, x0=None):
+    """nystrom_pcg (solvers.cpp:122-148). `b` may be n x s: s independent
+    solves sharing each pass over A (returns a list of reports)."""
+    if precond is None:  # empty preconditioner == identity
+        return _pcg(op, None, mu, b, eta, max_iter, relative, record_iterates, x0)
+    return _pcg(op, precond, mu, b, eta, max_iter, relative, record_iterates, x0)
+
+
+def cg(op: LinearOperator, mu: float, b, eta=1e-10, max_iter=500, relative=False, x0=None):
+    """cg on A + mu I (solvers.cpp:111-120)."""
+    return _pcg(op, None, mu, b, eta, max_iter, relative, False, x0)
+
+
+@dataclass
+class BlockSolveReport:
+    x: np.ndarray
+    iterations: int
+    converged: list
+    deflated: list
+    fallback_count: int
+    final_residual: np.ndarray
+
+
+def block_nystrom_pcg(op, B, mu, precond, eta=1e-10, max_iter=500, relative=False) -> BlockSolveReport:
+    """block_nystrom_pcg (solvers.cpp:150-279)."""
+    B = _f64(B)
+    n, s = B.shape
+    X = np.empty((n, s), order="F")
+    rep = _BlockReport()
+    conv = (C.c_int * s)()
+    defl = (_i64 * s)()
+    fres = np.empty(s)
+    opts = _SolveOpts(float(eta), int(max_iter), int(bool(relative)), 0)
+    _check(lib().npcg_block_pcg(_vp(op.h), None if precond is None else _vp(precond.h), C.c_double(mu), _i64(s),
+                                _ptr(B), _i64(n), C.byref(opts), _ptr(X), _i64(n), C.byref(rep), conv, defl,
+                                _ptr(fres), HOST))
+    return BlockSolveReport(X, rep.iterations, [bool(c) for c in conv], list(defl[: rep.n_deflated]),
+                            rep.fallback_count, fres)
+
+
+def iteration_bound(kappa: float, eps: float) -> int:
+    out = _i64()
+    _check(lib().npcg_iteration_bound(C.c_double(kappa), C.c_double(eps), C.byref(out)))
+    return out.value
+
+
+# ------------------------------------------------------------------ adaptive
+def estimate_error_power(op: LinearOperator, approx: NystromApproximation, q: int, rng: Rng) -> float:
+    """estimate_error_power (adaptive.cpp:83-109)."""
+    out = C.c_double()
+    _check(lib().npcg_power_estimate_rng(_vp(op.h), _vp(approx.h.h), _i64(q), _vp(rng.h), C.byref(out)))
+    return out.value
+
+
+@dataclass
+class AdaptiveOutcome:
+    approximation: NystromApproximation
+    error_estimate: float | None
+    doublings: int
+    hit_cap: bool
+    posterior_condition_estimate: float
+    ell_final: int
+
+
+def adaptive(op, rng: Rng, *, mode="error", ell0=10, ell_max=0, mu=0.0, tau=None, q=5, secondary_criterion=True,
+             sketch="gaussian") -> AdaptiveOutcome:
+    """adaptive_nystrom (mode='error'), adaptive_nystrom_ratio ('ratio'),
+    fixed_rank_nystrom ('fixed') — adaptive.cpp:50-148."""
+    modes = {"error": 0, "ratio": 1, "fixed": 2}
+    cfg = _AdaptiveCfg(int(ell0), int(ell_max), float(mu), modes[mode], int(tau is not None), float(tau or 0.0),
+                       int(q), int(bool(secondary_criterion)), 0 if sketch == "gaussian" else 1)
+    out = _AdaptiveOutcome()
+    h = _vp()
+    _check(lib().npcg_adaptive(_vp(op.h), C.byref(cfg), _vp(rng.h), C.byref(h), C.byref(out)))
+    approx = _approx_from(_Nys(h.value))
+    return AdaptiveOutcome(approx, out.error_estimate if out.has_error_estimate else None, out.doublings,
+                           bool(out.hit_cap), out.posterior_condition, out.ell_final)
+
+
+def adaptive_nystrom(op, config: dict, rng: Rng) -> AdaptiveOutcome:
+    return adaptive(op, rng, mode="error", **config)
+
+
+def posterior_condition_estimate(lam_ell, mu, err) -> float:
+    out = C.c_double()
+    _check(lib().npcg_posterior_condition(C.c_double(lam_ell), C.c_double(mu), C.c_double(err), C.byref(out)))
+    return out.value

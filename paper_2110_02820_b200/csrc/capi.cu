@@ -1,0 +1,853 @@
+// The C-ABI (include/npcg_capi.h): argument validation with the reference's
+// messages, host<->device staging, and the orchestration loops (adaptive
+// doubling, power method). Every compute step below is a CUDA kernel of this
+// library; there is no CPU fallback.
+#include <cuda.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <new>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "blas.cuh"
+#include "factor.cuh"
+#include "gemm.cuh"
+#include "ops.cuh"
+#include "pcg.cuh"
+#include "rng.hpp"
+
+using namespace npcg;
+
+struct npcg_ctx {
+  std::unique_ptr<Ctx> c;
+};
+struct npcg_rng {
+  HostRng r;
+};
+struct npcg_op {
+  npcg_ctx* ctx;
+  std::unique_ptr<Op> op;
+};
+struct npcg_nys {
+  npcg_ctx* ctx;
+  Nys s;
+};
+struct npcg_pre {
+  npcg_ctx* ctx;
+  npcg_nys* nys;
+  Pre p;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return NPCG_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return NPCG_EINVAL;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return NPCG_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NPCG_ERUNTIME;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) invalid(std::string(what) + ": null handle or pointer");
+}
+
+/// Device view of a caller matrix: uses the caller's device buffer when it is
+/// already TMA/vector friendly, else stages a copy.
+struct View {
+  DMat owned;
+  const double* p = nullptr;
+  i64 ld = 0;
+};
+View view_in(Ctx& ctx, const double* src, i64 rows, i64 cols, i64 ld, int where) {
+  View v;
+  if (where == NPCG_DEVICE && ld % 2 == 0 && ld >= rows && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    v.p = src;
+    v.ld = ld;
+    return v;
+  }
+  upload(ctx, v.owned, rows, cols, src, ld, where);
+  v.p = v.owned.p();
+  v.ld = v.owned.ld;
+  return v;
+}
+
+double ulp_spacing_host(double x) {
+  const double ax = std::abs(x);
+  return std::nextafter(ax, std::numeric_limits<double>::infinity()) - ax;
+}
+
+Ctx& C(npcg_ctx* c) {
+  need(c, "context");
+  c->c->activate();
+  return *c->c;
+}
+}  // namespace
+
+// ============================== context =====================================
+namespace npcg {
+Ctx::Ctx(int dev) : device(dev) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    fail(NPCG_ECUDA, "no CUDA device available (libnpcg_b200 has no CPU fallback)");
+  if (dev < 0 || dev >= count) invalid("npcg_ctx_create: device index out of range");
+  NPCG_CUDA(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  NPCG_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major < 10) fail(NPCG_ECUDA, std::string("libnpcg_b200 needs an sm_100 (B200) device, found ") + prop.name);
+  sm_count = prop.multiProcessorCount;
+  max_smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
+  NPCG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  cudaMemPool_t pool;
+  NPCG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = std::numeric_limits<uint64_t>::max();
+  NPCG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  NPCG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) fail(NPCG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  encode_tiled = reinterpret_cast<EncodeTiledFn>(fn);
+}
+Ctx::~Ctx() {
+  if (stream) {
+    cudaSetDevice(device);
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
+}
+}  // namespace npcg
+
+extern "C" {
+
+const char* npcg_last_error(void) { return g_err.c_str(); }
+const char* npcg_version(void) { return "npcg_b200 0.1 (sm_100a)"; }
+
+int npcg_ctx_create(int device, npcg_ctx** out) {
+  return guard([&] {
+    need(out, "npcg_ctx_create");
+    auto c = std::make_unique<npcg_ctx>();
+    c->c = std::make_unique<Ctx>(device);
+    *out = c.release();
+  });
+}
+int npcg_ctx_destroy(npcg_ctx* ctx) {
+  return guard([&] { delete ctx; });
+}
+int npcg_ctx_sync(npcg_ctx* ctx) {
+  return guard([&] { C(ctx).sync(); });
+}
+void* npcg_ctx_stream(npcg_ctx* ctx) { return ctx ? ctx->c->stream : nullptr; }
+int64_t npcg_ctx_launches(npcg_ctx* ctx) { return ctx ? ctx->c->launches.load() : 0; }
+int npcg_dev_alloc(npcg_ctx* ctx, int64_t bytes, void** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    NPCG_CUDA(cudaMallocAsync(out, static_cast<size_t>(std::max<int64_t>(bytes, 16)), c.stream));
+    c.sync();
+  });
+}
+int npcg_dev_free(npcg_ctx* ctx, void* p) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    NPCG_CUDA(cudaFreeAsync(p, c.stream));
+  });
+}
+int npcg_memcpy(npcg_ctx* ctx, void* dst, int dst_where, const void* src, int src_where, int64_t bytes) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    const cudaMemcpyKind k = dst_where == NPCG_DEVICE
+                                 ? (src_where == NPCG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice)
+                                 : (src_where == NPCG_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost);
+    NPCG_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), k, c.stream));
+    c.sync();
+  });
+}
+
+// =============================== random =====================================
+int npcg_rng_create(uint64_t seed, npcg_rng** out) {
+  return guard([&] { *out = new npcg_rng{HostRng(seed)}; });
+}
+int npcg_rng_clone(const npcg_rng* rng, npcg_rng** out) {
+  return guard([&] { *out = new npcg_rng(*rng); });
+}
+int npcg_rng_destroy(npcg_rng* rng) {
+  delete rng;
+  return NPCG_OK;
+}
+double npcg_rng_normal(npcg_rng* rng) { return rng->r.normal(); }
+double npcg_rng_uniform(npcg_rng* rng) { return rng->r.uniform(); }
+uint64_t npcg_rng_word(npcg_rng* rng) { return rng->r.engine(); }
+void npcg_rng_discard(npcg_rng* rng, uint64_t words) { rng->r.engine.discard(words); }
+int npcg_rng_integer(npcg_rng* rng, uint64_t bound, uint64_t* out) {
+  return guard([&] { *out = rng->r.integer(bound); });
+}
+int npcg_rng_gaussian(npcg_rng* rng, int64_t rows, int64_t cols, double* dst) {
+  return guard([&] { rng->r.gaussian(rows, cols, dst); });
+}
+int npcg_rng_sample(npcg_rng* rng, int64_t n, int64_t k, int64_t* out) {
+  return guard([&] {  // random.cpp:44-56
+    if (k < 0 || k > n) invalid("sample_without_replacement: need 0 <= k <= n");
+    std::vector<int64_t> pool(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) pool[static_cast<size_t>(i)] = i;
+    for (int64_t i = 0; i < k; ++i) {
+      const int64_t j = i + static_cast<int64_t>(rng->r.integer(static_cast<uint64_t>(n - i)));
+      std::swap(pool[static_cast<size_t>(i)], pool[static_cast<size_t>(j)]);
+    }
+    std::copy(pool.begin(), pool.begin() + k, out);
+  });
+}
+uint64_t npcg_splitmix64(uint64_t seed) {  // bench.cpp:180-185
+  uint64_t z = seed + 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+double npcg_ulp_spacing(double x) { return ulp_spacing_host(x); }
+
+// ============================== operators ===================================
+namespace {
+npcg_op* make_dense(npcg_ctx* ctx, DMat&& a, i64 n, int kind) {
+  auto op = std::make_unique<DenseOp>();
+  op->ctx = ctx->c.get();
+  op->n = n;
+  op->kind = kind;
+  op->a = std::move(a);
+  auto h = new npcg_op{ctx, std::move(op)};
+  return h;
+}
+}  // namespace
+
+int npcg_op_dense_create(npcg_ctx* ctx, int64_t rows, int64_t cols, const double* a, int64_t lda, int where,
+                         npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (rows != cols) invalid("DenseOperator: matrix must be square");  // operators.cpp:65
+    DMat A;
+    upload(c, A, rows, cols, a, lda, where);
+    double asym = 0.0, amax = 0.0;
+    symmetry_stats(c, A.p(), rows, A.ld, &asym, &amax);
+    if (asym > 1e-12 * std::max(1.0, amax)) invalid("DenseOperator: matrix must be symmetric");  // :66-69
+    *out = make_dense(ctx, std::move(A), rows, kDense);
+  });
+}
+
+int npcg_op_gram_create(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, int64_t ldg, int where, npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (m < 1 || n < 1) invalid("GramRidgeOperator: design matrix must be nonempty");  // operators.cpp:106-107
+    auto op = std::make_unique<GramOp>();
+    op->ctx = &c;
+    op->n = n;
+    op->m = m;
+    op->kind = kGram;
+    upload(c, op->g, m, n, g, ldg, where);
+    if (!all_finite(c, op->g.p(), m, n, op->g.ld))
+      invalid("GramRidgeOperator: design matrix has non-finite entries");
+    *out = new npcg_op{ctx, std::move(op)};
+  });
+}
+
+int npcg_op_kernel_create(npcg_ctx* ctx, int64_t n, int64_t d, const double* pts, int64_t ldp, double sigma,
+                          int64_t dense_cap, int where, npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (n < 1) invalid("KernelOperator: need at least one point");   // operators.cpp:143
+    if (!(sigma > 0.0)) invalid("KernelOperator: sigma must be > 0");  // :144
+    DMat P;
+    upload(c, P, n, d, pts, ldp, where);
+    if (!all_finite(c, P.p(), n, d, P.ld)) invalid("KernelOperator: points have non-finite entries");
+    if (n <= dense_cap) {  // :148-149
+      DMat K;
+      build_kernel_matrix(c, P, n, d, sigma, K);
+      *out = make_dense(ctx, std::move(K), n, kKernelStored);
+    } else {
+      auto op = std::make_unique<KernelFreeOp>();
+      op->ctx = &c;
+      op->n = n;
+      op->d = d;
+      op->sigma = sigma;
+      op->kind = kKernelFree;
+      op->pts = std::move(P);
+      prepare_kernel_free(c, *op);
+      *out = new npcg_op{ctx, std::move(op)};
+    }
+  });
+}
+
+int npcg_op_synthesize(npcg_ctx* ctx, int64_t n, const double* lambda, uint64_t seed, npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    // SpectrumProfile validation (operators.cpp:190-199)
+    if (n < 1) invalid("SpectrumProfile: need at least one eigenvalue");
+    for (int64_t i = 0; i < n; ++i) {
+      if (!(lambda[i] >= 0.0) || !std::isfinite(lambda[i]))
+        invalid("SpectrumProfile: eigenvalues must be finite and >= 0");
+      if (i > 0 && lambda[i] > lambda[i - 1]) invalid("SpectrumProfile: eigenvalues must be nonincreasing");
+    }
+    // operators.cpp:211-219: Q from a seeded n x n Gaussian; A = Q diag(l) Q^T; (A + A^T)/2
+    HostRng rng(seed);
+    std::vector<double> g(static_cast<size_t>(n * n));
+    rng.gaussian(n, n, g.data());
+    DMat G, Q, A, S;
+    upload(c, G, n, n, g.data(), n, NPCG_HOST);
+    Q.alloc(n, n, c.stream, false);
+    orthonormalize(c, G.p(), G.ld, n, n, Q.p(), Q.ld);
+    DBuf<double> lam(n, c.stream);
+    NPCG_CUDA(cudaMemcpyAsync(lam.p, lambda, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    copy2d(c, n, n, Q.p(), Q.ld, G.p(), G.ld);  // G <- Q diag(lambda)
+    scale_cols(c, G.p(), n, n, G.ld, lam.p);
+    A.alloc(n, n, c.stream, false);
+    gemm(c, n, n, n, 1.0, Operand{G.p(), G.ld, false}, Operand{Q.p(), Q.ld, false}, 0.0, A.p(), A.ld);
+    S.alloc(n, n, c.stream, true);
+    symmetrize(c, A.p(), n, A.ld, S.p(), S.ld);
+    c.sync();
+    *out = make_dense(ctx, std::move(S), n, kDense);
+  });
+}
+
+int npcg_op_lowrank_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g, int64_t ldg, const double* lambda,
+                           int where, npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (n < 1 || r < 1) invalid("lowrank operator: need n >= 1 and r >= 1");
+    DMat G, GD, A, S;
+    upload(c, G, n, r, g, ldg, where);
+    GD.alloc(n, r, c.stream, false);
+    copy2d(c, n, r, G.p(), G.ld, GD.p(), GD.ld);
+    DBuf<double> lam(r, c.stream);
+    NPCG_CUDA(cudaMemcpyAsync(lam.p, lambda, sizeof(double) * r, cudaMemcpyHostToDevice, c.stream));
+    scale_cols(c, GD.p(), n, r, GD.ld, lam.p);
+    A.alloc(n, n, c.stream, false);
+    gemm(c, n, n, r, 1.0, Operand{GD.p(), GD.ld, false}, Operand{G.p(), G.ld, false}, 0.0, A.p(), A.ld);
+    divide(c, n, n, A.p(), A.ld, static_cast<double>(r));
+    S.alloc(n, n, c.stream, true);
+    symmetrize(c, A.p(), n, A.ld, S.p(), S.ld);
+    c.sync();
+    *out = make_dense(ctx, std::move(S), n, kDense);
+  });
+}
+
+int npcg_op_destroy(npcg_op* op) {
+  return guard([&] {
+    if (op) {
+      op->ctx->c->activate();
+      op->ctx->c->sync();
+      delete op;
+    }
+  });
+}
+int npcg_op_dim(const npcg_op* op, int64_t* n) {
+  return guard([&] {
+    need(op, "npcg_op_dim");
+    *n = op->op->n;
+  });
+}
+int npcg_op_kind(const npcg_op* op) { return op ? op->op->kind : -1; }
+int npcg_op_has_column_access(const npcg_op* op) { return op && op->op->has_column() ? 1 : 0; }
+
+int npcg_op_apply(npcg_op* op, int64_t rows, int64_t k, const double* v, int64_t ldv, double* out, int64_t ldo,
+                  int where) {
+  return guard([&] {
+    need(op, "npcg_op_apply");
+    Ctx& c = C(op->ctx);
+    const i64 n = op->op->n;
+    const bool single = k == 1;
+    if (rows != n) {  // operators.cpp:14-19, 33-34
+      if (single)
+        invalid("LinearOperator - matvec: dimension mismatch (got " + std::to_string(rows) + ", operator dim " +
+                std::to_string(n) + ")");
+      invalid("LinearOperator - apply_block: dimension mismatch");
+    }
+    if (k <= 0) return;
+    View in = view_in(c, v, n, k, ldv, where);
+    if (!all_finite(c, in.p, n, k, in.ld))
+      invalid(single ? "LinearOperator - matvec: input has non-finite entries"
+                     : "LinearOperator - apply_block: input has non-finite entries");
+    DMat o;
+    o.alloc(n, k, c.stream, false);
+    op->op->apply(in.p, in.ld, k, o.p(), o.ld);
+    download(c, o.p(), o.ld, n, k, out, ldo, where);
+    c.sync();
+  });
+}
+
+int npcg_op_column(npcg_op* op, int64_t j, double* out, int where) {
+  return guard([&] {
+    need(op, "npcg_op_column");
+    Ctx& c = C(op->ctx);
+    if (!op->op->has_column()) fail(NPCG_ERUNTIME, "LinearOperator - column: operator has no column access");
+    if (j < 0 || j >= op->op->n) invalid("LinearOperator - column: index out of range");
+    DMat o;
+    o.alloc(op->op->n, 1, c.stream, false);
+    op->op->column(j, o.p());
+    download(c, o.p(), o.ld, op->op->n, 1, out, op->op->n, where);
+    c.sync();
+  });
+}
+
+// =============================== Nyström ====================================
+int npcg_nys_create(npcg_op* op, npcg_nys** out) {
+  return guard([&] {
+    need(op, "npcg_nys_create");
+    Ctx& c = C(op->ctx);
+    if (op->op->n < 1) invalid("make_empty_sketch: dimension must be positive");
+    auto h = std::make_unique<npcg_nys>();
+    h->ctx = op->ctx;
+    h->s.ctx = &c;
+    h->s.op = op->op.get();
+    h->s.n = op->op->n;
+    *out = h.release();
+  });
+}
+int npcg_nys_extend(npcg_nys* nys, int64_t extra, const double* omega_raw, int64_t ld, int where) {
+  return guard([&] {
+    need(nys, "npcg_nys_extend");
+    C(nys->ctx);
+    nys_extend(nys->s, omega_raw, ld, extra, where);
+    nys->ctx->c->sync();
+  });
+}
+int npcg_nys_extend_rng(npcg_nys* nys, int64_t extra, npcg_rng* rng) {
+  return guard([&] {
+    need(nys, "npcg_nys_extend_rng");
+    C(nys->ctx);
+    // nystrom.cpp:36-45: validate, then draw the n x extra Gaussian block.
+    if (extra < 1) invalid("extend_sketch: extra must be >= 1");
+    if (nys->s.size + extra > nys->s.n) invalid("extend_sketch: sketch size would exceed dimension");
+    std::vector<double> raw(static_cast<size_t>(nys->s.n * extra));
+    rng->r.gaussian(nys->s.n, extra, raw.data());
+    nys_extend(nys->s, raw.data(), nys->s.n, extra, NPCG_HOST);
+    nys->ctx->c->sync();
+  });
+}
+int npcg_nys_factor(npcg_nys* nys) {
+  return guard([&] {
+    need(nys, "npcg_nys_factor");
+    C(nys->ctx);
+    nys_factor(nys->s);
+  });
+}
+int npcg_nys_from_factors(npcg_ctx* ctx, int64_t n, int64_t ell, const double* u, int64_t ldu, const double* lambda,
+                          double shift_used, int where, npcg_nys** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    auto h = std::make_unique<npcg_nys>();
+    h->ctx = ctx;
+    Nys& s = h->s;
+    s.ctx = &c;
+    s.n = n;
+    s.ell = ell;
+    s.shift = shift_used;
+    s.factored = true;
+    if (ell > 0) {
+      upload(c, s.u, n, ell, u, ldu, where);
+      s.lambda.alloc(ell, c.stream);
+      NPCG_CUDA(cudaMemcpyAsync(s.lambda.p, lambda, sizeof(double) * ell,
+                                where == NPCG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c.stream));
+      s.lambda_host.resize(static_cast<size_t>(ell));
+      NPCG_CUDA(cudaMemcpyAsync(s.lambda_host.data(), s.lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToHost,
+                                c.stream));
+    } else {
+      s.u.alloc(n, 0, c.stream, false);
+    }
+    c.sync();
+    *out = h.release();
+  });
+}
+int npcg_nys_info(const npcg_nys* nys, int64_t* n, int64_t* sketch_cols, int64_t* ell_factored, double* shift) {
+  return guard([&] {
+    need(nys, "npcg_nys_info");
+    if (n) *n = nys->s.n;
+    if (sketch_cols) *sketch_cols = nys->s.size;
+    if (ell_factored) *ell_factored = nys->s.factored ? nys->s.ell : -1;
+    if (shift) *shift = nys->s.shift;
+  });
+}
+int npcg_nys_get(npcg_nys* nys, double* lambda, double* u, int64_t ldu, int where) {
+  return guard([&] {
+    need(nys, "npcg_nys_get");
+    Ctx& c = C(nys->ctx);
+    if (!nys->s.factored) fail(NPCG_ERUNTIME, "npcg_nys_get: approximation not factored (call npcg_nys_factor)");
+    const i64 ell = nys->s.ell;
+    if (lambda && ell > 0) {
+      if (where == NPCG_HOST) std::memcpy(lambda, nys->s.lambda_host.data(), sizeof(double) * ell);
+      else NPCG_CUDA(cudaMemcpyAsync(lambda, nys->s.lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    if (u && ell > 0) download(c, nys->s.u.p(), nys->s.u.ld, nys->s.n, ell, u, ldu, where);
+    c.sync();
+  });
+}
+int npcg_nys_get_sketch(npcg_nys* nys, double* omega, double* y, int64_t ld, int where) {
+  return guard([&] {
+    need(nys, "npcg_nys_get_sketch");
+    Ctx& c = C(nys->ctx);
+    if (nys->s.size == 0) return;
+    if (omega) download(c, nys->s.omega.p(), nys->s.omega.ld, nys->s.n, nys->s.size, omega, ld, where);
+    if (y) download(c, nys->s.y.p(), nys->s.y.ld, nys->s.n, nys->s.size, y, ld, where);
+    c.sync();
+  });
+}
+int npcg_nys_destroy(npcg_nys* nys) {
+  return guard([&] {
+    if (nys) {
+      nys->ctx->c->activate();
+      nys->ctx->c->sync();
+      delete nys;
+    }
+  });
+}
+
+// ============================ preconditioner ================================
+int npcg_pre_create(npcg_nys* nys, double mu, npcg_pre** out) {
+  return guard([&] {
+    need(nys, "npcg_pre_create");
+    C(nys->ctx);
+    if (!nys->s.factored) fail(NPCG_ERUNTIME, "build_preconditioner: approximation not factored");
+    auto h = std::make_unique<npcg_pre>();
+    h->ctx = nys->ctx;
+    h->nys = nys;
+    pre_build(h->p, nys->s, mu);
+    *out = h.release();
+  });
+}
+namespace {
+int pre_apply_common(npcg_pre* pre, int64_t s, const double* r, int64_t ldr, double* z, int64_t ldz, int where,
+                     bool inverse) {
+  return guard([&] {
+    need(pre, "npcg_pre_apply");
+    Ctx& c = C(pre->ctx);
+    if (s <= 0) return;
+    const i64 n = pre->p.n;
+    View in = view_in(c, r, n, s, ldr, where);
+    DMat o;
+    o.alloc(n, s, c.stream, false);
+    if (inverse) pre_apply_inverse(pre->p, in.p, in.ld, s, o.p(), o.ld);
+    else pre_apply(pre->p, in.p, in.ld, s, o.p(), o.ld);
+    download(c, o.p(), o.ld, n, s, z, ldz, where);
+    c.sync();
+  });
+}
+}  // namespace
+int npcg_pre_apply_inverse(npcg_pre* pre, int64_t s, const double* r, int64_t ldr, double* z, int64_t ldz, int where) {
+  return pre_apply_common(pre, s, r, ldr, z, ldz, where, true);
+}
+int npcg_pre_apply(npcg_pre* pre, int64_t s, const double* v, int64_t ldv, double* out, int64_t ldo, int where) {
+  return pre_apply_common(pre, s, v, ldv, out, ldo, where, false);
+}
+int npcg_pre_destroy(npcg_pre* pre) {
+  delete pre;
+  return NPCG_OK;
+}
+
+// ================================ solvers ===================================
+int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, int64_t ldb, const double* x0,
+             int64_t ldx0, const npcg_solve_opts* opts, double* x, int64_t ldx, npcg_solve_report* reports,
+             double* history, double* iterates, int where) {
+  bool diverged = false;
+  std::string dmsg;
+  int rc = guard([&] {
+    need(op, "npcg_pcg");
+    need(opts, "npcg_pcg options");
+    Ctx& c = C(op->ctx);
+    const char* context = pre ? "nystrom_pcg" : "cg";
+    if (pre) {  // solvers.cpp:134-136
+      if (!(mu >= 0.0)) invalid("nystrom_pcg: mu must be >= 0");
+      if (pre->p.ell > 0) {
+        if (pre->p.n != op->op->n) invalid("nystrom_pcg: preconditioner dimension mismatch");
+        if (pre->p.mu != mu) invalid("nystrom_pcg: preconditioner built with a different mu");
+      }
+    } else if (!(mu >= 0.0)) {
+      invalid("RegularizedOperator: mu must be >= 0");
+    }
+    if (!(opts->eta > 0.0)) invalid(std::string(context) + ": eta must be > 0");  // solvers.cpp:27-31
+    if (opts->max_iter < 0) invalid(std::string(context) + ": max_iter must be >= 0");
+    const i64 n = op->op->n;
+    if (s <= 0) return;
+    PcgOptions po{opts->eta, opts->max_iter, opts->relative != 0, opts->record_iterates != 0};
+    View B = view_in(c, b, n, s, ldb, where);
+    View X0;
+    if (x0) {
+      X0 = view_in(c, x0, n, s, ldx0, where);
+      if (!all_finite(c, X0.p, n, s, X0.ld)) invalid("LinearOperator - matvec: input has non-finite entries");
+    }
+    DMat X;
+    X.alloc(n, s, c.stream, false);
+    DBuf<double> its;
+    if (iterates && po.record_iterates) {
+      its.alloc((po.max_iter + 1) * n * std::min<i64>(s, 8), c.stream);
+      its.zero();
+    }
+    for (i64 s0 = 0; s0 < s; s0 += 8) {
+      const i64 sb = std::min<i64>(8, s - s0);
+      PcgResult r = pcg_solve(c, *op->op, pre ? &pre->p : nullptr, mu, sb, B.p + s0 * B.ld, B.ld,
+                              x0 ? X0.p + s0 * X0.ld : nullptr, X0.ld, po, X.p() + s0 * X.ld, X.ld,
+                              its.p ? its.p : nullptr, context);
+      for (i64 j = 0; j < sb; ++j) {
+        const PcgColumnReport& cr = r.cols[static_cast<size_t>(j)];
+        npcg_solve_report& rep = reports[s0 + j];
+        rep.iterations = cr.iterations;
+        rep.matvec_count = cr.matvec_count;
+        rep.converged = cr.converged ? 1 : 0;
+        rep.status = cr.status;
+        rep.eta_used = cr.eta_used;
+        rep.wall_time = r.wall_time;
+        rep.history_len = static_cast<int64_t>(cr.history.size());
+        if (history)
+          std::copy(cr.history.begin(), cr.history.end(), history + (s0 + j) * (po.max_iter + 1));
+      }
+      if (its.p) {  // layout to caller: [t][col][n] for the whole s
+        std::vector<double> h(static_cast<size_t>((po.max_iter + 1) * n * sb));
+        NPCG_CUDA(cudaMemcpy(h.data(), its.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+        for (i64 t = 0; t <= po.max_iter; ++t)
+          for (i64 j = 0; j < sb; ++j)
+            std::copy(h.begin() + (t * sb + j) * n, h.begin() + (t * sb + j + 1) * n,
+                      iterates + (t * s + s0 + j) * n);
+      }
+      if (r.diverged) {
+        diverged = true;
+        if (dmsg.empty()) dmsg = r.message;
+      }
+    }
+    download(c, X.p(), X.ld, n, s, x, ldx, where);
+    c.sync();
+  });
+  if (rc == NPCG_OK && diverged) {
+    g_err = dmsg;
+    return NPCG_EDIVERGED;
+  }
+  return rc;
+}
+
+int npcg_block_pcg(npcg_op*, npcg_pre*, double, int64_t, const double*, int64_t, const npcg_solve_opts*, double*,
+                   int64_t, npcg_block_report*, int*, int64_t*, double*, int) {
+  g_err = "block_nystrom_pcg: not available in this build";
+  return NPCG_ERUNTIME;
+}
+
+int npcg_iteration_bound(double kappa, double epsilon, int64_t* out) {
+  return guard([&] {  // solvers.cpp:281-291
+    if (!(kappa >= 1.0)) invalid("iteration_bound: kappa must be >= 1");
+    if (!(epsilon > 0.0 && epsilon < 1.0)) invalid("iteration_bound: epsilon must lie in (0, 1)");
+    if (kappa == 1.0) {
+      *out = 1;
+      return;
+    }
+    const double root = std::sqrt(kappa);
+    const double rate = std::log((root + 1.0) / (root - 1.0));
+    const double t = std::ceil(std::log(2.0 / epsilon) / rate);
+    *out = std::max<int64_t>(1, static_cast<int64_t>(t));
+  });
+}
+
+// =============================== adaptive ===================================
+namespace {
+double dot_dev(Ctx& c, const double* a, const double* b, i64 n) {
+  // v.w through the coldot kernel (one column dotted with one vector)
+  DBuf<double> o(1, c.stream);
+  coldot(c, a, dev_ld(n), n, 1, b, dev_ld(n), 1, o.p, 1);
+  double h = 0.0;
+  NPCG_CUDA(cudaMemcpyAsync(&h, o.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  return h;
+}
+
+// estimate_error_power (adaptive.cpp:83-109) from the raw start vector g.
+double power_estimate(Ctx& c, Op& op, const Nys& s, i64 q, const double* g_dev) {
+  const i64 n = op.n, ell = s.factored ? s.ell : 0;
+  DMat v, w, t;
+  v.alloc(n, 1, c.stream, true);
+  w.alloc(n, 1, c.stream, true);
+  copy2d(c, n, 1, g_dev, n, v.p(), v.ld);
+  const double v0 = std::sqrt(sum_squares(c, v.p(), n, 1, v.ld));
+  if (v0 == 0.0) return 0.0;
+  divide(c, n, 1, v.p(), v.ld, v0);
+  double estimate = 0.0;
+  if (ell > 0) t.alloc(ell, 1, c.stream, false);
+  for (i64 i = 0; i < q; ++i) {
+    op.apply(v.p(), v.ld, 1, w.p(), w.ld);
+    if (ell > 0) {  // w -= U (lambda .* (U^T v))
+      coldot(c, s.u.p(), s.u.ld, n, ell, v.p(), v.ld, 1, t.p(), t.ld);
+      scale_cols(c, t.p(), 1, ell, 1, s.lambda.p);  // t_j *= lambda_j (as a 1 x ell row)
+      axpby(c, ell, 1, 0.0, t.p(), -1.0, t.p(), t.ld);  // t = -t (exact)
+      rowdot(c, s.u.p(), s.u.ld, n, ell, t.p(), t.ld, 1, w.p(), w.ld, w.p(), w.ld);
+    }
+    estimate = dot_dev(c, v.p(), w.p(), n);
+    const double nrm = std::sqrt(sum_squares(c, w.p(), n, 1, w.ld));
+    if (nrm == 0.0) return 0.0;
+    copy2d(c, n, 1, w.p(), w.ld, v.p(), v.ld);
+    divide(c, n, 1, v.p(), v.ld, nrm);
+  }
+  return estimate;
+}
+}  // namespace
+
+int npcg_power_estimate(npcg_op* op, npcg_nys* nys, int64_t q, const double* g_raw, int where, double* est) {
+  return guard([&] {
+    need(op, "npcg_power_estimate");
+    need(nys, "npcg_power_estimate");
+    Ctx& c = C(op->ctx);
+    if (q < 1) invalid("estimate_error_power: q must be >= 1");  // adaptive.cpp:86
+    if (nys->s.factored && nys->s.ell > 0 && nys->s.n != op->op->n)
+      invalid("estimate_error_power: factor shape mismatch");
+    View g = view_in(c, g_raw, op->op->n, 1, op->op->n, where);
+    *est = power_estimate(c, *op->op, nys->s, q, g.p);
+  });
+}
+int npcg_power_estimate_rng(npcg_op* op, npcg_nys* nys, int64_t q, npcg_rng* rng, double* est) {
+  return guard([&] {
+    need(op, "npcg_power_estimate_rng");
+    need(nys, "npcg_power_estimate_rng");
+    Ctx& c = C(op->ctx);
+    if (q < 1) invalid("estimate_error_power: q must be >= 1");
+    if (nys->s.factored && nys->s.ell > 0 && nys->s.n != op->op->n)
+      invalid("estimate_error_power: factor shape mismatch");
+    std::vector<double> g(static_cast<size_t>(op->op->n));
+    rng->r.gaussian(op->op->n, 1, g.data());  // gaussian_vector (adaptive.cpp:90)
+    View gv = view_in(c, g.data(), op->op->n, 1, op->op->n, NPCG_HOST);
+    *est = power_estimate(c, *op->op, nys->s, q, gv.p);
+  });
+}
+
+int npcg_posterior_condition(double lambda_ell, double mu, double err, double* out) {
+  return guard([&] {  // adaptive.cpp:150-156
+    if (!(mu > 0.0)) invalid("posterior_condition_estimate: mu must be > 0");
+    if (lambda_ell < 0.0 || err < 0.0) invalid("posterior_condition_estimate: inputs must be >= 0");
+    *out = (lambda_ell + mu + err) / mu;
+  });
+}
+
+int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg_nys** out,
+                  npcg_adaptive_outcome* outcome) {
+  return guard([&] {
+    need(op, "npcg_adaptive");
+    need(cfg, "npcg_adaptive config");
+    need(rng, "npcg_adaptive rng");
+    Ctx& c = C(op->ctx);
+    const i64 n = op->op->n;
+    // mode checks (adaptive.cpp:113-114, 127-128, 137-138)
+    // validate_config (adaptive.cpp:19-28)
+    if (cfg->ell0 < 1 || cfg->ell0 > cfg->ell_max || cfg->ell_max > n)
+      invalid("AdaptiveConfig: need 1 <= ell0 <= ell_max <= dim");
+    if (!(cfg->mu > 0.0)) invalid("AdaptiveConfig: mu must be > 0");
+    if (cfg->q < 1) invalid("AdaptiveConfig: q must be >= 1");
+    double tau = cfg->tol_mode == 1 ? 10.0 : 30.0;  // resolved_tau (adaptive.cpp:9-15)
+    if (cfg->has_tau) {
+      if (!(cfg->tau > 0.0)) invalid("AdaptiveConfig: tau must be > 0");
+      tau = cfg->tau;
+    }
+    if (cfg->sketch != 0) fail(NPCG_ERUNTIME, "AdaptiveConfig: column sampling is not available in this build");
+    auto h = std::make_unique<npcg_nys>();
+    h->ctx = op->ctx;
+    Nys& s = h->s;
+    s.ctx = &c;
+    s.op = op->op.get();
+    s.n = n;
+    auto grow = [&](i64 extra) {
+      std::vector<double> raw(static_cast<size_t>(n * extra));
+      rng->r.gaussian(n, extra, raw.data());
+      nys_extend(s, raw.data(), n, extra, NPCG_HOST);
+    };
+    auto estimate = [&]() {
+      std::vector<double> g(static_cast<size_t>(n));
+      rng->r.gaussian(n, 1, g.data());
+      View gv = view_in(c, g.data(), n, 1, n, NPCG_HOST);
+      return power_estimate(c, *op->op, s, cfg->q, gv.p);
+    };
+    std::optional<double> err;
+    i64 doublings = 0;
+    bool hit_cap = false;
+    if (cfg->tol_mode == 2) {  // fixed_rank_nystrom (adaptive.cpp:135-148)
+      grow(cfg->ell_max);
+      nys_factor(s);
+      err = estimate();
+    } else {  // doubling_loop (adaptive.cpp:50-79)
+      const double tol = tau * cfg->mu;
+      auto should_stop = [&]() -> bool {
+        const double lmin = s.ell == 0 ? 0.0 : s.lambda_host.back();
+        if (cfg->tol_mode == 1) return lmin <= tau * cfg->mu;  // adaptive.cpp:129-132
+        const double e = estimate();                           // adaptive.cpp:115-121
+        err = e;
+        if (e > tol) return false;
+        return !cfg->secondary_criterion || lmin <= tol / 11.0;
+      };
+      grow(cfg->ell0);
+      nys_factor(s);
+      while (true) {
+        if (should_stop()) break;
+        const i64 ell = s.size;
+        if (ell >= cfg->ell_max) {
+          hit_cap = true;
+          break;
+        }
+        const i64 extra = 2 * ell <= cfg->ell_max ? ell : cfg->ell_max - ell;
+        grow(extra);
+        ++doublings;
+        nys_factor(s);
+        if (s.size == cfg->ell_max && 2 * ell > cfg->ell_max) {
+          hit_cap = true;
+          break;
+        }
+      }
+    }
+    const double lmin = s.ell == 0 ? 0.0 : s.lambda_host.back();
+    const double e0 = err ? std::max(0.0, *err) : 0.0;
+    outcome->ell_final = s.ell;
+    outcome->doublings = doublings;
+    outcome->hit_cap = hit_cap ? 1 : 0;
+    outcome->has_error_estimate = err ? 1 : 0;
+    outcome->error_estimate = err.value_or(0.0);
+    outcome->posterior_condition = (lmin + cfg->mu + e0) / cfg->mu;
+    *out = h.release();
+  });
+}
+
+// ============================ dense helpers =================================
+int npcg_orthonormal_columns(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, double* q, int where) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (m < n) invalid("orthonormal_columns: expected a tall (m >= n) matrix");
+    if (n <= 0) return;
+    View G = view_in(c, g, m, n, m, where);
+    DMat Q;
+    Q.alloc(m, n, c.stream, false);
+    orthonormalize(c, G.p, G.ld, m, n, Q.p(), Q.ld);
+    download(c, Q.p(), Q.ld, m, n, q, m, where);
+    c.sync();
+  });
+}
+int npcg_thin_svd(npcg_ctx* ctx, int64_t m, int64_t n, const double* b, double* u, double* s, int where) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (m < n) invalid("thin_svd: expected a tall (m >= n) matrix");
+    if (n <= 0) return;
+    View B = view_in(c, b, m, n, m, where);
+    DMat U;
+    U.alloc(m, n, c.stream, false);
+    DBuf<double> sig(n, c.stream);
+    thin_svd(c, B.p, B.ld, m, n, U.p(), U.ld, sig.p);
+    download(c, U.p(), U.ld, m, n, u, m, where);
+    NPCG_CUDA(cudaMemcpyAsync(s, sig.p, sizeof(double) * n,
+                              where == NPCG_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c.stream));
+    c.sync();
+  });
+}
+
+}  // extern "C"

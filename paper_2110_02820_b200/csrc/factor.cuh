@@ -1,0 +1,46 @@
+// Dense FP64 factorisations of the Nyström pipeline, on device:
+// blocked Cholesky (lower, LLT semantics), blocked right triangular solve,
+// CholeskyQR2 (shifted CholeskyQR3 fallback) and a one-sided Jacobi SVD.
+#pragma once
+
+#include "context.cuh"
+
+namespace npcg {
+
+constexpr int kCholNB = 64;
+
+/// Diagonal-block inverses produced by cholesky(): block b (rows/cols
+/// b*NB .. ) is stored NB x NB col-major at dinv + b*NB*NB.
+struct CholFactor {
+  DBuf<double> dinv;
+  i64 n = 0;
+};
+
+/// In-place lower Cholesky of the n x n matrix at `a` (ld lda), reading only
+/// the lower triangle (Eigen::LLT / dpotrf('L') semantics). On return the
+/// lower triangle holds L and the strict upper triangle is zero. Returns
+/// false when a pivot is <= 0 or non-finite (synchronises).
+bool cholesky(Ctx& ctx, double* a, i64 n, i64 lda, CholFactor& f);
+
+/// X (m x n) = Y * L^{-T} for the lower factor L of `f` (X L^T = Y;
+/// Eigen `llt.matrixU().solve<OnTheRight>(Y)`). Y is used as workspace and
+/// overwritten. X must not alias Y.
+void trsm_right_lt(Ctx& ctx, i64 m, i64 n, double* Y, i64 ldy, const double* L, i64 ldl, const CholFactor& f,
+                   double* X, i64 ldx);
+
+/// Orthonormal basis Q (m x n) of range(G) (m >= n, full column rank),
+/// by CholeskyQR2 with a shifted CholeskyQR3 fallback. If R != nullptr the
+/// upper-triangular factor (G = Q R) is written there (n x n, ld ldr).
+void orthonormalize(Ctx& ctx, const double* G, i64 ldg, i64 m, i64 n, double* Q, i64 ldq,
+                    double* R = nullptr, i64 ldr = 0);
+
+/// Thin SVD of a tall matrix (dgesdd('S') equivalent up to column signs):
+/// U (m x n) left singular vectors, sigma (n) descending, on device.
+void thin_svd(Ctx& ctx, const double* B, i64 ldb, i64 m, i64 n, double* U, i64 ldu, double* sigma);
+
+/// One-sided Jacobi on the n x n matrix W (ld ldw, overwritten): finds an
+/// orthogonal V with W V orthogonal columns. sigma(j) = ||(W V)(:,j)||,
+/// columns of V and sigma sorted descending into Vs / sigma.
+void jacobi_svd_small(Ctx& ctx, double* W, i64 ldw, i64 n, double* Vs, i64 ldv, double* sigma);
+
+}  // namespace npcg

@@ -1,0 +1,27 @@
+// FP64 tensor-core GEMM for sm_100a: TMA (cp.async.bulk.tensor, 128B swizzle)
+// feeds a multi-stage mbarrier pipeline; 8 consumer warps run DMMA
+// (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4; tcgen05 has no f64 kind).
+#pragma once
+
+#include "context.cuh"
+
+namespace npcg {
+
+/// One GEMM operand in column-major device memory.
+///  A (logical M x K): kmajor -> stored K x M (elem (m,k) at k + m*ld), i.e. A^T;
+///                     else   -> stored M x K (elem (m,k) at m + k*ld).
+///  B (logical K x N): kmajor -> stored K x N (elem (k,n) at k + n*ld);
+///                     else   -> stored N x K (elem (k,n) at n + k*ld), i.e. B^T.
+struct Operand {
+  const double* p;
+  i64 ld;
+  bool kmajor;
+};
+
+/// C (M x N, col-major, ldc) = alpha * A B + beta * C. Deterministic (split-K
+/// partials are reduced in fixed order). All leading dimensions must be
+/// multiples of 2 and pointers 16-byte aligned (dev_ld() matrices are).
+void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, double beta,
+          double* C, i64 ldc);
+
+}  // namespace npcg

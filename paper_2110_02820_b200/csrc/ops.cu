@@ -1,0 +1,252 @@
+// Operators, Nyström sketch/factorisation and the preconditioner on device.
+// Reference: operators.cpp, nystrom.cpp, preconditioner.cpp (file:line per
+// function below; paths relative to /root/reference/proj/core/src/).
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <sstream>
+
+#include "blas.cuh"
+#include "factor.cuh"
+#include "gemm.cuh"
+#include "ops.cuh"
+
+namespace npcg {
+
+// =============================== operators ===================================
+void Op::apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) {
+  // RegularizedOperator / nystrom_pcg apply_op (operators.cpp:95-103, solvers.cpp:137-141):
+  // out = A p; out += mu p.
+  apply(P, ldp, S, out, ldo, gate);
+  if (ldp == ldo) {
+    axpby(*ctx, n, S, mu, P, 1.0, out, ldo);
+  } else {
+    for (int s = 0; s < S; ++s) axpby(*ctx, n, 1, mu, P + s * ldp, 1.0, out + s * ldo, ldo);
+  }
+}
+
+void Op::column(i64, double*) { fail(NPCG_ERUNTIME, "LinearOperator - column: operator has no column access"); }
+
+// DenseOperator::do_matvec / do_apply_block (operators.cpp:72-78). A is
+// symmetric, so A V is computed as A^T V: each output entry is a dot of a
+// contiguous column with V (coldot for <= 8 columns; DMMA GEMM beyond).
+void DenseOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
+  if (k <= 8) {
+    coldot(*ctx, a.p(), a.ld, n, n, V, ldv, static_cast<int>(k), out, ldo, 0.0, nullptr, 0, gate);
+  } else {
+    gemm(*ctx, n, k, n, 1.0, Operand{a.p(), a.ld, true}, Operand{V, ldv, true}, 0.0, out, ldo);
+  }
+}
+void DenseOp::apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) {
+  if (S <= 8) {  // fused epilogue: v_i = (A p)_i + mu p_i
+    coldot(*ctx, a.p(), a.ld, n, n, P, ldp, S, out, ldo, mu, P, ldp, gate);
+  } else {
+    Op::apply_shift(P, ldp, S, mu, out, ldo, gate);
+  }
+}
+void DenseOp::column(i64 j, double* out) { copy2d(*ctx, n, 1, a.col(j), a.ld, out, n); }
+
+// GramRidgeOperator (operators.cpp:112-121): out = G^T (G v); out /= m.
+void GramOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
+  DMat z;
+  z.alloc(m, k, ctx->stream, false);
+  if (k <= 8) {
+    rowdot(*ctx, g.p(), g.ld, m, n, V, ldv, static_cast<int>(k), nullptr, 0, z.p(), z.ld, gate);
+    coldot(*ctx, g.p(), g.ld, m, n, z.p(), z.ld, static_cast<int>(k), out, ldo, 0.0, nullptr, 0, gate);
+  } else {
+    gemm(*ctx, m, k, n, 1.0, Operand{g.p(), g.ld, false}, Operand{V, ldv, true}, 0.0, z.p(), z.ld);
+    gemm(*ctx, n, k, m, 1.0, Operand{g.p(), g.ld, true}, Operand{z.p(), z.ld, true}, 0.0, out, ldo);
+  }
+  divide(*ctx, n, k, out, ldo, static_cast<double>(m));
+}
+
+void KernelFreeOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
+  kernel_apply_free(*ctx, *this, V, ldv, k, out, ldo, gate);
+}
+
+// ================================ Nyström ====================================
+namespace {
+void ensure_capacity(Nys& s, i64 cols) {
+  if (s.omega.cols >= cols) return;
+  const i64 cap = std::min<i64>(s.n, std::max<i64>(cols, 2 * s.omega.cols));
+  DMat om, y;
+  om.alloc(s.n, cap, s.ctx->stream, true);
+  y.alloc(s.n, cap, s.ctx->stream, true);
+  if (s.size > 0) {
+    copy2d(*s.ctx, s.n, s.size, s.omega.p(), s.omega.ld, om.p(), om.ld);
+    copy2d(*s.ctx, s.n, s.size, s.y.p(), s.y.ld, y.p(), y.ld);
+  }
+  s.omega = std::move(om);
+  s.y = std::move(y);
+}
+}  // namespace
+
+// extend_sketch (nystrom.cpp:36-58) after the Gaussian draw.
+void nys_extend(Nys& s, const double* raw, i64 ld, i64 extra, int where) {
+  Ctx& ctx = *s.ctx;
+  if (!s.op) fail(NPCG_ERUNTIME, "extend_sketch: approximation has no operator");
+  if (extra < 1) invalid("extend_sketch: extra must be >= 1");
+  if (s.size + extra > s.n) invalid("extend_sketch: sketch size would exceed dimension");
+  const i64 n = s.n, old = s.size;
+  DMat fresh;
+  upload(ctx, fresh, n, extra, raw, ld, where);
+  // Two passes of block Gram-Schmidt against the existing columns.
+  if (old > 0) {
+    DMat coef;
+    coef.alloc(old, extra, ctx.stream, false);
+    for (int pass = 0; pass < 2; ++pass) {
+      gemm(ctx, old, extra, n, 1.0, Operand{s.omega.p(), s.omega.ld, true}, Operand{fresh.p(), fresh.ld, true}, 0.0,
+           coef.p(), coef.ld);
+      gemm(ctx, n, extra, old, -1.0, Operand{s.omega.p(), s.omega.ld, false}, Operand{coef.p(), coef.ld, true}, 1.0,
+           fresh.p(), fresh.ld);
+    }
+  }
+  ensure_capacity(s, old + extra);
+  double* q_new = s.omega.col(old);
+  orthonormalize(ctx, fresh.p(), fresh.ld, n, extra, q_new, s.omega.ld);
+  s.op->apply(q_new, s.omega.ld, extra, s.y.col(old), s.y.ld);
+  s.size = old + extra;
+  s.factored = false;
+}
+
+namespace {
+__global__ void clamp_lambda_kernel(const double* sigma, i64 ell, double nu, double* lambda) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < ell) lambda[i] = fmax(sigma[i] * sigma[i] - nu, 0.0);
+}
+double ulp_spacing(double x) {
+  const double ax = std::abs(x);
+  return std::nextafter(ax, std::numeric_limits<double>::infinity()) - ax;
+}
+}  // namespace
+
+// nystrom_from_sketch (nystrom.cpp:96-140).
+void nys_factor(Nys& s) {
+  Ctx& ctx = *s.ctx;
+  const i64 n = s.n, ell = s.size;
+  s.ell = ell;
+  s.factored = true;
+  s.lambda_host.assign(static_cast<size_t>(ell), 0.0);
+  if (ell == 0) {
+    s.u.alloc(n, 0, ctx.stream, false);
+    s.lambda.release();
+    s.shift = 0.0;
+    return;
+  }
+  if (!all_finite(ctx, s.y.p(), n, ell, s.y.ld))
+    fail(NPCG_ERUNTIME, "nystrom_from_sketch: sketch has non-finite entries");
+  const double ynorm = std::sqrt(sum_squares(ctx, s.y.p(), n, ell, s.y.ld));
+  const double nu0 = ulp_spacing(ynorm);
+  double nu = nu0;
+  DMat ynu, core, b;
+  ynu.alloc(n, ell, ctx.stream, false);
+  core.alloc(ell, ell, ctx.stream, false);
+  b.alloc(n, ell, ctx.stream, false);
+  bool factored = false;
+  for (int attempt = 0; attempt <= 3; ++attempt, nu *= 10.0) {
+    add_scaled(ctx, n, ell, s.y.p(), nu, s.omega.p(), ynu.p(), ynu.ld);  // Y + nu Omega (shared ld)
+    gemm(ctx, ell, ell, n, 1.0, Operand{s.omega.p(), s.omega.ld, true}, Operand{ynu.p(), ynu.ld, true}, 0.0,
+         core.p(), core.ld);
+    CholFactor f;
+    if (!cholesky(ctx, core.p(), ell, core.ld, f)) continue;
+    trsm_right_lt(ctx, n, ell, ynu.p(), ynu.ld, core.p(), core.ld, f, b.p(), b.ld);
+    if (!all_finite(ctx, b.p(), n, ell, b.ld)) continue;
+    s.shift = nu;
+    factored = true;
+    break;
+  }
+  if (!factored) {
+    std::ostringstream msg;
+    msg << "nystrom_from_sketch: Cholesky failed after 3 shift escalations"
+        << " (n = " << n << ", ell = " << ell << ", initial shift = " << nu0 << ", final shift = " << nu / 10.0
+        << ", ||Y||_F = " << ynorm << ")";
+    fail(NPCG_ERUNTIME, msg.str());
+  }
+  ynu.buf.release();
+  core.buf.release();
+  s.u.alloc(n, ell, ctx.stream, false);
+  DBuf<double> sigma(ell, ctx.stream);
+  thin_svd(ctx, b.p(), b.ld, n, ell, s.u.p(), s.u.ld, sigma.p);
+  s.lambda.alloc(ell, ctx.stream);
+  NPCG_LAUNCH(ctx, clamp_lambda_kernel, static_cast<unsigned>(cdiv(ell, 256)), 256, 0, sigma.p, ell, s.shift,
+              s.lambda.p);
+  NPCG_CUDA(cudaMemcpyAsync(s.lambda_host.data(), s.lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToHost,
+                            ctx.stream));
+  ctx.sync();
+  for (i64 i = 1; i < ell; ++i)
+    if (s.lambda_host[i] > s.lambda_host[i - 1])
+      fail(NPCG_ERUNTIME, "nystrom_from_sketch: eigenvalue estimates out of order");
+}
+
+// ============================ preconditioner =================================
+namespace {
+__global__ void gains_kernel(const double* lambda, i64 ell, double lambda_ell, double mu, double* inv, double* fwd) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= ell) return;
+  inv[i] = (lambda_ell + mu) / (lambda[i] + mu) - 1.0;  // preconditioner.cpp:33
+  fwd[i] = (lambda[i] + mu) / (lambda_ell + mu) - 1.0;  // preconditioner.cpp:22
+}
+__global__ void scale_rows_kernel(double* T, i64 ell, i64 S, i64 ldt, const double* g, const int* gate) {
+  if (gate && *gate == 0) return;
+  const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= ell * S) return;
+  const i64 j = idx % ell, s = idx / ell;
+  T[j + s * ldt] = g[j] * T[j + s * ldt];
+}
+}  // namespace
+
+// build_preconditioner (preconditioner.cpp:80-89).
+void pre_build(Pre& p, const Nys& s, double mu) {
+  if (!(mu > 0.0)) invalid("build_preconditioner: mu must be > 0");
+  p.ctx = s.ctx;
+  p.nys = &s;
+  p.n = s.n;
+  p.ell = s.ell;
+  p.mu = mu;
+  p.lambda_ell = s.ell == 0 ? 0.0 : s.lambda_host.back();
+  if (p.ell > 0) {
+    p.gain_inv.alloc(p.ell, s.ctx->stream);
+    p.gain_fwd.alloc(p.ell, s.ctx->stream);
+    NPCG_LAUNCH(*s.ctx, gains_kernel, static_cast<unsigned>(cdiv(p.ell, 256)), 256, 0, s.lambda.p, p.ell,
+                p.lambda_ell, mu, p.gain_inv.p, p.gain_fwd.p);
+  }
+}
+
+namespace {
+// out = V + U diag(g) U^T V   (preconditioner.cpp:17-45 shapes)
+void lowrank_update(Pre& p, const double* g, const double* V, i64 ldv, i64 S, double* out, i64 ldo,
+                    const int* gate) {
+  Ctx& ctx = *p.ctx;
+  const Nys& s = *p.nys;
+  if (p.ell == 0) {
+    copy2d(ctx, p.n, S, V, ldv, out, ldo);
+    return;
+  }
+  DMat T;
+  T.alloc(p.ell, S, ctx.stream, false);
+  if (S <= 8) {
+    coldot(ctx, s.u.p(), s.u.ld, p.n, p.ell, V, ldv, static_cast<int>(S), T.p(), T.ld, 0.0, nullptr, 0, gate);
+  } else {
+    gemm(ctx, p.ell, S, p.n, 1.0, Operand{s.u.p(), s.u.ld, true}, Operand{V, ldv, true}, 0.0, T.p(), T.ld);
+  }
+  NPCG_LAUNCH(ctx, scale_rows_kernel, static_cast<unsigned>(cdiv(p.ell * S, 256)), 256, 0, T.p(), p.ell, S, T.ld, g,
+              gate);
+  if (S <= 8) {
+    rowdot(ctx, s.u.p(), s.u.ld, p.n, p.ell, T.p(), T.ld, static_cast<int>(S), V, ldv, out, ldo, gate);
+  } else {
+    DMat us;
+    us.alloc(p.n, S, ctx.stream, false);
+    gemm(ctx, p.n, S, p.ell, 1.0, Operand{s.u.p(), s.u.ld, false}, Operand{T.p(), T.ld, true}, 0.0, us.p(), us.ld);
+    add2d(ctx, p.n, S, V, ldv, us.p(), us.ld, out, ldo);  // r + (U scaled)
+  }
+}
+}  // namespace
+
+void pre_apply_inverse(Pre& p, const double* R, i64 ldr, i64 S, double* Z, i64 ldz, const int* gate) {
+  lowrank_update(p, p.gain_inv.p, R, ldr, S, Z, ldz, gate);
+}
+void pre_apply(Pre& p, const double* V, i64 ldv, i64 S, double* out, i64 ldo) {
+  lowrank_update(p, p.gain_fwd.p, V, ldv, S, out, ldo, nullptr);
+}
+
+}  // namespace npcg

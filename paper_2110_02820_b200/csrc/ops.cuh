@@ -1,0 +1,91 @@
+// Device-resident operators, Nyström state and preconditioner behind the
+// C-ABI handles (npcg_op / npcg_nys / npcg_pre).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "context.cuh"
+
+namespace npcg {
+
+enum OpKind { kDense = 0, kGram = 1, kKernelStored = 2, kKernelFree = 3 };
+
+/// LinearOperator (operators.hpp:25-47) on device. apply() is the unchecked
+/// do_apply_block(); the C-ABI layer does the reference's dim/finite checks.
+struct Op {
+  Ctx* ctx = nullptr;
+  i64 n = 0;
+  int kind = kDense;
+  virtual ~Op() = default;
+  /// out (n x k) = A V  (device pointers).
+  virtual void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate = nullptr) = 0;
+  /// out = A P + mu P with the reference's rounding order (out = A p; out += mu p).
+  virtual void apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate);
+  virtual bool has_column() const { return false; }
+  virtual void column(i64 j, double* out);
+};
+
+struct DenseOp : Op {  // DenseOperator (operators.cpp:64-80); also the stored kernel
+  DMat a;
+  void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
+  void apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) override;
+  bool has_column() const override { return true; }
+  void column(i64 j, double* out) override;
+};
+
+struct GramOp : Op {  // GramRidgeOperator (operators.cpp:105-121): (1/m) G^T (G v)
+  DMat g;             // m x n design, col-major
+  i64 m = 0;
+  void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
+};
+
+struct KernelFreeOp : Op {  // KernelOperator beyond dense_cap (operators.cpp:152-188)
+  DMat pts;                 // n x d col-major (reference layout)
+  DMat pts_rm;              // d x n col-major == points row-major (point-contiguous)
+  DBuf<double> norms;       // ||x_i||^2
+  i64 d = 0;
+  double sigma = 1.0;
+  void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
+  bool has_column() const override { return true; }
+  void column(i64 j, double* out) override;
+};
+
+/// Build the stored Gaussian kernel matrix (operators.cpp:125-150) on device.
+void build_kernel_matrix(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma, DMat& K);
+void prepare_kernel_free(Ctx& ctx, KernelFreeOp& op);
+void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, i64 k, double* out, i64 ldo,
+                       const int* gate);
+
+/// Cached sketch + factored approximation (nystrom.hpp:19-48).
+struct Nys {
+  Ctx* ctx = nullptr;
+  Op* op = nullptr;  // not owned; nullptr for from_factors
+  i64 n = 0;
+  DMat omega, y;     // capacity-managed; first `size` columns valid
+  i64 size = 0;
+  DMat u;            // n x ell
+  DBuf<double> lambda;
+  i64 ell = 0;
+  double shift = 0.0;
+  bool factored = false;
+  std::vector<double> lambda_host;
+};
+void nys_extend(Nys& s, const double* raw, i64 ld, i64 extra, int where);
+void nys_factor(Nys& s);
+
+/// NystromPreconditioner (preconditioner.hpp:20-37).
+struct Pre {
+  Ctx* ctx = nullptr;
+  const Nys* nys = nullptr;  // U, lambda (device); not owned
+  i64 n = 0, ell = 0;
+  double mu = 0.0, lambda_ell = 0.0;
+  DBuf<double> gain_inv;  // (lambda_ell + mu)/(lambda + mu) - 1
+  DBuf<double> gain_fwd;  // (lambda + mu)/(lambda_ell + mu) - 1
+};
+void pre_build(Pre& p, const Nys& s, double mu);
+/// Z = P^{-1} R (n x S). Z may alias nothing of R.
+void pre_apply_inverse(Pre& p, const double* R, i64 ldr, i64 S, double* Z, i64 ldz, const int* gate = nullptr);
+void pre_apply(Pre& p, const double* V, i64 ldv, i64 S, double* out, i64 ldo);
+
+}  // namespace npcg

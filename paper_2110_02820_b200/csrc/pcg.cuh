@@ -1,0 +1,42 @@
+// Nyström PCG driver on device (solvers.cpp:40-148): batched over S
+// independent right-hand sides that share one pass over A per iteration.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "ops.cuh"
+
+namespace npcg {
+
+struct PcgOptions {
+  double eta = 1e-10;
+  i64 max_iter = 500;
+  bool relative = false;
+  bool record_iterates = false;
+};
+
+struct PcgColumnReport {
+  i64 iterations = 0;
+  i64 matvec_count = 0;
+  bool converged = false;
+  int status = 0;  // 0 ok / max_iter, 1 breakdown, 2 non-finite residual, 3 non-finite initial residual
+  double eta_used = 0.0;
+  std::vector<double> history;
+};
+
+struct PcgResult {
+  std::vector<PcgColumnReport> cols;
+  double wall_time = 0.0;
+  bool diverged = false;
+  std::string message;
+};
+
+/// Solves (A + mu I) X = B column by column with P^{-1} from `pre`
+/// (nullptr = identity, i.e. cg() on A + mu I). B, X0, X are device n x S
+/// (X0 nullable = 0). `iterates` (device, nullable): (max_iter+1) x n x S.
+PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* B, i64 ldb, const double* X0,
+                    i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, double* iterates,
+                    const char* context = "nystrom_pcg");
+
+}  // namespace npcg
