@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Nyström-PCG hot path (BASELINE.json metric).
+
+One step = one full solve of BASELINE config 2 (configs[1]; ridge regression,
+X 20000 x 4000, ell = 400, mu = 1e-3, relative tol 1e-10): Nyström sketch of the
+raw Gaussian Omega (orthonormalise + Y = A Omega on DMMA), on-device
+factorisation (shift, Cholesky, TRSM, thin SVD), preconditioner, PCG to 1e-10.
+
+  value     solves/s with inputs (X, b, Omega) resident in HBM, device-timed
+            with CUDA events on the library's stream, max over ranks
+  e2e       solves/s through the public C-ABI with host buffers: X, Omega, b
+            copied host->device and x device->host inside every step
+  roofline  the dominant kernel of the step (per-kernel CUDA-event timing in
+            an instrumented step of the same run) against its roofline
+  cpu_baseline  the CPU oracle (restatement of the reference) on this host
+
+`--impl reference` times the reference's CPU path (the oracle port; the
+reference itself cannot be built here: Eigen3/LAPACKE are absent) on all host
+cores, rank 0 only. Under torchrun each rank runs an independent replica of the
+workload (the single-GPU ridge path is replicated; "replicas only").
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="cfg2")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--small", action="store_true", help="reduced sizes (smoke runs)")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload_kwargs(args):
+    if args.small:
+        return {"cfg1": dict(n=500, ell=50), "cfg2": dict(m=4000, n=800, ell=100), "cfg3": dict(n=4000, ell=200),
+                "cfg4": dict(n=4000, ell_max=200), "cfg5": dict(n=4000, r=400, ell=200)}[args.config]
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except OSError:
+        return {}
+
+
+def dgemm_peak_tflops(torch):
+    """cuBLAS DGEMM 8192^3 best-of-5 on this GPU: the FP64 tensor-pipe
+    denominator (MEASURED_PEAKS.json carries no FP64 figure)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e9
+    for _ in range(5):
+        s.record()
+        a @ b
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e) / 1e3)
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * n ** 3 / best / 1e12
+
+
+# ----------------------------------------------------------------- device path
+class DevicePath:
+    """Drives the C-ABI with device-resident inputs (NPCG_DEVICE pointers)."""
+
+    def __init__(self, npcg, torch, w, ctx):
+        self.npcg, self.torch, self.w, self.ctx = npcg, torch, w, ctx
+        L = npcg.lib()
+        self.L = L
+        self.op = npcg.workloads.build_operator(npcg, w, ctx=ctx)
+        n = w.n
+        dev = torch.device("cuda", ctx.device)
+        # column-major device buffers: torch (cols, rows) row-major == (rows, cols) col-major
+        self.omega = torch.from_numpy(np.ascontiguousarray(w.omega.T)).to(dev)
+        b = w.b.reshape(n, -1, order="F")
+        self.s = b.shape[1]
+        self.b = torch.from_numpy(np.ascontiguousarray(b.T)).to(dev)
+        self.x = torch.empty((self.s, n), dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        self.reports = (npcg._SolveReport * self.s)()
+        self.opts = npcg._SolveOpts(w.eta, w.max_iter, int(w.relative), 0)
+
+    def step(self):
+        npcg, L, w, vp, i64 = self.npcg, self.L, self.w, C.c_void_p, C.c_int64
+        nys, pre = vp(), vp()
+        npcg._check(L.npcg_nys_create(vp(self.op.h), C.byref(nys)))
+        try:
+            npcg._check(L.npcg_nys_extend(nys, i64(w.ell), vp(self.omega.data_ptr()), i64(w.n), npcg.DEVICE))
+            npcg._check(L.npcg_nys_factor(nys))
+            npcg._check(L.npcg_pre_create(nys, C.c_double(w.mu), C.byref(pre)))
+            rc = L.npcg_pcg(vp(self.op.h), pre, C.c_double(w.mu), i64(self.s), vp(self.b.data_ptr()), i64(w.n), None,
+                            i64(w.n), C.byref(self.opts), vp(self.x.data_ptr()), i64(w.n), self.reports, None, None,
+                            npcg.DEVICE)
+            npcg._check(rc)
+        finally:
+            if pre.value:
+                L.npcg_pre_destroy(pre)
+            L.npcg_nys_destroy(nys)
+        return [(r.iterations, bool(r.converged)) for r in self.reports]
+
+
+def e2e_step(npcg, w, ctx, host):
+    """Public API with host buffers: every input crosses PCIe inside the step."""
+    op = npcg.workloads.build_operator(npcg, host, ctx=ctx)
+    pair = npcg.make_empty_sketch(op)
+    pair = npcg.extend_sketch_with(pair, op, host.omega)
+    approx = npcg.nystrom_from_sketch(pair)
+    pre = npcg.build_preconditioner(approx, w.mu)
+    rep = npcg.nystrom_pcg(op, host.b, w.mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
+    x = rep.x if not isinstance(rep, list) else np.column_stack([r.x for r in rep])
+    return float(x.sum())
+
+
+def input_bytes(w):
+    if w.kind == "gram":
+        op_bytes = w.data["x"].nbytes
+    elif w.kind == "kernel":
+        op_bytes = w.data["points"].nbytes
+    elif w.kind == "lowrank":
+        op_bytes = w.data["g"].nbytes
+    elif w.kind == "dense":
+        op_bytes = w.data["a"].nbytes
+    else:
+        op_bytes = w.data["lambda"].nbytes
+    return op_bytes + w.omega.nbytes + w.b.nbytes
+
+
+ALGO_NOTE = {
+    "gemm_dmma_kernel": ("tensor", "2*M*N*K flops per launch (sketch X*Omega, X^T*Z, Gram/TRSM/CholeskyQR GEMMs)"),
+    "coldot_kernel": ("hbm", "8*rows*cols matrix bytes + vectors per launch (X^T z, U^T r)"),
+    "rowdot_kernel": ("hbm", "8*rows*cols matrix bytes + vectors per launch (X v, U t)"),
+}
+
+
+def roofline_from_profile(prof, peaks, dgemm_peak, ncu_traffic):
+    """Dominant kernel by total device time; achieved = its algorithmic
+    work / its summed launch time."""
+    named = {k.split("<")[0].split("(")[0].strip(): v for k, v in prof.items()}
+    total = sum(v[1] for v in named.values())
+    name, (cnt, ms, flops, byts) = max(named.items(), key=lambda kv: kv[1][1])
+    bound, note = ALGO_NOTE.get(name, ("hbm", "bytes per launch"))
+    if bound == "tensor":
+        achieved = flops / (ms / 1e3) / 1e12
+        peak, unit, src = dgemm_peak, "TFLOP/s", "measured cuBLAS DGEMM 8192^3 on this GPU (this run)"
+    else:
+        achieved = byts / (ms / 1e3) / 1e9
+        peak, unit, src = peaks.get("hbm_gbs", 6650.0), "GB/s", "MEASURED_PEAKS.json hbm_gbs (of measured)"
+    traffic = None
+    if ncu_traffic and name in ncu_traffic:
+        traffic = ncu_traffic[name]
+    return {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak if peak else None, "traffic": traffic, "launches": cnt,
+            "share_of_step": ms / total if total else None, "peak_source": src, "work_per_launch": note,
+            "kernels": {k: {"launches": v[0], "ms": round(v[1], 4),
+                            "achieved": (v[2] / (v[1] / 1e3) / 1e12 if ALGO_NOTE.get(k, ("hbm",))[0] == "tensor"
+                                         else v[3] / (v[1] / 1e3) / 1e9) if v[1] > 0 else None}
+                        for k, v in sorted(named.items(), key=lambda kv: -kv[1][1])[:8]}}
+
+
+def cpu_baseline(w, steps=1):
+    """The oracle (CPU restatement of the reference path) on this host, all cores."""
+    from oracle import oracle as orc
+    from oracle.workload_ops import build_oracle_operator
+    ncores = os.cpu_count() or 1
+    orc.set_threads(ncores)
+    op = build_oracle_operator(orc, w)
+    times, iters = [], []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        pair = orc.extend_sketch_with(orc.make_empty_sketch(w.n), op, w.omega)
+        approx = orc.nystrom_from_sketch(pair)
+        pre = orc.build_preconditioner(approx, w.mu)
+        b = w.b.reshape(w.n, -1, order="F")
+        for j in range(b.shape[1]):
+            rep = orc.nystrom_pcg(op, b[:, j], w.mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
+            iters.append(rep.iterations)
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    return {"value": 1.0 / t, "unit": "solves/s", "cores": ncores, "kind": "port",
+            "sample": f"{len(times)} full solve(s) of {w.name} (sketch+factor+PCG), OpenBLAS {orc.corename()} "
+                      f"x{orc.get_threads()} threads", "seconds_per_solve": t, "iterations": iters[-1]}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2110_02820_b200 as npcg_mod  # for the input generators only (host Rng)
+    from paper_2110_02820_b200 import workloads
+    from oracle import oracle as orc
+    w = workloads.make(args.config, orc.Rng, orc.splitmix64, **workload_kwargs(args))
+    del npcg_mod
+    t0 = time.perf_counter()
+    base = cpu_baseline(w, steps=args.steps)
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "solves/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": 0, "ms_per_step": 1e3 / base["value"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng, seeded)",
+            "config": {**w.describe(), "rhs": "data" if args.config == "cfg2" else "Rng"},
+            "cpu_baseline": base, "e2e": {"value": base["value"], "unit": "solves/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t0}
+    print(json.dumps(line))
+    return 0
+
+
+def run_b200(args):
+    import torch
+    import paper_2110_02820_b200 as npcg
+    from paper_2110_02820_b200 import workloads
+    npcg.workloads = workloads
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    ctx = npcg.Context(local)
+    t_gen = time.perf_counter()
+    w = workloads.make(args.config, npcg.Rng, npcg.splitmix64,
+                       gemm=lambda a, b, transa=False: npcg.gemm(a, b, transa=transa, ctx=ctx), **workload_kwargs(args))
+    t_gen = time.perf_counter() - t_gen
+    path = DevicePath(npcg, torch, w, ctx)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        info = path.step()
+    barrier()
+    l0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            info = path.step()
+        ev1.record(stream)
+        ev1.synchronize()
+    barrier()
+    launches = (ctx.launches - l0) // max(args.steps, 1)
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed = float(t.item())
+    ms_per_step = elapsed / args.steps * 1e3
+    value = world * args.steps / elapsed
+
+    # per-kernel CUDA-event timing in one instrumented step (same run, same stream)
+    ctx.prof_enable(True)
+    path.step()
+    prof = ctx.prof_report()
+    ctx.prof_enable(False)
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: _pinned(torch, a)
+        host = workloads.Workload(**{**w.__dict__})
+        host.data = {k: (pin(v) if isinstance(v, np.ndarray) and v.size > 1 else v) for k, v in w.data.items()}
+        host.omega, host.b = pin(w.omega), pin(w.b)
+        for _ in range(1):
+            e2e_step(npcg, w, ctx, host)
+        barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        k2 = max(1, min(args.steps, 3))
+        for _ in range(k2):
+            e2e_step(npcg, w, ctx, host)
+        e1.record(stream)
+        e1.synchronize()
+        el = max(e0.elapsed_time(e1) / 1e3, 1e-9)
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": world * k2 / el, "unit": "solves/s", "h2d_bytes_per_step": int(input_bytes(w)),
+               "d2h_bytes_per_step": int(w.b.nbytes + 8 * w.ell), "steps": k2,
+               "wall_s": time.perf_counter() - t0}
+
+    if rank != 0:
+        return 0
+    peaks = measured_peaks()
+    dg = dgemm_peak_tflops(torch)
+    ncu_traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        ncu_traffic = json.loads(tf.read_text()).get(args.config)
+    roof = roofline_from_profile(prof, peaks, dg, ncu_traffic)
+    cpu = None
+    if not args.no_cpu and world == 1:
+        from oracle import oracle as orc
+        wc = workloads.make(args.config, orc.Rng, orc.splitmix64,
+                            gemm=lambda a, b, transa=False: npcg.gemm(a, b, transa=transa, ctx=ctx),
+                            **workload_kwargs(args))
+        cpu = cpu_baseline(wc, steps=1)
+    line = {
+        "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng mt19937_64+Box-Muller, seeded)",
+        "config": {**w.describe(), "parallelism": f"replicas{world}", "l2": "inputs larger than L2 (X 640 MB)",
+                   "iterations": info[0][0], "converged": info[0][1]},
+        "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
+        "clocks": clk.summary(), "input_generation_s": t_gen,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def _pinned(torch, a):
+    t = torch.empty(a.shape[::-1] if a.ndim == 2 else a.shape, dtype=torch.float64, pin_memory=True)
+    arr = t.numpy()
+    if a.ndim == 2:
+        arr = arr.T  # Fortran view
+    arr[...] = a
+    return arr
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -60,6 +60,10 @@ int npcg_dev_free(npcg_ctx* ctx, void* p);
 int npcg_memcpy(npcg_ctx* ctx, void* dst, int dst_where, const void* src, int src_where, int64_t bytes);
 /* Number of this library's kernel launches issued on ctx so far. */
 int64_t npcg_ctx_launches(npcg_ctx* ctx);
+/* Per-kernel CUDA-event timing on the context stream (on != 0 clears and
+ * starts recording). Report: one "name\tlaunches\ttotal_ms\n" line per kernel. */
+int npcg_prof_enable(npcg_ctx* ctx, int on);
+int npcg_prof_report(npcg_ctx* ctx, char* buf, int64_t cap);
 
 /* ---- random (random.hpp:21-50, random.cpp:11-56) -------------------------
  * The reference generator, bit for bit: std::mt19937_64 + cache-free
@@ -77,6 +81,8 @@ int npcg_rng_integer(npcg_rng* rng, uint64_t bound, uint64_t* out);   /* random.
 /* gaussian_matrix (random.cpp:27-32) into dst (col-major, ld = rows). */
 int npcg_rng_gaussian(npcg_rng* rng, int64_t rows, int64_t cols, double* dst);
 int npcg_rng_sample(npcg_rng* rng, int64_t n, int64_t k, int64_t* out); /* random.cpp:44-56 */
+/* count successive Rng::uniform() draws (random.cpp:20) into dst. */
+int npcg_rng_uniform_fill(npcg_rng* rng, int64_t count, double* dst);
 uint64_t npcg_splitmix64(uint64_t seed);                       /* bench.cpp:180-185 */
 
 /* ---- operators (operators.hpp:25-168) ----------------------------------- */
@@ -225,6 +231,13 @@ int npcg_orthonormal_columns(npcg_ctx* ctx, int64_t m, int64_t n, const double* 
 int npcg_thin_svd(npcg_ctx* ctx, int64_t m, int64_t n, const double* b, double* u, double* s,
                   int where);                                               /* dense.cpp:81-96  */
 double npcg_ulp_spacing(double x);                                          /* dense.cpp:119-122 */
+/* The FP64 DMMA GEMM every O(n l^2) / O(n^2 l) step runs on:
+ * C = alpha op(A) op(B) + beta C. a_kmajor: A stored K x M (A^T), else M x K;
+ * b_kmajor: B stored K x N, else N x K (B^T). (Eigen GEMM call sites:
+ * operators.cpp:76-78,118-121; nystrom.cpp:48-49,116; dense.cpp:98-117.) */
+int npcg_gemm(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda,
+              int a_kmajor, const double* b, int64_t ldb, int b_kmajor, double beta, double* c, int64_t ldc,
+              int where);
 
 #ifdef __cplusplus
 }

@@ -84,7 +84,12 @@ def lib():
         L.orc_rng_discard.argtypes = [_vp, C.c_uint64]
         L.orc_rng_integer.argtypes = [_vp, C.c_uint64, C.POINTER(C.c_uint64)]
         L.orc_gaussian_matrix.argtypes = [_vp, _i64, _i64, _dp]
+        L.orc_rng_uniform_fill.argtypes = [_vp, _i64, _dp]
+        L.orc_rng_uniform_fill.restype = None
         L.orc_sample_without_replacement.argtypes = [_vp, _i64, _i64, C.POINTER(_i64)]
+        L.orc_orthonormal_columns.argtypes = [_i64, _i64, _dp, _dp]
+        L.orc_thin_svd.argtypes = [_i64, _i64, _dp, _dp, _dp]
+        L.orc_sym_eig.argtypes = [_i64, _dp, _dp, _dp]
         L.orc_splitmix64.restype = C.c_uint64
         L.orc_splitmix64.argtypes = [C.c_uint64]
         L.orc_ulp_spacing.restype = C.c_double
@@ -179,6 +184,11 @@ class Rng:
 
     def gaussian_vector(self, n: int) -> np.ndarray:
         return self.gaussian_matrix(n, 1)[:, 0].copy()
+
+    def uniform_fill(self, count: int) -> np.ndarray:
+        out = np.empty(count)
+        lib().orc_rng_uniform_fill(self.h, _i64(count), _ptr(out))
+        return out
 
     def sample_without_replacement(self, n: int, k: int) -> np.ndarray:
         out = np.empty(max(k, 0), dtype=np.int64)

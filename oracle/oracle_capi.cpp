@@ -110,6 +110,9 @@ int orc_sample_without_replacement(void* r, int64_t n, int64_t k, int64_t* out) 
   });
 }
 uint64_t orc_splitmix64(uint64_t s) { return synthetic_operator_seed(s); }
+void orc_rng_uniform_fill(void* r, int64_t count, double* out) {
+  for (int64_t i = 0; i < count; ++i) out[i] = static_cast<Rng*>(r)->uniform();
+}
 
 // ---- dense ------------------------------------------------------------------
 double orc_ulp_spacing(double x) { return dense::ulp_spacing(x); }

@@ -164,6 +164,20 @@ class Context:
     def launches(self) -> int:
         return lib().npcg_ctx_launches(_vp(self.h))
 
+    def prof_enable(self, on: bool = True):
+        """Per-kernel CUDA-event timing on this context's stream."""
+        _check(lib().npcg_prof_enable(_vp(self.h), C.c_int(int(on))))
+
+    def prof_report(self) -> dict:
+        """{kernel name: (launches, total_ms)} since prof_enable(True)."""
+        buf = C.create_string_buffer(1 << 20)
+        _check(lib().npcg_prof_report(_vp(self.h), buf, _i64(1 << 20)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split("\t")
+            out[name] = (int(cnt), float(ms))
+        return out
+
     @property
     def stream(self) -> int:
         return lib().npcg_ctx_stream(_vp(self.h))
@@ -225,6 +239,11 @@ class Rng:
     def gaussian_vector(self, n: int) -> np.ndarray:
         return self.gaussian_matrix(n, 1)[:, 0].copy()
 
+    def uniform_fill(self, count: int) -> np.ndarray:
+        out = np.empty(count)
+        _check(lib().npcg_rng_uniform_fill(_vp(self.h), _i64(count), _ptr(out)))
+        return out
+
     def sample_without_replacement(self, n: int, k: int) -> np.ndarray:
         out = np.empty(max(k, 0), dtype=np.int64)
         _check(lib().npcg_rng_sample(_vp(self.h), _i64(n), _i64(k), out.ctypes.data_as(C.POINTER(_i64))))
@@ -245,6 +264,21 @@ def orthonormal_columns(g, ctx: Context | None = None) -> np.ndarray:
     q = np.empty_like(g, order="F")
     _check(lib().npcg_orthonormal_columns(_vp(ctx.h), _i64(g.shape[0]), _i64(g.shape[1]), _ptr(g), _ptr(q), HOST))
     return q
+
+
+def gemm(a, b, transa=False, transb=False, alpha=1.0, beta=0.0, c=None, ctx: Context | None = None):
+    """alpha op(a) op(b) + beta c on the FP64 DMMA GEMM (npcg_gemm)."""
+    ctx = ctx or default_context()
+    a, b = _f64(a), _f64(b)
+    m, k = (a.shape[1], a.shape[0]) if transa else a.shape
+    kb, n = (b.shape[1], b.shape[0]) if transb else b.shape
+    if k != kb:
+        raise InvalidArgument("gemm: inner dimensions differ")
+    out = np.zeros((m, n), order="F") if c is None else _f64(c).copy(order="F")
+    _check(lib().npcg_gemm(_vp(ctx.h), _i64(m), _i64(n), _i64(k), C.c_double(alpha), _ptr(a),
+                           _i64(max(a.shape[0], 1)), C.c_int(int(transa)), _ptr(b), _i64(max(b.shape[0], 1)),
+                           C.c_int(int(not transb)), C.c_double(beta), _ptr(out), _i64(max(m, 1)), HOST))
+    return out
 
 
 def thin_svd(b, ctx: Context | None = None):

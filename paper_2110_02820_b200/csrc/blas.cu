@@ -399,6 +399,46 @@ void divide(Ctx& ctx, i64 rows, i64 cols, double* y, i64 ld, double d) {
   if (rows <= 0 || cols <= 0) return;
   NPCG_LAUNCH(ctx, divide_kernel, grid_for(ctx, rows * cols), 256, 0, rows, cols, y, ld, d);
 }
+namespace {
+__global__ void maxabs_kernel(const double* __restrict__ a, i64 rows, i64 cols, i64 ld, unsigned long long* out) {
+  const i64 total = rows * cols;
+  double m = 0.0;
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const double v = fabs(a[idx % rows + idx / rows * ld]);
+    m = isnan(v) ? CUDART_INF : fmax(m, v);
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, dbits(m));
+}
+__global__ void scale_pow2_kernel(i64 rows, i64 cols, double* a, i64 ld, int e) {
+  const i64 total = rows * cols;
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    double* p = a + idx % rows + idx / rows * ld;
+    *p = ldexp(*p, e);
+  }
+}
+}  // namespace
+
+double max_abs(Ctx& ctx, const double* a, i64 rows, i64 cols, i64 ld) {
+  if (rows <= 0 || cols <= 0) return 0.0;
+  DBuf<unsigned long long> out(1, ctx.stream);
+  out.zero();
+  NPCG_LAUNCH(ctx, maxabs_kernel, grid_for(ctx, rows * cols), 256, 0, a, rows, cols, ld, out.p);
+  unsigned long long h = 0;
+  NPCG_CUDA(cudaMemcpyAsync(&h, out.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  double r;
+  std::memcpy(&r, &h, 8);
+  return r;
+}
+
+void scale_pow2(Ctx& ctx, i64 rows, i64 cols, double* a, i64 ld, int e) {
+  if (rows <= 0 || cols <= 0 || e == 0) return;
+  NPCG_LAUNCH(ctx, scale_pow2_kernel, grid_for(ctx, rows * cols), 256, 0, rows, cols, a, ld, e);
+}
+
 void set_identity(Ctx& ctx, double* a, i64 rows, i64 cols, i64 ld) {
   if (rows <= 0 || cols <= 0) return;
   NPCG_LAUNCH(ctx, identity_kernel, grid_for(ctx, rows * cols), 256, 0, a, rows, cols, ld);
@@ -417,11 +457,13 @@ void coldot_s(Ctx& ctx, const double* M, i64 ldm, i64 nrows, i64 ncols, const do
   if (splits <= 1) {
     NPCG_LAUNCH(ctx, coldot_kernel<S>, dim3(static_cast<unsigned>(cblocks), 1), 256, 0, M, ldm, nrows, ncols, X,
                 ldx, std::max<i64>(nrows, 1), out, ldo, mu, shift, ldsh, static_cast<double*>(nullptr), gate);
+    ctx.prof_work(2.0 * nrows * ncols * S, 8.0 * (nrows * ncols + S * (nrows + ncols)));
     return;
   }
   DBuf<double> part(splits * S * ncols, ctx.stream);
   NPCG_LAUNCH(ctx, coldot_kernel<S>, dim3(static_cast<unsigned>(cblocks), static_cast<unsigned>(splits)), 256, 0, M,
               ldm, nrows, ncols, X, ldx, rps, out, ldo, mu, shift, ldsh, part.p, gate);
+  ctx.prof_work(2.0 * nrows * ncols * S, 8.0 * (nrows * ncols + S * (nrows + ncols)));
   NPCG_LAUNCH(ctx, coldot_reduce_kernel, static_cast<unsigned>(cdiv(ncols * S, 256)), 256, 0, part.p,
               static_cast<int>(splits), ncols, S, out, ldo, mu, shift, ldsh, gate);
 }
@@ -438,11 +480,13 @@ void rowdot_s(Ctx& ctx, const double* M, i64 ldm, i64 nrows, i64 ncols, const do
   if (splits <= 1) {
     NPCG_LAUNCH(ctx, rowdot_kernel<S>, dim3(static_cast<unsigned>(rblocks), 1), 128, 0, M, ldm, nrows, ncols, c, ldc,
                 std::max<i64>(ncols, 1), base, ldb, out, ldo, static_cast<double*>(nullptr), gate);
+    ctx.prof_work(2.0 * nrows * ncols * S, 8.0 * (nrows * ncols + S * (2 * nrows + ncols)));
     return;
   }
   DBuf<double> part(splits * S * nrows, ctx.stream);
   NPCG_LAUNCH(ctx, rowdot_kernel<S>, dim3(static_cast<unsigned>(rblocks), static_cast<unsigned>(splits)), 128, 0, M,
               ldm, nrows, ncols, c, ldc, cps, base, ldb, out, ldo, part.p, gate);
+  ctx.prof_work(2.0 * nrows * ncols * S, 8.0 * (nrows * ncols + S * (2 * nrows + ncols)));
   NPCG_LAUNCH(ctx, rowdot_reduce_kernel, static_cast<unsigned>(cdiv(nrows * S, 256)), 256, 0, part.p,
               static_cast<int>(splits), nrows, S, base, ldb, out, ldo, gate);
 }

@@ -157,6 +157,52 @@ int npcg_ctx_sync(npcg_ctx* ctx) {
 }
 void* npcg_ctx_stream(npcg_ctx* ctx) { return ctx ? ctx->c->stream : nullptr; }
 int64_t npcg_ctx_launches(npcg_ctx* ctx) { return ctx ? ctx->c->launches.load() : 0; }
+int npcg_prof_enable(npcg_ctx* ctx, int on) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    c.sync();
+    for (auto& r : c.prof_recs) {
+      cudaEventDestroy(r.start);
+      cudaEventDestroy(r.stop);
+    }
+    c.prof_recs.clear();
+    c.prof = on != 0;
+  });
+}
+int npcg_prof_report(npcg_ctx* ctx, char* buf, int64_t cap) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    c.sync();
+    struct Agg {
+      int64_t count = 0;
+      double ms = 0.0, flops = 0.0, bytes = 0.0;
+    };
+    std::vector<std::pair<std::string, Agg>> agg;
+    for (auto& r : c.prof_recs) {
+      float ms = 0.f;
+      NPCG_CUDA(cudaEventElapsedTime(&ms, r.start, r.stop));
+      auto it = std::find_if(agg.begin(), agg.end(), [&](auto& p) { return p.first == r.name; });
+      if (it == agg.end()) {
+        agg.emplace_back(r.name, Agg{});
+        it = agg.end() - 1;
+      }
+      it->second.count += 1;
+      it->second.ms += ms;
+      it->second.flops += r.flops;
+      it->second.bytes += r.bytes;
+    }
+    std::string out;
+    char line[512];
+    for (auto& [name, a] : agg) {
+      std::snprintf(line, sizeof(line), "%s\t%lld\t%.6f\t%.6e\t%.6e\n", name.c_str(),
+                    static_cast<long long>(a.count), a.ms, a.flops, a.bytes);
+      out += line;
+    }
+    if (static_cast<int64_t>(out.size()) + 1 > cap) invalid("npcg_prof_report: buffer too small");
+    std::memcpy(buf, out.c_str(), out.size() + 1);
+  });
+}
+
 int npcg_dev_alloc(npcg_ctx* ctx, int64_t bytes, void** out) {
   return guard([&] {
     Ctx& c = C(ctx);
@@ -201,6 +247,11 @@ int npcg_rng_integer(npcg_rng* rng, uint64_t bound, uint64_t* out) {
 }
 int npcg_rng_gaussian(npcg_rng* rng, int64_t rows, int64_t cols, double* dst) {
   return guard([&] { rng->r.gaussian(rows, cols, dst); });
+}
+int npcg_rng_uniform_fill(npcg_rng* rng, int64_t count, double* dst) {
+  return guard([&] {
+    for (int64_t i = 0; i < count; ++i) dst[i] = rng->r.uniform();
+  });
 }
 int npcg_rng_sample(npcg_rng* rng, int64_t n, int64_t k, int64_t* out) {
   return guard([&] {  // random.cpp:44-56
@@ -833,6 +884,23 @@ int npcg_orthonormal_columns(npcg_ctx* ctx, int64_t m, int64_t n, const double* 
     c.sync();
   });
 }
+int npcg_gemm(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda,
+              int a_kmajor, const double* b, int64_t ldb, int b_kmajor, double beta, double* c, int64_t ldc,
+              int where) {
+  return guard([&] {
+    Ctx& cx = C(ctx);
+    if (m < 0 || n < 0 || k < 0) invalid("npcg_gemm: negative dimension");
+    if (m == 0 || n == 0) return;
+    View A = view_in(cx, a, a_kmajor ? k : m, a_kmajor ? m : k, lda, where);
+    View B = view_in(cx, b, b_kmajor ? k : n, b_kmajor ? n : k, ldb, where);
+    View Cv = view_in(cx, c, m, n, ldc, where);
+    gemm(cx, m, n, k, alpha, Operand{A.p, A.ld, a_kmajor != 0}, Operand{B.p, B.ld, b_kmajor != 0}, beta,
+         const_cast<double*>(Cv.p), Cv.ld);
+    if (Cv.owned.p() != nullptr || where == NPCG_HOST) download(cx, Cv.p, Cv.ld, m, n, c, ldc, where);
+    cx.sync();
+  });
+}
+
 int npcg_thin_svd(npcg_ctx* ctx, int64_t m, int64_t n, const double* b, double* u, double* s, int where) {
   return guard([&] {
     Ctx& c = C(ctx);

@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -17,6 +18,15 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+/// Optional per-launch event timing (npcg_prof_enable): CUDA events recorded
+/// on the context stream around every kernel this library launches.
+struct ProfRec {
+  const char* name;
+  cudaEvent_t start, stop;
+  double flops = 0.0;  // algorithmic work of this launch (when the caller knows it)
+  double bytes = 0.0;
+};
+
 struct Ctx {
   int device = 0;
   int sm_count = 148;
@@ -25,6 +35,8 @@ struct Ctx {
   std::atomic<int64_t> launches{0};
   EncodeTiledFn encode_tiled = nullptr;
   std::mutex mu;  // serialises public calls sharing this context
+  bool prof = false;
+  std::vector<ProfRec> prof_recs;
 
   explicit Ctx(int dev);
   ~Ctx();
@@ -35,6 +47,24 @@ struct Ctx {
     if (e != cudaSuccess) fail(NPCG_ECUDA, std::string("kernel launch failed (") + what + "): " + cudaGetErrorString(e));
     count();
   }
+  void prof_begin(const char* name) {
+    if (!prof) return;
+    ProfRec r{name, nullptr, nullptr};
+    NPCG_CUDA(cudaEventCreate(&r.start));
+    NPCG_CUDA(cudaEventCreate(&r.stop));
+    NPCG_CUDA(cudaEventRecord(r.start, stream));
+    prof_recs.push_back(r);
+  }
+  void prof_end() {
+    if (!prof) return;
+    NPCG_CUDA(cudaEventRecord(prof_recs.back().stop, stream));
+  }
+  /// Attach algorithmic flops / bytes to the most recent launch record.
+  void prof_work(double flops, double bytes) {
+    if (!prof || prof_recs.empty()) return;
+    prof_recs.back().flops += flops;
+    prof_recs.back().bytes += bytes;
+  }
   /// Make `dev` current for the calling thread.
   void activate() const { NPCG_CUDA(cudaSetDevice(device)); }
 };
@@ -42,8 +72,10 @@ struct Ctx {
 /// Launch helper: <<<>>> on the context stream + error check + accounting.
 #define NPCG_LAUNCH(ctx, kernel, grid, block, smem, ...)                \
   do {                                                                  \
+    (ctx).prof_begin(#kernel);                                          \
     kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);     \
     (ctx).check_launch(#kernel);                                        \
+    (ctx).prof_end();                                                   \
   } while (0)
 
 }  // namespace npcg

@@ -257,8 +257,24 @@ bool cholqr_pass(Ctx& ctx, double* Y, i64 ldy, i64 m, i64 n, double shift, DMat&
 }
 }  // namespace
 
-void orthonormalize(Ctx& ctx, const double* G, i64 ldg, i64 m, i64 n, double* Q, i64 ldq, double* Rt, i64 ldr) {
+void orthonormalize(Ctx& ctx, const double* G_in, i64 ldg_in, i64 m, i64 n, double* Q, i64 ldq, double* Rt, i64 ldr) {
   if (n <= 0) return;
+  // Scale by an exact power of two so max|G| ~ 1: the Gram G^T G neither
+  // underflows (e.g. the nu-shifted zero matrix, whose B ~ sqrt(nu) ~ 1e-162)
+  // nor overflows. Q is scale-invariant; R^T is scaled back exactly.
+  const double amax = max_abs(ctx, G_in, m, n, ldg_in);
+  int e2 = 0;
+  if (amax > 0.0 && std::isfinite(amax)) std::frexp(amax, &e2);
+  DMat scaled;
+  const double* G = G_in;
+  i64 ldg = ldg_in;
+  if (e2 != 0) {
+    scaled.alloc(m, n, ctx.stream, false);
+    copy2d(ctx, m, n, G_in, ldg_in, scaled.p(), scaled.ld);
+    scale_pow2(ctx, m, n, scaled.p(), scaled.ld, -e2);
+    G = scaled.p();
+    ldg = scaled.ld;
+  }
   DMat work;
   work.alloc(m, n, ctx.stream, false);
   copy2d(ctx, m, n, G, ldg, work.p(), work.ld);
@@ -291,6 +307,7 @@ void orthonormalize(Ctx& ctx, const double* G, i64 ldg, i64 m, i64 n, double* Q,
       gemm(ctx, n, n, n, 1.0, Operand{L1.p(), L1.ld, false}, Operand{L2.p(), L2.ld, true}, 0.0, t.p(), t.ld);
       gemm(ctx, n, n, n, 1.0, Operand{t.p(), t.ld, false}, Operand{L3.p(), L3.ld, true}, 0.0, Rt, ldr);
     }
+    if (e2 != 0) scale_pow2(ctx, n, n, Rt, ldr, e2);
   }
 }
 
@@ -313,8 +330,10 @@ void jacobi_svd_small(Ctx& ctx, double* W, i64 ldw, i64 n, double* Vs, i64 ldv, 
   i64 ldvv = V.ld;
   unsigned int* cp = counters.p;
   void* args[] = {&Wp, &ldw, &Vp, &ldvv, &nn, &tol, &max_sweeps, &cp};
+  ctx.prof_begin("jacobi_kernel");
   NPCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_kernel), grid, 256, args, 0, ctx.stream));
   ctx.check_launch("jacobi_kernel");
+  ctx.prof_end();
   DBuf<double> sig(n, ctx.stream);
   DBuf<int> perm(n, ctx.stream);
   NPCG_LAUNCH(ctx, colnorm_kernel, static_cast<unsigned>(cdiv(n * 32, 256)), 256, 0, W, ldw, nn, sig.p);

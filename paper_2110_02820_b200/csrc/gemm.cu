@@ -140,10 +140,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           a[f][0] = v.x;
           a[f][1] = v.y;
         }
-      } else {  // slabs of [16 k][16 m]; m-pair (2g, 2g+1) -> fragments 2p / 2p+1
+      } else {  // slabs of [16 k][16 m]; m-pair (2g, 2g+1) -> fragments 2p / 2p+1, k = 8kc + 2t + ss
 #pragma unroll
         for (int ss = 0; ss < 2; ++ss) {
-          const int k = kc * 8 + ss * 4 + t;
+          const int k = kc * 8 + 2 * t + ss;  // same k <-> (lane, step) map as the K-major path
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
             const double2 v = lds128(As + (wm * 4 + p) * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       } else {
 #pragma unroll
         for (int ss = 0; ss < 2; ++ss) {
-          const int k = kc * 8 + ss * 4 + t;
+          const int k = kc * 8 + 2 * t + ss;
 #pragma unroll
           for (int p = 0; p < 2; ++p) {
             const double2 v = lds128(Bs + (wn * 2 + p) * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
@@ -286,6 +286,8 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
   else if (A.kmajor) launch<true, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
   else if (B.kmajor) launch<false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
   else launch<false, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  ctx.prof_work(2.0 * static_cast<double>(M) * N * K, 8.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N +
+                                                              static_cast<double>(M) * N));
   if (splits > 1) {
     const i64 total = M * N;
     NPCG_LAUNCH(ctx, splitk_reduce_kernel, static_cast<unsigned>(cdiv(total, 256)), 256, 0, pp, splits, m, n,
