@@ -169,13 +169,14 @@ class Context:
         _check(lib().npcg_prof_enable(_vp(self.h), C.c_int(int(on))))
 
     def prof_report(self) -> dict:
-        """{kernel name: (launches, total_ms)} since prof_enable(True)."""
+        """{kernel name: (launches, total_ms, algorithmic flops, algorithmic bytes)}
+        since prof_enable(True)."""
         buf = C.create_string_buffer(1 << 20)
         _check(lib().npcg_prof_report(_vp(self.h), buf, _i64(1 << 20)))
         out = {}
         for line in buf.value.decode().splitlines():
-            name, cnt, ms = line.split("\t")
-            out[name] = (int(cnt), float(ms))
+            name, cnt, ms, fl, by = line.split("\t")
+            out[name] = (int(cnt), float(ms), float(fl), float(by))
         return out
 
     @property

@@ -130,12 +130,13 @@ __global__ void __launch_bounds__(128) rowdot_kernel(const double* __restrict__ 
 #pragma unroll
   for (int s = 0; s < S; ++s) acc0[s] = acc1[s] = 0.0;
   i64 k = k0;
-  for (; k + 3 < k1; k += 4) {
-    double2 a[4];
+  constexpr int U = 8;  // 8 x 16 B loads in flight per thread
+  for (; k + U - 1 < k1; k += U) {
+    double2 a[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = __ldg(reinterpret_cast<const double2*>(M + (k + u) * ldm + i));
+    for (int u = 0; u < U; ++u) a[u] = __ldg(reinterpret_cast<const double2*>(M + (k + u) * ldm + i));
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const double cv = __ldg(c + s * ldc + k + u);
@@ -420,6 +421,29 @@ __global__ void scale_pow2_kernel(i64 rows, i64 cols, double* a, i64 ld, int e) 
   }
 }
 }  // namespace
+
+namespace {
+__global__ void transpose_tile_kernel(const double* __restrict__ src, i64 lds, i64 rows, i64 cols,
+                                      double* __restrict__ dst, i64 ldd) {
+  __shared__ double tile[32][33];
+  const i64 r0 = static_cast<i64>(blockIdx.x) * 32, c0 = static_cast<i64>(blockIdx.y) * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const i64 r = r0 + threadIdx.x, c = c0 + k;
+    tile[k][threadIdx.x] = (r < rows && c < cols) ? src[r + c * lds] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const i64 c = c0 + threadIdx.x, r = r0 + k;  // dst(c, r) = src(r, c)
+    if (r < rows && c < cols) dst[c + r * ldd] = tile[threadIdx.x][k];
+  }
+}
+}  // namespace
+
+void transpose(Ctx& ctx, const double* src, i64 lds, i64 rows, i64 cols, double* dst, i64 ldd) {
+  if (rows <= 0 || cols <= 0) return;
+  NPCG_LAUNCH(ctx, transpose_tile_kernel, dim3(static_cast<unsigned>(cdiv(rows, 32)), static_cast<unsigned>(cdiv(cols, 32))),
+              dim3(32, 8), 0, src, lds, rows, cols, dst, ldd);
+}
 
 double max_abs(Ctx& ctx, const double* a, i64 rows, i64 cols, i64 ld) {
   if (rows <= 0 || cols <= 0) return 0.0;

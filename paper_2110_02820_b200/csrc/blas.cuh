@@ -31,6 +31,8 @@ void divide(Ctx& ctx, i64 rows, i64 cols, double* y, i64 ld, double d);
 void symmetrize(Ctx& ctx, const double* a, i64 n, i64 lda, double* out, i64 ldo);
 /// a(:, j) *= d(j)  (d on device).
 void scale_cols(Ctx& ctx, double* a, i64 rows, i64 cols, i64 lda, const double* d);
+/// dst (cols x rows) = src^T (src rows x cols).
+void transpose(Ctx& ctx, const double* src, i64 lds, i64 rows, i64 cols, double* dst, i64 ldd);
 /// max |a_ij| of a block (synchronises).
 double max_abs(Ctx& ctx, const double* a, i64 rows, i64 cols, i64 ld);
 /// a *= 2^e exactly (ldexp).

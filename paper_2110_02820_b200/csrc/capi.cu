@@ -309,9 +309,14 @@ int npcg_op_gram_create(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, in
     op->n = n;
     op->m = m;
     op->kind = kGram;
-    upload(c, op->g, m, n, g, ldg, where);
-    if (!all_finite(c, op->g.p(), m, n, op->g.ld))
-      invalid("GramRidgeOperator: design matrix has non-finite entries");
+    {
+      DMat colmajor;  // caller layout, then the row-major copy the kernels stream
+      upload(c, colmajor, m, n, g, ldg, where);
+      if (!all_finite(c, colmajor.p(), m, n, colmajor.ld))
+        invalid("GramRidgeOperator: design matrix has non-finite entries");
+      op->xr.alloc(n, m, c.stream, true);
+      transpose(c, colmajor.p(), colmajor.ld, m, n, op->xr.p(), op->xr.ld);
+    }
     *out = new npcg_op{ctx, std::move(op)};
   });
 }

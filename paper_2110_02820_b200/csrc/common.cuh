@@ -126,4 +126,20 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return sh[0];
 }
 
+/// Block max (result valid in every thread); `sh` needs blockDim.x/32 doubles.
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = lane < nw ? sh[lane] : -1e308;
+    t = warp_max(t);
+    if (lane == 0) sh[0] = t;
+  }
+  __syncthreads();
+  return sh[0];
+}
+
 }  // namespace npcg

@@ -1,0 +1,345 @@
+// Symmetric eigenvectors of a small dense l x l matrix on device, for the
+// thin SVD of the Nyström pipeline (factor.cu).
+//
+//   1. Householder tridiagonalisation in one cooperative kernel: per column,
+//      every CTA forms the reflector redundantly, the trailing symmetric
+//      matvec and the rank-2 update are split over CTAs by column (two
+//      grid-wide barriers per column).
+//   2. Bisection with Sturm counts, one eigenvalue per thread.
+//   3. Inverse iteration on the tridiagonal (partial-pivoting LU), one
+//      eigenvector per thread, deterministic pseudo-random starts; exact
+//      repeats are split by a tiny shift.
+//   4. Back-transformation by the stored reflectors, one warp per column.
+// The caller re-orthonormalises the vectors (CholeskyQR2) and takes the
+// singular values as column norms of W V, so their relative accuracy does not
+// depend on this solver's eigenvalue accuracy (see factor.cu).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "eig.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace npcg {
+namespace {
+
+constexpr int TRI_THREADS = 256;
+
+__global__ void __launch_bounds__(TRI_THREADS) tridiag_kernel(double* M, i64 ld, int n, double* d, double* e,
+                                                               double* tau, double* H, i64 ldh, double* p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double tsm[];  // v (n) then w (n)
+  __shared__ double red[32];
+  __shared__ double s_scal[3];
+  double* v = tsm;
+  double* w = tsm + n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int G = gridDim.x, bid = blockIdx.x;
+  for (int k = 0; k < n - 2; ++k) {
+    const int L = n - k - 1;
+    const double* x = M + (k + 1) + static_cast<i64>(k) * ld;
+    // ---- reflector (redundant in every CTA): beta, tau, v (v_0 = 1)
+    double s = 0.0;
+    for (int i = 1 + tid; i < L; i += blockDim.x) s += x[i] * x[i];
+    s = block_sum(s, red);
+    const double alpha = x[0];
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (s > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + s), alpha);
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int i = tid; i < L; i += blockDim.x) v[i] = i == 0 ? 1.0 : x[i] * scal;
+    if (bid == 0 && tid == 0) {
+      d[k] = M[k + static_cast<i64>(k) * ld];
+      e[k] = beta;
+      tau[k] = t;
+    }
+    if (bid == 0)
+      for (int i = tid; i < L; i += blockDim.x) H[(k + 1 + i) + static_cast<i64>(k) * ldh] = v[i];
+    __syncthreads();
+    if (t == 0.0) {  // nothing to eliminate; uniform across CTAs
+      grid.sync();
+      continue;
+    }
+    // ---- p = tau * A22 v   (A22 = M[k+1:, k+1:], symmetric: column c == row c)
+    for (int c = bid * nw + warp; c < L; c += G * nw) {
+      const double* col = M + (k + 1) + static_cast<i64>(k + 1 + c) * ld;
+      double acc = 0.0;
+      for (int i = lane; i < L; i += 32) acc += col[i] * v[i];
+      acc = warp_sum(acc);
+      if (lane == 0) p[c] = t * acc;
+    }
+    grid.sync();
+    // ---- w = p - (tau/2)(p.v) v  (redundant per CTA)
+    double pv = 0.0;
+    for (int i = tid; i < L; i += blockDim.x) {
+      const double pi = p[i];
+      w[i] = pi;
+      pv += pi * v[i];
+    }
+    pv = block_sum(pv, red);
+    const double K = 0.5 * t * pv;
+    for (int i = tid; i < L; i += blockDim.x) w[i] -= K * v[i];
+    __syncthreads();
+    // ---- A22 -= v w^T + w v^T  (column c owned by warp)
+    for (int c = bid * nw + warp; c < L; c += G * nw) {
+      double* col = M + (k + 1) + static_cast<i64>(k + 1 + c) * ld;
+      const double vc = v[c], wc = w[c];
+      for (int i = lane; i < L; i += 32) col[i] -= v[i] * wc + w[i] * vc;
+    }
+    grid.sync();
+  }
+  if (bid == 0 && tid == 0) {
+    if (n >= 2) {
+      d[n - 2] = M[(n - 2) + static_cast<i64>(n - 2) * ld];
+      d[n - 1] = M[(n - 1) + static_cast<i64>(n - 1) * ld];
+      e[n - 2] = M[(n - 1) + static_cast<i64>(n - 2) * ld];
+      tau[n - 2] = 0.0;
+    } else {
+      d[0] = M[0];
+    }
+    if (n >= 1) {
+      e[n - 1] = 0.0;
+      tau[n - 1] = 0.0;
+    }
+  }
+}
+
+// number of eigenvalues of T strictly below x (Sturm sequence of LDL^T)
+__device__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += q < 0.0;
+  for (int i = 1; i < n; ++i) {
+    q = d[i] - x - e2[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// Gershgorin interval, ||T|| bound, pivmin and e_i^2 (one CTA).
+__global__ void tri_bounds_kernel(const double* d, const double* e, int n, double* e2, double* info) {
+  __shared__ double sh[32];
+  double lo = 1e308, hi = -1e308, emax = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < n - 1 ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+    if (i < n - 1) {
+      emax = fmax(emax, fabs(e[i]));
+      e2[i] = e[i] * e[i];
+    }
+  }
+  lo = -block_max(-lo, sh);
+  hi = block_max(hi, sh);
+  emax = block_max(emax, sh);
+  if (threadIdx.x == 0) {
+    const double tnorm = fmax(fmax(fabs(lo), fabs(hi)), 1e-300);
+    const double eps = 2.220446049250313e-16;
+    info[0] = lo - 4.0 * eps * tnorm - 1e-300;
+    info[1] = hi + 4.0 * eps * tnorm + 1e-300;
+    info[2] = fmax(1e-300, 4.0 * 2.2250738585072014e-308 * fmax(1.0, emax * emax));
+    info[3] = tnorm;
+  }
+}
+
+// Multisection: one warp per eigenvalue, 32 Sturm counts per step shrink the
+// bracket 33x (about 9 steps to 1e-13 ||T||). Eigenvalue j is the (j+1)-th
+// smallest. Only inverse-iteration shifts are needed from here.
+__global__ void bisect_kernel(const double* d, const double* e2, int n, const double* info, double* lam) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (j >= n) return;
+  double lo = info[0], hi = info[1];
+  const double pivmin = info[2], tnorm = info[3];
+  const double eps = 2.220446049250313e-16;
+  for (int it = 0; it < 40; ++it) {
+    const double tol = fmax(2.0 * eps * fmax(fabs(lo), fabs(hi)), 1e-13 * tnorm);
+    if (hi - lo <= tol) break;
+    const double x = lo + (hi - lo) * static_cast<double>(lane + 1) / 33.0;
+    const int c = sturm_count(d, e2, n, x, pivmin);
+    const unsigned ball = __ballot_sync(0xffffffffu, c > j);
+    const int k = ball ? __ffs(ball) - 1 : 32;
+    const double xk = __shfl_sync(0xffffffffu, x, k < 32 ? k : 31);
+    const double xk1 = __shfl_sync(0xffffffffu, x, k > 0 ? k - 1 : 0);
+    const double nlo = k == 0 ? lo : xk1;
+    const double nhi = k == 32 ? hi : xk;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) lam[j] = 0.5 * (lo + hi);
+}
+
+__device__ __forceinline__ double hash_unit(unsigned long long a) {
+  a ^= a >> 33;
+  a *= 0xff51afd7ed558ccdULL;
+  a ^= a >> 33;
+  a *= 0xc4ceb9fe1a85ec53ULL;
+  a ^= a >> 33;
+  return static_cast<double>(a >> 11) * 0x1.0p-53 - 0.5;
+}
+
+// Inverse iteration on T for eigenvalue lam[j] (three solves), one thread per
+// eigenvector. Work arrays are interleaved [i][j] so a warp's threads touch
+// consecutive addresses at every step; the vector lands in Zr[i][j]
+// (row-major n x n, i.e. Z^T column-major).
+__global__ void invit_kernel(const double* d, const double* e, const double* lam, int n, const double* info,
+                             double* Zr, double* wk, unsigned char* pvk) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double eps = 2.220446049250313e-16;
+  const double tnorm = info[3];
+  const i64 N = n;
+  int rep = 0;  // exact repeats get distinct shifts so the solves differ
+  while (j - rep - 1 >= 0 && lam[j] - lam[j - rep - 1] <= 4.0 * eps * tnorm) ++rep;
+  const double shift = lam[j] + rep * 8.0 * eps * tnorm;
+  const double tiny = fmax(eps * tnorm, 1e-300);
+  double* u0 = wk;
+  double* u1 = wk + N * N;
+  double* u2 = wk + 2 * N * N;
+  double* lm = wk + 3 * N * N;
+#define IX(i) (static_cast<i64>(i) * N + j)
+  for (int i = 0; i < n; ++i) {
+    u0[IX(i)] = d[i] - shift;
+    u1[IX(i)] = i < n - 1 ? e[i] : 0.0;
+    u2[IX(i)] = 0.0;
+  }
+  for (int i = 0; i < n - 1; ++i) {  // dgttrf on T - shift I
+    const double sub = e[i];
+    const double a = u0[IX(i)];
+    if (fabs(a) >= fabs(sub)) {
+      pvk[IX(i)] = 0;
+      const double piv = a == 0.0 ? tiny : a;
+      u0[IX(i)] = piv;
+      const double f = sub / piv;
+      lm[IX(i)] = f;
+      u0[IX(i + 1)] -= f * u1[IX(i)];
+    } else {
+      pvk[IX(i)] = 1;
+      const double f = a / sub;
+      lm[IX(i)] = f;
+      u0[IX(i)] = sub;
+      const double old_u1 = u1[IX(i)];
+      const double old_d1 = u0[IX(i + 1)];
+      u1[IX(i)] = old_d1;
+      u0[IX(i + 1)] = old_u1 - f * old_d1;
+      if (i < n - 2) {
+        const double old_u1n = u1[IX(i + 1)];
+        u2[IX(i)] = old_u1n;
+        u1[IX(i + 1)] = -f * old_u1n;
+      }
+    }
+  }
+  if (u0[IX(n - 1)] == 0.0) u0[IX(n - 1)] = tiny;
+  double* z = Zr;
+  for (int i = 0; i < n; ++i) z[IX(i)] = hash_unit((static_cast<unsigned long long>(j) << 32) ^ static_cast<unsigned>(i));
+  for (int it = 0; it < 3; ++it) {
+    for (int i = 0; i < n - 1; ++i) {
+      const double zi = z[IX(i)], zi1 = z[IX(i + 1)], f = lm[IX(i)];
+      if (pvk[IX(i)]) {
+        z[IX(i)] = zi1;
+        z[IX(i + 1)] = zi - f * zi1;
+      } else {
+        z[IX(i + 1)] = zi1 - f * zi;
+      }
+    }
+    z[IX(n - 1)] /= u0[IX(n - 1)];
+    if (n >= 2) z[IX(n - 2)] = (z[IX(n - 2)] - u1[IX(n - 2)] * z[IX(n - 1)]) / u0[IX(n - 2)];
+    for (int i = n - 3; i >= 0; --i)
+      z[IX(i)] = (z[IX(i)] - u1[IX(i)] * z[IX(i + 1)] - u2[IX(i)] * z[IX(i + 2)]) / u0[IX(i)];
+    double nrm = 0.0;
+    for (int i = 0; i < n; ++i) nrm += z[IX(i)] * z[IX(i)];
+    const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+    for (int i = 0; i < n; ++i) z[IX(i)] *= inv;
+  }
+#undef IX
+}
+
+__global__ void transpose_sq_kernel(const double* __restrict__ src, int n, double* __restrict__ dst, i64 ldd) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = by + k, c = bx + threadIdx.x;
+    tile[k][threadIdx.x] = (r < n && c < n) ? src[static_cast<i64>(r) * n + c] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = bx + k, c = by + threadIdx.x;  // dst(c, r) = src(r', c')
+    if (r < n && c < n) dst[c + static_cast<i64>(r) * ldd] = tile[threadIdx.x][k];
+  }
+}
+// Z <- H_0 H_1 ... H_{n-3} Z, one warp per column of Z.
+__global__ void backtransform_kernel(const double* H, i64 ldh, const double* tau, int n, double* Z, i64 ldz) {
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (col >= n) return;
+  double* z = Z + static_cast<i64>(col) * ldz;
+  for (int k = n - 3; k >= 0; --k) {
+    const double t = tau[k];
+    if (t == 0.0) continue;
+    const double* v = H + static_cast<i64>(k) * ldh;  // v_0 = 1 at row k+1
+    double s = 0.0;
+    for (int i = k + 1 + lane; i < n; i += 32) s += v[i] * z[i];
+    s = warp_sum(s);
+    const double ts = t * s;
+    for (int i = k + 1 + lane; i < n; i += 32) z[i] -= ts * v[i];
+  }
+}
+
+}  // namespace
+
+void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
+  if (n <= 0) return;
+  int nn = static_cast<int>(n);
+  DBuf<double> d(n, ctx.stream), e(n, ctx.stream), tau(n, ctx.stream), p(n, ctx.stream), lam(n, ctx.stream);
+  DMat H;
+  H.alloc(n, n, ctx.stream, true);
+  if (n >= 3) {
+    const int smem = static_cast<int>(2 * n * 8);
+    NPCG_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   std::max(smem, 48 * 1024)));
+    int per_sm = 0;
+    NPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_kernel, TRI_THREADS, smem));
+    // enough CTAs to stream the trailing matrix, few enough for cheap barriers
+    const int want = static_cast<int>(std::max<i64>(1, std::min<i64>(cdiv(n, 8), ctx.sm_count)));
+    int grid = std::max(1, std::min(want, std::max(per_sm, 1) * ctx.sm_count));
+    double* Mp = M;
+    double* dp = d.p;
+    double* ep = e.p;
+    double* tp = tau.p;
+    double* Hp = H.p();
+    i64 ldh = H.ld;
+    double* pp = p.p;
+    void* args[] = {&Mp, &ldm, &nn, &dp, &ep, &tp, &Hp, &ldh, &pp};
+    ctx.prof_begin("tridiag_kernel");
+    NPCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tridiag_kernel), grid, TRI_THREADS, args, smem,
+                                          ctx.stream));
+    ctx.check_launch("tridiag_kernel");
+    ctx.prof_end();
+  } else {
+    // n <= 2: already tridiagonal
+    std::vector<double> h(static_cast<size_t>(n * n));
+    download(ctx, M, ldm, n, n, h.data(), n, NPCG_HOST);
+    double hd[2] = {h[0], n == 2 ? h[3] : 0.0}, he[2] = {n == 2 ? h[1] : 0.0, 0.0}, ht[2] = {0.0, 0.0};
+    NPCG_CUDA(cudaMemcpyAsync(d.p, hd, 8 * n, cudaMemcpyHostToDevice, ctx.stream));
+    NPCG_CUDA(cudaMemcpyAsync(e.p, he, 8 * n, cudaMemcpyHostToDevice, ctx.stream));
+    NPCG_CUDA(cudaMemcpyAsync(tau.p, ht, 8 * n, cudaMemcpyHostToDevice, ctx.stream));
+    ctx.sync();
+  }
+  DBuf<double> e2(n, ctx.stream), info(4, ctx.stream);
+  NPCG_LAUNCH(ctx, tri_bounds_kernel, 1, 256, 0, d.p, e.p, nn, e2.p, info.p);
+  NPCG_LAUNCH(ctx, bisect_kernel, static_cast<unsigned>(cdiv(n * 32, 256)), 256, 0, d.p, e2.p, nn, info.p, lam.p);
+  DBuf<double> iw(4 * n * n, ctx.stream), zr(n * n, ctx.stream);
+  DBuf<unsigned char> ipv(n * n, ctx.stream);
+  NPCG_LAUNCH(ctx, invit_kernel, static_cast<unsigned>(cdiv(n, 64)), 64, 0, d.p, e.p, lam.p, nn, info.p, zr.p, iw.p,
+              ipv.p);
+  NPCG_LAUNCH(ctx, transpose_sq_kernel, dim3(static_cast<unsigned>(cdiv(n, 32)), static_cast<unsigned>(cdiv(n, 32))),
+              dim3(32, 8), 0, zr.p, nn, Z, ldz);
+  NPCG_LAUNCH(ctx, backtransform_kernel, static_cast<unsigned>(cdiv(n * 32, 256)), 256, 0, H.p(), H.ld, tau.p, nn, Z,
+              ldz);
+}
+
+}  // namespace npcg

@@ -34,6 +34,9 @@ void trsm_right_lt(Ctx& ctx, i64 m, i64 n, double* Y, i64 ldy, const double* L, 
 void orthonormalize(Ctx& ctx, const double* G, i64 ldg, i64 m, i64 n, double* Q, i64 ldq,
                     double* R = nullptr, i64 ldr = 0);
 
+/// orthonormalize() that reports a CholeskyQR breakdown instead of throwing.
+bool try_orthonormalize(Ctx& ctx, const double* G, i64 ldg, i64 m, i64 n, double* Q, i64 ldq);
+
 /// Thin SVD of a tall matrix (dgesdd('S') equivalent up to column signs):
 /// U (m x n) left singular vectors, sigma (n) descending, on device.
 void thin_svd(Ctx& ctx, const double* B, i64 ldb, i64 m, i64 n, double* U, i64 ldu, double* sigma);
@@ -42,5 +45,10 @@ void thin_svd(Ctx& ctx, const double* B, i64 ldb, i64 m, i64 n, double* U, i64 l
 /// orthogonal V with W V orthogonal columns. sigma(j) = ||(W V)(:,j)||,
 /// columns of V and sigma sorted descending into Vs / sigma.
 void jacobi_svd_small(Ctx& ctx, double* W, i64 ldw, i64 n, double* Vs, i64 ldv, double* sigma);
+
+/// Same contract via the symmetric eigenvectors of W^T W (eig.cu) and
+/// sigma_j = ||(W V)(:, j)||. The default path (NPCG_SVD=jacobi selects the
+/// one-sided Jacobi instead).
+void small_svd_eig(Ctx& ctx, double* W, i64 ldw, i64 n, double* Vs, i64 ldv, double* sigma);
 
 }  // namespace npcg

@@ -46,20 +46,6 @@ void DenseOp::apply_shift(const double* P, i64 ldp, int S, double mu, double* ou
 }
 void DenseOp::column(i64 j, double* out) { copy2d(*ctx, n, 1, a.col(j), a.ld, out, n); }
 
-// GramRidgeOperator (operators.cpp:112-121): out = G^T (G v); out /= m.
-void GramOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
-  DMat z;
-  z.alloc(m, k, ctx->stream, false);
-  if (k <= 8) {
-    rowdot(*ctx, g.p(), g.ld, m, n, V, ldv, static_cast<int>(k), nullptr, 0, z.p(), z.ld, gate);
-    coldot(*ctx, g.p(), g.ld, m, n, z.p(), z.ld, static_cast<int>(k), out, ldo, 0.0, nullptr, 0, gate);
-  } else {
-    gemm(*ctx, m, k, n, 1.0, Operand{g.p(), g.ld, false}, Operand{V, ldv, true}, 0.0, z.p(), z.ld);
-    gemm(*ctx, n, k, m, 1.0, Operand{g.p(), g.ld, true}, Operand{z.p(), z.ld, true}, 0.0, out, ldo);
-  }
-  divide(*ctx, n, k, out, ldo, static_cast<double>(m));
-}
-
 void KernelFreeOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
   kernel_apply_free(*ctx, *this, V, ldv, k, out, ldo, gate);
 }

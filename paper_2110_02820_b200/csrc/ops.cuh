@@ -35,9 +35,10 @@ struct DenseOp : Op {  // DenseOperator (operators.cpp:64-80); also the stored k
 };
 
 struct GramOp : Op {  // GramRidgeOperator (operators.cpp:105-121): (1/m) G^T (G v)
-  DMat g;             // m x n design, col-major
+  DMat xr;            // design stored row-major: n x m col-major, data row a contiguous
   i64 m = 0;
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
+  void apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) override;
 };
 
 struct KernelFreeOp : Op {  // KernelOperator beyond dense_cap (operators.cpp:152-188)
