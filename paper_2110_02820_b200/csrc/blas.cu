@@ -475,7 +475,7 @@ void coldot_s(Ctx& ctx, const double* M, i64 ldm, i64 nrows, i64 ncols, const do
   const i64 cblocks = cdiv(ncols, CD_COLS);
   i64 splits = 1;
   const i64 target = 2 * ctx.sm_count;
-  if (cblocks < target) splits = std::max<i64>(1, std::min<i64>(cdiv(target, cblocks), nrows / 2048));
+  if (cblocks < target) splits = std::max<i64>(1, std::min<i64>(cdiv(target, cblocks), nrows / 256));
   i64 rps = round_up(cdiv(nrows, splits), 64);
   splits = cdiv(nrows, rps);
   if (splits <= 1) {

@@ -181,9 +181,10 @@ int npcg_prof_report(npcg_ctx* ctx, char* buf, int64_t cap) {
     for (auto& r : c.prof_recs) {
       float ms = 0.f;
       NPCG_CUDA(cudaEventElapsedTime(&ms, r.start, r.stop));
-      auto it = std::find_if(agg.begin(), agg.end(), [&](auto& p) { return p.first == r.name; });
+      const std::string key = r.label.empty() ? std::string(r.name) : r.label;
+      auto it = std::find_if(agg.begin(), agg.end(), [&](auto& p) { return p.first == key; });
       if (it == agg.end()) {
-        agg.emplace_back(r.name, Agg{});
+        agg.emplace_back(key, Agg{});
         it = agg.end() - 1;
       }
       it->second.count += 1;

@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -25,6 +26,7 @@ struct ProfRec {
   cudaEvent_t start, stop;
   double flops = 0.0;  // algorithmic work of this launch (when the caller knows it)
   double bytes = 0.0;
+  std::string label;   // optional finer aggregation key (e.g. GEMM shape class)
 };
 
 struct Ctx {
@@ -64,6 +66,10 @@ struct Ctx {
     if (!prof || prof_recs.empty()) return;
     prof_recs.back().flops += flops;
     prof_recs.back().bytes += bytes;
+  }
+  void prof_label(std::string l) {
+    if (!prof || prof_recs.empty()) return;
+    prof_recs.back().label = std::move(l);
   }
   /// Make `dev` current for the calling thread.
   void activate() const { NPCG_CUDA(cudaSetDevice(device)); }

@@ -288,6 +288,12 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
   else launch<false, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
   ctx.prof_work(2.0 * static_cast<double>(M) * N * K, 8.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N +
                                                               static_cast<double>(M) * N));
+  if (ctx.prof) {
+    const double fl = 2.0 * static_cast<double>(M) * N * K;
+    ctx.prof_label(fl >= 1e10 ? "gemm_dmma_kernel[" + std::to_string(M) + "x" + std::to_string(N) + "x" +
+                                    std::to_string(K) + "]"
+                              : fl >= 1e8 ? "gemm_dmma_kernel[medium]" : "gemm_dmma_kernel[small]");
+  }
   if (splits > 1) {
     const i64 total = M * N;
     NPCG_LAUNCH(ctx, splitk_reduce_kernel, static_cast<unsigned>(cdiv(total, 256)), 256, 0, pp, splits, m, n,

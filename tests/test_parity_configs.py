@@ -1,0 +1,160 @@
+"""Parity of the B200 path with the CPU oracle on the BASELINE.json configs
+(configs 1-2 at full size; 3-5 at reduced sizes in the default GPU run, the
+full-size ones marked `slow`). Both sides get identical inputs: the same data
+from the reference generator and the same raw Gaussian Omega.
+
+Bar (BASELINE.json north_star): PCG iterations within +-1 of the oracle,
+solution relative error <= 1e-8, Nystrom eigenvalues relative error <= 1e-10
+for every lambda_j >= 1e-6 lambda_1, U equal up to
+column sign on separated eigenvalues, shift_used within a factor 2.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+LAMBDA_RTOL = 1e-10
+X_RTOL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def npcg():
+    import paper_2110_02820_b200 as m
+    from paper_2110_02820_b200 import workloads
+    m.workloads = workloads
+    return m
+
+
+def shared_inputs(npcg, orc, name, **kw):
+    from paper_2110_02820_b200 import workloads
+    w = workloads.make(name, orc.Rng, orc.splitmix64, **kw)
+    w2 = workloads.make(name, npcg.Rng, npcg.splitmix64, **kw)
+    # the two reference-generator implementations agree bit for bit
+    assert np.array_equal(w.omega, w2.omega) if w.omega is not None else True
+    assert np.array_equal(w.b, w2.b)
+    return w
+
+
+def operators(npcg, orc, w):
+    """Product and oracle operators over the *same* matrix entries."""
+    if w.kind == "synth":
+        oop = orc.synthesize_operator(w.data["lambda"], w.data["seed"])
+        a = oop.dense()
+        return npcg.DenseOperator(a), oop
+    if w.kind == "gram":
+        return npcg.GramRidgeOperator(w.data["x"]), orc.GramRidgeOperator(w.data["x"])
+    if w.kind == "kernel":
+        p, s, cap = w.data["points"], w.data["sigma"], w.data["dense_cap"]
+        return npcg.KernelOperator(p, s, cap), orc.KernelOperator(p, s, cap)
+    if w.kind == "lowrank":
+        g, lam = w.data["g"], w.data["lambda"]
+        op = npcg.LowRankOperator(g, lam)
+        return op, orc.DenseOperator(op.dense())
+    raise ValueError(w.kind)
+
+
+def compare_approx(ap, ao):
+    lam, lo = ap.lam, ao.lam
+    assert lam.shape == lo.shape
+    keep = lo >= 1e-6 * lo[0]
+    rel = np.abs(lam[keep] - lo[keep]) / lo[keep]
+    assert rel.max() <= LAMBDA_RTOL, f"lambda rel err {rel.max():.3e}"
+    assert 0.5 <= ap.shift_used / ao.shift_used <= 2.0
+    # U up to sign on eigenvalues separated from their neighbours by > 1e-4 relative
+    gaps = np.minimum(np.abs(np.diff(lo, prepend=np.inf)), np.abs(np.diff(lo, append=-np.inf))) / lo[0]
+    sep = keep & (gaps > 1e-4)
+    dots = np.abs(np.einsum("ij,ij->j", ap.u[:, sep], ao.u[:, sep]))
+    assert dots.size == 0 or dots.min() >= 1 - 1e-8, f"min |u.u_ref| = {dots.min():.12f}"
+    return rel.max()
+
+
+def compare_solve(rp, ro):
+    assert abs(rp.iterations - ro.iterations) <= 1, (rp.iterations, ro.iterations)
+    assert rp.converged == ro.converged
+    err = np.linalg.norm(rp.x - ro.x) / np.linalg.norm(ro.x)
+    assert err <= X_RTOL, f"x rel err {err:.3e}"
+    return err
+
+
+def run_fixed(npcg, orc, w):
+    op, oop = operators(npcg, orc, w)
+    pair = npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, w.omega)
+    ap = npcg.nystrom_from_sketch(pair)
+    ao = orc.nystrom_from_sketch(orc.extend_sketch_with(orc.make_empty_sketch(w.n), oop, w.omega))
+    lam_err = compare_approx(ap, ao)
+    pre = npcg.build_preconditioner(ap, w.mu)
+    opre = orc.build_preconditioner(ao, w.mu)
+    b = w.b.reshape(w.n, -1, order="F")
+    for j in range(b.shape[1]):
+        rp = npcg.nystrom_pcg(op, b[:, j], w.mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
+        ro = orc.nystrom_pcg(oop, b[:, j], w.mu, opre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
+        compare_solve(rp, ro)
+    return lam_err
+
+
+def test_cfg1_dense_synthetic_full(npcg, orc):
+    w = shared_inputs(npcg, orc, "cfg1")
+    run_fixed(npcg, orc, w)
+
+
+def test_cfg1_synthesize_operator_matches(npcg, orc):
+    # A = Q diag(j^-2) Q^T from the same seeded draw; Q is unique up to column
+    # signs (Householder vs CholeskyQR), which A does not see.
+    from paper_2110_02820_b200 import workloads
+    w = workloads.make("cfg1", orc.Rng, orc.splitmix64, n=600, ell=60)
+    a_gpu = npcg.synthesize_operator(w.data["lambda"], w.data["seed"]).dense()
+    a_cpu = orc.synthesize_operator(w.data["lambda"], w.data["seed"]).dense()
+    assert np.abs(a_gpu - a_cpu).max() <= 1e-13
+
+
+def test_cfg2_ridge_full(npcg, orc):
+    w = shared_inputs(npcg, orc, "cfg2", gemm=lambda a, b, transa=False: (a.T if transa else a) @ b)
+    run_fixed(npcg, orc, w)
+
+
+def test_cfg3_kernel_stored_reduced(npcg, orc):
+    w = shared_inputs(npcg, orc, "cfg3", n=6000, ell=300)
+    run_fixed(npcg, orc, w)
+
+
+@pytest.mark.slow
+def test_cfg3_kernel_stored_full(npcg, orc):
+    w = shared_inputs(npcg, orc, "cfg3")
+    run_fixed(npcg, orc, w)
+
+
+def test_cfg4_kernel_matrix_free_adaptive_reduced(npcg, orc):
+    w = shared_inputs(npcg, orc, "cfg4", n=3000, ell_max=300)
+    w.data["dense_cap"] = 1000  # n > dense_cap: both sides take the matrix-free path
+    op, oop = operators(npcg, orc, w)
+    assert op.kind == 3  # matrix-free path (n > dense_cap is forced below)
+    cfg = dict(mode="error", ell0=w.adaptive["ell0"], ell_max=w.adaptive["ell_max"], mu=w.mu,
+               tau=w.adaptive["tau"], q=w.adaptive["q"])
+    rng, orng = npcg.Rng(4), orc.Rng(4)
+    rng.gaussian_vector(w.n)  # b was drawn first (bench.cpp:207-209)
+    orng.gaussian_vector(w.n)
+    out = npcg.adaptive(op, rng, **cfg)
+    oout = orc.adaptive(oop, orng, **cfg)
+    assert (out.ell_final, out.doublings, out.hit_cap) == (oout.ell_final, oout.doublings, oout.hit_cap)
+    assert abs(out.error_estimate - oout.error_estimate) <= 1e-8 * abs(oout.error_estimate)
+    compare_approx(out.approximation, oout.approximation)
+    pre = npcg.build_preconditioner(out.approximation, w.mu)
+    opre = orc.build_preconditioner(oout.approximation, w.mu)
+    rp = npcg.nystrom_pcg(op, w.b, w.mu, pre, eta=w.eta, relative=True)
+    ro = orc.nystrom_pcg(oop, w.b, w.mu, opre, eta=w.eta, relative=True)
+    compare_solve(rp, ro)
+
+
+def test_cfg5_regularization_path_reduced(npcg, orc):
+    w = shared_inputs(npcg, orc, "cfg5", n=3000, r=300, ell=150, nmu=4)
+    op, oop = operators(npcg, orc, w)
+    pair = npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, w.omega)
+    ap = npcg.nystrom_from_sketch(pair)
+    ao = orc.nystrom_from_sketch(orc.extend_sketch_with(orc.make_empty_sketch(w.n), oop, w.omega))
+    compare_approx(ap, ao)
+    for mu in w.mus:  # one sketch reused across the regularisation path
+        pre, opre = npcg.build_preconditioner(ap, mu), orc.build_preconditioner(ao, mu)
+        reps = npcg.nystrom_pcg(op, w.b, mu, pre, eta=w.eta, relative=True)  # 4 RHS share each pass over A
+        for j, rp in enumerate(reps):
+            ro = orc.nystrom_pcg(oop, w.b[:, j], mu, opre, eta=w.eta, relative=True)
+            compare_solve(rp, ro)
