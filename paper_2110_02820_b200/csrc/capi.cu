@@ -693,10 +693,37 @@ int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, 
   return rc;
 }
 
-int npcg_block_pcg(npcg_op*, npcg_pre*, double, int64_t, const double*, int64_t, const npcg_solve_opts*, double*,
-                   int64_t, npcg_block_report*, int*, int64_t*, double*, int) {
-  g_err = "block_nystrom_pcg: not available in this build";
-  return NPCG_ERUNTIME;
+int npcg_block_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, int64_t ldb,
+                   const npcg_solve_opts* opts, double* x, int64_t ldx, npcg_block_report* rep, int* converged,
+                   int64_t* deflated, double* final_residual, int where) {
+  return guard([&] {
+    need(op, "npcg_block_pcg");
+    need(opts, "npcg_block_pcg options");
+    Ctx& c = C(op->ctx);
+    const i64 n = op->op->n;
+    // solvers.cpp:156-165
+    if (s < 1) invalid("block_nystrom_pcg: need at least one column");
+    if (s > 8) invalid("block_nystrom_pcg: at most 8 right-hand sides per block in this build");
+    if (!(opts->eta > 0.0)) invalid("block_nystrom_pcg: eta must be > 0");
+    if (!(mu >= 0.0)) invalid("block_nystrom_pcg: mu must be >= 0");
+    if (pre && pre->p.ell > 0 && pre->p.n != n) invalid("block_nystrom_pcg: preconditioner dimension mismatch");
+    View B = view_in(c, b, n, s, ldb, where);
+    DMat X;
+    X.alloc(n, s, c.stream, false);
+    PcgOptions po{opts->eta, opts->max_iter, opts->relative != 0, false};
+    BlockPcgResult r = block_pcg_solve(c, *op->op, pre ? &pre->p : nullptr, mu, s, B.p, B.ld, po, X.p(), X.ld);
+    download(c, X.p(), X.ld, n, s, x, ldx, where);
+    rep->iterations = r.iterations;
+    rep->fallback_count = r.fallback_count;
+    rep->n_deflated = static_cast<int64_t>(r.deflated.size());
+    rep->eta_used = r.eta_used;
+    rep->wall_time = r.wall_time;
+    for (i64 j = 0; j < s; ++j) {
+      converged[j] = r.converged[static_cast<size_t>(j)] ? 1 : 0;
+      final_residual[j] = r.history[static_cast<size_t>(j)].back();
+    }
+    for (size_t i = 0; i < r.deflated.size(); ++i) deflated[i] = r.deflated[i];
+  });
 }
 
 int npcg_iteration_bound(double kappa, double epsilon, int64_t* out) {

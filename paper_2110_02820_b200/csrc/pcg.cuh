@@ -39,4 +39,18 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
                     i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, double* iterates,
                     const char* context = "nystrom_pcg");
 
+struct BlockPcgResult {
+  i64 iterations = 0;
+  i64 fallback_count = 0;
+  std::vector<i64> deflated;
+  std::vector<bool> converged;
+  std::vector<std::vector<double>> history;
+  double eta_used = 0.0;
+  double wall_time = 0.0;
+};
+
+/// block_nystrom_pcg (solvers.cpp:150-279) on device; B, X device n x s (s <= 8).
+BlockPcgResult block_pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 s, const double* B, i64 ldb,
+                               const PcgOptions& opt, double* X, i64 ldx);
+
 }  // namespace npcg
