@@ -222,10 +222,18 @@ ALGO_NOTE = {
 def roofline_from_profile(prof, peaks, dgemm_peak, ncu_traffic):
     """Dominant kernel by total device time; achieved = its algorithmic
     work / its summed launch time."""
-    named = {k.split("<")[0].split("(")[0].strip(): v for k, v in prof.items()}
+    def clean(k):
+        k = k.strip().lstrip("(")
+        base = k.split("<")[0].split("[")[0].strip()
+        return base + (k[k.index("["):] if "[" in k else "")
+
+    def family(k):
+        return k.split("[")[0]
+
+    named = {clean(k): v for k, v in prof.items()}
     total = sum(v[1] for v in named.values())
     name, (cnt, ms, flops, byts) = max(named.items(), key=lambda kv: kv[1][1])
-    bound, note = ALGO_NOTE.get(name, ("hbm", "bytes per launch"))
+    bound, note = ALGO_NOTE.get(family(name), ("hbm", "bytes per launch"))
     if bound == "tensor":
         achieved = flops / (ms / 1e3) / 1e12
         peak, unit, src = dgemm_peak, "TFLOP/s", "measured cuBLAS DGEMM 8192^3 on this GPU (this run)"
@@ -239,9 +247,10 @@ def roofline_from_profile(prof, peaks, dgemm_peak, ncu_traffic):
             "frac": achieved / peak if peak else None, "traffic": traffic, "launches": cnt,
             "share_of_step": ms / total if total else None, "peak_source": src, "work_per_launch": note,
             "kernels": {k: {"launches": v[0], "ms": round(v[1], 4),
-                            "achieved": (v[2] / (v[1] / 1e3) / 1e12 if ALGO_NOTE.get(k, ("hbm",))[0] == "tensor"
-                                         else v[3] / (v[1] / 1e3) / 1e9) if v[1] > 0 else None}
-                        for k, v in sorted(named.items(), key=lambda kv: -kv[1][1])[:8]}}
+                            "achieved": ((v[2] / (v[1] / 1e3) / 1e12 if ALGO_NOTE.get(family(k), ("hbm",))[0] == "tensor"
+                                          else v[3] / (v[1] / 1e3) / 1e9) if v[1] > 0 and (v[2] or v[3]) else None),
+                            "unit": "TFLOP/s" if ALGO_NOTE.get(family(k), ("hbm",))[0] == "tensor" else "GB/s"}
+                        for k, v in sorted(named.items(), key=lambda kv: -kv[1][1])[:10]}}
 
 
 def cpu_baseline(w, steps=1):

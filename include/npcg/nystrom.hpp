@@ -1,0 +1,94 @@
+// reference: nystrom.hpp:19-89 — randomized Nyström approximation. The sketch
+// pair and the factored approximation are device-resident (npcg_nys); u and
+// lambda are mirrored to the host on construction as in the reference struct.
+#pragma once
+
+#include <memory>
+
+#include "operators.hpp"
+
+namespace npcg {
+
+struct NystromApproximation {  // nystrom.hpp:19-33
+  Matrix u;        // n-by-ell, orthonormal columns
+  Vector lambda;   // nonincreasing, >= 0
+  double shift_used = 0.0;
+  std::shared_ptr<npcg_nys> device;  // factored approximation on the B200
+
+  Index dim() const { return u.rows(); }
+  Index size() const { return u.cols(); }
+  Index rank() const {
+    Index r = 0;
+    for (Index i = 0; i < lambda.size(); ++i) r += lambda(i) > 0.0;
+    return r;
+  }
+  double lambda_min() const { return lambda.size() == 0 ? 0.0 : lambda(lambda.size() - 1); }
+};
+
+/// Cached test matrix and sketch (nystrom.hpp:42-48), on device and grown in place.
+struct SketchPair {
+  std::shared_ptr<npcg_nys> device;
+  Index n = 0;
+  Index size() const {
+    std::int64_t cols = 0;
+    if (device) check_status(npcg_nys_info(device.get(), nullptr, &cols, nullptr, nullptr));
+    return cols;
+  }
+  Index dim() const { return n; }
+};
+
+namespace detail {
+inline std::shared_ptr<npcg_nys> own(npcg_nys* h) {
+  return std::shared_ptr<npcg_nys>(h, [](npcg_nys* p) { npcg_nys_destroy(p); });
+}
+inline NystromApproximation fetch(const std::shared_ptr<npcg_nys>& nys) {
+  std::int64_t n = 0, size = 0, ell = 0;
+  double shift = 0.0;
+  check_status(npcg_nys_info(nys.get(), &n, &size, &ell, &shift));
+  NystromApproximation a;
+  a.u = Matrix(n, ell);
+  a.lambda = Vector(ell);
+  a.shift_used = shift;
+  check_status(npcg_nys_get(nys.get(), a.lambda.data(), ell ? a.u.data() : nullptr, std::max<std::int64_t>(n, 1),
+                            NPCG_HOST));
+  a.device = nys;
+  return a;
+}
+}  // namespace detail
+
+/// make_empty_sketch (nystrom.cpp:28-34), bound to its operator on device.
+inline SketchPair make_empty_sketch(const LinearOperator& op) {
+  npcg_nys* h = nullptr;
+  check_status(npcg_nys_create(device_handle(op), &h));
+  return SketchPair{detail::own(h), op.dim()};
+}
+
+/// extend_sketch (nystrom.cpp:36-58): draws the n x extra Gaussian from rng in
+/// the reference's stream order; Gram-Schmidt, QR and Y = A Omega on device.
+inline SketchPair extend_sketch(const SketchPair& pair, const LinearOperator& op, Index extra, Rng& rng) {
+  if (pair.dim() != op.dim()) throw std::invalid_argument("extend_sketch: dimension mismatch");
+  check_status(npcg_nys_extend_rng(pair.device.get(), extra, rng.handle()));
+  return pair;
+}
+
+/// nystrom_from_sketch (nystrom.cpp:96-140).
+inline NystromApproximation nystrom_from_sketch(const SketchPair& pair) {
+  check_status(npcg_nys_factor(pair.device.get()));
+  return detail::fetch(pair.device);
+}
+
+/// randomized_nystrom (nystrom.cpp:142-148).
+inline NystromApproximation randomized_nystrom(const LinearOperator& op, Index ell, Rng& rng) {
+  if (ell < 1 || ell > op.dim()) throw std::invalid_argument("randomized_nystrom: need 1 <= ell <= dim");
+  return nystrom_from_sketch(extend_sketch(make_empty_sketch(op), op, ell, rng));
+}
+
+/// An approximation given by its factors (e.g. read from disk) placed on device.
+inline NystromApproximation make_approximation(const Matrix& u, const Vector& lambda, double shift_used = 0.0) {
+  npcg_nys* h = nullptr;
+  check_status(npcg_nys_from_factors(default_context(), u.rows(), lambda.size(), u.data(),
+                                     std::max<Index>(u.rows(), 1), lambda.data(), shift_used, NPCG_HOST, &h));
+  return detail::fetch(detail::own(h));
+}
+
+}  // namespace npcg

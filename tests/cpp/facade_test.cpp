@@ -1,0 +1,109 @@
+// Drop-in check of the C++ facade (include/npcg/*.hpp): reference-style calls
+// (names, signatures, exception types of /root/reference/proj/core) running
+// on the B200 through libnpcg_b200.so. Mirrors cases of the reference's
+// operators/preconditioner/solvers/nystrom tests. Exit code 0 = all passed.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+
+#include "npcg/npcg.hpp"
+
+using namespace npcg;
+
+static int failures = 0;
+#define CHECK(cond)                                                   \
+  do {                                                                \
+    if (!(cond)) {                                                    \
+      std::fprintf(stderr, "FAILED %s:%d  %s\n", __FILE__, __LINE__, #cond); \
+      ++failures;                                                     \
+    }                                                                 \
+  } while (0)
+
+int main() {
+  // operators_test.cpp:55-62 — dense matvec on a 2x2 example
+  Matrix a(2, 2);
+  a(0, 0) = 2; a(0, 1) = 1; a(1, 0) = 1; a(1, 1) = 2;
+  const DenseOperator op(a);
+  const Vector y = op.matvec(Vector{1.0, 0.0});
+  CHECK(y(0) == 2.0 && y(1) == 1.0);
+  CHECK(op.has_column_access());
+  const Vector c1 = op.column(1);
+  CHECK(c1(0) == 1.0 && c1(1) == 2.0);
+  // operators_test.cpp:64-70 — dimension / finiteness contract
+  bool threw = false;
+  try { op.matvec(Vector{1.0, 2.0, 3.0}); } catch (const std::invalid_argument&) { threw = true; }
+  CHECK(threw);
+  // preconditioner_test.cpp:80-86 — U = [e1 e2], Lambda = (4, 2), mu = 1: (5,3,7) -> (3,3,7)
+  Matrix u(3, 2);
+  u(0, 0) = 1; u(1, 1) = 1;
+  const NystromApproximation basis = make_approximation(u, Vector{4.0, 2.0}, 1e-16);
+  const NystromPreconditioner p = build_preconditioner(basis, 1.0);
+  const Vector z = p.apply_inverse(Vector{5.0, 3.0, 7.0});
+  CHECK(std::abs(z(0) - 3.0) < 1e-14 && std::abs(z(1) - 3.0) < 1e-14 && std::abs(z(2) - 7.0) < 1e-14);
+  threw = false;
+  try { build_preconditioner(basis, 0.0); } catch (const std::invalid_argument&) { threw = true; }
+  CHECK(threw);
+  // nystrom_test.cpp:12-20 — zero matrix gives exactly zero eigenvalues
+  {
+    const DenseOperator zero(Matrix::Zero(10, 10));
+    Rng rng(1);
+    const NystromApproximation ap = randomized_nystrom(zero, 3, rng);
+    CHECK(ap.lambda.size() == 3);
+    for (Index i = 0; i < 3; ++i) CHECK(ap.lambda(i) == 0.0);
+  }
+  // solvers_test.cpp:112-127 — known solution through Nyström PCG
+  {
+    const Index n = 60;
+    Vector lam(n);
+    for (Index j = 0; j < n; ++j) lam(j) = std::pow(j + 1.0, -2.0);
+    const DenseOperator A = synthesize_operator(SpectrumProfile(lam), 5);
+    Rng rng(5);
+    const Vector star = gaussian_vector(rng, n);
+    const double mu = 0.01;
+    Vector b = A.matvec(star);
+    for (Index i = 0; i < n; ++i) b(i) += mu * star(i);
+    const NystromApproximation ap = randomized_nystrom(A, 10, rng);
+    const NystromPreconditioner pre = build_preconditioner(ap, mu);
+    SolveOptions opt;
+    opt.relative = true;
+    const SolveReport rep = nystrom_pcg(A, b, mu, pre, opt);
+    double err = 0.0, nrm = 0.0;
+    for (Index i = 0; i < n; ++i) {
+      err += (rep.x(i) - star(i)) * (rep.x(i) - star(i));
+      nrm += star(i) * star(i);
+    }
+    CHECK(rep.converged);
+    CHECK(std::sqrt(err / nrm) < 1e-8);
+    CHECK(rep.matvec_count == rep.iterations + 1);
+    threw = false;
+    try { nystrom_pcg(A, b, 0.2, pre, opt); } catch (const std::invalid_argument&) { threw = true; }
+    CHECK(threw);
+    // adaptive_test.cpp:220-226
+    CHECK(posterior_condition_estimate(1.0, 1.0, 2.0) == 4.0);
+    AdaptiveConfig cfg;
+    cfg.ell0 = 4;
+    cfg.ell_max = 32;
+    cfg.mu = mu;
+    cfg.tau = 10.0;
+    Rng r2(7);
+    const AdaptiveOutcome out = adaptive_nystrom(A, cfg, r2);
+    CHECK(out.ell_final >= 4 && out.ell_final <= 32);
+    CHECK(out.error_estimate.has_value());
+  }
+  // solvers_test.cpp:76-90 — breakdown raises SolveDivergenceError with its report
+  {
+    Matrix ind = Matrix::Identity(2, 2);
+    ind(1, 1) = -1.0;
+    const DenseOperator bad(ind);
+    threw = false;
+    try {
+      cg(bad, 0.0, Vector{1.0, 1.0});
+    } catch (const SolveDivergenceError& e) {
+      threw = e.report.iterations == 1 && !e.report.converged;
+    }
+    CHECK(threw);
+  }
+  CHECK(iteration_bound(56.0, 1e-6) == 54);
+  if (failures == 0) std::printf("facade ok\n");
+  return failures == 0 ? 0 : 1;
+}
