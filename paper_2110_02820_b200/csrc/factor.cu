@@ -7,9 +7,10 @@
 // flop of nystrom_from_sketch runs on the FP64 tensor pipe.
 //
 // SVD of the tall B: CholeskyQR2 (B = Q R, Gram matrices on DMMA, shifted
-// CholeskyQR3 when the Gram Cholesky breaks down), then a one-sided Jacobi
-// SVD of the l x l R^T in one cooperative kernel (round-robin pairs, one
-// warp per pair, grid-wide barrier between rounds), then U = Q V on DMMA.
+// CholeskyQR3 when the Gram Cholesky breaks down; a re-orthogonalisation pass
+// is skipped when Q^T Q is already I to 1e-14), then the SVD of the l x l R^T
+// (small_svd_eig: tridiagonal eigenvectors of R R^T + Jacobi refinement, or a
+// one-CTA one-sided Jacobi for l <= 110), then U = Q V on DMMA.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -129,6 +130,20 @@ __global__ void refine_angles_kernel(const double* G, i64 ldg, i64 n, double* C,
     const double rel = gjj > 0.0 ? err / gjj : (err > 0.0 ? 1.0 : 0.0);
     atomicMax(reinterpret_cast<unsigned long long*>(qual), static_cast<unsigned long long>(__double_as_longlong(rel)));
   }
+}
+
+__global__ void identity_dev_kernel(const double* G, i64 ldg, i64 n, double* out) {
+  const i64 total = n * n;
+  double m = 0.0;
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = idx % n, j = idx / n;
+    const double d = fabs(G[i + j * ldg] - (i == j ? 1.0 : 0.0));
+    m = isnan(d) ? 1e308 : fmax(m, d);
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(out), static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
 __global__ void add_diag_kernel(double* a, i64 n, i64 lda, double s) {
@@ -419,37 +434,63 @@ void orthonormalize(Ctx& ctx, const double* G_in, i64 ldg_in, i64 m, i64 n, doub
   DMat work;
   work.alloc(m, n, ctx.stream, false);
   copy2d(ctx, m, n, G, ldg, work.p(), work.ld);
-  DMat L1, L2, L3;
-  int passes = 2;
-  if (!cholqr_pass(ctx, work.p(), work.ld, m, n, 0.0, L1, Q, ldq)) {
+  std::vector<DMat> Ls(1);
+  bool shifted = false;
+  if (!cholqr_pass(ctx, work.p(), work.ld, m, n, 0.0, Ls[0], Q, ldq)) {
     // Shifted CholeskyQR (Fukaya et al.): s = 11 (m n + n(n+1)) u ||G||_F^2.
     const double fro2 = sum_squares(ctx, G, m, n, ldg);
     const double s = 11.0 * (static_cast<double>(m) * n + static_cast<double>(n) * (n + 1)) * 2.220446049250313e-16 * fro2;
     copy2d(ctx, m, n, G, ldg, work.p(), work.ld);
-    if (!cholqr_pass(ctx, work.p(), work.ld, m, n, s, L1, Q, ldq))
+    if (!cholqr_pass(ctx, work.p(), work.ld, m, n, s, Ls[0], Q, ldq))
       fail(NPCG_ERUNTIME, "orthonormal_columns: shifted CholeskyQR broke down (rank-deficient input)");
-    passes = 3;
+    shifted = true;
   }
-  // second (and third) pass on Q
-  copy2d(ctx, m, n, Q, ldq, work.p(), work.ld);
-  if (!cholqr_pass(ctx, work.p(), work.ld, m, n, 0.0, L2, Q, ldq))
-    fail(NPCG_ERUNTIME, "orthonormal_columns: CholeskyQR2 second pass broke down");
-  if (passes == 3) {
+  // Further passes on Q (CholeskyQR2 / shifted CholeskyQR3). The Gram Q^T Q of
+  // the next pass is formed first; when Q is already orthonormal to working
+  // accuracy (well-conditioned input, e.g. a Gaussian Omega) the pass is skipped.
+  for (int more = 0; more < (shifted ? 2 : 1); ++more) {
+    DMat L;
+    L.alloc(n, n, ctx.stream, false);
+    gemm(ctx, n, n, m, 1.0, Operand{Q, ldq, true}, Operand{Q, ldq, true}, 0.0, L.p(), L.ld);
+    if (!shifted || more > 0) {
+      if (identity_deviation(ctx, L.p(), L.ld, n) <= 1e-14) break;
+    }
+    CholFactor f;
+    if (!cholesky(ctx, L.p(), n, L.ld, f))
+      fail(NPCG_ERUNTIME, "orthonormal_columns: CholeskyQR re-orthogonalisation pass broke down");
     copy2d(ctx, m, n, Q, ldq, work.p(), work.ld);
-    if (!cholqr_pass(ctx, work.p(), work.ld, m, n, 0.0, L3, Q, ldq))
-      fail(NPCG_ERUNTIME, "orthonormal_columns: CholeskyQR3 third pass broke down");
+    trsm_right_lt(ctx, m, n, work.p(), work.ld, L.p(), L.ld, f, Q, ldq);
+    Ls.push_back(std::move(L));
   }
   if (Rt) {  // R^T = L1 L2 (L3)
-    if (passes == 2) {
-      gemm(ctx, n, n, n, 1.0, Operand{L1.p(), L1.ld, false}, Operand{L2.p(), L2.ld, true}, 0.0, Rt, ldr);
+    if (Ls.size() == 1) {
+      copy2d(ctx, n, n, Ls[0].p(), Ls[0].ld, Rt, ldr);
     } else {
-      DMat t;
-      t.alloc(n, n, ctx.stream, false);
-      gemm(ctx, n, n, n, 1.0, Operand{L1.p(), L1.ld, false}, Operand{L2.p(), L2.ld, true}, 0.0, t.p(), t.ld);
-      gemm(ctx, n, n, n, 1.0, Operand{t.p(), t.ld, false}, Operand{L3.p(), L3.ld, true}, 0.0, Rt, ldr);
+      DMat acc, t;
+      acc.alloc(n, n, ctx.stream, false);
+      copy2d(ctx, n, n, Ls[0].p(), Ls[0].ld, acc.p(), acc.ld);
+      for (size_t k = 1; k < Ls.size(); ++k) {
+        double* dst = k + 1 == Ls.size() ? Rt : nullptr;
+        if (!dst) t.alloc(n, n, ctx.stream, false);
+        gemm(ctx, n, n, n, 1.0, Operand{acc.p(), acc.ld, false}, Operand{Ls[k].p(), Ls[k].ld, true}, 0.0,
+             dst ? dst : t.p(), dst ? ldr : t.ld);
+        if (!dst) std::swap(acc, t);
+      }
     }
     if (e2 != 0) scale_pow2(ctx, n, n, Rt, ldr, e2);
   }
+}
+
+// max |G_ij - delta_ij| (synchronises).
+double identity_deviation(Ctx& ctx, const double* G, i64 ldg, i64 n) {
+  DBuf<double> out(1, ctx.stream);
+  out.zero();
+  NPCG_LAUNCH(ctx, identity_dev_kernel, static_cast<unsigned>(std::min<i64>(cdiv(n * n, 256), 1024)), 256, 0, G, ldg,
+              n, out.p);
+  double h = 0.0;
+  NPCG_CUDA(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  return h;
 }
 
 void jacobi_svd_small(Ctx& ctx, double* W, i64 ldw, i64 n, double* Vs, i64 ldv, double* sigma) {

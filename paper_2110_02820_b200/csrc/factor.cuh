@@ -34,6 +34,9 @@ void trsm_right_lt(Ctx& ctx, i64 m, i64 n, double* Y, i64 ldy, const double* L, 
 void orthonormalize(Ctx& ctx, const double* G, i64 ldg, i64 m, i64 n, double* Q, i64 ldq,
                     double* R = nullptr, i64 ldr = 0);
 
+/// max_ij |G_ij - delta_ij| of an n x n matrix (synchronises the stream).
+double identity_deviation(Ctx& ctx, const double* G, i64 ldg, i64 n);
+
 /// orthonormalize() that reports a CholeskyQR breakdown instead of throwing.
 bool try_orthonormalize(Ctx& ctx, const double* G, i64 ldg, i64 m, i64 n, double* Q, i64 ldq);
 

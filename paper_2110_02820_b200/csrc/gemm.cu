@@ -1,17 +1,19 @@
 // FP64 GEMM on the B200 tensor pipe (DMMA) fed by TMA — see gemm.cuh.
 //
-// CTA tile 128x128x16, 5-stage smem ring (32 KB/stage), warp-specialised:
-// warp 8 (one elected lane) issues cp.async.bulk.tensor loads with
-// 128-byte swizzle and arms the stage's mbarrier with expect_tx; warps 0-7
-// each own a 64x32 accumulator block (8x4 m8n8 fragments, 64 FP64 regs) and
-// issue mma.sync.m8n8k4.f64. Fragment reads are 16-byte LDS that hit all 32
-// banks once per 128 B (the swizzle + a k-pair / m-pair register mapping
-// makes every fragment load conflict-free for both K-major and M-major
-// operands, so all four transpose combinations run at the same speed).
-// Small output grids split K across CTAs; partials are summed in fixed order.
+// CTA tiles 128x128 (8 consumer warps, 64x32 each) or 128x80 (10 warps,
+// 64x16 each; N = 400 = 5 x 80 runs without padding), BK = 16, 5-stage smem
+// ring, warp-specialised: the last warp (one elected lane) issues
+// cp.async.bulk.tensor loads with 128-byte swizzle and arms the stage's
+// mbarrier with expect_tx; the consumer warps issue mma.sync.m8n8k4.f64.
+// Fragment reads are 16-byte LDS that hit all 32 banks once per 128 B (the
+// swizzle + a k-pair / m-pair register mapping makes every fragment load
+// conflict-free for both K-major and M-major operands, so all four transpose
+// combinations run at the same speed). A wave model picks the tile and the
+// split-K count per shape; split partials are summed in fixed order.
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -19,12 +21,26 @@
 namespace npcg {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 5, NCW = 8;
-constexpr int THREADS = (NCW + 1) * 32;
-constexpr int A_BYTES = BM * BK * 8;
-constexpr int B_BYTES = BN * BK * 8;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+constexpr int BK = 16, STAGES = 5;
+
+// CTA tile BM x BN with WM x WN consumer warps (warp tile TM x TN of m8n8
+// fragments) plus one TMA producer warp.
+template <int BM_, int BN_, int WM_, int WN_>
+struct Tile {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_;
+  static constexpr int NCW = WM * WN;
+  // Whole consumer warpgroups: the producer gets its own warpgroup and hands
+  // its registers to the consumers (setmaxnreg); otherwise a single producer warp.
+  static constexpr bool WG = NCW % 4 == 0;
+  static constexpr int THREADS = (NCW + (WG ? 4 : 1)) * 32;
+  static constexpr int TM = BM / WM, TN = BN / WN, FM = TM / 8, FN = TN / 8;
+  static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8, STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+  static_assert(TM % 16 == 0 && TN % 16 == 0, "warp tile must hold m/n pairs of fragments");
+  static_assert(STAGE_BYTES % 1024 == 0 && A_BYTES % 1024 == 0, "128B-swizzle atoms need 1 KB alignment");
+};
+using TileWide = Tile<128, 128, 2, 4>;    // 64 x 32 warp tiles
+using TileNarrow = Tile<128, 80, 2, 5>;   // 64 x 16 warp tiles; N = 80 k (e.g. l = 400) without padding
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -66,13 +82,18 @@ __device__ __forceinline__ double2 lds128(const uint8_t* p) {
   return *reinterpret_cast<const double2*>(p);
 }
 
-template <bool AK, bool BKM>
-__global__ void __launch_bounds__(THREADS, 1)
+template <class T, bool AK, bool BKM>
+__global__ void __launch_bounds__(T::THREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                      int M, int N, int ktiles, int ktiles_per_split, double alpha, double beta,
                      double* __restrict__ C, i64 ldc, double* __restrict__ partial) {
+  constexpr int BM = T::BM, BN = T::BN, NCW = T::NCW, TM = T::TM, TN = T::TN, FM = T::FM, FN = T::FN;
+  constexpr int A_BYTES = T::A_BYTES, STAGE_BYTES = T::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB-aligned ring; offsetting smem_raw (not casting through an integer)
+  // keeps the pointer in the shared window, so fragment reads compile to LDS
+  // (generic loads are not ordered before the mbarrier arrive that frees a stage).
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -89,8 +110,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
 
-  if (warp == NCW) {  // ---- TMA producer
-    if (lane == 0) {
+  if (warp >= NCW) {  // ---- TMA producer
+    if constexpr (T::WG) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == NCW && lane == 0) {
       for (int i = 0; i < nk; ++i) {
         const int s = i % STAGES, r = i / STAGES;
         if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
@@ -115,14 +137,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     return;
   }
 
-  // ---- DMMA consumers: warp (wm, wn) owns rows wm*64.., cols wn*32..
-  const int wm = warp >> 2, wn = warp & 3;
+  // ---- DMMA consumers: warp (wm, wn) owns rows wm*TM.., cols wn*TN..
+  if constexpr (T::WG) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+  const int wm = warp / T::WN, wn = warp % T::WN;
   const int g = lane >> 2, t = lane & 3;
-  double acc[8][4][2];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   for (int i = 0; i < nk; ++i) {
     const int s = i % STAGES, r = i / STAGES;
@@ -131,11 +154,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint8_t* Bs = As + A_BYTES;
 #pragma unroll
     for (int kc = 0; kc < 2; ++kc) {
-      double a[8][2], b[4][2];
+      double a[FM][2], b[FN][2];
       if (AK) {  // [m][16 k] rows of 128 B; k-pair (2t, 2t+1) -> steps 0/1
 #pragma unroll
-        for (int f = 0; f < 8; ++f) {
-          const int m = wm * 64 + f * 8 + g;
+        for (int f = 0; f < FM; ++f) {
+          const int m = wm * TM + f * 8 + g;
           const double2 v = lds128(As + m * 128 + (((kc * 4 + t) ^ g) << 4));
           a[f][0] = v.x;
           a[f][1] = v.y;
@@ -145,8 +168,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int ss = 0; ss < 2; ++ss) {
           const int k = kc * 8 + 2 * t + ss;  // same k <-> (lane, step) map as the K-major path
 #pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            const double2 v = lds128(As + (wm * 4 + p) * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
+          for (int p = 0; p < FM / 2; ++p) {
+            const double2 v = lds128(As + (wm * (TM / 16) + p) * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
             a[2 * p][ss] = v.x;
             a[2 * p + 1][ss] = v.y;
           }
@@ -154,8 +177,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (BKM) {
 #pragma unroll
-        for (int f = 0; f < 4; ++f) {
-          const int n = wn * 32 + f * 8 + g;
+        for (int f = 0; f < FN; ++f) {
+          const int n = wn * TN + f * 8 + g;
           const double2 v = lds128(Bs + n * 128 + (((kc * 4 + t) ^ g) << 4));
           b[f][0] = v.x;
           b[f][1] = v.y;
@@ -165,8 +188,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int ss = 0; ss < 2; ++ss) {
           const int k = kc * 8 + 2 * t + ss;
 #pragma unroll
-          for (int p = 0; p < 2; ++p) {
-            const double2 v = lds128(Bs + (wn * 2 + p) * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
+          for (int p = 0; p < FN / 2; ++p) {
+            const double2 v = lds128(Bs + (wn * (TN / 16) + p) * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
             b[2 * p][ss] = v.x;
             b[2 * p + 1][ss] = v.y;
           }
@@ -175,9 +198,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int ss = 0; ss < 2; ++ss)
 #pragma unroll
-        for (int f = 0; f < 8; ++f)
+        for (int f = 0; f < FM; ++f)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma(acc[f][j][0], acc[f][j][1], a[f][ss], b[j][ss]);
+          for (int j = 0; j < FN; ++j) dmma(acc[f][j][0], acc[f][j][1], a[f][ss], b[j][ss]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -185,16 +208,16 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   // ---- epilogue
 #pragma unroll
-  for (int f = 0; f < 8; ++f) {
-    const int row = AK ? wm * 64 + f * 8 + g : wm * 64 + (f >> 1) * 16 + 2 * g + (f & 1);
+  for (int f = 0; f < FM; ++f) {
+    const int row = AK ? wm * TM + f * 8 + g : wm * TM + (f >> 1) * 16 + 2 * g + (f & 1);
     const int gm = m0 + row;
     if (gm >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < FN; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int x = 2 * t + e;
-        const int col = BKM ? wn * 32 + j * 8 + x : wn * 32 + (j >> 1) * 16 + 2 * x + (j & 1);
+        const int col = BKM ? wn * TN + j * 8 + x : wn * TN + (j >> 1) * 16 + 2 * x + (j & 1);
         const int gn = n0 + col;
         if (gn >= N) continue;
         if (partial) {
@@ -237,17 +260,69 @@ CUtensorMap make_map(Ctx& ctx, const double* p, i64 inner, i64 outer, i64 ld, in
   return m;
 }
 
-template <bool AK, bool BKM>
+template <class T, bool AK, bool BKM>
 void launch(Ctx& ctx, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int ktiles, int kps,
             int splits, double alpha, double beta, double* C, i64 ldc, double* partial) {
   static std::once_flag once;
   std::call_once(once, [] {
-    NPCG_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   SMEM_BYTES));
+    NPCG_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<T, AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   T::SMEM_BYTES));
   });
-  dim3 grid(static_cast<unsigned>(cdiv(M, BM)), static_cast<unsigned>(cdiv(N, BN)), static_cast<unsigned>(splits));
-  NPCG_LAUNCH(ctx, (gemm_dmma_kernel<AK, BKM>), grid, THREADS, SMEM_BYTES, ma, mb, M, N, ktiles, kps,
+  dim3 grid(static_cast<unsigned>(cdiv(M, T::BM)), static_cast<unsigned>(cdiv(N, T::BN)),
+            static_cast<unsigned>(splits));
+  NPCG_LAUNCH(ctx, (gemm_dmma_kernel<T, AK, BKM>), grid, T::THREADS, T::SMEM_BYTES, ma, mb, M, N, ktiles, kps,
               alpha, beta, C, ldc, partial);
+}
+
+// Tile shape + split-K count minimising a wave model of the launch: every CTA
+// of a wave runs kps k-tiles at the per-SM DMMA rate (narrow tiles a little
+// slower: less fragment reuse), plus a fixed pipeline fill / epilogue cost and,
+// when split, the fixed-order reduction of the partials through HBM.
+struct Plan {
+  bool narrow;
+  int splits, kps;
+};
+Plan plan_gemm(const Ctx& ctx, i64 M, i64 N, i64 K) {
+  const int ktiles = static_cast<int>(cdiv(K, BK));
+  const double sm_rate = 34e12 / 148.0;  // measured DMMA flop/s per SM
+  Plan best{false, 1, ktiles};
+  double best_us = 1e300;
+  for (int narrow = 0; narrow < 2; ++narrow) {
+    const int bm = narrow ? TileNarrow::BM : TileWide::BM, bn = narrow ? TileNarrow::BN : TileWide::BN;
+    const double eff = narrow ? 0.95 : 1.0;
+    const i64 tiles = cdiv(M, bm) * cdiv(N, bn);
+    const int max_split = std::max(1, std::min(64, ktiles / 4));
+    for (int s = 1; s <= max_split; ++s) {
+      const int kps = static_cast<int>(cdiv(ktiles, s));
+      const int se = static_cast<int>(cdiv(ktiles, kps));
+      if (se != s) continue;
+      const i64 waves = cdiv(tiles * se, ctx.sm_count);
+      double us = waves * (kps * 2.0 * bm * bn * BK / (sm_rate * eff) * 1e6 + 4.0);
+      if (se > 1) us += (se + 2.0) * M * N * 8.0 / 6e12 * 1e6 + 3.0;
+      if (us < best_us * 0.999) {
+        best_us = us;
+        best = Plan{narrow != 0, se, kps};
+      }
+    }
+  }
+  if (const char* f = std::getenv("NPCG_GEMM_FORCE")) {  // diagnostics: "<w|n>:<splits>"
+    const int s = std::max(1, std::min(ktiles, std::atoi(f + 2)));
+    best.narrow = f[0] == 'n';
+    best.kps = static_cast<int>(cdiv(ktiles, s));
+    best.splits = static_cast<int>(cdiv(ktiles, best.kps));
+  }
+  return best;
+}
+
+template <class T>
+void dispatch(Ctx& ctx, Operand A, Operand B, int m, int n, i64 K, int ktiles, int kps, int splits, double alpha,
+              double beta, double* C, i64 ldc, double* pp) {
+  const CUtensorMap ma = A.kmajor ? make_map(ctx, A.p, K, m, A.ld, T::BM) : make_map(ctx, A.p, m, K, A.ld, 16);
+  const CUtensorMap mb = B.kmajor ? make_map(ctx, B.p, K, n, B.ld, T::BN) : make_map(ctx, B.p, n, K, B.ld, 16);
+  if (A.kmajor && B.kmajor) launch<T, true, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  else if (A.kmajor) launch<T, true, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  else if (B.kmajor) launch<T, false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  else launch<T, false, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
 }
 
 }  // namespace
@@ -265,16 +340,9 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
                 beta, C, ldc);
     return;
   }
-  const CUtensorMap ma = A.kmajor ? make_map(ctx, A.p, K, M, A.ld, BM) : make_map(ctx, A.p, M, K, A.ld, 16);
-  const CUtensorMap mb = B.kmajor ? make_map(ctx, B.p, K, N, B.ld, BN) : make_map(ctx, B.p, N, K, B.ld, 16);
   const int ktiles = static_cast<int>(cdiv(K, BK));
-  const i64 tiles = cdiv(M, BM) * cdiv(N, BN);
-  int splits = 1;
-  if (tiles < ctx.sm_count && ktiles >= 16) {
-    splits = static_cast<int>(std::max<i64>(1, std::min<i64>(ctx.sm_count / tiles, ktiles / 8)));
-  }
-  const int kps = static_cast<int>(cdiv(ktiles, splits));
-  splits = static_cast<int>(cdiv(ktiles, kps));
+  const Plan plan = plan_gemm(ctx, M, N, K);
+  const int splits = plan.splits, kps = plan.kps;
   DBuf<double> part;
   double* pp = nullptr;
   if (splits > 1) {
@@ -282,10 +350,8 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
     pp = part.p;
   }
   const int m = static_cast<int>(M), n = static_cast<int>(N);
-  if (A.kmajor && B.kmajor) launch<true, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-  else if (A.kmajor) launch<true, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-  else if (B.kmajor) launch<false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-  else launch<false, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  if (plan.narrow) dispatch<TileNarrow>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  else dispatch<TileWide>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp);
   ctx.prof_work(2.0 * static_cast<double>(M) * N * K, 8.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N +
                                                               static_cast<double>(M) * N));
   if (ctx.prof) {

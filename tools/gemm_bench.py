@@ -25,7 +25,7 @@ def run(m, n, k, ak, bk, reps=5):
         best = min(best, s.elapsed_time(e) / 1e3)
     return 2 * m * n * k / best / 1e12
 out = {}
-for (m, n, k) in [(8192, 8192, 8192), (20000, 400, 4000), (4000, 400, 20000), (50000, 1000, 50000), (4000, 400, 400), (400, 400, 4000)]:
+for (m, n, k) in [(8192, 8192, 8192), (20000, 400, 4000), (4000, 400, 20000), (50000, 1000, 50000), (4000, 400, 400), (400, 400, 4000), (20000, 400, 400), (400, 400, 20000), (20000, 64, 64), (336, 336, 64)]:
     for ak, bk in [(1, 1), (0, 1), (1, 0), (0, 0)]:
         if m * k > 3e9: 
             if (ak, bk) != (1, 1): continue
