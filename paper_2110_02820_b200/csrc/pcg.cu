@@ -12,7 +12,10 @@
 // snapshot of the status shows every column finished; iterations enqueued
 // after that early-exit on a device flag (the matvec/preconditioner kernels
 // read it first), so overshoot costs only empty launches.
+#include <cooperative_groups.h>
+
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <sstream>
@@ -216,6 +219,383 @@ __global__ void snapshot_running_kernel(const State* __restrict__ st, int S, int
   if (s < S) flags[s] = st->c[s].status == 0 ? 1 : 0;
 }
 
+// ============================================================================
+// Persistent PCG loop: one cooperative launch runs every iteration, one CTA
+// per SM, grid-wide barriers between the phases of an iteration. Every CTA
+// keeps an identical copy of the column states: the scalars (p.v, ||r||^2,
+// r.z) are reduced from per-CTA partials in the same fixed order by every
+// CTA, so all CTAs take the same branch (converged / breakdown / max_iter)
+// without a broadcast. The loop stops on the device when no column runs.
+//
+// Iteration t (vector slices: CTA c owns entries [c*slice, (c+1)*slice)):
+//   P1  p_t = z + beta p_{t-1} (ping-pong buffers; each CTA recomputes what
+//       it needs, the slice owner stores it); v = A p_t:
+//         gram:  CTA c streams its rows of X once: partial_c = X_c^T (X_c p)
+//         dense: CTA c computes (A p)_j for the columns j of its slice
+//   P2  gram: v_j = (sum_c partial_c)_j / m + mu p_j for the slice (fixed
+//       order over c); partial p.v of the slice                  | barrier
+//   P3  alpha = rz / p.v; x += alpha p, r -= alpha v; partial ||r||^2 | barrier
+//   P4  ||r|| -> history / status; identity P: beta = ||r||^2 / rz
+//       Nystrom P: t = gain * (U^T r) for CTA c's columns of U   | barrier
+//   P5  z = r + U t for the slice; partial r.z                   | barrier
+//       beta = r.z / rz (next iteration's P1)
+// ============================================================================
+constexpr int PT = 512;  // threads per CTA
+constexpr int PV = 4;    // double2 slots per thread in the gram row pass: n <= 2*PT*PV
+constexpr int PW = 2 * PT * PV;
+
+struct PersistArgs {
+  i64 n, m;
+  const double* A;
+  i64 lda;  // gram: X row-major (row a at A + a*lda); dense: n x n col-major
+  double mu, div;
+  const double* U;
+  i64 ldu, ell;
+  const double* gain;
+  double* X;
+  i64 ldx;
+  double *R, *Z, *P0, *P1, *V;
+  i64 ldw;
+  double* T;
+  double* part;                       // gram: G x PW
+  double *pv_part, *rr_part, *rz_part;  // G x S
+  State* st;
+  double* hist;
+  i64 hstride, max_iter, rows_per_cta, slice, uslice;
+};
+
+template <int S, bool GRAM>
+__global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[32];
+  __shared__ double red[2][PT / 32];
+  __shared__ double zred[PT / 32][32];
+  __shared__ ColState cs[S];
+  __shared__ int running_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, c = blockIdx.x;
+  const i64 n = a.n;
+  const i64 r0 = min(n, static_cast<i64>(c) * a.slice), r1 = min(n, r0 + a.slice);
+  const bool nys = a.ell > 0;
+  const double* zsrc = nys ? a.Z : a.R;
+
+  if (tid < S) cs[tid] = a.st->c[tid];
+  __syncthreads();
+  auto count_running = [&]() {
+    int k = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) k += cs[s].status == 0;
+    return k;
+  };
+  // sum over CTAs of part[b*S + s] in fixed order (identical in every CTA)
+  auto all_sum = [&](const double* part, int s) {
+    double v = 0.0;
+    for (int b = tid; b < G; b += PT) v += part[b * S + s];
+    return block_sum(v, sh);
+  };
+
+  if (count_running() > 0) {
+    for (i64 t = 1; t <= a.max_iter; ++t) {
+      const double* pold = (t & 1) ? a.P1 : a.P0;  // p_{t-1} (unused at t = 1)
+      double* pcur = (t & 1) ? a.P0 : a.P1;         // p_t
+      const bool first = t == 1;
+      // p_t entry (i, s): z + beta p_{t-1} for running columns, else unchanged
+      auto p_at = [&](i64 i, int s) -> double {
+        if (first) return pcur[i + s * a.ldw];
+        const double po = pold[i + s * a.ldw];
+        return cs[s].status == 0 ? zsrc[i + s * a.ldw] + cs[s].beta * po : po;
+      };
+      // ---- P1
+      if (!first)
+        for (i64 i = r0 + tid; i < r1; i += PT)
+#pragma unroll
+          for (int s = 0; s < S; ++s) pcur[i + s * a.ldw] = p_at(i, s);
+      if constexpr (GRAM) {
+        static_assert(S == 1, "gram persistent path is single right-hand side");
+        double2 pv[PV], acc[PV], cur[PV], nxt[PV];
+        bool ok[PV];
+#pragma unroll
+        for (int k = 0; k < PV; ++k) {
+          const i64 j = 2 * (tid + static_cast<i64>(PT) * k);
+          ok[k] = j < n;
+          pv[k] = make_double2(j < n ? p_at(j, 0) : 0.0, j + 1 < n ? p_at(j + 1, 0) : 0.0);
+          acc[k] = make_double2(0.0, 0.0);
+        }
+        const i64 a0 = static_cast<i64>(c) * a.rows_per_cta, a1 = min(a.m, a0 + a.rows_per_cta);
+        auto load_row = [&](i64 row, double2* dst) {
+          const double* x = a.A + row * a.lda;
+#pragma unroll
+          for (int k = 0; k < PV; ++k)
+            dst[k] = ok[k] ? __ldcs(reinterpret_cast<const double2*>(x + 2 * (tid + PT * k))) : make_double2(0.0, 0.0);
+        };
+        if (a0 < a1) load_row(a0, cur);
+        int par = 0;
+        for (i64 row = a0; row < a1; ++row) {
+          if (row + 1 < a1) load_row(row + 1, nxt);
+          double d = 0.0;
+#pragma unroll
+          for (int k = 0; k < PV; ++k) d += cur[k].x * pv[k].x + cur[k].y * pv[k].y;
+          d = warp_sum(d);
+          if (lane == 0) red[par][warp] = d;
+          __syncthreads();
+          double sa = 0.0;
+#pragma unroll
+          for (int w = 0; w < PT / 32; ++w) sa += red[par][w];
+#pragma unroll
+          for (int k = 0; k < PV; ++k) {
+            acc[k].x += sa * cur[k].x;
+            acc[k].y += sa * cur[k].y;
+          }
+          par ^= 1;
+#pragma unroll
+          for (int k = 0; k < PV; ++k) cur[k] = nxt[k];
+        }
+        double* dst = a.part + static_cast<i64>(c) * PW;
+#pragma unroll
+        for (int k = 0; k < PV; ++k)
+          if (ok[k]) reinterpret_cast<double2*>(dst)[tid + PT * k] = acc[k];
+        grid.sync();
+        // ---- P2: column slice of v, partial p.v
+        double pvl = 0.0;
+        for (i64 j = r0 + warp; j < r1; j += PT / 32) {
+          double s = 0.0;
+          for (int b = lane; b < G; b += 32) s += a.part[static_cast<i64>(b) * PW + j];
+          s = warp_sum(s);
+          const double pj = pcur[j];
+          double v = s / a.div;  // operators.cpp:115 (division), then out += mu p
+          v += a.mu * pj;
+          if (lane == 0) {
+            a.V[j] = v;
+            pvl += pj * v;
+          }
+        }
+        pvl = block_sum(pvl, sh);
+        if (tid == 0) a.pv_part[c] = pvl;
+      } else {
+        // dense: (A p)_j for the slice columns; p_t recomputed on the fly
+        double pvl[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) pvl[s] = 0.0;
+        for (i64 j = r0 + warp; j < r1; j += PT / 32) {
+          const double* col = a.A + j * a.lda;
+          double acc[S];
+#pragma unroll
+          for (int s = 0; s < S; ++s) acc[s] = 0.0;
+          for (i64 i = lane; i < n; i += 32) {
+            const double aij = col[i];
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s] += aij * p_at(i, s);
+          }
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const double av = warp_sum(acc[s]);
+            const double pj = p_at(j, s);
+            double v = av;
+            v += a.mu * pj;
+            if (lane == 0) {
+              a.V[j + s * a.ldw] = v;
+              pvl[s] += pj * v;
+            }
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const double tot = block_sum(pvl[s], sh);
+          if (tid == 0) a.pv_part[c * S + s] = tot;
+        }
+      }
+      grid.sync();
+      // ---- P3: alpha (fin_dot kind 1), x and r updates, partial ||r||^2
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const double pv = all_sum(a.pv_part, s);
+        if (tid == 0 && cs[s].status == 0) {
+          cs[s].pv = pv;
+          cs[s].iters = static_cast<int>(t);
+          if (!(pv > 0.0) || !isfinite(pv)) cs[s].status = 2;  // solvers.cpp:76-81
+          else cs[s].alpha = cs[s].rz / pv;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        double rr = 0.0;
+        if (cs[s].status == 0) {
+          const double al = cs[s].alpha;
+          for (i64 i = r0 + tid; i < r1; i += PT) {
+            const i64 o = i + s * a.ldw;
+            a.X[i + s * a.ldx] += al * pcur[o];
+            const double r = a.R[o] - al * a.V[o];
+            a.R[o] = r;
+            rr += r * r;
+          }
+        }
+        rr = block_sum(rr, sh);
+        if (tid == 0) a.rr_part[c * S + s] = rr;
+      }
+      grid.sync();
+      // ---- P4: residual norm, status (fin_res), then the preconditioner's U^T r
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const double rr = all_sum(a.rr_part, s);
+        if (tid == 0 && cs[s].status == 0) {
+          const double res = sqrt(rr);
+          cs[s].res = res;
+          if (c == 0) a.hist[s * a.hstride + t] = res;
+          if (!isfinite(res)) cs[s].status = 3;      // solvers.cpp:88-93
+          else if (res <= cs[s].eta) cs[s].status = 1;  // :94-97
+          else if (t >= a.max_iter) cs[s].status = 5;
+          if (!nys && cs[s].status == 0) {  // z = r: r.z = ||r||^2 (fin_dot kind 2)
+            cs[s].beta = rr / cs[s].rz;
+            cs[s].rz = rr;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) running_sh = count_running();
+      __syncthreads();
+      if (running_sh == 0) break;
+      if (!nys) continue;
+      {
+        const i64 u0 = min(a.ell, static_cast<i64>(c) * a.uslice), u1 = min(a.ell, u0 + a.uslice);
+        for (i64 j = u0; j < u1; ++j) {
+          const double* uc = a.U + j * a.ldu;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            double w = 0.0;
+            for (i64 i = tid; i < n; i += PT) w += uc[i] * a.R[i + s * a.ldw];
+            w = block_sum(w, sh);
+            if (tid == 0) a.T[j + s * a.ell] = w * a.gain[j];
+          }
+        }
+      }
+      grid.sync();
+      // ---- P5: z = r + U t on the slice (32 rows x 16 column groups), partial r.z
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        double rz = 0.0;
+        for (i64 i0 = r0; i0 < r1; i0 += 32) {
+          const i64 i = i0 + lane;
+          double acc = 0.0;
+          if (i < r1)
+            for (i64 j = warp; j < a.ell; j += PT / 32) acc += a.U[i + j * a.ldu] * a.T[j + s * a.ell];
+          zred[warp][lane] = acc;
+          __syncthreads();
+          if (warp == 0 && i < r1) {
+            double u = 0.0;
+#pragma unroll
+            for (int w = 0; w < PT / 32; ++w) u += zred[w][lane];
+            const double r = a.R[i + s * a.ldw];
+            const double z = r + u;
+            a.Z[i + s * a.ldw] = z;
+            rz += r * z;
+          }
+          __syncthreads();
+        }
+        rz = block_sum(rz, sh);
+        if (tid == 0) a.rz_part[c * S + s] = rz;
+      }
+      grid.sync();
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const double rz = all_sum(a.rz_part, s);
+        if (tid == 0 && cs[s].status == 0) {  // fin_dot kind 2
+          cs[s].beta = rz / cs[s].rz;
+          cs[s].rz = rz;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (c == 0 && tid < S) a.st->c[tid] = cs[tid];
+  if (c == 0 && tid == 0) a.st->any_running = 0;
+}
+
+bool persistent_eligible(const Ctx& ctx, Op& op, i64 S) {
+  (void)ctx;
+  if (auto* g = dynamic_cast<GramOp*>(&op)) return S == 1 && g->n <= PW && g->m >= 1;
+  if (dynamic_cast<DenseOp*>(&op)) return S <= 2;
+  return false;
+}
+
+template <int S, bool GRAM>
+void launch_persistent(Ctx& ctx, PersistArgs& pa, int G) {
+  void* args[] = {&pa};
+  ctx.prof_begin(GRAM ? "pcg_persistent_kernel<gram>" : "pcg_persistent_kernel<dense>");
+  NPCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(pcg_persistent_kernel<S, GRAM>), G, PT, args, 0,
+                                        ctx.stream));
+  ctx.check_launch("pcg_persistent_kernel");
+  ctx.prof_end();
+}
+
+template <int S, bool GRAM>
+int persistent_grid(const Ctx& ctx) {
+  int per_sm = 0;
+  NPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_persistent_kernel<S, GRAM>, PT, 0));
+  if (per_sm < 1) fail(NPCG_ECUDA, "pcg_persistent_kernel does not fit on an SM");
+  return ctx.sm_count;  // one CTA per SM: cheapest grid barrier, enough bytes in flight
+}
+
+void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64 ldx, DMat& R, DMat& Z, DMat& P,
+                    DMat& V, State* st, double* hist, i64 hstride, i64 max_iter) {
+  auto* gram = dynamic_cast<GramOp*>(&op);
+  auto* dense = dynamic_cast<DenseOp*>(&op);
+  const i64 n = op.n;
+  const bool nys = pre != nullptr && pre->ell > 0;
+  const int G = gram ? persistent_grid<1, true>(ctx) : (S == 1 ? persistent_grid<1, false>(ctx)
+                                                               : persistent_grid<2, false>(ctx));
+  DMat P1;
+  P1.alloc(n, S, ctx.stream, false);
+  DBuf<double> part, T, scal(3 * static_cast<i64>(G) * S, ctx.stream);
+  if (gram) part.alloc(static_cast<i64>(G) * PW, ctx.stream);
+  if (nys) T.alloc(pre->ell * S, ctx.stream);
+  PersistArgs pa{};
+  pa.n = n;
+  pa.mu = mu;
+  if (gram) {
+    pa.m = gram->m;
+    pa.A = gram->xr.p();
+    pa.lda = gram->xr.ld;
+    pa.div = static_cast<double>(gram->m);
+    pa.rows_per_cta = cdiv(gram->m, G);
+  } else {
+    pa.A = dense->a.p();
+    pa.lda = dense->a.ld;
+    pa.div = 1.0;
+  }
+  if (nys) {
+    pa.U = pre->nys->u.p();
+    pa.ldu = pre->nys->u.ld;
+    pa.ell = pre->ell;
+    pa.gain = pre->gain_inv.p;
+    pa.T = T.p;
+    pa.uslice = cdiv(pre->ell, G);
+  }
+  pa.X = X;
+  pa.ldx = ldx;
+  pa.R = R.p();
+  pa.Z = nys ? Z.p() : nullptr;
+  pa.P0 = P.p();
+  pa.P1 = P1.p();
+  pa.V = V.p();
+  pa.ldw = R.ld;
+  pa.part = part.p;
+  pa.pv_part = scal.p;
+  pa.rr_part = scal.p + G * S;
+  pa.rz_part = scal.p + 2 * G * S;
+  pa.st = st;
+  pa.hist = hist;
+  pa.hstride = hstride;
+  pa.max_iter = max_iter;
+  pa.slice = cdiv(n, G);
+  if (P.ld != R.ld || V.ld != R.ld || P1.ld != R.ld || (nys && Z.ld != R.ld)) fail(NPCG_ERUNTIME, "pcg: work layout");
+  if (gram) launch_persistent<1, true>(ctx, pa, G);
+  else if (S == 1) launch_persistent<1, false>(ctx, pa, G);
+  else launch_persistent<2, false>(ctx, pa, G);
+  ctx.sync();  // work buffers are released on return
+}
+
 }  // namespace
 
 PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* B, i64 ldb, const double* X0,
@@ -263,53 +643,57 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
   NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), R.p(), R.ld, Zp, ldz, P.p(), P.ld, st.p, part.p);
   NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, 0, 0);
 
-  // pinned status snapshots, one per in-flight iteration
-  State* snap = nullptr;
-  NPCG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&snap), sizeof(State) * (kDepth + 1)));
-  cudaEvent_t ev[kDepth + 1];
-  for (auto& e : ev) NPCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  struct Cleanup {
-    State* snap;
-    cudaEvent_t* ev;
-    ~Cleanup() {
-      for (int k = 0; k <= kDepth; ++k) cudaEventDestroy(ev[k]);
-      cudaFreeHost(snap);
-    }
-  } cleanup{snap, ev};
+  if (!iterates && persistent_eligible(ctx, op, S) && !(std::getenv("NPCG_PCG") && std::string(std::getenv("NPCG_PCG")) == "classic")) {
+    run_persistent(ctx, op, pre, mu, S, X, ldx, R, Z, P, V, st.p, hist.p, hstride, opt.max_iter);
+  } else {
+    // pinned status snapshots, one per in-flight iteration
+    State* snap = nullptr;
+    NPCG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&snap), sizeof(State) * (kDepth + 1)));
+    cudaEvent_t ev[kDepth + 1];
+    for (auto& e : ev) NPCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct Cleanup {
+      State* snap;
+      cudaEvent_t* ev;
+      ~Cleanup() {
+        for (int k = 0; k <= kDepth; ++k) cudaEventDestroy(ev[k]);
+        cudaFreeHost(snap);
+      }
+    } cleanup{snap, ev};
 
-  auto enqueue_snapshot = [&](i64 t) {
-    const int slot = static_cast<int>(t % (kDepth + 1));
-    NPCG_CUDA(cudaMemcpyAsync(&snap[slot], st.p, sizeof(State), cudaMemcpyDeviceToHost, ctx.stream));
-    NPCG_CUDA(cudaEventRecord(ev[slot], ctx.stream));
-  };
-  auto finished = [&](i64 t) {
-    const int slot = static_cast<int>(t % (kDepth + 1));
-    NPCG_CUDA(cudaEventSynchronize(ev[slot]));
-    return snap[slot].any_running == 0;
-  };
-  enqueue_snapshot(0);
-  bool done = false;
-  if (opt.max_iter == 0 || finished(0)) done = true;
-  for (i64 t = 1; t <= opt.max_iter && !done; ++t) {
-    if (iterates) NPCG_LAUNCH(ctx, snapshot_running_kernel, 1, 32, 0, st.p, static_cast<int>(S), run_flags.p);
-    op.apply_shift(P.p(), P.ld, static_cast<int>(S), mu, V.p(), V.ld, gate);
-    NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), P.p(), P.ld, V.p(), V.ld,
-                static_cast<double*>(nullptr), 0, st.p, part.p);
-    NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, 1, static_cast<int>(t));
-    NPCG_LAUNCH(ctx, update_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, P.p(), P.ld, V.p(), V.ld, R.p(),
-                R.ld, st.p, part.p);
-    NPCG_LAUNCH(ctx, fin_res_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, static_cast<int>(t),
-                opt.max_iter, hist.p, hstride);
-    if (iterates)
-      NPCG_LAUNCH(ctx, record_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, iterates + t * n * S, st.p,
-                  run_flags.p);
-    if (!identity) pre_apply_inverse(*pre, R.p(), R.ld, S, Z.p(), Z.ld, gate);
-    NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), R.p(), R.ld, Zp, ldz,
-                static_cast<double*>(nullptr), 0, st.p, part.p);
-    NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, 2, static_cast<int>(t));
-    NPCG_LAUNCH(ctx, pupdate_kernel, nblk, 256, 0, n, static_cast<int>(S), P.p(), P.ld, Zp, ldz, st.p);
-    enqueue_snapshot(t);
-    if (t > kDepth && finished(t - kDepth)) done = true;
+    auto enqueue_snapshot = [&](i64 t) {
+      const int slot = static_cast<int>(t % (kDepth + 1));
+      NPCG_CUDA(cudaMemcpyAsync(&snap[slot], st.p, sizeof(State), cudaMemcpyDeviceToHost, ctx.stream));
+      NPCG_CUDA(cudaEventRecord(ev[slot], ctx.stream));
+    };
+    auto finished = [&](i64 t) {
+      const int slot = static_cast<int>(t % (kDepth + 1));
+      NPCG_CUDA(cudaEventSynchronize(ev[slot]));
+      return snap[slot].any_running == 0;
+    };
+    enqueue_snapshot(0);
+    bool done = false;
+    if (opt.max_iter == 0 || finished(0)) done = true;
+    for (i64 t = 1; t <= opt.max_iter && !done; ++t) {
+      if (iterates) NPCG_LAUNCH(ctx, snapshot_running_kernel, 1, 32, 0, st.p, static_cast<int>(S), run_flags.p);
+      op.apply_shift(P.p(), P.ld, static_cast<int>(S), mu, V.p(), V.ld, gate);
+      NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), P.p(), P.ld, V.p(), V.ld,
+                  static_cast<double*>(nullptr), 0, st.p, part.p);
+      NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, 1, static_cast<int>(t));
+      NPCG_LAUNCH(ctx, update_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, P.p(), P.ld, V.p(), V.ld, R.p(),
+                  R.ld, st.p, part.p);
+      NPCG_LAUNCH(ctx, fin_res_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, static_cast<int>(t),
+                  opt.max_iter, hist.p, hstride);
+      if (iterates)
+        NPCG_LAUNCH(ctx, record_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, iterates + t * n * S, st.p,
+                    run_flags.p);
+      if (!identity) pre_apply_inverse(*pre, R.p(), R.ld, S, Z.p(), Z.ld, gate);
+      NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), R.p(), R.ld, Zp, ldz,
+                  static_cast<double*>(nullptr), 0, st.p, part.p);
+      NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, 2, static_cast<int>(t));
+      NPCG_LAUNCH(ctx, pupdate_kernel, nblk, 256, 0, n, static_cast<int>(S), P.p(), P.ld, Zp, ldz, st.p);
+      enqueue_snapshot(t);
+      if (t > kDepth && finished(t - kDepth)) done = true;
+    }
   }
   ctx.sync();
 
