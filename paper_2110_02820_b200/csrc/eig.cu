@@ -2,9 +2,9 @@
 // thin SVD of the Nyström pipeline (factor.cu).
 //
 //   1. Householder tridiagonalisation in one cooperative kernel: per column,
-//      every CTA forms the reflector redundantly, the trailing symmetric
-//      matvec and the rank-2 update are split over CTAs by column (two
-//      grid-wide barriers per column).
+//      every CTA forms the reflector redundantly; the previous step's rank-2
+//      update and this step's trailing symmetric matvec are fused in one pass
+//      split over CTAs by column (one grid-wide barrier per column).
 //   2. Bisection with Sturm counts, one eigenvalue per thread.
 //   3. Inverse iteration on the tridiagonal (partial-pivoting LU), one
 //      eigenvector per thread, deterministic pseudo-random starts; exact
@@ -27,77 +27,96 @@ namespace {
 
 constexpr int TRI_THREADS = 256;
 
+// One grid-wide barrier per column: the rank-2 update of step k-1 is kept
+// pending (vp, wp) and applied on the fly -- redundantly by every CTA to
+// column k (which yields the reflector of step k), and by the column owners
+// in the same pass that forms p = tau A22 v for step k (each trailing column
+// is read and written once per step). p is double-buffered across steps.
 __global__ void __launch_bounds__(TRI_THREADS) tridiag_kernel(double* M, i64 ld, int n, double* d, double* e,
                                                                double* tau, double* H, i64 ldh, double* p) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ double tsm[];  // v (n) then w (n)
+  extern __shared__ double tsm[];  // v (n), vp (n), wp (n)
   __shared__ double red[32];
-  __shared__ double s_scal[3];
-  double* v = tsm;
-  double* w = tsm + n;
+  double* v = tsm;           // step k reflector: v[i] <-> row k+1+i
+  double* vp = tsm + n;      // pending update of step k-1: index i <-> row k+i
+  double* wp = tsm + 2 * n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int G = gridDim.x, bid = blockIdx.x;
+  bool pend = false;
   for (int k = 0; k < n - 2; ++k) {
     const int L = n - k - 1;
-    const double* x = M + (k + 1) + static_cast<i64>(k) * ld;
-    // ---- reflector (redundant in every CTA): beta, tau, v (v_0 = 1)
+    const double* colk = M + k + static_cast<i64>(k) * ld;  // column k, rows k..n-1
+    // ---- column k with the pending update applied; reflector (redundant in every CTA)
     double s = 0.0;
-    for (int i = 1 + tid; i < L; i += blockDim.x) s += x[i] * x[i];
-    s = block_sum(s, red);
-    const double alpha = x[0];
+    for (int j = tid; j < L; j += blockDim.x) {
+      double x = colk[j + 1];
+      if (pend) x -= vp[j + 1] * wp[0] + wp[j + 1] * vp[0];
+      v[j] = x;
+      if (j > 0) s += x * x;
+    }
+    s = block_sum(s, red);  // (barrier: v complete)
+    const double alpha = v[0];
     double t = 0.0, beta = alpha, scal = 0.0;
     if (s > 0.0) {
       beta = -copysign(sqrt(alpha * alpha + s), alpha);
       t = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    for (int i = tid; i < L; i += blockDim.x) v[i] = i == 0 ? 1.0 : x[i] * scal;
+    __syncthreads();
+    for (int j = tid; j < L; j += blockDim.x) v[j] = j == 0 ? 1.0 : v[j] * scal;
     if (bid == 0 && tid == 0) {
-      d[k] = M[k + static_cast<i64>(k) * ld];
+      d[k] = pend ? colk[0] - (vp[0] * wp[0] + wp[0] * vp[0]) : colk[0];
       e[k] = beta;
       tau[k] = t;
     }
+    __syncthreads();
     if (bid == 0)
       for (int i = tid; i < L; i += blockDim.x) H[(k + 1 + i) + static_cast<i64>(k) * ldh] = v[i];
-    __syncthreads();
-    if (t == 0.0) {  // nothing to eliminate; uniform across CTAs
-      grid.sync();
-      continue;
-    }
-    // ---- p = tau * A22 v   (A22 = M[k+1:, k+1:], symmetric: column c == row c)
-    for (int c = bid * nw + warp; c < L; c += G * nw) {
-      const double* col = M + (k + 1) + static_cast<i64>(k + 1 + c) * ld;
-      double acc = 0.0;
-      for (int i = lane; i < L; i += 32) acc += col[i] * v[i];
-      acc = warp_sum(acc);
-      if (lane == 0) p[c] = t * acc;
-    }
-    grid.sync();
-    // ---- w = p - (tau/2)(p.v) v  (redundant per CTA)
-    double pv = 0.0;
-    for (int i = tid; i < L; i += blockDim.x) {
-      const double pi = p[i];
-      w[i] = pi;
-      pv += pi * v[i];
-    }
-    pv = block_sum(pv, red);
-    const double K = 0.5 * t * pv;
-    for (int i = tid; i < L; i += blockDim.x) w[i] -= K * v[i];
-    __syncthreads();
-    // ---- A22 -= v w^T + w v^T  (column c owned by warp)
+    // ---- owners: A22 -= pending (written back), p = tau A22 v
+    double* pk = p + (k & 1) * n;
     for (int c = bid * nw + warp; c < L; c += G * nw) {
       double* col = M + (k + 1) + static_cast<i64>(k + 1 + c) * ld;
-      const double vc = v[c], wc = w[c];
-      for (int i = lane; i < L; i += 32) col[i] -= v[i] * wc + w[i] * vc;
+      const double vc = pend ? vp[c + 1] : 0.0, wc = pend ? wp[c + 1] : 0.0;
+      double acc = 0.0;
+      if (pend) {
+        for (int i = lane; i < L; i += 32) {
+          const double a = col[i] - (vp[i + 1] * wc + wp[i + 1] * vc);
+          col[i] = a;
+          acc += a * v[i];
+        }
+      } else {
+        for (int i = lane; i < L; i += 32) acc += col[i] * v[i];
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) pk[c] = t * acc;
     }
     grid.sync();
+    // ---- w = p - (tau/2)(p.v) v (redundant per CTA) becomes the pending update
+    double pv = 0.0;
+    for (int i = tid; i < L; i += blockDim.x) pv += pk[i] * v[i];
+    pv = block_sum(pv, red);
+    const double K = 0.5 * t * pv;
+    for (int i = tid; i < L; i += blockDim.x) {
+      double w = pk[i];
+      w -= K * v[i];
+      wp[i] = w;
+      vp[i] = v[i];
+    }
+    pend = true;
+    __syncthreads();
   }
   if (bid == 0 && tid == 0) {
-    if (n >= 2) {
-      d[n - 2] = M[(n - 2) + static_cast<i64>(n - 2) * ld];
-      d[n - 1] = M[(n - 1) + static_cast<i64>(n - 1) * ld];
-      e[n - 2] = M[(n - 1) + static_cast<i64>(n - 2) * ld];
+    if (n >= 3) {  // last 2 x 2 block with the pending update of step n-3
+      const double* m2 = M + (n - 2) + static_cast<i64>(n - 2) * ld;
+      d[n - 2] = m2[0] - (vp[0] * wp[0] + wp[0] * vp[0]);
+      e[n - 2] = m2[1] - (vp[1] * wp[0] + wp[1] * vp[0]);
+      d[n - 1] = m2[1 + ld] - (vp[1] * wp[1] + wp[1] * vp[1]);
       tau[n - 2] = 0.0;
+    } else if (n == 2) {
+      d[0] = M[0];
+      d[1] = M[1 + ld];
+      e[0] = M[1];
+      tau[0] = 0.0;
     } else {
       d[0] = M[0];
     }
@@ -294,11 +313,11 @@ __global__ void backtransform_kernel(const double* H, i64 ldh, const double* tau
 void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
   if (n <= 0) return;
   int nn = static_cast<int>(n);
-  DBuf<double> d(n, ctx.stream), e(n, ctx.stream), tau(n, ctx.stream), p(n, ctx.stream), lam(n, ctx.stream);
+  DBuf<double> d(n, ctx.stream), e(n, ctx.stream), tau(n, ctx.stream), p(2 * n, ctx.stream), lam(n, ctx.stream);
   DMat H;
   H.alloc(n, n, ctx.stream, true);
   if (n >= 3) {
-    const int smem = static_cast<int>(2 * n * 8);
+    const int smem = static_cast<int>(3 * n * 8);
     NPCG_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    std::max(smem, 48 * 1024)));
     int per_sm = 0;
