@@ -352,6 +352,9 @@ __global__ void gather_cols_kernel(const double* V, i64 ldv, int n, const int* p
 bool cholesky(Ctx& ctx, double* a, i64 n, i64 lda, CholFactor& f) {
   f.n = n;
   if (n <= 0) return true;
+  static const bool blocked_only = std::getenv("NPCG_CHOL") && std::string(std::getenv("NPCG_CHOL")) == "blocked";
+  if (n <= kCholFusedMax && !blocked_only) return cholesky_fused(ctx, a, n, lda, f);
+  f.nb = NB;
   const i64 nblk = cdiv(n, NB);
   f.dinv.alloc(nblk * NB * NB, ctx.stream);
   DBuf<int> flag(1, ctx.stream);
@@ -387,10 +390,15 @@ bool cholesky(Ctx& ctx, double* a, i64 n, i64 lda, CholFactor& f) {
 
 void trsm_right_lt(Ctx& ctx, i64 m, i64 n, double* Y, i64 ldy, const double* L, i64 ldl, const CholFactor& f,
                    double* X, i64 ldx) {
-  const i64 nblk = cdiv(n, NB);
+  if (f.linv.p()) {  // X = Y L^{-T}: one DMMA GEMM with the explicit inverse
+    gemm(ctx, m, n, n, 1.0, Operand{Y, ldy, false}, Operand{f.linv.p(), f.linv.ld, false}, 0.0, X, ldx);
+    return;
+  }
+  const i64 nb = f.nb;
+  const i64 nblk = cdiv(n, nb);
   for (i64 b = 0; b < nblk; ++b) {
-    const i64 k0 = b * NB, kb = std::min<i64>(NB, n - k0);
-    gemm(ctx, m, kb, kb, 1.0, Operand{Y + k0 * ldy, ldy, false}, Operand{f.dinv.p + b * NB * NB, NB, false}, 0.0,
+    const i64 k0 = b * nb, kb = std::min<i64>(nb, n - k0);
+    gemm(ctx, m, kb, kb, 1.0, Operand{Y + k0 * ldy, ldy, false}, Operand{f.dinv.p + b * nb * nb, nb, false}, 0.0,
          X + k0 * ldx, ldx);
     const i64 r0 = k0 + kb, rem = n - r0;
     if (rem <= 0) break;

@@ -9,12 +9,20 @@ namespace npcg {
 
 constexpr int kCholNB = 64;
 
-/// Diagonal-block inverses produced by cholesky(): block b (rows/cols
-/// b*NB .. ) is stored NB x NB col-major at dinv + b*NB*NB.
+/// What cholesky() leaves besides L: the diagonal-block inverses (block b,
+/// rows/cols b*nb.., stored nb x nb col-major at dinv + b*nb*nb) and, from
+/// the fused path (n <= kCholFusedMax), the full inverse L^{-1} in `linv`.
 struct CholFactor {
   DBuf<double> dinv;
+  DMat linv;
   i64 n = 0;
+  int nb = kCholNB;
 };
+
+constexpr i64 kCholFusedMax = 4096;
+
+/// Fused single-launch Cholesky + L^{-1} (chol.cu); same contract as cholesky().
+bool cholesky_fused(Ctx& ctx, double* a, i64 n, i64 lda, CholFactor& f);
 
 /// In-place lower Cholesky of the n x n matrix at `a` (ld lda), reading only
 /// the lower triangle (Eigen::LLT / dpotrf('L') semantics). On return the
