@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "factor.cuh"
 
@@ -120,14 +121,16 @@ __device__ __noinline__ bool diag_factor(Tile& T, int b, int nr, const CholArgs&
 #pragma unroll
   for (int k = 0; k < CB; ++k) T[lane][k] = k <= lane ? row[k] : 0.0;
   __syncwarp();
-  // X = L^{-1}, lane c computes column c: X[i][c] = (delta_ic - sum_{c<=k<i} L[i][k] X[k][c]) / L[i][i]
+  // X = L^{-1}, lane c computes column c, right-looking: once x_k is final,
+  // every later row takes its contribution at once (short dependency chain).
   double x[CB];
 #pragma unroll
-  for (int i = 0; i < CB; ++i) {
-    double s = i == lane ? 1.0 : 0.0;
+  for (int i = 0; i < CB; ++i) x[i] = i == lane ? 1.0 : 0.0;
 #pragma unroll
-    for (int k = 0; k < i; ++k) s -= T[i][k] * x[k];  // x[k] = 0 for k < lane
-    x[i] = i < lane ? 0.0 : s * rs[i];
+  for (int k = 0; k < CB; ++k) {
+    x[k] *= rs[k];  // rows < lane stay exactly 0
+#pragma unroll
+    for (int i = k + 1; i < CB; ++i) x[i] -= T[i][k] * x[k];
   }
   double* dv = a.dinv + static_cast<i64>(b) * CB * CB;
 #pragma unroll
@@ -183,6 +186,12 @@ __global__ void __launch_bounds__(CT) chol_fused_kernel(const CholArgs a) {
         const i64 oi = static_cast<i64>(ti) * CB, oj = static_cast<i64>(tj) * CB;
         load_tile(Ai, a.a, a.lda, oi, ob, nri, nrb);
         if (tj != ti) load_tile(Aj, a.a, a.lda, oj, ob, nrj, nrb);
+        double old[4];  // destination values, fetched early (off the dependency chain)
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          const int c = c0 + qq;
+          old[qq] = (r < nri && c < nrj && (ti != tj || c <= r)) ? a.a[(oi + r) + (oj + c) * a.lda] : 0.0;
+        }
         __syncthreads();
         mul_abt(Ai, Dn, acc);  // L_ib = A_ib Dinv_b^T
         store_acc(Li, acc);
@@ -201,9 +210,8 @@ __global__ void __launch_bounds__(CT) chol_fused_kernel(const CholArgs a) {
         for (int qq = 0; qq < 4; ++qq) {
           const int c = c0 + qq;
           if (r < nri && c < nrj && (ti != tj || c <= r)) {
-            double* p = a.a + (oi + r) + (oj + c) * a.lda;
-            const double v = *p - acc[qq];
-            *p = v;
+            const double v = old[qq] - acc[qq];
+            a.a[(oi + r) + (oj + c) * a.lda] = v;
             if (ti == b + 1 && tj == b + 1) Ct[r][c] = v;
           }
         }
@@ -219,6 +227,12 @@ __global__ void __launch_bounds__(CT) chol_fused_kernel(const CholArgs a) {
         const i64 oi = static_cast<i64>(ti) * CB, oj = static_cast<i64>(tj) * CB;
         load_tile(Ai, a.a, a.lda, oi, ob, nri, nrb);       // A_ib
         load_tile_t(Aj, a.W, a.ldw, ob, oj, nrb, nrj);     // W_bj^T
+        double old[4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          const int c = c0 + qq;
+          old[qq] = (r < nri && c < nrj) ? a.W[(oi + r) + (oj + c) * a.ldw] : 0.0;
+        }
         __syncthreads();
         mul_abt(Ai, Dn, acc);                              // L_ib
         store_acc(Li, acc);
@@ -236,7 +250,7 @@ __global__ void __launch_bounds__(CT) chol_fused_kernel(const CholArgs a) {
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
           const int c = c0 + qq;
-          if (r < nri && c < nrj) a.W[(oi + r) + (oj + c) * a.ldw] -= acc[qq];
+          if (r < nri && c < nrj) a.W[(oi + r) + (oj + c) * a.ldw] = old[qq] - acc[qq];
         }
         __syncthreads();
       }
@@ -301,9 +315,11 @@ bool cholesky_fused(Ctx& ctx, double* A, i64 n, i64 lda, CholFactor& f) {
   NPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_fused_kernel, CT, smem));
   const i64 t1 = static_cast<i64>(nb - 1) * nb / 2 + (nb - 1);  // widest U phase (b = 0)
   const int G = static_cast<int>(std::max<i64>(1, std::min<i64>(t1, static_cast<i64>(std::max(per_sm, 1)) * ctx.sm_count)));
+  int G2 = G;
+  if (const char* g = std::getenv("NPCG_CHOL_GRID")) G2 = std::max(1, std::min(G, std::atoi(g)));  // diagnostics
   void* kargs[] = {&args};
   ctx.prof_begin("chol_fused_kernel");
-  NPCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(chol_fused_kernel), G, CT, kargs, smem, ctx.stream));
+  NPCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(chol_fused_kernel), G2, CT, kargs, smem, ctx.stream));
   ctx.check_launch("chol_fused_kernel");
   ctx.prof_end();
   int h = 0;

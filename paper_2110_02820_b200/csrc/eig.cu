@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "eig.cuh"
 
@@ -125,6 +127,113 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_kernel(double* M, i64 ld,
       tau[n - 1] = 0.0;
     }
   }
+}
+
+// Same algorithm inside one thread-block cluster with the matrix resident in
+// shared memory: CTA r of C owns columns c = r (mod C) whole (n <= ~620 at
+// C = 16). Column k and the matvec results p are read across the cluster
+// through DSMEM; one cluster barrier per column, no global-memory traffic.
+__global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const double* M, i64 ld, int n, double* d,
+                                                                       double* e, double* tau, double* H, i64 ldh) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
+  extern __shared__ double csm_t[];
+  const int ncl = (n + C - 1) / C;
+  double* cols = csm_t;            // [ncl][n]: local column lc is global column lc*C + rank
+  double* v = cols + static_cast<i64>(ncl) * n;
+  double* vp = v + n;
+  double* wp = vp + n;
+  double* pt = wp + n;
+  double* pl = pt + n;             // [2][ncl] matvec results of the owned columns
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int lc = 0; lc < ncl; ++lc) {
+    const int c = lc * C + rank;
+    if (c >= n) break;
+    for (int i = tid; i < n; i += blockDim.x) cols[static_cast<i64>(lc) * n + i] = M[i + static_cast<i64>(c) * ld];
+  }
+  cl.sync();
+  bool pend = false;
+  for (int k = 0; k < n - 2; ++k) {
+    const int L = n - k - 1;
+    const double* ck = cl.map_shared_rank(cols + static_cast<i64>(k / C) * n, k % C);
+    double s = 0.0;
+    for (int j = tid; j < L; j += blockDim.x) {
+      double x = ck[k + 1 + j];
+      if (pend) x -= vp[j + 1] * wp[0] + wp[j + 1] * vp[0];
+      v[j] = x;
+      if (j > 0) s += x * x;
+    }
+    s = block_sum(s, red);
+    const double alpha = v[0];
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (s > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + s), alpha);
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    __syncthreads();
+    for (int j = tid; j < L; j += blockDim.x) v[j] = j == 0 ? 1.0 : v[j] * scal;
+    if (rank == 0 && tid == 0) {
+      d[k] = pend ? ck[k] - (vp[0] * wp[0] + wp[0] * vp[0]) : ck[k];
+      e[k] = beta;
+      tau[k] = t;
+    }
+    __syncthreads();
+    if (rank == 0)
+      for (int i = tid; i < L; i += blockDim.x) H[(k + 1 + i) + static_cast<i64>(k) * ldh] = v[i];
+    double* pk = pl + (k & 1) * ncl;
+    for (int lc = warp; lc < ncl; lc += nw) {
+      const int c = lc * C + rank;
+      if (c <= k || c >= n) continue;
+      const int ci = c - (k + 1);
+      double* col = cols + static_cast<i64>(lc) * n + (k + 1);
+      const double vc = pend ? vp[ci + 1] : 0.0, wc = pend ? wp[ci + 1] : 0.0;
+      double acc = 0.0;
+      if (pend) {
+        for (int i = lane; i < L; i += 32) {
+          const double a = col[i] - (vp[i + 1] * wc + wp[i + 1] * vc);
+          col[i] = a;
+          acc += a * v[i];
+        }
+      } else {
+        for (int i = lane; i < L; i += 32) acc += col[i] * v[i];
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) pk[lc] = t * acc;
+    }
+    cl.sync();
+    double pv = 0.0;
+    for (int i = tid; i < L; i += blockDim.x) {
+      const int c = k + 1 + i;
+      const double pi = *cl.map_shared_rank(pk + c / C, c % C);
+      pt[i] = pi;
+      pv += pi * v[i];
+    }
+    pv = block_sum(pv, red);
+    const double K = 0.5 * t * pv;
+    for (int i = tid; i < L; i += blockDim.x) {
+      double w = pt[i];
+      w -= K * v[i];
+      wp[i] = w;
+      vp[i] = v[i];
+    }
+    pend = true;
+    __syncthreads();
+  }
+  if (rank == 0 && tid == 0) {
+    if (n >= 3) {
+      const double* c2 = cl.map_shared_rank(cols + static_cast<i64>((n - 2) / C) * n, (n - 2) % C);
+      const double* c1 = cl.map_shared_rank(cols + static_cast<i64>((n - 1) / C) * n, (n - 1) % C);
+      d[n - 2] = c2[n - 2] - (vp[0] * wp[0] + wp[0] * vp[0]);
+      e[n - 2] = c2[n - 1] - (vp[1] * wp[0] + wp[1] * vp[0]);
+      d[n - 1] = c1[n - 1] - (vp[1] * wp[1] + wp[1] * vp[1]);
+      tau[n - 2] = 0.0;
+      e[n - 1] = 0.0;
+      tau[n - 1] = 0.0;
+    }
+  }
+  cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
 // number of eigenvalues of T strictly below x (Sturm sequence of LDL^T)
@@ -278,6 +387,83 @@ __global__ void invit_kernel(const double* d, const double* e, const double* lam
 #undef IX
 }
 
+// Inverse iteration with the working set in shared memory: V eigenvectors per
+// CTA, one per thread, layout [i][v]. The LU of T - shift I (partial
+// pivoting, dgttrf) is recomputed in each of the three iterations and applied
+// to z on the fly, so only U (three diagonals) and z are stored. Writes
+// Zr[i][j] like invit_kernel.
+__global__ void invit_smem_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                  const double* __restrict__ lam, int n, const double* __restrict__ info,
+                                  double* __restrict__ Zr) {
+  extern __shared__ double ism[];
+  const int V = blockDim.x, v = threadIdx.x;
+  const int j = blockIdx.x * V + v;
+  double* u0 = ism;
+  double* u1 = ism + static_cast<i64>(n) * V;
+  double* u2 = ism + 2 * static_cast<i64>(n) * V;
+  double* z = ism + 3 * static_cast<i64>(n) * V;
+#define SX(i) (static_cast<i64>(i) * V + v)
+  if (j >= n) return;
+  const double eps = 2.220446049250313e-16;
+  const double tnorm = info[3];
+  int rep = 0;
+  while (j - rep - 1 >= 0 && lam[j] - lam[j - rep - 1] <= 4.0 * eps * tnorm) ++rep;
+  const double shift = lam[j] + rep * 8.0 * eps * tnorm;
+  const double tiny = fmax(eps * tnorm, 1e-300);
+  for (int i = 0; i < n; ++i) z[SX(i)] = hash_unit((static_cast<unsigned long long>(j) << 32) ^ static_cast<unsigned>(i));
+  double scale = 1.0;
+  for (int it = 0; it < 3; ++it) {
+    // factor + forward elimination; a/b: diagonal/superdiagonal of row i, nd/nb: of row i+1
+    double a = d[0] - shift, b = n > 1 ? e[0] : 0.0;
+    double zi = z[SX(0)] * scale;
+    for (int i = 0; i < n - 1; ++i) {
+      const double sub = e[i];
+      double nd = d[i + 1] - shift, nb = i + 1 < n - 1 ? e[i + 1] : 0.0;
+      const double zi1 = z[SX(i + 1)] * scale;
+      double nz;
+      if (fabs(a) >= fabs(sub)) {
+        const double piv = a == 0.0 ? tiny : a;
+        const double f = sub / piv;
+        u0[SX(i)] = piv;
+        u1[SX(i)] = b;
+        u2[SX(i)] = 0.0;
+        nd -= f * b;
+        z[SX(i)] = zi;
+        nz = zi1 - f * zi;
+      } else {
+        const double f = a / sub;
+        u0[SX(i)] = sub;
+        u1[SX(i)] = nd;
+        u2[SX(i)] = nb;
+        const double nd2 = b - f * nd;
+        nb = -f * nb;
+        nd = nd2;
+        z[SX(i)] = zi1;
+        nz = zi - f * zi1;
+      }
+      a = nd;
+      b = nb;
+      zi = nz;
+    }
+    u0[SX(n - 1)] = a == 0.0 ? tiny : a;
+    z[SX(n - 1)] = zi;
+    // back substitution
+    double x2 = 0.0, x1 = z[SX(n - 1)] / u0[SX(n - 1)];
+    z[SX(n - 1)] = x1;
+    double nrm = x1 * x1;
+    for (int i = n - 2; i >= 0; --i) {
+      const double x = (z[SX(i)] - u1[SX(i)] * x1 - u2[SX(i)] * x2) / u0[SX(i)];
+      z[SX(i)] = x;
+      nrm += x * x;
+      x2 = x1;
+      x1 = x;
+    }
+    scale = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+  }
+  for (int i = 0; i < n; ++i) Zr[static_cast<i64>(i) * n + j] = z[SX(i)] * scale;
+#undef SX
+}
+
 __global__ void transpose_sq_kernel(const double* __restrict__ src, int n, double* __restrict__ dst, i64 ldd) {
   __shared__ double tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
@@ -308,6 +494,35 @@ __global__ void backtransform_kernel(const double* H, i64 ldh, const double* tau
   }
 }
 
+// Same with the column of Z staged in shared memory (one warp per column,
+// each lane owns rows lane + 32m): the reflector loads are the only global
+// traffic on the serial chain.
+__global__ void __launch_bounds__(256) backtransform_smem_kernel(const double* __restrict__ H, i64 ldh,
+                                                                 const double* __restrict__ tau, int n, double* Z,
+                                                                 i64 ldz) {
+  extern __shared__ double bsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (col >= n) return;
+  double* z = bsm + static_cast<i64>(warp) * n;
+  double* zg = Z + static_cast<i64>(col) * ldz;
+  for (int i = lane; i < n; i += 32) z[i] = zg[i];
+  for (int k = n - 3; k >= 0; --k) {
+    const double t = tau[k];
+    if (t == 0.0) continue;
+    const double* v = H + static_cast<i64>(k) * ldh;
+    const int i0 = ((k + 1) & ~31) + lane;
+    double s = 0.0;
+    for (int i = i0; i < n; i += 32)
+      if (i > k) s += v[i] * z[i];
+    s = warp_sum(s);
+    const double ts = t * s;
+    for (int i = i0; i < n; i += 32)
+      if (i > k) z[i] -= ts * v[i];
+  }
+  for (int i = lane; i < n; i += 32) zg[i] = z[i];
+}
+
 }  // namespace
 
 void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
@@ -316,7 +531,42 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
   DBuf<double> d(n, ctx.stream), e(n, ctx.stream), tau(n, ctx.stream), p(2 * n, ctx.stream), lam(n, ctx.stream);
   DMat H;
   H.alloc(n, n, ctx.stream, true);
-  if (n >= 3) {
+  bool done_tri = false;
+  if (n >= 3 && !(std::getenv("NPCG_TRIDIAG") && std::string(std::getenv("NPCG_TRIDIAG")) == "global")) {
+    for (int C : {16, 8}) {  // cluster-resident variant when the matrix fits in C CTAs' shared memory
+      const i64 ncl = cdiv(n, C);
+      const i64 smem = (ncl * n + 4 * n + 2 * ncl) * 8;
+      if (smem > 220 * 1024) continue;
+      NPCG_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      NPCG_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(C);
+      cfg.blockDim = dim3(TRI_THREADS);
+      cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+      cfg.stream = ctx.stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = C;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, tridiag_cluster_kernel, &cfg) != cudaSuccess || nclusters < 1) {
+        (void)cudaGetLastError();
+        continue;
+      }
+      ctx.prof_begin("tridiag_cluster_kernel");
+      NPCG_CUDA(cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, static_cast<const double*>(M), ldm, nn, d.p, e.p,
+                                   tau.p, H.p(), H.ld));
+      ctx.check_launch("tridiag_cluster_kernel");
+      ctx.prof_end();
+      done_tri = true;
+      break;
+    }
+  }
+  if (n >= 3 && !done_tri) {
     const int smem = static_cast<int>(3 * n * 8);
     NPCG_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    std::max(smem, 48 * 1024)));
@@ -338,7 +588,7 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
                                           ctx.stream));
     ctx.check_launch("tridiag_kernel");
     ctx.prof_end();
-  } else {
+  } else if (n < 3) {
     // n <= 2: already tridiagonal
     std::vector<double> h(static_cast<size_t>(n * n));
     download(ctx, M, ldm, n, n, h.data(), n, NPCG_HOST);
@@ -351,14 +601,31 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
   DBuf<double> e2(n, ctx.stream), info(4, ctx.stream);
   NPCG_LAUNCH(ctx, tri_bounds_kernel, 1, 256, 0, d.p, e.p, nn, e2.p, info.p);
   NPCG_LAUNCH(ctx, bisect_kernel, static_cast<unsigned>(cdiv(n * 32, 256)), 256, 0, d.p, e2.p, nn, info.p, lam.p);
-  DBuf<double> iw(4 * n * n, ctx.stream), zr(n * n, ctx.stream);
-  DBuf<unsigned char> ipv(n * n, ctx.stream);
-  NPCG_LAUNCH(ctx, invit_kernel, static_cast<unsigned>(cdiv(n, 64)), 64, 0, d.p, e.p, lam.p, nn, info.p, zr.p, iw.p,
-              ipv.p);
+  DBuf<double> zr(n * n, ctx.stream);
+  const i64 per_vec = 4 * n * 8;
+  const int V = static_cast<int>(std::min<i64>(8, (200 * 1024) / per_vec));
+  if (V >= 1) {
+    const int smem = static_cast<int>(V * per_vec);
+    NPCG_CUDA(cudaFuncSetAttribute(invit_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    NPCG_LAUNCH(ctx, invit_smem_kernel, static_cast<unsigned>(cdiv(n, V)), V, smem, d.p, e.p, lam.p, nn, info.p,
+                zr.p);
+  } else {
+    DBuf<double> iw(4 * n * n, ctx.stream);
+    DBuf<unsigned char> ipv(n * n, ctx.stream);
+    NPCG_LAUNCH(ctx, invit_kernel, static_cast<unsigned>(cdiv(n, 64)), 64, 0, d.p, e.p, lam.p, nn, info.p, zr.p,
+                iw.p, ipv.p);
+  }
   NPCG_LAUNCH(ctx, transpose_sq_kernel, dim3(static_cast<unsigned>(cdiv(n, 32)), static_cast<unsigned>(cdiv(n, 32))),
               dim3(32, 8), 0, zr.p, nn, Z, ldz);
-  NPCG_LAUNCH(ctx, backtransform_kernel, static_cast<unsigned>(cdiv(n * 32, 256)), 256, 0, H.p(), H.ld, tau.p, nn, Z,
-              ldz);
+  if (8 * n * 8 <= 200 * 1024) {
+    const int smem = static_cast<int>(8 * n * 8);
+    NPCG_CUDA(cudaFuncSetAttribute(backtransform_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    NPCG_LAUNCH(ctx, backtransform_smem_kernel, static_cast<unsigned>(cdiv(n, 8)), 256, smem, H.p(), H.ld, tau.p, nn,
+                Z, ldz);
+  } else {
+    NPCG_LAUNCH(ctx, backtransform_kernel, static_cast<unsigned>(cdiv(n * 32, 256)), 256, 0, H.p(), H.ld, tau.p, nn,
+                Z, ldz);
+  }
 }
 
 }  // namespace npcg
