@@ -216,6 +216,8 @@ ALGO_NOTE = {
     "gemm_dmma_kernel": ("tensor", "2*M*N*K flops per launch (sketch X*Omega, X^T*Z, Gram/TRSM/CholeskyQR GEMMs)"),
     "coldot_kernel": ("hbm", "8*rows*cols matrix bytes + vectors per launch (X^T z, U^T r)"),
     "rowdot_kernel": ("hbm", "8*rows*cols matrix bytes + vectors per launch (X v, U t)"),
+    "pcg_persistent_kernel": ("hbm", "per PCG iteration: X once (8*m*n B; dense: 8*n^2), U twice (2*8*n*l B) "
+                                     "and ~10 n-vectors (80*n B); x iterations of the launch"),
 }
 
 

@@ -494,33 +494,48 @@ __global__ void backtransform_kernel(const double* H, i64 ldh, const double* tau
   }
 }
 
-// Same with the column of Z staged in shared memory (one warp per column,
-// each lane owns rows lane + 32m): the reflector loads are the only global
-// traffic on the serial chain.
+// Blocked: reflectors are staged 32 at a time in shared memory (one
+// coalesced load per block, shared by the CTA's 8 columns), each warp applies
+// them to its column of Z, also held in shared memory.
+constexpr int BT_KB = 32;
 __global__ void __launch_bounds__(256) backtransform_smem_kernel(const double* __restrict__ H, i64 ldh,
                                                                  const double* __restrict__ tau, int n, double* Z,
                                                                  i64 ldz) {
   extern __shared__ double bsm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int col = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (col >= n) return;
-  double* z = bsm + static_cast<i64>(warp) * n;
-  double* zg = Z + static_cast<i64>(col) * ldz;
-  for (int i = lane; i < n; i += 32) z[i] = zg[i];
-  for (int k = n - 3; k >= 0; --k) {
-    const double t = tau[k];
-    if (t == 0.0) continue;
-    const double* v = H + static_cast<i64>(k) * ldh;
-    const int i0 = ((k + 1) & ~31) + lane;
-    double s = 0.0;
-    for (int i = i0; i < n; i += 32)
-      if (i > k) s += v[i] * z[i];
-    s = warp_sum(s);
-    const double ts = t * s;
-    for (int i = i0; i < n; i += 32)
-      if (i > k) z[i] -= ts * v[i];
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * nw + warp;
+  double* vb = bsm;                                   // [BT_KB][n]: reflector k1 - kk at vb + kk*n
+  double* z = bsm + static_cast<i64>(BT_KB) * n + static_cast<i64>(warp) * n;
+  __shared__ double tb[BT_KB];
+  if (col < n)
+    for (int i = lane; i < n; i += 32) z[i] = Z[i + static_cast<i64>(col) * ldz];
+  for (int k1 = n - 3; k1 >= 0; k1 -= BT_KB) {
+    const int kb = min(BT_KB, k1 + 1);
+    __syncthreads();
+    for (int kk = warp; kk < kb; kk += nw) {
+      const int k = k1 - kk;
+      const double* v = H + static_cast<i64>(k) * ldh;
+      for (int i = lane; i < n; i += 32) vb[static_cast<i64>(kk) * n + i] = i > k ? v[i] : 0.0;
+      if (lane == 0) tb[kk] = tau[k];
+    }
+    __syncthreads();
+    if (col < n) {
+      for (int kk = 0; kk < kb; ++kk) {
+        const double t = tb[kk];
+        if (t == 0.0) continue;
+        const int k = k1 - kk;
+        const double* v = vb + static_cast<i64>(kk) * n;
+        const int i0 = ((k + 1) & ~31) + lane;
+        double s = 0.0;
+        for (int i = i0; i < n; i += 32) s += v[i] * z[i];
+        s = warp_sum(s);
+        const double ts = t * s;
+        for (int i = i0; i < n; i += 32) z[i] -= ts * v[i];
+      }
+    }
   }
-  for (int i = lane; i < n; i += 32) zg[i] = z[i];
+  if (col < n)
+    for (int i = lane; i < n; i += 32) Z[i + static_cast<i64>(col) * ldz] = z[i];
 }
 
 }  // namespace
@@ -617,8 +632,8 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
   }
   NPCG_LAUNCH(ctx, transpose_sq_kernel, dim3(static_cast<unsigned>(cdiv(n, 32)), static_cast<unsigned>(cdiv(n, 32))),
               dim3(32, 8), 0, zr.p, nn, Z, ldz);
-  if (8 * n * 8 <= 200 * 1024) {
-    const int smem = static_cast<int>(8 * n * 8);
+  if ((8 + BT_KB) * n * 8 <= 200 * 1024) {
+    const int smem = static_cast<int>((8 + BT_KB) * n * 8);
     NPCG_CUDA(cudaFuncSetAttribute(backtransform_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     NPCG_LAUNCH(ctx, backtransform_smem_kernel, static_cast<unsigned>(cdiv(n, 8)), 256, smem, H.p(), H.ld, tau.p, nn,
                 Z, ldz);

@@ -594,6 +594,17 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   else if (S == 1) launch_persistent<1, false>(ctx, pa, G);
   else launch_persistent<2, false>(ctx, pa, G);
   ctx.sync();  // work buffers are released on return
+  if (ctx.prof) {  // algorithmic traffic of the launch: per iteration A once, U twice, ~10 n-vectors
+    State h;
+    NPCG_CUDA(cudaMemcpy(&h, st, sizeof(State), cudaMemcpyDeviceToHost));
+    i64 iters = 0;
+    for (i64 s = 0; s < S; ++s) iters = std::max<i64>(iters, h.c[s].iters);
+    const double a_bytes = gram ? 8.0 * gram->m * n : 8.0 * n * n;
+    const double a_flops = gram ? 4.0 * gram->m * n * S : 2.0 * n * n * S;
+    const double u_bytes = nys ? 2.0 * 8.0 * n * pre->ell : 0.0;
+    const double u_flops = nys ? 4.0 * n * pre->ell * S : 0.0;
+    ctx.prof_work(iters * (a_flops + u_flops + 10.0 * n * S), iters * (a_bytes + u_bytes + 80.0 * n * S));
+  }
 }
 
 }  // namespace
