@@ -461,7 +461,8 @@ void orthonormalize(Ctx& ctx, const double* G_in, i64 ldg_in, i64 m, i64 n, doub
     L.alloc(n, n, ctx.stream, false);
     gemm(ctx, n, n, m, 1.0, Operand{Q, ldq, true}, Operand{Q, ldq, true}, 0.0, L.p(), L.ld);
     if (!shifted || more > 0) {
-      if (identity_deviation(ctx, L.p(), L.ld, n) <= 1e-14) break;
+      const double tol = std::max(1e-14, 4.0 * std::sqrt(static_cast<double>(m)) * 2.220446049250313e-16);
+      if (identity_deviation(ctx, L.p(), L.ld, n) <= tol) break;
     }
     CholFactor f;
     if (!cholesky(ctx, L.p(), n, L.ld, f))
@@ -577,6 +578,29 @@ void thin_svd(Ctx& ctx, const double* B, i64 ldb, i64 m, i64 n, double* U, i64 l
   gemm(ctx, m, n, n, 1.0, Operand{Q.p(), Q.ld, false}, Operand{Vs.p(), Vs.ld, true}, 0.0, U, ldu);
 }
 
+// Orthonormalise a square, nearly orthogonal Z by Newton-Schulz iteration
+// towards its polar factor, V <- 1.5 V - 0.5 V (V^T V): two DMMA GEMMs per
+// step, quadratic convergence, no factorisation. Returns false when Z is too
+// far from orthogonal for the iteration (max |Z^T Z - I| > 0.5).
+bool polar_orthonormalize(Ctx& ctx, const double* Z, i64 ldz, i64 n, double* V, i64 ldv) {
+  DMat G, Y;
+  G.alloc(n, n, ctx.stream, false);
+  Y.alloc(n, n, ctx.stream, false);
+  copy2d(ctx, n, n, Z, ldz, V, ldv);
+  const double tol = std::max(1e-14, 4.0 * std::sqrt(static_cast<double>(n)) * 2.220446049250313e-16);
+  double prev = 1e300;
+  for (int it = 0; it < 8; ++it) {
+    gemm(ctx, n, n, n, 1.0, Operand{V, ldv, true}, Operand{V, ldv, true}, 0.0, G.p(), G.ld);
+    const double dev = identity_deviation(ctx, G.p(), G.ld, n);
+    if (dev <= tol || (dev <= 1e-12 && dev > 0.25 * prev)) return true;  // converged / at the rounding floor
+    if (!(dev <= 0.5)) return false;
+    prev = dev;
+    copy2d(ctx, n, n, V, ldv, Y.p(), Y.ld);
+    gemm(ctx, n, n, n, -0.5, Operand{Y.p(), Y.ld, false}, Operand{G.p(), G.ld, true}, 1.5, V, ldv);
+  }
+  return false;
+}
+
 // SVD of R via the eigenvectors of R R^T = W^T W (W = R^T): the eigensolver
 // only has to deliver an orthogonal V that diagonalises W^T W to working
 // accuracy; the singular values are then the column norms of W V, which are
@@ -607,7 +631,7 @@ void small_svd_eig(Ctx& ctx, double* W, i64 ldw, i64 n, double* Vs, i64 ldv, dou
   scale_pow2(ctx, n, n, Ws.p(), Ws.ld, -e2);
   gemm(ctx, n, n, n, 1.0, Operand{Ws.p(), Ws.ld, true}, Operand{Ws.p(), Ws.ld, true}, 0.0, M.p(), M.ld);  // W^T W
   sym_eigvecs(ctx, M.p(), M.ld, n, Z.p(), Z.ld);
-  bool ok = try_orthonormalize(ctx, Z.p(), Z.ld, n, n, V.p(), V.ld);
+  bool ok = polar_orthonormalize(ctx, Z.p(), Z.ld, n, V.p(), V.ld) || try_orthonormalize(ctx, Z.p(), Z.ld, n, n, V.p(), V.ld);
   // Simultaneous-Jacobi refinement: G = (W V)^T (W V) has entries accurate
   // relative to the column norms; the first-order angles C_ij = G_ij/(G_jj -
   // G_ii) rotate V towards the singular vectors of the small sigma too (the
@@ -632,7 +656,7 @@ void small_svd_eig(Ctx& ctx, double* W, i64 ldw, i64 n, double* Vs, i64 ldv, dou
     }
     copy2d(ctx, n, n, V.p(), V.ld, T.p(), T.ld);
     gemm(ctx, n, n, n, 1.0, Operand{V.p(), V.ld, false}, Operand{Cm.p(), Cm.ld, true}, 1.0, T.p(), T.ld);
-    ok = try_orthonormalize(ctx, T.p(), T.ld, n, n, V.p(), V.ld);
+    ok = polar_orthonormalize(ctx, T.p(), T.ld, n, V.p(), V.ld) || try_orthonormalize(ctx, T.p(), T.ld, n, n, V.p(), V.ld);
   }
   if (!ok) {
     if (std::getenv("NPCG_DEBUG")) std::fprintf(stderr, "[npcg] svd: eigenvector path fell back to Jacobi\n");
