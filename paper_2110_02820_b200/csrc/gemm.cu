@@ -21,13 +21,13 @@
 namespace npcg {
 namespace {
 
-constexpr int BK = 16, STAGES = 5;
+constexpr int BK = 16;
 
 // CTA tile BM x BN with WM x WN consumer warps (warp tile TM x TN of m8n8
 // fragments) plus one TMA producer warp.
-template <int BM_, int BN_, int WM_, int WN_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_>
 struct Tile {
-  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_;
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_;
   static constexpr int NCW = WM * WN;
   // Whole consumer warpgroups: the producer gets its own warpgroup and hands
   // its registers to the consumers (setmaxnreg); otherwise a single producer warp.
@@ -36,11 +36,12 @@ struct Tile {
   static constexpr int TM = BM / WM, TN = BN / WN, FM = TM / 8, FN = TN / 8;
   static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8, STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
-  static_assert(TM % 16 == 0 && TN % 16 == 0, "warp tile must hold m/n pairs of fragments");
+  static_assert(TM % 16 == 0 && TN % 8 == 0, "warp tile must hold m pairs / whole n fragments");
   static_assert(STAGE_BYTES % 1024 == 0 && A_BYTES % 1024 == 0, "128B-swizzle atoms need 1 KB alignment");
 };
-using TileWide = Tile<128, 128, 2, 4>;    // 64 x 32 warp tiles
-using TileNarrow = Tile<128, 80, 2, 5>;   // 64 x 16 warp tiles; N = 80 k (e.g. l = 400) without padding
+using TileWide = Tile<128, 128, 2, 4, 6>;    // 64 x 32 warp tiles, 6 x 32 KB stages
+using TileNarrow = Tile<128, 80, 2, 5, 8>;   // 64 x 16 warp tiles, 8 x 26 KB stages; N = 80 k without padding
+using TileTall = Tile<256, 80, 4, 2, 5>;     // 64 x 40 warp tiles (odd n-fragment count: K-major B only)
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -88,7 +89,8 @@ __global__ void __launch_bounds__(T::THREADS, 1)
                      int M, int N, int ktiles, int ktiles_per_split, double alpha, double beta,
                      double* __restrict__ C, i64 ldc, double* __restrict__ partial) {
   constexpr int BM = T::BM, BN = T::BN, NCW = T::NCW, TM = T::TM, TN = T::TN, FM = T::FM, FN = T::FN;
-  constexpr int A_BYTES = T::A_BYTES, STAGE_BYTES = T::STAGE_BYTES;
+  constexpr int A_BYTES = T::A_BYTES, STAGE_BYTES = T::STAGE_BYTES, STAGES = T::STAGES;
+  static_assert(BKM || T::TN % 16 == 0, "N-major B reads n fragments in pairs");
   extern __shared__ uint8_t smem_raw[];
   // 1 KB-aligned ring; offsetting smem_raw (not casting through an integer)
   // keeps the pointer in the shared window, so fragment reads compile to LDS
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(T::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, split = blockIdx.z;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN, split = blockIdx.z;
   const int kt0 = split * ktiles_per_split;
   const int nk = max(0, min(kt0 + ktiles_per_split, ktiles) - kt0);
 
@@ -268,7 +270,8 @@ void launch(Ctx& ctx, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N
     NPCG_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<T, AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    T::SMEM_BYTES));
   });
-  dim3 grid(static_cast<unsigned>(cdiv(M, T::BM)), static_cast<unsigned>(cdiv(N, T::BN)),
+  // n-tiles fastest: the CTAs that share an A row block run together (A is read once from HBM)
+  dim3 grid(static_cast<unsigned>(cdiv(N, T::BN)), static_cast<unsigned>(cdiv(M, T::BM)),
             static_cast<unsigned>(splits));
   NPCG_LAUNCH(ctx, (gemm_dmma_kernel<T, AK, BKM>), grid, T::THREADS, T::SMEM_BYTES, ma, mb, M, N, ktiles, kps,
               alpha, beta, C, ldc, partial);
@@ -278,18 +281,21 @@ void launch(Ctx& ctx, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N
 // of a wave runs kps k-tiles at the per-SM DMMA rate (narrow tiles a little
 // slower: less fragment reuse), plus a fixed pipeline fill / epilogue cost and,
 // when split, the fixed-order reduction of the partials through HBM.
+enum TileKind { kWide = 0, kNarrow = 1, kTall = 2 };
 struct Plan {
-  bool narrow;
+  TileKind tile;
   int splits, kps;
 };
-Plan plan_gemm(const Ctx& ctx, i64 M, i64 N, i64 K) {
+Plan plan_gemm(const Ctx& ctx, i64 M, i64 N, i64 K, bool b_kmajor) {
   const int ktiles = static_cast<int>(cdiv(K, BK));
-  const double sm_rate = 34e12 / 148.0;  // measured DMMA flop/s per SM
-  Plan best{false, 1, ktiles};
+  const double sm_rate = 36e12 / 148.0;  // measured DMMA flop/s per SM (wide tile, 8192^3)
+  Plan best{kWide, 1, ktiles};
   double best_us = 1e300;
-  for (int narrow = 0; narrow < 2; ++narrow) {
-    const int bm = narrow ? TileNarrow::BM : TileWide::BM, bn = narrow ? TileNarrow::BN : TileWide::BN;
-    const double eff = narrow ? 0.95 : 1.0;
+  for (int tk = 0; tk < 3; ++tk) {
+    if (tk == kTall && !b_kmajor) continue;
+    const int bm = tk == kWide ? TileWide::BM : tk == kNarrow ? TileNarrow::BM : TileTall::BM;
+    const int bn = tk == kWide ? TileWide::BN : tk == kNarrow ? TileNarrow::BN : TileTall::BN;
+    const double eff = tk == kNarrow ? 0.83 : 1.0;  // measured at 8192^3: 30.1 vs 36.1 TF/s
     const i64 tiles = cdiv(M, bm) * cdiv(N, bn);
     const int max_split = std::max(1, std::min(64, ktiles / 4));
     for (int s = 1; s <= max_split; ++s) {
@@ -301,13 +307,13 @@ Plan plan_gemm(const Ctx& ctx, i64 M, i64 N, i64 K) {
       if (se > 1) us += (se + 2.0) * M * N * 8.0 / 6e12 * 1e6 + 3.0;
       if (us < best_us * 0.999) {
         best_us = us;
-        best = Plan{narrow != 0, se, kps};
+        best = Plan{static_cast<TileKind>(tk), se, kps};
       }
     }
   }
-  if (const char* f = std::getenv("NPCG_GEMM_FORCE")) {  // diagnostics: "<w|n>:<splits>"
+  if (const char* f = std::getenv("NPCG_GEMM_FORCE")) {  // diagnostics: "<w|n|t>:<splits>"
     const int s = std::max(1, std::min(ktiles, std::atoi(f + 2)));
-    best.narrow = f[0] == 'n';
+    best.tile = f[0] == 'n' ? kNarrow : (f[0] == 't' && b_kmajor) ? kTall : kWide;
     best.kps = static_cast<int>(cdiv(ktiles, s));
     best.splits = static_cast<int>(cdiv(ktiles, best.kps));
   }
@@ -319,10 +325,16 @@ void dispatch(Ctx& ctx, Operand A, Operand B, int m, int n, i64 K, int ktiles, i
               double beta, double* C, i64 ldc, double* pp) {
   const CUtensorMap ma = A.kmajor ? make_map(ctx, A.p, K, m, A.ld, T::BM) : make_map(ctx, A.p, m, K, A.ld, 16);
   const CUtensorMap mb = B.kmajor ? make_map(ctx, B.p, K, n, B.ld, T::BN) : make_map(ctx, B.p, n, K, B.ld, 16);
-  if (A.kmajor && B.kmajor) launch<T, true, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-  else if (A.kmajor) launch<T, true, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-  else if (B.kmajor) launch<T, false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-  else launch<T, false, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  if constexpr (T::TN % 16 == 0) {
+    if (A.kmajor && B.kmajor) launch<T, true, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+    else if (A.kmajor) launch<T, true, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+    else if (B.kmajor) launch<T, false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+    else launch<T, false, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  } else {
+    if (!B.kmajor) fail(NPCG_ERUNTIME, "gemm: tile needs a K-major B operand");
+    if (A.kmajor) launch<T, true, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+    else launch<T, false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  }
 }
 
 }  // namespace
@@ -341,7 +353,7 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
     return;
   }
   const int ktiles = static_cast<int>(cdiv(K, BK));
-  const Plan plan = plan_gemm(ctx, M, N, K);
+  const Plan plan = plan_gemm(ctx, M, N, K, B.kmajor);
   const int splits = plan.splits, kps = plan.kps;
   DBuf<double> part;
   double* pp = nullptr;
@@ -350,7 +362,8 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
     pp = part.p;
   }
   const int m = static_cast<int>(M), n = static_cast<int>(N);
-  if (plan.narrow) dispatch<TileNarrow>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  if (plan.tile == kNarrow) dispatch<TileNarrow>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  else if (plan.tile == kTall) dispatch<TileTall>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp);
   else dispatch<TileWide>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp);
   ctx.prof_work(2.0 * static_cast<double>(M) * N * K, 8.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N +
                                                               static_cast<double>(M) * N));
