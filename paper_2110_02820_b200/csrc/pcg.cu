@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[32];
-  __shared__ double red[2][PT / 32];
+  __shared__ double red[2][PT / 32], red2[2][PT / 32];
   __shared__ double zred[PT / 32][32];
   __shared__ ColState cs[S];
   __shared__ int running_sh;
@@ -327,29 +327,55 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
           const double* x = a.A + row * a.lda;
 #pragma unroll
           for (int k = 0; k < PV; ++k)
-            dst[k] = ok[k] ? __ldcs(reinterpret_cast<const double2*>(x + 2 * (tid + PT * k))) : make_double2(0.0, 0.0);
+            dst[k] = (ok[k] && row < a1) ? __ldcs(reinterpret_cast<const double2*>(x + 2 * (tid + PT * k)))
+                                         : make_double2(0.0, 0.0);
         };
-        if (a0 < a1) load_row(a0, cur);
+        // two rows per step (one barrier per pair), the next pair in flight
+        double2 cur2[PV], nxt2[PV];
+        load_row(a0, cur);
+        load_row(a0 + 1, cur2);
         int par = 0;
-        for (i64 row = a0; row < a1; ++row) {
-          if (row + 1 < a1) load_row(row + 1, nxt);
-          double d = 0.0;
+        for (i64 row = a0; row < a1; row += 2) {
+          load_row(row + 2, nxt);
+          load_row(row + 3, nxt2);
+          double d = 0.0, d2 = 0.0;
 #pragma unroll
-          for (int k = 0; k < PV; ++k) d += cur[k].x * pv[k].x + cur[k].y * pv[k].y;
-          d = warp_sum(d);
-          if (lane == 0) red[par][warp] = d;
+          for (int k = 0; k < PV; ++k) {
+            d += cur[k].x * pv[k].x + cur[k].y * pv[k].y;
+            d2 += cur2[k].x * pv[k].x + cur2[k].y * pv[k].y;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            d += __shfl_xor_sync(0xffffffffu, d, o);
+            d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+          }
+          if (lane == 0) {
+            red[par][warp] = d;
+            red2[par][warp] = d2;
+          }
           __syncthreads();
-          double sa = 0.0;
+          double sa0 = 0.0, sa1 = 0.0, sb0 = 0.0, sb1 = 0.0;  // fixed pairing: identical in every thread
 #pragma unroll
-          for (int w = 0; w < PT / 32; ++w) sa += red[par][w];
+          for (int w = 0; w < PT / 32; w += 2) {
+            sa0 += red[par][w];
+            sa1 += red[par][w + 1];
+            sb0 += red2[par][w];
+            sb1 += red2[par][w + 1];
+          }
+          const double sa = sa0 + sa1, sb = sb0 + sb1;
 #pragma unroll
           for (int k = 0; k < PV; ++k) {
             acc[k].x += sa * cur[k].x;
             acc[k].y += sa * cur[k].y;
+            acc[k].x += sb * cur2[k].x;
+            acc[k].y += sb * cur2[k].y;
           }
           par ^= 1;
 #pragma unroll
-          for (int k = 0; k < PV; ++k) cur[k] = nxt[k];
+          for (int k = 0; k < PV; ++k) {
+            cur[k] = nxt[k];
+            cur2[k] = nxt2[k];
+          }
         }
         double* dst = a.part + static_cast<i64>(c) * PW;
 #pragma unroll
