@@ -16,8 +16,12 @@ factorisation (shift, Cholesky, TRSM, thin SVD), preconditioner, PCG to 1e-10.
 
 `--impl reference` times the reference's CPU path (the oracle port; the
 reference itself cannot be built here: Eigen3/LAPACKE are absent) on all host
-cores, rank 0 only. Under torchrun each rank runs an independent replica of the
-workload (the single-GPU ridge path is replicated; "replicas only").
+cores, rank 0 only. Under torchrun (N > 1) the ridge workload is row-sharded
+(SURVEY §8e): rank g holds rows R_g of X, vectors are replicated, and every
+operator product is completed by an NCCL all-reduce (n doubles per PCG
+iteration, n x ell for the sketch) enqueued on the library stream through
+paper_2110_02820_b200/dist.py -- one solve split over N GPUs ("strong"
+scaling). Other workloads run one independent replica per GPU ("weak").
 """
 from __future__ import annotations
 
@@ -49,6 +53,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--small", action="store_true", help="reduced sizes (smoke runs)")
+    p.add_argument("--shard", action="store_true", help="row-sharded operator even at N = 1 (exercises the exchange)")
     return p.parse_args()
 
 
@@ -150,11 +155,11 @@ def dgemm_peak_tflops(torch):
 class DevicePath:
     """Drives the C-ABI with device-resident inputs (NPCG_DEVICE pointers)."""
 
-    def __init__(self, npcg, torch, w, ctx):
+    def __init__(self, npcg, torch, w, ctx, exchange=None):
         self.npcg, self.torch, self.w, self.ctx = npcg, torch, w, ctx
         L = npcg.lib()
         self.L = L
-        self.op = npcg.workloads.build_operator(npcg, w, ctx=ctx)
+        self.op = npcg.workloads.build_operator(npcg, w, ctx=ctx, exchange=exchange)
         n = w.n
         dev = torch.device("cuda", ctx.device)
         # column-major device buffers: torch (cols, rows) row-major == (rows, cols) col-major
@@ -186,9 +191,9 @@ class DevicePath:
         return [(r.iterations, bool(r.converged)) for r in self.reports]
 
 
-def e2e_step(npcg, w, ctx, host):
+def e2e_step(npcg, w, ctx, host, exchange=None):
     """Public API with host buffers: every input crosses PCIe inside the step."""
-    op = npcg.workloads.build_operator(npcg, host, ctx=ctx)
+    op = npcg.workloads.build_operator(npcg, host, ctx=ctx, exchange=exchange)
     pair = npcg.make_empty_sketch(op)
     pair = npcg.extend_sketch_with(pair, op, host.omega)
     approx = npcg.nystrom_from_sketch(pair)
@@ -299,7 +304,7 @@ def run_reference(args):
             "cpu_baseline": base, "e2e": {"value": base["value"], "unit": "solves/s", "h2d_bytes_per_step": 0,
                                           "d2h_bytes_per_step": 0},
             "wall_s": time.perf_counter() - t0}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -309,9 +314,14 @@ def run_b200(args):
     from paper_2110_02820_b200 import workloads
     npcg.workloads = workloads
     world, rank, local = dist_env()
-    if world > 1:
+    if world > 1 or args.shard:
         import torch.distributed as dist
         torch.cuda.set_device(local)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(local)
@@ -320,7 +330,12 @@ def run_b200(args):
     w = workloads.make(args.config, npcg.Rng, npcg.splitmix64,
                        gemm=lambda a, b, transa=False: npcg.gemm(a, b, transa=transa, ctx=ctx), **workload_kwargs(args))
     t_gen = time.perf_counter() - t_gen
-    path = DevicePath(npcg, torch, w, ctx)
+    exchange = None
+    sharded = (world > 1 or args.shard) and w.kind == "gram"
+    if sharded:
+        from paper_2110_02820_b200 import dist as pd
+        exchange = pd.TorchExchange()
+    path = DevicePath(npcg, torch, w, ctx, exchange)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 
     def barrier():
@@ -348,7 +363,7 @@ def run_b200(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed = float(t.item())
     ms_per_step = elapsed / args.steps * 1e3
-    value = world * args.steps / elapsed
+    value = (1 if sharded else world) * args.steps / elapsed  # sharded: the N GPUs share each solve
 
     # per-kernel CUDA-event timing in one instrumented step (same run, same stream)
     ctx.prof_enable(True)
@@ -364,7 +379,7 @@ def run_b200(args):
         host.data = {k: (pin(v) if isinstance(v, np.ndarray) and v.size > 1 else v) for k, v in w.data.items()}
         host.omega, host.b = pin(w.omega), pin(w.b)
         for _ in range(1):
-            e2e_step(npcg, w, ctx, host)
+            e2e_step(npcg, w, ctx, host, exchange)
         barrier()
         t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -372,7 +387,7 @@ def run_b200(args):
         e0.record(stream)
         k2 = max(1, min(args.steps, 3))
         for _ in range(k2):
-            e2e_step(npcg, w, ctx, host)
+            e2e_step(npcg, w, ctx, host, exchange)
         e1.record(stream)
         e1.synchronize()
         el = max(e0.elapsed_time(e1) / 1e3, 1e-9)
@@ -380,7 +395,8 @@ def run_b200(args):
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": world * k2 / el, "unit": "solves/s", "h2d_bytes_per_step": int(input_bytes(w)),
+        h2d = input_bytes(w) - (w.data["x"].nbytes * (1 - 1 / world) if sharded else 0)  # this rank's X block
+        e2e = {"value": (1 if sharded else world) * k2 / el, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(w.b.nbytes + 8 * w.ell), "steps": k2,
                "wall_s": time.perf_counter() - t0}
 
@@ -402,15 +418,17 @@ def run_b200(args):
         cpu = cpu_baseline(wc, steps=1)
     line = {
         "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng mt19937_64+Box-Muller, seeded)",
-        "config": {**w.describe(), "parallelism": f"replicas{world}", "l2": "inputs larger than L2 (X 640 MB)",
+        "config": {**w.describe(), "parallelism": f"rowshard{world}" if sharded else f"replicas{world}",
+                   "l2": "inputs larger than L2 (X 640 MB)",
                    "iterations": info[0][0], "converged": info[0][1]},
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
         "clocks": clk.summary(), "input_generation_s": t_gen,
     }
-    print(json.dumps(line))
-    if world > 1:
+    print(json.dumps(line), flush=True)
+    if world > 1 or args.shard:
         torch.distributed.destroy_process_group()
     return 0
 

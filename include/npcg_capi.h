@@ -103,6 +103,22 @@ int npcg_op_synthesize(npcg_ctx* ctx, int64_t n, const double* lambda, uint64_t 
 /* A = G diag(lambda) G^T / r (low-rank synthetic psd; BASELINE config 5). */
 int npcg_op_lowrank_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g, int64_t ldg,
                            const double* lambda, int where, npcg_op** out);
+/* Row-sharded operators for one-process-per-GPU runs (no
+ * reference counterpart: the reference is single-process). Vectors stay
+ * replicated; `fn` completes each local product on the library stream:
+ *   kind 0: in-place sum all-reduce of `count` doubles (send == recv);
+ *   kind 1: all-gather of `count` doubles per rank into recv, rank-major.
+ * The host binds it to NCCL (paper_2110_02820_b200/dist.py, torch.distributed). */
+typedef int (*npcg_exchange_fn)(void* user, int kind, double* send, double* recv, int64_t count, void* stream);
+/* GramRidgeOperator over the row block X_g (m_local x n) of a design with
+ * m_total rows: A v = all-reduce_g X_g^T (X_g v) / m_total. */
+int npcg_op_gram_shard_create(npcg_ctx* ctx, int64_t m_local, int64_t n, const double* g, int64_t ldg,
+                              int where, int64_t m_total, npcg_exchange_fn fn, void* user, npcg_op** out);
+/* DenseOperator over the column block A[:, rank*nb : rank*nb + nloc] (n x nloc,
+ * nb = ceil(n / nranks)) of a symmetric A: A v = all-gather_g A[:, R_g]^T v.
+ * (The symmetry check needs the whole matrix and is the caller's.) */
+int npcg_op_dense_shard_create(npcg_ctx* ctx, int64_t n, int64_t nranks, int64_t rank, const double* a_block,
+                               int64_t lda, int where, npcg_exchange_fn fn, void* user, npcg_op** out);
 int npcg_op_destroy(npcg_op* op);
 int npcg_op_dim(const npcg_op* op, int64_t* n);
 int npcg_op_kind(const npcg_op* op); /* 0 dense, 1 gram, 2 kernel stored, 3 kernel matrix-free */

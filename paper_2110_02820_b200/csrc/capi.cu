@@ -309,6 +309,7 @@ int npcg_op_gram_create(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, in
     op->ctx = &c;
     op->n = n;
     op->m = m;
+    op->div = static_cast<double>(m);
     op->kind = kGram;
     {
       DMat colmajor;  // caller layout, then the row-major copy the kernels stream
@@ -318,6 +319,69 @@ int npcg_op_gram_create(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, in
       op->xr.alloc(n, m, c.stream, true);
       transpose(c, colmajor.p(), colmajor.ld, m, n, op->xr.p(), op->xr.ld);
     }
+    *out = new npcg_op{ctx, std::move(op)};
+  });
+}
+
+int npcg_op_gram_shard_create(npcg_ctx* ctx, int64_t m_local, int64_t n, const double* g, int64_t ldg, int where,
+                              int64_t m_total, npcg_exchange_fn fn, void* user, npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (m_local < 1 || n < 1 || m_total < m_local) invalid("GramRidgeOperator shard: bad block dimensions");
+    if (!fn) invalid("sharded operator: exchange callback required");
+    auto local = std::make_unique<GramOp>();
+    local->ctx = &c;
+    local->n = n;
+    local->m = m_local;
+    local->div = static_cast<double>(m_total);
+    local->kind = kGram;
+    {
+      DMat colmajor;
+      upload(c, colmajor, m_local, n, g, ldg, where);
+      if (!all_finite(c, colmajor.p(), m_local, n, colmajor.ld))
+        invalid("GramRidgeOperator: design matrix has non-finite entries");
+      local->xr.alloc(n, m_local, c.stream, true);
+      transpose(c, colmajor.p(), colmajor.ld, m_local, n, local->xr.p(), local->xr.ld);
+    }
+    auto op = std::make_unique<ShardOp>();
+    op->ctx = &c;
+    op->n = n;
+    op->kind = kGram;
+    op->mode = 0;
+    op->local = std::move(local);
+    op->fn = fn;
+    op->user = user;
+    *out = new npcg_op{ctx, std::move(op)};
+  });
+}
+
+int npcg_op_dense_shard_create(npcg_ctx* ctx, int64_t n, int64_t nranks, int64_t rank, const double* a_block,
+                               int64_t lda, int where, npcg_exchange_fn fn, void* user, npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks) invalid("DenseOperator shard: bad rank layout");
+    if (!fn) invalid("sharded operator: exchange callback required");
+    const i64 nmax = cdiv(n, nranks), off = rank * nmax, nloc = std::min<i64>(nmax, n - off);
+    if (nloc < 1) invalid("DenseOperator shard: more ranks than rows");
+    auto local = std::make_unique<DenseColBlockOp>();
+    local->ctx = &c;
+    local->n = n;
+    local->nloc = nloc;
+    local->kind = kDense;
+    upload(c, local->a, n, nloc, a_block, lda, where);
+    if (!all_finite(c, local->a.p(), n, nloc, local->a.ld))
+      invalid("DenseOperator: matrix has non-finite entries");
+    auto op = std::make_unique<ShardOp>();
+    op->ctx = &c;
+    op->n = n;
+    op->kind = kDense;
+    op->mode = 1;
+    op->nranks = nranks;
+    op->rank = rank;
+    op->nmax = nmax;
+    op->local = std::move(local);
+    op->fn = fn;
+    op->user = user;
     *out = new npcg_op{ctx, std::move(op)};
   });
 }

@@ -125,7 +125,7 @@ void gram_single_pass(Ctx& ctx, const GramOp& op, const double* V, i64 ldv, doub
                 gate);
     ctx.prof_work(4.0 * op.m * std::min(width, op.n - col0) * S, 8.0 * op.m * std::min(width, op.n - col0));
     NPCG_LAUNCH(ctx, gram_finish_kernel, static_cast<unsigned>(cdiv(width * S, 256)), 256, 0, part.p, parts, S,
-                op.n, col0, static_cast<double>(op.m), mu, P, ldp, out, ldo, gate);
+                op.n, col0, op.div, mu, P, ldp, out, ldo, gate);
   }
 }
 
@@ -150,7 +150,7 @@ void GramOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const 
     gemm(*ctx, m, k, n, 1.0, Operand{xr.p(), xr.ld, true}, Operand{V, ldv, true}, 0.0, z.p(), z.ld);
     gemm(*ctx, n, k, m, 1.0, Operand{xr.p(), xr.ld, false}, Operand{z.p(), z.ld, true}, 0.0, out, ldo);
   }
-  divide(*ctx, n, k, out, ldo, static_cast<double>(m));
+  divide(*ctx, n, k, out, ldo, div);
 }
 
 void GramOp::apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) {

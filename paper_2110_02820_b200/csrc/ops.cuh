@@ -37,6 +37,7 @@ struct DenseOp : Op {  // DenseOperator (operators.cpp:64-80); also the stored k
 struct GramOp : Op {  // GramRidgeOperator (operators.cpp:105-121): (1/m) G^T (G v)
   DMat xr;            // design stored row-major: n x m col-major, data row a contiguous
   i64 m = 0;
+  double div = 0.0;   // out /= div (operators.cpp:115); the global row count when X is a row shard
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
   void apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) override;
 };
@@ -50,6 +51,33 @@ struct KernelFreeOp : Op {  // KernelOperator beyond dense_cap (operators.cpp:15
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
   bool has_column() const override { return true; }
   void column(i64 j, double* out) override;
+};
+
+/// Exchange callback of a sharded operator (npcg_exchange_fn in the C-ABI):
+/// kind 0 = in-place sum all-reduce of `count` doubles (send == recv);
+/// kind 1 = all-gather of `count` doubles per rank into recv (rank-major).
+/// Enqueued on `stream`; returns 0 on success.
+using ExchangeFn = int (*)(void* user, int kind, double* send, double* recv, int64_t count, void* stream);
+
+/// Column block A[:, off : off+nloc] of a symmetric A held by one rank; its
+/// apply gives rows off.. of A V (A^T V restricted to the block).
+struct DenseColBlockOp : Op {
+  DMat a;   // n x nloc
+  i64 nloc = 0;
+  void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
+};
+
+/// Row-sharded operator for one-process-per-GPU runs: `local` computes this
+/// rank's share, `fn` completes it (mode 0: all-reduce of partial products --
+/// Gram over a row block of X; mode 1: all-gather of row blocks -- dense
+/// column block). Vectors are replicated on every rank.
+struct ShardOp : Op {
+  std::unique_ptr<Op> local;
+  int mode = 0;
+  i64 nranks = 1, rank = 0, nmax = 0;  // mode 1: equal blocks of nmax rows (last one short)
+  ExchangeFn fn = nullptr;
+  void* user = nullptr;
+  void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
 };
 
 /// Build the stored Gaussian kernel matrix (operators.cpp:125-150) on device.

@@ -583,7 +583,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
     pa.m = gram->m;
     pa.A = gram->xr.p();
     pa.lda = gram->xr.ld;
-    pa.div = static_cast<double>(gram->m);
+    pa.div = gram->div;
     pa.rows_per_cta = cdiv(gram->m, G);
   } else {
     pa.A = dense->a.p();
