@@ -608,7 +608,10 @@ bool polar_orthonormalize(Ctx& ctx, const double* Z, i64 ldz, i64 n, double* V, 
 // Gram moves them only at second order), not just relative to sigma_1.
 void small_svd_eig(Ctx& ctx, double* W, i64 ldw, i64 n, double* Vs, i64 ldv, double* sigma) {
   if (n <= 0) return;
-  if (n <= 110) {  // the whole one-sided Jacobi fits one CTA's shared memory: exact and fast
+  // Tiny R: one-CTA one-sided Jacobi (its sweeps cost O(n^3) per CTA, so beyond
+  // a few dozen columns the eigenvector path is faster; Jacobi stays the fallback).
+  static const int jacobi_max = std::getenv("NPCG_JACOBI_MAX") ? std::atoi(std::getenv("NPCG_JACOBI_MAX")) : 24;
+  if (n <= jacobi_max) {
     jacobi_svd_small(ctx, W, ldw, n, Vs, ldv, sigma);
     return;
   }

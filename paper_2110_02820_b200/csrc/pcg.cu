@@ -257,7 +257,8 @@ struct PersistArgs {
   double *R, *Z, *P0, *P1, *V;
   i64 ldw;
   double* T;
-  double* part;                       // gram: G x PW
+  double* part;                       // gram: G x PW; dense: ncb x S x pstride
+  i64 nrb, ncb, cpb, pstride;         // dense: row blocks of PW rows, column blocks of cpb columns
   double *pv_part, *rr_part, *rz_part;  // G x S
   State* st;
   double* hist;
@@ -399,25 +400,80 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         pvl = block_sum(pvl, sh);
         if (tid == 0) a.pv_part[c] = pvl;
       } else {
-        // dense: (A p)_j for the slice columns; p_t recomputed on the fly
+        // dense: v = A p_t streamed column by column (axpy form, A col-major):
+        // CTA (rb, cb) owns rows [rb*PW, +PW) x columns [cb*cpb, +cpb); each
+        // column segment is one contiguous 32 KB read, two columns per step
+        // with the next two in flight; partial_cb = A[rows, cols_cb] p_t[cols_cb].
+        const int nrb = static_cast<int>(a.nrb), ncb = static_cast<int>(a.ncb);
+        if (c < nrb * ncb) {
+          const int rb = c % nrb, cb = c / nrb;
+          const i64 rb0 = static_cast<i64>(rb) * PW;
+          const i64 cb0 = static_cast<i64>(cb) * a.cpb, cb1 = min(n, cb0 + a.cpb);
+          double2 acc[S][PV];
+          bool ok[PV];
+#pragma unroll
+          for (int k = 0; k < PV; ++k) {
+            ok[k] = rb0 + 2 * (tid + static_cast<i64>(PT) * k) < n;
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s][k] = make_double2(0.0, 0.0);
+          }
+          auto load_col = [&](i64 j, double2* dst) {
+            const double* colp = a.A + j * a.lda + rb0;
+#pragma unroll
+            for (int k = 0; k < PV; ++k)
+              dst[k] = (ok[k] && j < cb1) ? __ldcs(reinterpret_cast<const double2*>(colp + 2 * (tid + PT * k)))
+                                          : make_double2(0.0, 0.0);
+          };
+          double2 c0[PV], c1[PV], n0[PV], n1[PV];
+          load_col(cb0, c0);
+          load_col(cb0 + 1, c1);
+          for (i64 j = cb0; j < cb1; j += 2) {
+            load_col(j + 2, n0);
+            load_col(j + 3, n1);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              const double p0 = p_at(j, s), p1 = j + 1 < cb1 ? p_at(j + 1, s) : 0.0;
+#pragma unroll
+              for (int k = 0; k < PV; ++k) {
+                acc[s][k].x += c0[k].x * p0;
+                acc[s][k].y += c0[k].y * p0;
+                acc[s][k].x += c1[k].x * p1;
+                acc[s][k].y += c1[k].y * p1;
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < PV; ++k) {
+              c0[k] = n0[k];
+              c1[k] = n1[k];
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            double* dst = a.part + (static_cast<i64>(cb) * S + s) * a.pstride + rb0;
+#pragma unroll
+            for (int k = 0; k < PV; ++k) {
+              const i64 i = 2 * (tid + static_cast<i64>(PT) * k);
+              if (rb0 + i + 1 < n) {
+                reinterpret_cast<double2*>(dst)[tid + PT * k] = acc[s][k];
+              } else if (rb0 + i < n) {
+                dst[i] = acc[s][k].x;
+              }
+            }
+          }
+        }
+        grid.sync();
+        // ---- P2 (dense): v = (sum_cb partial_cb) + mu p for the slice, partial p.v
         double pvl[S];
 #pragma unroll
         for (int s = 0; s < S; ++s) pvl[s] = 0.0;
         for (i64 j = r0 + warp; j < r1; j += PT / 32) {
-          const double* col = a.A + j * a.lda;
-          double acc[S];
-#pragma unroll
-          for (int s = 0; s < S; ++s) acc[s] = 0.0;
-          for (i64 i = lane; i < n; i += 32) {
-            const double aij = col[i];
-#pragma unroll
-            for (int s = 0; s < S; ++s) acc[s] += aij * p_at(i, s);
-          }
 #pragma unroll
           for (int s = 0; s < S; ++s) {
-            const double av = warp_sum(acc[s]);
-            const double pj = p_at(j, s);
-            double v = av;
+            double sum = 0.0;
+            for (int b = lane; b < ncb; b += 32) sum += a.part[(static_cast<i64>(b) * S + s) * a.pstride + j];
+            sum = warp_sum(sum);
+            const double pj = pcur[j + s * a.ldw];
+            double v = sum;  // operators.cpp:72-78 then solvers.cpp:137-141: out = A p; out += mu p
             v += a.mu * pj;
             if (lane == 0) {
               a.V[j + s * a.ldw] = v;
@@ -541,7 +597,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
 bool persistent_eligible(const Ctx& ctx, Op& op, i64 S) {
   (void)ctx;
   if (auto* g = dynamic_cast<GramOp*>(&op)) return S == 1 && g->n <= PW && g->m >= 1;
-  if (dynamic_cast<DenseOp*>(&op)) return S <= 2;
+  if (dynamic_cast<DenseOp*>(&op)) return S <= 2 && cdiv(op.n, PW) <= ctx.sm_count;
   return false;
 }
 
@@ -575,6 +631,15 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   P1.alloc(n, S, ctx.stream, false);
   DBuf<double> part, T, scal(3 * static_cast<i64>(G) * S, ctx.stream);
   if (gram) part.alloc(static_cast<i64>(G) * PW, ctx.stream);
+  i64 nrb = 0, ncb = 0, cpb = 0, pstride = 0;
+  if (dense) {
+    nrb = cdiv(n, PW);
+    ncb = std::max<i64>(1, G / nrb);
+    cpb = cdiv(n, ncb);
+    ncb = cdiv(n, cpb);
+    pstride = round_up(n, 2);
+    part.alloc(ncb * S * pstride, ctx.stream);
+  }
   if (nys) T.alloc(pre->ell * S, ctx.stream);
   PersistArgs pa{};
   pa.n = n;
@@ -607,6 +672,10 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   pa.V = V.p();
   pa.ldw = R.ld;
   pa.part = part.p;
+  pa.nrb = nrb;
+  pa.ncb = ncb;
+  pa.cpb = cpb;
+  pa.pstride = pstride;
   pa.pv_part = scal.p;
   pa.rr_part = scal.p + G * S;
   pa.rz_part = scal.p + 2 * G * S;
