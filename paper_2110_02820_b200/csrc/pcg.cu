@@ -312,6 +312,9 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         for (i64 i = r0 + tid; i < r1; i += PT)
 #pragma unroll
           for (int s = 0; s < S; ++s) pcur[i + s * a.ldw] = p_at(i, s);
+      if constexpr (!GRAM) {
+        if (!first) grid.sync();  // dense streams p_t from pcur
+      }
       if constexpr (GRAM) {
         static_assert(S == 1, "gram persistent path is single right-hand side");
         double2 pv[PV], acc[PV], cur[PV], nxt[PV];
@@ -404,15 +407,17 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         // CTA (rb, cb) owns rows [rb*PW, +PW) x columns [cb*cpb, +cpb); each
         // column segment is one contiguous 32 KB read, two columns per step
         // with the next two in flight; partial_cb = A[rows, cols_cb] p_t[cols_cb].
+        constexpr int PVD = S <= 2 ? PV : 2;  // fewer row slots per thread when 3-4 RHS share the pass
+        constexpr int PWD = 2 * PT * PVD;
         const int nrb = static_cast<int>(a.nrb), ncb = static_cast<int>(a.ncb);
         if (c < nrb * ncb) {
           const int rb = c % nrb, cb = c / nrb;
-          const i64 rb0 = static_cast<i64>(rb) * PW;
+          const i64 rb0 = static_cast<i64>(rb) * PWD;
           const i64 cb0 = static_cast<i64>(cb) * a.cpb, cb1 = min(n, cb0 + a.cpb);
-          double2 acc[S][PV];
-          bool ok[PV];
+          double2 acc[S][PVD];
+          bool ok[PVD];
 #pragma unroll
-          for (int k = 0; k < PV; ++k) {
+          for (int k = 0; k < PVD; ++k) {
             ok[k] = rb0 + 2 * (tid + static_cast<i64>(PT) * k) < n;
 #pragma unroll
             for (int s = 0; s < S; ++s) acc[s][k] = make_double2(0.0, 0.0);
@@ -420,21 +425,31 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
           auto load_col = [&](i64 j, double2* dst) {
             const double* colp = a.A + j * a.lda + rb0;
 #pragma unroll
-            for (int k = 0; k < PV; ++k)
+            for (int k = 0; k < PVD; ++k)
               dst[k] = (ok[k] && j < cb1) ? __ldcs(reinterpret_cast<const double2*>(colp + 2 * (tid + PT * k)))
                                           : make_double2(0.0, 0.0);
           };
-          double2 c0[PV], c1[PV], n0[PV], n1[PV];
+          // p_t of the whole vector is in pcur (slice owners wrote it before the barrier)
+          auto load_p = [&](i64 j, double* dst) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) dst[s] = j < cb1 ? pcur[j + s * a.ldw] : 0.0;
+          };
+          double2 c0[PVD], c1[PVD], n0[PVD], n1[PVD];
+          double q0[S], q1[S], m0[S], m1[S];
           load_col(cb0, c0);
           load_col(cb0 + 1, c1);
+          load_p(cb0, q0);
+          load_p(cb0 + 1, q1);
           for (i64 j = cb0; j < cb1; j += 2) {
             load_col(j + 2, n0);
             load_col(j + 3, n1);
+            load_p(j + 2, m0);
+            load_p(j + 3, m1);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-              const double p0 = p_at(j, s), p1 = j + 1 < cb1 ? p_at(j + 1, s) : 0.0;
+              const double p0 = q0[s], p1 = q1[s];
 #pragma unroll
-              for (int k = 0; k < PV; ++k) {
+              for (int k = 0; k < PVD; ++k) {
                 acc[s][k].x += c0[k].x * p0;
                 acc[s][k].y += c0[k].y * p0;
                 acc[s][k].x += c1[k].x * p1;
@@ -442,16 +457,21 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
               }
             }
 #pragma unroll
-            for (int k = 0; k < PV; ++k) {
+            for (int k = 0; k < PVD; ++k) {
               c0[k] = n0[k];
               c1[k] = n1[k];
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              q0[s] = m0[s];
+              q1[s] = m1[s];
             }
           }
 #pragma unroll
           for (int s = 0; s < S; ++s) {
             double* dst = a.part + (static_cast<i64>(cb) * S + s) * a.pstride + rb0;
 #pragma unroll
-            for (int k = 0; k < PV; ++k) {
+            for (int k = 0; k < PVD; ++k) {
               const i64 i = 2 * (tid + static_cast<i64>(PT) * k);
               if (rb0 + i + 1 < n) {
                 reinterpret_cast<double2*>(dst)[tid + PT * k] = acc[s][k];
@@ -597,7 +617,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
 bool persistent_eligible(const Ctx& ctx, Op& op, i64 S) {
   (void)ctx;
   if (auto* g = dynamic_cast<GramOp*>(&op)) return S == 1 && g->n <= PW && g->m >= 1;
-  if (dynamic_cast<DenseOp*>(&op)) return S <= 2 && cdiv(op.n, PW) <= ctx.sm_count;
+  if (dynamic_cast<DenseOp*>(&op)) return S <= 4 && cdiv(op.n, S <= 2 ? PW : 2 * PT * 2) <= ctx.sm_count;
   return false;
 }
 
@@ -625,15 +645,17 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   auto* dense = dynamic_cast<DenseOp*>(&op);
   const i64 n = op.n;
   const bool nys = pre != nullptr && pre->ell > 0;
-  const int G = gram ? persistent_grid<1, true>(ctx) : (S == 1 ? persistent_grid<1, false>(ctx)
-                                                               : persistent_grid<2, false>(ctx));
+  const int G = gram ? persistent_grid<1, true>(ctx)
+                     : S == 1 ? persistent_grid<1, false>(ctx)
+                     : S == 2 ? persistent_grid<2, false>(ctx)
+                     : S == 3 ? persistent_grid<3, false>(ctx) : persistent_grid<4, false>(ctx);
   DMat P1;
   P1.alloc(n, S, ctx.stream, false);
   DBuf<double> part, T, scal(3 * static_cast<i64>(G) * S, ctx.stream);
   if (gram) part.alloc(static_cast<i64>(G) * PW, ctx.stream);
   i64 nrb = 0, ncb = 0, cpb = 0, pstride = 0;
   if (dense) {
-    nrb = cdiv(n, PW);
+    nrb = cdiv(n, S <= 2 ? PW : 2 * PT * 2);  // PWD of the kernel
     ncb = std::max<i64>(1, G / nrb);
     cpb = cdiv(n, ncb);
     ncb = cdiv(n, cpb);
@@ -687,7 +709,9 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   if (P.ld != R.ld || V.ld != R.ld || P1.ld != R.ld || (nys && Z.ld != R.ld)) fail(NPCG_ERUNTIME, "pcg: work layout");
   if (gram) launch_persistent<1, true>(ctx, pa, G);
   else if (S == 1) launch_persistent<1, false>(ctx, pa, G);
-  else launch_persistent<2, false>(ctx, pa, G);
+  else if (S == 2) launch_persistent<2, false>(ctx, pa, G);
+  else if (S == 3) launch_persistent<3, false>(ctx, pa, G);
+  else launch_persistent<4, false>(ctx, pa, G);
   ctx.sync();  // work buffers are released on return
   if (ctx.prof) {  // algorithmic traffic of the launch: per iteration A once, U twice, ~10 n-vectors
     State h;
