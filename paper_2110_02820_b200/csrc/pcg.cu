@@ -20,6 +20,7 @@
 #include <cstring>
 #include <sstream>
 
+#include "async.cuh"
 #include "blas.cuh"
 #include "pcg.cuh"
 
@@ -243,6 +244,8 @@ __global__ void snapshot_running_kernel(const State* __restrict__ st, int S, int
 constexpr int PT = 512;  // threads per CTA
 constexpr int PV = 4;    // double2 slots per thread in the gram row pass: n <= 2*PT*PV
 constexpr int PW = 2 * PT * PV;
+constexpr int NST = 6;   // shared-memory ring stages of one PW-double segment (a row of X / a column segment of A)
+constexpr int RING_BYTES = NST * PW * 8;
 
 struct PersistArgs {
   i64 n, m;
@@ -274,7 +277,27 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   __shared__ double zred[PT / 32][32];
   __shared__ ColState cs[S];
   __shared__ int running_sh;
+  __shared__ uint64_t full_bar[NST];
+  extern __shared__ __align__(128) double ring[];  // NST x PW doubles, fed by bulk copies (TMA)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t ring_head = 0, ring_tail = 0;  // segments consumed (all threads) / issued (thread 0)
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) mbarrier_init(&full_bar[q], 1);
+    mbarrier_fence_init();
+  }
+  auto ring_issue = [&](const double* src, i64 count) {  // thread 0 only
+    const int slot = static_cast<int>(ring_tail % NST);
+    const uint32_t bytes = static_cast<uint32_t>(round_up(count, 2) * 8);
+    mbarrier_expect_tx(&full_bar[slot], bytes);
+    bulk_copy_g2s(ring + static_cast<i64>(slot) * PW, src, bytes, &full_bar[slot]);
+    ++ring_tail;
+  };
+  auto ring_wait = [&]() -> const double* {  // next segment, in issue order
+    const int slot = static_cast<int>(ring_head % NST);
+    mbarrier_wait_parity(&full_bar[slot], (ring_head / NST) & 1u);
+    ++ring_head;
+    return ring + static_cast<i64>(slot) * PW;
+  };
   const int G = gridDim.x, c = blockIdx.x;
   const i64 n = a.n;
   const i64 r0 = min(n, static_cast<i64>(c) * a.slice), r1 = min(n, r0 + a.slice);
@@ -405,77 +428,68 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
       } else {
         // dense: v = A p_t streamed column by column (axpy form, A col-major):
         // CTA (rb, cb) owns rows [rb*PW, +PW) x columns [cb*cpb, +cpb); each
-        // column segment is one contiguous 32 KB read, two columns per step
-        // with the next two in flight; partial_cb = A[rows, cols_cb] p_t[cols_cb].
-        constexpr int PVD = S <= 2 ? PV : 2;  // fewer row slots per thread when 3-4 RHS share the pass
-        constexpr int PWD = 2 * PT * PVD;
+        // column segment is one contiguous bulk copy into the shared-memory
+        // ring (NST segments in flight); two columns per step, one block
+        // barrier per step frees their slots. partial_cb = A[rows, cols_cb] p_t[cols_cb].
         const int nrb = static_cast<int>(a.nrb), ncb = static_cast<int>(a.ncb);
         if (c < nrb * ncb) {
           const int rb = c % nrb, cb = c / nrb;
-          const i64 rb0 = static_cast<i64>(rb) * PWD;
+          const i64 rb0 = static_cast<i64>(rb) * PW, cnt = min(static_cast<i64>(PW), n - rb0);
           const i64 cb0 = static_cast<i64>(cb) * a.cpb, cb1 = min(n, cb0 + a.cpb);
-          double2 acc[S][PVD];
-          bool ok[PVD];
+          double2 acc[S][PV];
+          bool ok[PV];
 #pragma unroll
-          for (int k = 0; k < PVD; ++k) {
-            ok[k] = rb0 + 2 * (tid + static_cast<i64>(PT) * k) < n;
+          for (int k = 0; k < PV; ++k) {
+            ok[k] = 2 * (tid + static_cast<i64>(PT) * k) < cnt;
 #pragma unroll
             for (int s = 0; s < S; ++s) acc[s][k] = make_double2(0.0, 0.0);
           }
-          auto load_col = [&](i64 j, double2* dst) {
-            const double* colp = a.A + j * a.lda + rb0;
-#pragma unroll
-            for (int k = 0; k < PVD; ++k)
-              dst[k] = (ok[k] && j < cb1) ? __ldcs(reinterpret_cast<const double2*>(colp + 2 * (tid + PT * k)))
-                                          : make_double2(0.0, 0.0);
-          };
+          if (tid == 0)
+            for (i64 j = cb0; j < min(cb1, cb0 + NST); ++j) ring_issue(a.A + j * a.lda + rb0, cnt);
           // p_t of the whole vector is in pcur (slice owners wrote it before the barrier)
           auto load_p = [&](i64 j, double* dst) {
 #pragma unroll
             for (int s = 0; s < S; ++s) dst[s] = j < cb1 ? pcur[j + s * a.ldw] : 0.0;
           };
-          double2 c0[PVD], c1[PVD], n0[PVD], n1[PVD];
-          double q0[S], q1[S], m0[S], m1[S];
-          load_col(cb0, c0);
-          load_col(cb0 + 1, c1);
-          load_p(cb0, q0);
-          load_p(cb0 + 1, q1);
+          double q0[S], q1[S];
           for (i64 j = cb0; j < cb1; j += 2) {
-            load_col(j + 2, n0);
-            load_col(j + 3, n1);
-            load_p(j + 2, m0);
-            load_p(j + 3, m1);
+            const bool two = j + 1 < cb1;
+            load_p(j, q0);
+            load_p(j + 1, q1);
+            const double* s0 = ring_wait();
+            const double* s1 = two ? ring_wait() : nullptr;
+            double2 c0[PV], c1[PV];
+#pragma unroll
+            for (int k = 0; k < PV; ++k) {
+              c0[k] = ok[k] ? reinterpret_cast<const double2*>(s0)[tid + PT * k] : make_double2(0.0, 0.0);
+              c1[k] = (ok[k] && two) ? reinterpret_cast<const double2*>(s1)[tid + PT * k] : make_double2(0.0, 0.0);
+            }
+            __syncthreads();  // every thread holds its values: the two slots may be refilled
+            if (tid == 0) {
+              if (j + NST < cb1) ring_issue(a.A + (j + NST) * a.lda + rb0, cnt);
+              if (j + NST + 1 < cb1) ring_issue(a.A + (j + NST + 1) * a.lda + rb0, cnt);
+            }
 #pragma unroll
             for (int s = 0; s < S; ++s) {
               const double p0 = q0[s], p1 = q1[s];
 #pragma unroll
-              for (int k = 0; k < PVD; ++k) {
+              for (int k = 0; k < PV; ++k) {
                 acc[s][k].x += c0[k].x * p0;
                 acc[s][k].y += c0[k].y * p0;
                 acc[s][k].x += c1[k].x * p1;
                 acc[s][k].y += c1[k].y * p1;
               }
             }
-#pragma unroll
-            for (int k = 0; k < PVD; ++k) {
-              c0[k] = n0[k];
-              c1[k] = n1[k];
-            }
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-              q0[s] = m0[s];
-              q1[s] = m1[s];
-            }
           }
 #pragma unroll
           for (int s = 0; s < S; ++s) {
             double* dst = a.part + (static_cast<i64>(cb) * S + s) * a.pstride + rb0;
 #pragma unroll
-            for (int k = 0; k < PVD; ++k) {
+            for (int k = 0; k < PV; ++k) {
               const i64 i = 2 * (tid + static_cast<i64>(PT) * k);
-              if (rb0 + i + 1 < n) {
+              if (i + 1 < cnt) {
                 reinterpret_cast<double2*>(dst)[tid + PT * k] = acc[s][k];
-              } else if (rb0 + i < n) {
+              } else if (i < cnt) {
                 dst[i] = acc[s][k].x;
               }
             }
@@ -617,7 +631,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
 bool persistent_eligible(const Ctx& ctx, Op& op, i64 S) {
   (void)ctx;
   if (auto* g = dynamic_cast<GramOp*>(&op)) return S == 1 && g->n <= PW && g->m >= 1;
-  if (dynamic_cast<DenseOp*>(&op)) return S <= 4 && cdiv(op.n, S <= 2 ? PW : 2 * PT * 2) <= ctx.sm_count;
+  if (dynamic_cast<DenseOp*>(&op)) return S <= 4 && cdiv(op.n, PW) <= ctx.sm_count;
   return false;
 }
 
@@ -625,16 +639,19 @@ template <int S, bool GRAM>
 void launch_persistent(Ctx& ctx, PersistArgs& pa, int G) {
   void* args[] = {&pa};
   ctx.prof_begin(GRAM ? "pcg_persistent_kernel<gram>" : "pcg_persistent_kernel<dense>");
-  NPCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(pcg_persistent_kernel<S, GRAM>), G, PT, args, 0,
-                                        ctx.stream));
+  NPCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(pcg_persistent_kernel<S, GRAM>), G, PT, args,
+                                        GRAM ? 0 : RING_BYTES, ctx.stream));  // the ring streams A (dense only)
   ctx.check_launch("pcg_persistent_kernel");
   ctx.prof_end();
 }
 
 template <int S, bool GRAM>
 int persistent_grid(const Ctx& ctx) {
+  NPCG_CUDA(cudaFuncSetAttribute(pcg_persistent_kernel<S, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 RING_BYTES));
   int per_sm = 0;
-  NPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_persistent_kernel<S, GRAM>, PT, 0));
+  NPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_persistent_kernel<S, GRAM>, PT,
+                                                          GRAM ? 0 : RING_BYTES));
   if (per_sm < 1) fail(NPCG_ECUDA, "pcg_persistent_kernel does not fit on an SM");
   return ctx.sm_count;  // one CTA per SM: cheapest grid barrier, enough bytes in flight
 }
@@ -655,7 +672,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   if (gram) part.alloc(static_cast<i64>(G) * PW, ctx.stream);
   i64 nrb = 0, ncb = 0, cpb = 0, pstride = 0;
   if (dense) {
-    nrb = cdiv(n, S <= 2 ? PW : 2 * PT * 2);  // PWD of the kernel
+    nrb = cdiv(n, PW);
     ncb = std::max<i64>(1, G / nrb);
     cpb = cdiv(n, ncb);
     ncb = cdiv(n, cpb);
