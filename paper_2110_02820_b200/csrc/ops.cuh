@@ -24,6 +24,9 @@ struct Op {
   virtual void apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate);
   virtual bool has_column() const { return false; }
   virtual void column(i64 j, double* out);
+  /// A product costs far more than a host round trip (matrix-free kernel):
+  /// the PCG driver then keeps one iteration in flight instead of several.
+  virtual bool costly() const { return false; }
 };
 
 struct DenseOp : Op {  // DenseOperator (operators.cpp:64-80); also the stored kernel

@@ -839,7 +839,8 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
       NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, 2, static_cast<int>(t));
       NPCG_LAUNCH(ctx, pupdate_kernel, nblk, 256, 0, n, static_cast<int>(S), P.p(), P.ld, Zp, ldz, st.p);
       enqueue_snapshot(t);
-      if (t > kDepth && finished(t - kDepth)) done = true;
+      const i64 depth = op.costly() ? 1 : kDepth;  // no overshoot products when one product is expensive
+      if (t > depth && finished(t - depth)) done = true;
     }
   }
   ctx.sync();
