@@ -141,6 +141,163 @@ void free_apply_s(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, do
               op.pts_rm.ld, op.n, static_cast<int>(op.d), op.norms.p, c, V, ldv, out, ldo, gate);
 }
 
+// ---------------------------------------------------------------------------
+// Fused matrix-free K V (k <= 2), flash-style: a CTA owns 128 output rows and
+// streams every column tile of 128 points. Per tile the 128x128 block of dot
+// products x_i . x_j runs on the FP64 tensor pipe (mma.sync.m8n8k4.f64 from
+// shared memory, K = d), the kernel epilogue (norms, clamp, exp, unit
+// diagonal) is applied to the accumulators in registers and multiplied into
+// the row sums with V -- K never touches HBM. Tiles are double-buffered with
+// cp.async. 8 warps, each a 64 x 32 slice of the tile.
+constexpr int KF_B = 128, KF_THREADS = 256;
+
+__device__ __forceinline__ void kf_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(saddr), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int S>
+__global__ void __launch_bounds__(KF_THREADS, 1)
+    kfree_fused_kernel(const double* __restrict__ pts, i64 ldp, i64 n, int d, int dp,
+                       const double* __restrict__ norms, double c, const double* __restrict__ V, i64 ldv,
+                       double* __restrict__ out, i64 ldo, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
+  extern __shared__ double kfs[];
+  const int lds = dp + 1;  // odd stride: the fragment reads hit distinct banks
+  double* XI = kfs;                                   // [128][lds]
+  double* XJ = XI + KF_B * lds;                       // [2][128][lds]
+  double* NJ = XJ + 2 * KF_B * lds;                   // [2][128]
+  double* VJ = NJ + 2 * KF_B;                         // [2][S][128]
+  double* RED = VJ + 2 * S * KF_B;                    // [4][128][S]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3, wm = warp >> 2, wn = warp & 3;
+  const i64 i0 = static_cast<i64>(blockIdx.x) * KF_B;
+
+  auto load_tile = [&](i64 j0, int buf) {
+    double* xj = XJ + buf * KF_B * lds;
+    for (int idx = tid; idx < KF_B * dp; idx += KF_THREADS) {
+      const int r = idx % KF_B, k = idx / KF_B;
+      const bool ok = j0 + r < n && k < d;
+      cp_async8(xj + r * lds + k, ok ? pts + (j0 + r) + static_cast<i64>(k) * ldp : pts, ok);
+    }
+    for (int r = tid; r < KF_B; r += KF_THREADS) {
+      const bool ok = j0 + r < n;
+      cp_async8(NJ + buf * KF_B + r, ok ? norms + j0 + r : norms, ok);
+#pragma unroll
+      for (int s = 0; s < S; ++s) cp_async8(VJ + (buf * S + s) * KF_B + r, ok ? V + (j0 + r) + s * ldv : V, ok);
+    }
+    cp_async_commit();
+  };
+
+  for (int idx = tid; idx < KF_B * dp; idx += KF_THREADS) {
+    const int r = idx % KF_B, k = idx / KF_B;
+    XI[r * lds + k] = (i0 + r < n && k < d) ? pts[(i0 + r) + static_cast<i64>(k) * ldp] : 0.0;
+  }
+  double ni[8];
+#pragma unroll
+  for (int f = 0; f < 8; ++f) {
+    const i64 i = i0 + wm * 64 + f * 8 + g;
+    ni[f] = i < n ? norms[i] : 0.0;
+  }
+  double racc[8][S];
+#pragma unroll
+  for (int f = 0; f < 8; ++f)
+#pragma unroll
+    for (int s = 0; s < S; ++s) racc[f][s] = 0.0;
+
+  load_tile(0, 0);
+  const i64 ntiles = (n + KF_B - 1) / KF_B;
+  for (i64 jt = 0; jt < ntiles; ++jt) {
+    const int buf = static_cast<int>(jt & 1);
+    cp_async_wait_all();
+    __syncthreads();  // tile jt resident; everyone is done with the other buffer
+    if (jt + 1 < ntiles) load_tile((jt + 1) * KF_B, buf ^ 1);
+    const double* xj = XJ + buf * KF_B * lds;
+    double acc[8][4][2];
+#pragma unroll
+    for (int f = 0; f < 8; ++f)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[f][q][0] = acc[f][q][1] = 0.0;
+    for (int kk = 0; kk < dp; kk += 4) {
+      double a[8], b[4];
+#pragma unroll
+      for (int f = 0; f < 8; ++f) a[f] = XI[(wm * 64 + f * 8 + g) * lds + kk + t];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) b[q] = xj[(wn * 32 + q * 8 + g) * lds + kk + t];
+#pragma unroll
+      for (int f = 0; f < 8; ++f)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) kf_dmma(acc[f][q][0], acc[f][q][1], a[f], b[q]);
+    }
+    // epilogue: K entries (operators.cpp:125-137 rounding order) times V into the row sums
+    const i64 j0 = jt * KF_B;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * 32 + q * 8 + 2 * t + e;
+        const double nj = NJ[buf * KF_B + col];
+        double vj[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) vj[s] = VJ[(buf * S + s) * KF_B + col];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          double sq = -2.0 * acc[f][q][e] + ni[f];
+          sq = sq + nj;
+          const bool diag = i0 + wm * 64 + f * 8 + g == j0 + col;
+          const double kij = diag ? 1.0 : exp(fmax(sq, 0.0) * c);
+#pragma unroll
+          for (int s = 0; s < S; ++s) racc[f][s] += kij * vj[s];
+        }
+      }
+  }
+  // row sums: over the 4 lanes of a row group, then over the 4 column warps (fixed order)
+#pragma unroll
+  for (int f = 0; f < 8; ++f)
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      double v = racc[f][s];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (t == 0) RED[(wn * KF_B + wm * 64 + f * 8 + g) * S + s] = v;
+    }
+  __syncthreads();
+  for (int idx = tid; idx < KF_B * S; idx += KF_THREADS) {
+    const int r = idx / S, s = idx % S;
+    const i64 i = i0 + r;
+    if (i < n) {
+      double v = RED[(0 * KF_B + r) * S + s];
+      v += RED[(1 * KF_B + r) * S + s];
+      v += RED[(2 * KF_B + r) * S + s];
+      v += RED[(3 * KF_B + r) * S + s];
+      out[i + s * ldo] = v;
+    }
+  }
+}
+
+template <int S>
+void kfree_fused(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, double* out, i64 ldo, const int* gate) {
+  const int d = static_cast<int>(op.d), dp = (d + 3) / 4 * 4;
+  const i64 smem = (3 * KF_B * static_cast<i64>(dp + 1) + 2 * KF_B + 2 * S * KF_B + 4 * KF_B * S) * 8;
+  static bool attr = false;
+  if (!attr) {
+    NPCG_CUDA(cudaFuncSetAttribute(kfree_fused_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  const double c = -1.0 / (2.0 * op.sigma * op.sigma);
+  NPCG_LAUNCH(ctx, kfree_fused_kernel<S>, static_cast<unsigned>(cdiv(op.n, KF_B)), KF_THREADS,
+              static_cast<int>(smem), op.pts.p(), op.pts.ld, op.n, d, dp, op.norms.p, c, V, ldv, out, ldo, gate);
+  ctx.prof_work(static_cast<double>(op.n) * op.n * (2.0 * dp + 2.0 * S), 8.0 * op.n * (d + 2 * S));
+}
+
 }  // namespace
 
 void build_kernel_matrix(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma, DMat& K) {
@@ -165,7 +322,15 @@ void prepare_kernel_free(Ctx& ctx, KernelFreeOp& op) {
 
 void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, i64 k, double* out, i64 ldo,
                        const int* gate) {
-  if (k > 0 && !(std::getenv("NPCG_KFREE") && std::string(std::getenv("NPCG_KFREE")) == "fused")) {
+  static const char* mode = std::getenv("NPCG_KFREE");  // diagnostics: "blocked" / "scalar"
+  const bool force_blocked = mode && std::string(mode) == "blocked";
+  const bool force_scalar = mode && std::string(mode) == "scalar";
+  if (k <= 2 && op.d <= 64 && !force_blocked && !force_scalar) {
+    if (k == 1) kfree_fused<1>(ctx, op, V, ldv, out, ldo, gate);
+    else kfree_fused<2>(ctx, op, V, ldv, out, ldo, gate);
+    return;
+  }
+  if (k > 0 && !force_scalar) {
     // Recompute K by row blocks like do_apply_block (operators.cpp:166-177):
     // K_R = kernel(-2 X_R X^T on DMMA + norms, clamp, exp), then out_R = K_R V
     // on DMMA (k > 8) or the coldot GEMV; the exps are paid once per block,

@@ -1,16 +1,26 @@
-"""Matrix-free RBF operator: apply time for k = 1 (fused) and k = 400 (row blocks on DMMA) (diagnostic)."""
-import sys, time
+"""Matrix-free RBF operator: time and agreement of the fused (k <= 2), row-block and scalar paths (diagnostic)."""
+import os, subprocess, sys, time
 sys.path.insert(0, '.')
-import numpy as np
-import paper_2110_02820_b200 as npcg
-ctx = npcg.Context(0)
-n, d = int(sys.argv[1]) if len(sys.argv) > 1 else 50000, 32
-pts = np.random.default_rng(0).random((n, d))
-op = npcg.KernelOperator(pts, 0.5, dense_cap=1000, ctx=ctx)
-for k in (1, 400):
-    V = np.random.default_rng(1).standard_normal((n, k))
-    op.apply_block(V)
-    ctx.prof_enable(True)
-    t = time.perf_counter(); op.apply_block(V); ctx.sync(); dt = time.perf_counter() - t
-    prof = ctx.prof_report(); ctx.prof_enable(False)
-    print("n=%d k=%d %.3f s" % (n, k, dt), {kk: (v[0], round(v[1], 2)) for kk, v in prof.items()})
+if len(sys.argv) > 2:
+    import numpy as np
+    import paper_2110_02820_b200 as npcg
+    ctx = npcg.Context(0)
+    n, d = int(sys.argv[1]), int(sys.argv[2])
+    pts = np.random.default_rng(0).random((n, d))
+    op = npcg.KernelOperator(pts, 0.5, dense_cap=1000, ctx=ctx)
+    for k in (1, 2, 400):
+        V = np.random.default_rng(1).standard_normal((n, k))
+        r = op.apply_block(V)
+        ctx.sync(); t = time.perf_counter(); op.apply_block(V); ctx.sync(); dt = time.perf_counter() - t
+        np.save('/tmp/kf_%s_%d.npy' % (os.environ.get('NPCG_KFREE', 'auto'), k), r)
+        print(os.environ.get('NPCG_KFREE', 'auto'), "n=%d d=%d k=%d %.4f s" % (n, d, k, dt), flush=True)
+else:
+    import numpy as np
+    n, d = (sys.argv[1] if len(sys.argv) > 1 else '50000'), '32'
+    for mode in ['', 'blocked']:
+        env = dict(os.environ)
+        if mode: env['NPCG_KFREE'] = mode
+        subprocess.run([sys.executable, __file__, n, d], env=env)
+    for k in (1, 2):
+        a, b = np.load('/tmp/kf_auto_%d.npy' % k), np.load('/tmp/kf_blocked_%d.npy' % k)
+        print('k=%d fused vs blocked max rel diff %.2e' % (k, np.abs(a - b).max() / np.abs(b).max()))
