@@ -16,11 +16,13 @@ factorisation (shift, Cholesky, TRSM, thin SVD), preconditioner, PCG to 1e-10.
 
 `--impl reference` times the reference's CPU path (the oracle port; the
 reference itself cannot be built here: Eigen3/LAPACKE are absent) on all host
-cores, rank 0 only. Under torchrun (N > 1) the ridge workload is row-sharded
-(SURVEY §8e): rank g holds rows R_g of X, vectors are replicated, and every
-operator product is completed by an NCCL all-reduce (n doubles per PCG
-iteration, n x ell for the sketch) enqueued on the library stream through
-paper_2110_02820_b200/dist.py -- one solve split over N GPUs ("strong"
+cores, rank 0 only. Under torchrun (N > 1) the operator is row-sharded
+ and vectors are replicated: ridge (cfg 2) -- rank g holds rows
+R_g of X, products completed by an NCCL all-reduce of n doubles per PCG
+iteration (n x ell for the sketch); stored kernel (cfg 3) / low-rank (cfg 5)
+-- rank g builds the column block A[:, R_g], products completed by an NCCL
+all-gather. The exchange is enqueued on the library stream through
+paper_2110_02820_b200/dist.py: one solve split over N GPUs ("strong"
 scaling). Other workloads run one independent replica per GPU ("weak").
 """
 from __future__ import annotations
@@ -331,7 +333,8 @@ def run_b200(args):
                        gemm=lambda a, b, transa=False: npcg.gemm(a, b, transa=transa, ctx=ctx), **workload_kwargs(args))
     t_gen = time.perf_counter() - t_gen
     exchange = None
-    sharded = (world > 1 or args.shard) and w.kind == "gram"
+    sharded = (world > 1 or args.shard) and (w.kind in ("gram", "lowrank") or
+                                             (w.kind == "kernel" and w.n <= w.data.get("dense_cap", 0)))
     if sharded:
         from paper_2110_02820_b200 import dist as pd
         exchange = pd.TorchExchange()
@@ -395,7 +398,7 @@ def run_b200(args):
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             el = float(t.item())
-        h2d = input_bytes(w) - (w.data["x"].nbytes * (1 - 1 / world) if sharded else 0)  # this rank's X block
+        h2d = input_bytes(w) - (w.data["x"].nbytes * (1 - 1 / world) if sharded and w.kind == "gram" else 0)
         e2e = {"value": (1 if sharded else world) * k2 / el, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(w.b.nbytes + 8 * w.ell), "steps": k2,
                "wall_s": time.perf_counter() - t0}

@@ -119,6 +119,15 @@ int npcg_op_gram_shard_create(npcg_ctx* ctx, int64_t m_local, int64_t n, const d
  * (The symmetry check needs the whole matrix and is the caller's.) */
 int npcg_op_dense_shard_create(npcg_ctx* ctx, int64_t n, int64_t nranks, int64_t rank, const double* a_block,
                                int64_t lda, int where, npcg_exchange_fn fn, void* user, npcg_op** out);
+/* Stored KernelOperator shard: this rank builds the column block K[:, R_g]
+ * of the Gaussian kernel on device from all n points (operators.cpp:125-150). */
+int npcg_op_kernel_shard_create(npcg_ctx* ctx, int64_t n, int64_t d, const double* pts, int64_t ldp, double sigma,
+                                int64_t nranks, int64_t rank, int where, npcg_exchange_fn fn, void* user,
+                                npcg_op** out);
+/* Low-rank synthetic operator shard: A[:, R_g] = G diag(lambda) G[R_g, :]^T / r. */
+int npcg_op_lowrank_shard_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g, int64_t ldg,
+                                 const double* lambda, int64_t nranks, int64_t rank, int where, npcg_exchange_fn fn,
+                                 void* user, npcg_op** out);
 int npcg_op_destroy(npcg_op* op);
 int npcg_op_dim(const npcg_op* op, int64_t* n);
 int npcg_op_kind(const npcg_op* op); /* 0 dense, 1 gram, 2 kernel stored, 3 kernel matrix-free */

@@ -386,6 +386,79 @@ int npcg_op_dense_shard_create(npcg_ctx* ctx, int64_t n, int64_t nranks, int64_t
   });
 }
 
+namespace {
+npcg_op* make_colblock_shard(npcg_ctx* ctx, DMat&& block, i64 n, i64 nranks, i64 rank, int kind,
+                             npcg_exchange_fn fn, void* user) {
+  Ctx& c = C(ctx);
+  const i64 nmax = cdiv(n, nranks), nloc = std::min<i64>(nmax, n - rank * nmax);
+  auto local = std::make_unique<DenseColBlockOp>();
+  local->ctx = &c;
+  local->n = n;
+  local->nloc = nloc;
+  local->kind = kind;
+  local->a = std::move(block);
+  auto op = std::make_unique<ShardOp>();
+  op->ctx = &c;
+  op->n = n;
+  op->kind = kind;
+  op->mode = 1;
+  op->nranks = nranks;
+  op->rank = rank;
+  op->nmax = nmax;
+  op->local = std::move(local);
+  op->fn = fn;
+  op->user = user;
+  return new npcg_op{ctx, std::move(op)};
+}
+void check_shard(i64 n, i64 nranks, i64 rank, npcg_exchange_fn fn) {
+  if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks) invalid("sharded operator: bad rank layout");
+  if (!fn) invalid("sharded operator: exchange callback required");
+  if (n - rank * cdiv(n, nranks) < 1) invalid("sharded operator: more ranks than rows");
+}
+}  // namespace
+
+int npcg_op_kernel_shard_create(npcg_ctx* ctx, int64_t n, int64_t d, const double* pts, int64_t ldp, double sigma,
+                                int64_t nranks, int64_t rank, int where, npcg_exchange_fn fn, void* user,
+                                npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (n < 1) invalid("KernelOperator: need at least one point");   // operators.cpp:143
+    if (!(sigma > 0.0)) invalid("KernelOperator: sigma must be > 0");  // :144
+    check_shard(n, nranks, rank, fn);
+    DMat P;
+    upload(c, P, n, d, pts, ldp, where);
+    if (!all_finite(c, P.p(), n, d, P.ld)) invalid("KernelOperator: points have non-finite entries");
+    const i64 nmax = cdiv(n, nranks), off = rank * nmax, nloc = std::min<i64>(nmax, n - off);
+    DMat K;
+    build_kernel_colblock(c, P, n, d, sigma, off, nloc, K);
+    *out = make_colblock_shard(ctx, std::move(K), n, nranks, rank, kKernelStored, fn, user);
+  });
+}
+
+int npcg_op_lowrank_shard_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g, int64_t ldg,
+                                 const double* lambda, int64_t nranks, int64_t rank, int where, npcg_exchange_fn fn,
+                                 void* user, npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (n < 1 || r < 1) invalid("lowrank operator: need n >= 1 and r >= 1");
+    check_shard(n, nranks, rank, fn);
+    DMat G, GD;
+    upload(c, G, n, r, g, ldg, where);
+    GD.alloc(n, r, c.stream, false);
+    copy2d(c, n, r, G.p(), G.ld, GD.p(), GD.ld);
+    DBuf<double> lam(r, c.stream);
+    NPCG_CUDA(cudaMemcpyAsync(lam.p, lambda, sizeof(double) * r, cudaMemcpyHostToDevice, c.stream));
+    scale_cols(c, GD.p(), n, r, GD.ld, lam.p);
+    const i64 nmax = cdiv(n, nranks), off = rank * nmax, nloc = std::min<i64>(nmax, n - off);
+    DMat A;  // A[:, R_g] = G diag(lambda) G[R_g, :]^T / r
+    A.alloc(n, nloc, c.stream, false);
+    gemm(c, n, nloc, r, 1.0, Operand{GD.p(), GD.ld, false}, Operand{G.p() + off, G.ld, false}, 0.0, A.p(), A.ld);
+    divide(c, n, nloc, A.p(), A.ld, static_cast<double>(r));
+    c.sync();
+    *out = make_colblock_shard(ctx, std::move(A), n, nranks, rank, kDense, fn, user);
+  });
+}
+
 int npcg_op_kernel_create(npcg_ctx* ctx, int64_t n, int64_t d, const double* pts, int64_t ldp, double sigma,
                           int64_t dense_cap, int where, npcg_op** out) {
   return guard([&] {

@@ -311,6 +311,17 @@ void build_kernel_matrix(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma, 
               256, 0, K.p(), K.ld, n, norms.p, c);
 }
 
+void build_kernel_colblock(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma, i64 r0, i64 cols, DMat& K) {
+  DBuf<double> norms(n, ctx.stream);
+  NPCG_LAUNCH(ctx, row_norms_kernel, static_cast<unsigned>(cdiv(n, 256)), 256, 0, pts.p(), pts.ld, n, d, norms.p);
+  K.alloc(n, cols, ctx.stream, false);
+  gemm(ctx, n, cols, d, -2.0, Operand{pts.p(), pts.ld, false}, Operand{pts.p() + r0, pts.ld, false}, 0.0, K.p(), K.ld);
+  const double c = -1.0 / (2.0 * sigma * sigma);
+  NPCG_LAUNCH(ctx, kernel_colblock_epilogue_kernel,
+              static_cast<unsigned>(std::min<i64>(cdiv(n * cols, 256), ctx.sm_count * 16)), 256, 0, K.p(), K.ld, n,
+              cols, r0, norms.p, c);
+}
+
 void prepare_kernel_free(Ctx& ctx, KernelFreeOp& op) {
   op.norms.alloc(op.n, ctx.stream);
   NPCG_LAUNCH(ctx, row_norms_kernel, static_cast<unsigned>(cdiv(op.n, 256)), 256, 0, op.pts.p(), op.pts.ld, op.n,

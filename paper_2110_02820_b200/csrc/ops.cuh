@@ -86,6 +86,8 @@ struct ShardOp : Op {
 /// Build the stored Gaussian kernel matrix (operators.cpp:125-150) on device.
 void build_kernel_matrix(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma, DMat& K);
 void prepare_kernel_free(Ctx& ctx, KernelFreeOp& op);
+/// Column block K[:, r0 : r0+cols] (n x cols) of the stored Gaussian kernel.
+void build_kernel_colblock(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma, i64 r0, i64 cols, DMat& K);
 void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, i64 k, double* out, i64 ldo,
                        const int* gate);
 

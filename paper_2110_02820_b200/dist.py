@@ -141,3 +141,35 @@ def ShardedDenseOperator(a_block, n: int, exchange: TorchExchange, ctx=None):
     op = LinearOperator(h.value, ctx)
     op._exchange = exchange
     return op
+
+
+def ShardedKernelOperator(points, sigma: float, exchange: TorchExchange, ctx=None):
+    """Stored Gaussian KernelOperator over this rank's column block K[:, R_g],
+    built on device from all n points (npcg_op_kernel_shard_create)."""
+    from . import HOST, _check, _f64, _i64, _ptr, _vp, default_context, lib, LinearOperator
+    ctx = ctx or default_context()
+    p = _f64(points)
+    n, d = p.shape
+    h = _vp()
+    _check(lib().npcg_op_kernel_shard_create(_vp(ctx.h), _i64(n), _i64(d), _ptr(p), _i64(max(n, 1)),
+                                             C.c_double(sigma), _i64(exchange.world), _i64(exchange.rank), HOST,
+                                             exchange.cfn, None, C.byref(h)))
+    op = LinearOperator(h.value, ctx)
+    op._exchange = exchange
+    return op
+
+
+def ShardedLowRankOperator(g, lam, exchange: TorchExchange, ctx=None):
+    """A = G diag(lam) G^T / r over this rank's column block (npcg_op_lowrank_shard_create)."""
+    from . import HOST, _check, _f64, _i64, _ptr, _vp, default_context, lib, LinearOperator
+    ctx = ctx or default_context()
+    g = _f64(g)
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    n, r = g.shape
+    h = _vp()
+    _check(lib().npcg_op_lowrank_shard_create(_vp(ctx.h), _i64(n), _i64(r), _ptr(g), _i64(max(n, 1)), _ptr(lam),
+                                              _i64(exchange.world), _i64(exchange.rank), HOST, exchange.cfn, None,
+                                              C.byref(h)))
+    op = LinearOperator(h.value, ctx)
+    op._exchange = exchange
+    return op

@@ -125,6 +125,15 @@ def gpu_checks(port, q):
         A = X.T @ X / m
         dop = pd.ShardedDenseOperator(A, n, ex)
         out["dense"] = (dop.matvec(b), A @ b)
+        pts = rng.standard_normal((700, 16))
+        kfull, kshard = npcg.KernelOperator(pts, 3.0, dense_cap=5000), pd.ShardedKernelOperator(pts, 3.0, ex)
+        W = rng.standard_normal((700, 3))
+        out["kernel"] = (kshard.apply_block(W), kfull.apply_block(W))
+        G = rng.standard_normal((500, 40))
+        lam = np.exp(-np.arange(40) / 10.0)
+        lfull, lshard = npcg.LowRankOperator(G, lam), pd.ShardedLowRankOperator(G, lam, ex)
+        W2 = rng.standard_normal((500, 2))
+        out["lowrank"] = (lshard.apply_block(W2), lfull.apply_block(W2))
         out["calls"] = ex.calls
         out["errors"] = [repr(e) for e in ex.errors]
         q.put((0, out))
