@@ -19,7 +19,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "factor.cuh"
 
@@ -43,7 +45,14 @@ struct CholArgs {
   i64 ldw;
   double* dinv;  // nb tiles CB x CB col-major
   int* flag;
+  unsigned long long* trace;  // diagnostics (NPCG_CHOL_TRACE): CTA 0 phase timestamps, nullable
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 using Tile = double[CB][TS];
 
@@ -90,14 +99,16 @@ __device__ __forceinline__ void store_acc(Tile& C, const double acc[4]) {
   for (int q = 0; q < 4; ++q) C[r][c0 + q] = acc[q];
 }
 // Factor + invert the diagonal tile held in smem T (lower part; rows >= nr
-// padded with the identity). Warp 0 only. Writes L_bb to args.L, Dinv_b to
-// args.dinv. Returns false (uniform in the warp) on a non-positive pivot.
-__device__ __noinline__ bool diag_factor(Tile& T, int b, int nr, const CholArgs& a) {
+// padded with the identity). Warp 0 only: L goes back to T, L^{-1} to Xs
+// (both [row][col]); the caller publishes them with the whole CTA. Returns
+// false (uniform in the warp) on a non-positive pivot.
+__device__ __noinline__ bool diag_factor(Tile& T, Tile& Xs, int nr) {
   const int lane = threadIdx.x & 31;
   double row[CB];
 #pragma unroll
   for (int k = 0; k < CB; ++k) row[k] = lane < nr ? (k < nr ? T[lane][k] : 0.0) : (k == lane ? 1.0 : 0.0);
-  __shared__ double rs[CB];  // 1 / L_jj (identical in every lane)
+  __shared__ double rs[CB];      // 1 / L_jj (identical in every lane)
+  __shared__ double lv[2][CB];   // column j of L, broadcast through shared memory
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < CB; ++j) {
@@ -110,9 +121,11 @@ __device__ __noinline__ bool diag_factor(Tile& T, int b, int nr, const CholArgs&
     if (lane == 0) rs[j] = r;
     const double l = lane == j ? d * r : row[j] * r;
     if (lane >= j) row[j] = l;
+    lv[j & 1][lane] = l;
+    __syncwarp();
 #pragma unroll
     for (int c = j + 1; c < CB; ++c) {
-      const double lc = __shfl_sync(0xffffffffu, l, c);
+      const double lc = lv[j & 1][c];
       if (lane >= c) row[c] -= l * lc;
     }
   }
@@ -132,13 +145,20 @@ __device__ __noinline__ bool diag_factor(Tile& T, int b, int nr, const CholArgs&
 #pragma unroll
     for (int i = k + 1; i < CB; ++i) x[i] -= T[i][k] * x[k];
   }
-  double* dv = a.dinv + static_cast<i64>(b) * CB * CB;
 #pragma unroll
-  for (int i = 0; i < CB; ++i) dv[i + lane * CB] = x[i];
-  const i64 o = static_cast<i64>(b) * CB;
-  for (int i = 0; i < nr; ++i)
-    if (lane < nr) a.L[(o + i) + (o + lane) * a.ldw] = lane <= i ? T[i][lane] : 0.0;
+  for (int i = 0; i < CB; ++i) Xs[i][lane] = x[i];
   return true;
+}
+
+// Publish the factored diagonal tile b (T = L_bb, Xs = L_bb^{-1}) with the whole CTA.
+__device__ __forceinline__ void publish_diag(const Tile& T, const Tile& Xs, int b, int nr, const CholArgs& a) {
+  const i64 o = static_cast<i64>(b) * CB;
+  double* dv = a.dinv + static_cast<i64>(b) * CB * CB;
+  for (int idx = threadIdx.x; idx < CB * CB; idx += CT) {
+    const int i = idx & 31, k = idx >> 5;
+    dv[i + k * CB] = Xs[i][k];
+    if (i < nr && k < nr) a.L[(o + i) + (o + k) * a.ldw] = k <= i ? T[i][k] : 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(CT) chol_fused_kernel(const CholArgs a) {
@@ -159,7 +179,9 @@ __global__ void __launch_bounds__(CT) chol_fused_kernel(const CholArgs a) {
   if (bid == 0) {
     load_tile(Ct, a.a, a.lda, 0, 0, tile_rows(0, n), tile_rows(0, n));
     __syncthreads();
-    if (tid < 32 && !diag_factor(Ct, 0, tile_rows(0, n), a) && tid == 0) *flag = 1;
+    if (tid < 32 && !diag_factor(Ct, Lj, tile_rows(0, n)) && tid == 0) *flag = 1;
+    __syncthreads();
+    if (!*flag) publish_diag(Ct, Lj, 0, tile_rows(0, n), a);
   }
   grid.sync();
   if (*flag) return;
@@ -170,6 +192,7 @@ __global__ void __launch_bounds__(CT) chol_fused_kernel(const CholArgs a) {
     const i64 ob = static_cast<i64>(b) * CB;
     const int nrb = tile_rows(b, n);
     bool have_dinv = false;
+    if (a.trace && bid == 0 && tid == 0) a.trace[4 * b] = gtimer();
     for (int q = bid; q < ntrail + ninv; q += G) {
       if (!have_dinv) {
         load_dinv(Dn, a.dinv + static_cast<i64>(b) * CB * CB);
@@ -217,7 +240,11 @@ __global__ void __launch_bounds__(CT) chol_fused_kernel(const CholArgs a) {
         }
         if (ti == b + 1 && tj == b + 1) {  // D(b+1) right away (CTA 0, q == 0)
           __syncthreads();
-          if (tid < 32 && !diag_factor(Ct, b + 1, nri, a) && tid == 0) *flag = 1;
+          if (a.trace && tid == 0) a.trace[4 * b + 1] = gtimer();
+          if (tid < 32 && !diag_factor(Ct, Lj, nri) && tid == 0) *flag = 1;
+          __syncthreads();
+          if (!*flag) publish_diag(Ct, Lj, b + 1, nri, a);
+          if (a.trace && tid == 0) a.trace[4 * b + 2] = gtimer();
         }
         __syncthreads();
       } else {  // ---- inverse tile: W_ij -= L_ib X_bj,  b < i, j <= b
@@ -255,6 +282,7 @@ __global__ void __launch_bounds__(CT) chol_fused_kernel(const CholArgs a) {
         __syncthreads();
       }
     }
+    if (a.trace && bid == 0 && tid == 0) a.trace[4 * b + 3] = gtimer();
     grid.sync();
     if (*flag) return;
   }
@@ -304,7 +332,14 @@ bool cholesky_fused(Ctx& ctx, double* A, i64 n, i64 lda, CholFactor& f) {
   DBuf<int> flag(1, ctx.stream);
   flag.zero();
   if (Lw.ld != f.linv.ld || Ww.ld != f.linv.ld) fail(NPCG_ERUNTIME, "cholesky_fused: layout");
-  CholArgs args{A, lda, static_cast<int>(n), nb, Lw.p(), Ww.p(), f.linv.p(), f.linv.ld, f.dinv.p, flag.p};
+  DBuf<unsigned long long> trace;
+  static const bool tracing = std::getenv("NPCG_CHOL_TRACE") != nullptr;
+  if (tracing) {
+    trace.alloc(4 * nb, ctx.stream);
+    trace.zero();
+  }
+  CholArgs args{A, lda, static_cast<int>(n), nb, Lw.p(), Ww.p(), f.linv.p(), f.linv.ld, f.dinv.p, flag.p,
+                tracing ? trace.p : nullptr};
   constexpr int smem = NTILE * CB * TS * 8;
   static bool attr = false;
   if (!attr) {
@@ -325,6 +360,15 @@ bool cholesky_fused(Ctx& ctx, double* A, i64 n, i64 lda, CholFactor& f) {
   int h = 0;
   NPCG_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   ctx.sync();
+  if (tracing) {
+    std::vector<unsigned long long> tr(4 * nb);
+    NPCG_CUDA(cudaMemcpy(tr.data(), trace.p, 8 * tr.size(), cudaMemcpyDeviceToHost));
+    for (int b = 0; b + 1 < nb; ++b)
+      std::fprintf(stderr, "[chol n=%lld] b=%d tile->D %.2f us  D %.2f us  D->end %.2f us  end->next %.2f us\n",
+                   static_cast<long long>(n), b, (tr[4 * b + 1] - tr[4 * b]) * 1e-3,
+                   (tr[4 * b + 2] - tr[4 * b + 1]) * 1e-3, (tr[4 * b + 3] - tr[4 * b + 2]) * 1e-3,
+                   b + 2 < nb ? (tr[4 * b + 4] - tr[4 * b + 3]) * 1e-3 : 0.0);
+  }
   return h == 0;
 }
 
