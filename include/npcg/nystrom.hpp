@@ -4,6 +4,7 @@
 #pragma once
 
 #include <memory>
+#include <vector>
 
 #include "operators.hpp"
 
@@ -81,6 +82,36 @@ inline NystromApproximation nystrom_from_sketch(const SketchPair& pair) {
 inline NystromApproximation randomized_nystrom(const LinearOperator& op, Index ell, Rng& rng) {
   if (ell < 1 || ell > op.dim()) throw std::invalid_argument("randomized_nystrom: need 1 <= ell <= dim");
   return nystrom_from_sketch(extend_sketch(make_empty_sketch(op), op, ell, rng));
+}
+
+/// extend_sketch_columns (nystrom.cpp:60-94): `extra` unused columns of A
+/// drawn from rng; `used` receives every index drawn so far on this sketch.
+inline SketchPair extend_sketch_columns(const SketchPair& pair, const LinearOperator& op, Index extra,
+                                        std::vector<Index>& used, Rng& rng) {
+  if (pair.dim() != op.dim()) throw std::invalid_argument("extend_sketch_columns: dimension mismatch");
+  check_status(npcg_nys_extend_columns(pair.device.get(), extra, rng.handle()));
+  int64_t count = 0;
+  check_status(npcg_nys_used(pair.device.get(), nullptr, &count));
+  std::vector<int64_t> idx(static_cast<size_t>(count));
+  check_status(npcg_nys_used(pair.device.get(), idx.data(), &count));
+  used.assign(idx.begin(), idx.end());
+  return pair;
+}
+
+/// column_sampling_nystrom (nystrom.cpp:150-158): ell distinct columns from rng.
+inline NystromApproximation column_sampling_nystrom(const LinearOperator& op, Index ell, Rng& rng) {
+  npcg_nys* h = nullptr;
+  check_status(npcg_column_sampling_nystrom(device_handle(op), ell, nullptr, rng.handle(), &h));
+  return detail::fetch(detail::own(h));
+}
+
+/// column_sampling_nystrom with caller-chosen distinct indices (nystrom.cpp:160-184).
+inline NystromApproximation column_sampling_nystrom(const LinearOperator& op, const std::vector<Index>& indices) {
+  std::vector<int64_t> idx(indices.begin(), indices.end());
+  npcg_nys* h = nullptr;
+  check_status(npcg_column_sampling_nystrom(device_handle(op), static_cast<int64_t>(idx.size()), idx.data(),
+                                            nullptr, &h));
+  return detail::fetch(detail::own(h));
 }
 
 /// An approximation given by its factors (e.g. read from disk) placed on device.

@@ -148,6 +148,15 @@ int npcg_nys_create(npcg_op* op, npcg_nys** out);
 int npcg_nys_extend(npcg_nys* nys, int64_t extra, const double* omega_raw, int64_t ld, int where);
 /* Same, drawing the block from `rng` (exact reference stream order). */
 int npcg_nys_extend_rng(npcg_nys* nys, int64_t extra, npcg_rng* rng);
+/* extend_sketch_columns (nystrom.cpp:60-94): `extra` distinct unused columns
+ * drawn from `rng` (Fisher-Yates over the unused indices); Omega gets unit
+ * columns, Y the columns of A. The drawn indices accumulate in the handle. */
+int npcg_nys_extend_columns(npcg_nys* nys, int64_t extra, npcg_rng* rng);
+/* Indices drawn so far by column-sampling sketches (out nullable: count only). */
+int npcg_nys_used(const npcg_nys* nys, int64_t* out, int64_t* count);
+/* column_sampling_nystrom (nystrom.cpp:150-184): `ell` indices drawn from rng
+ * (indices == NULL), or the caller's distinct indices; returns the factored handle. */
+int npcg_column_sampling_nystrom(npcg_op* op, int64_t ell, const int64_t* indices, npcg_rng* rng, npcg_nys** out);
 /* nystrom_from_sketch (nystrom.cpp:96-140): shift, Cholesky (x10 escalation,
  * <= 3 retries), triangular solve, thin SVD, clamp. */
 int npcg_nys_factor(npcg_nys* nys);
@@ -231,7 +240,7 @@ typedef struct {
   double tau;         /* default 30 (error) / 10 (ratio) */
   int64_t q;          /* power iterations, default 5 */
   int secondary_criterion;
-  int sketch;         /* 0 gaussian */
+  int sketch;         /* 0 gaussian, 1 column sampling (needs column access) */
 } npcg_adaptive_cfg;
 
 typedef struct {

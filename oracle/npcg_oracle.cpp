@@ -452,6 +452,37 @@ SketchPair extend_sketch_columns(const SketchPair& pair, const LinearOperator& o
   return grown;
 }
 
+NystromApproximation column_sampling_nystrom(const LinearOperator& op, const std::vector<Index>& indices) {
+  // nystrom.cpp:160-184: Omega = distinct unit columns, Y = the matching columns of A
+  const Index n = op.dim();
+  const Index ell = static_cast<Index>(indices.size());
+  if (ell < 1 || ell > n) throw std::invalid_argument("column_sampling_nystrom: need 1 <= #indices <= dim");
+  if (!op.has_column_access())
+    throw std::runtime_error("column_sampling_nystrom: operator has no column access");
+  SketchPair pair;
+  pair.omega = Matrix(n, ell);
+  pair.y = Matrix(n, ell);
+  std::vector<bool> seen(static_cast<size_t>(n), false);
+  for (Index i = 0; i < ell; ++i) {
+    const Index j = indices[static_cast<size_t>(i)];
+    if (j < 0 || j >= n) throw std::invalid_argument("column_sampling_nystrom: index out of range");
+    if (seen[static_cast<size_t>(j)]) throw std::invalid_argument("column_sampling_nystrom: indices must be distinct");
+    seen[static_cast<size_t>(j)] = true;
+    pair.omega(j, i) = 1.0;
+    const Vector c = op.column(j);
+    std::copy(c.begin(), c.end(), pair.y.col(i));
+  }
+  return nystrom_from_sketch(pair);
+}
+
+NystromApproximation column_sampling_nystrom(const LinearOperator& op, Index ell, Rng& rng) {  // nystrom.cpp:150-158
+  const Index n = op.dim();
+  if (ell < 1 || ell > n) throw std::invalid_argument("column_sampling_nystrom: need 1 <= ell <= dim");
+  if (!op.has_column_access())
+    throw std::runtime_error("column_sampling_nystrom: operator has no column access");
+  return column_sampling_nystrom(op, sample_without_replacement(rng, n, ell));
+}
+
 NystromApproximation nystrom_from_sketch(const SketchPair& pair) {  // nystrom.cpp:96-140
   const Index n = pair.omega.rows;
   const Index ell = pair.size();

@@ -156,6 +156,8 @@ SketchPair extend_sketch_with(const SketchPair&, const LinearOperator&, Matrix f
 SketchPair extend_sketch_columns(const SketchPair&, const LinearOperator&, Index extra,
                                  std::vector<Index>& used, Rng&);               // :60-94
 NystromApproximation nystrom_from_sketch(const SketchPair&);                    // :96-140
+NystromApproximation column_sampling_nystrom(const LinearOperator&, const std::vector<Index>&);  // :160-184
+NystromApproximation column_sampling_nystrom(const LinearOperator&, Index ell, Rng&);          // :150-158
 NystromApproximation randomized_nystrom(const LinearOperator&, Index ell, Rng&);  // :142-148
 
 // ---- preconditioner.cpp -----------------------------------------------------

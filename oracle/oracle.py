@@ -386,6 +386,31 @@ def extend_sketch_with(pair: SketchPair, op: LinearOperator, fresh) -> SketchPai
     return SketchPair(h.value)
 
 
+def extend_sketch_columns(pair: SketchPair, op: LinearOperator, extra: int, used: list, rng: Rng) -> SketchPair:
+    """extend_sketch_columns (nystrom.cpp:60-94); `used` is extended in place."""
+    u = np.ascontiguousarray(used, dtype=np.int64)
+    uo = np.zeros(len(used) + max(int(extra), 0), dtype=np.int64)
+    h = C.c_void_p()
+    _check(lib().orc_sketch_extend_columns(C.c_void_p(pair.h), C.c_void_p(op.h), _i64(extra),
+                                           u.ctypes.data_as(C.c_void_p), _i64(len(used)), C.c_void_p(rng.h),
+                                           uo.ctypes.data_as(C.c_void_p), C.byref(h)))
+    used[:] = [int(v) for v in uo]
+    return SketchPair(h.value)
+
+
+def column_sampling_nystrom(op: LinearOperator, ell_or_indices, rng: Rng | None = None) -> NystromApproximation:
+    """column_sampling_nystrom (nystrom.cpp:150-184): by count with an Rng, or by caller indices."""
+    h = C.c_void_p()
+    if rng is not None:
+        _check(lib().orc_column_sampling_nystrom_rng(C.c_void_p(op.h), _i64(ell_or_indices), C.c_void_p(rng.h),
+                                                     C.byref(h)))
+    else:
+        idx = np.ascontiguousarray(ell_or_indices, dtype=np.int64)
+        _check(lib().orc_column_sampling_nystrom(C.c_void_p(op.h), _i64(idx.size), idx.ctypes.data_as(C.c_void_p),
+                                                 C.byref(h)))
+    return _approx_from_handle(h.value)
+
+
 def nystrom_from_sketch(pair: SketchPair) -> NystromApproximation:
     h = C.c_void_p()
     _check(lib().orc_nystrom_from_sketch(C.c_void_p(pair.h), C.byref(h)))

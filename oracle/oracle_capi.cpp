@@ -214,6 +214,27 @@ int orc_sketch_extend_with(void* p, void* op, int64_t extra, const double* fresh
         extend_sketch_with(*static_cast<SketchPair*>(p), *o, mat(o->dim(), extra, fresh)));
   });
 }
+int orc_sketch_extend_columns(void* p, void* op, int64_t extra, const int64_t* used_in, int64_t n_used, void* rng,
+                              int64_t* used_out, void** out) {
+  return guard([&] {
+    std::vector<Index> used(used_in, used_in + n_used);
+    *out = new SketchPair(extend_sketch_columns(*static_cast<SketchPair*>(p), *static_cast<LinearOperator*>(op), extra,
+                                                used, *static_cast<Rng*>(rng)));
+    std::copy(used.begin(), used.end(), used_out);
+  });
+}
+int orc_column_sampling_nystrom(void* op, int64_t k, const int64_t* indices, void** out) {
+  return guard([&] {
+    *out = new NystromApproximation(column_sampling_nystrom(*static_cast<LinearOperator*>(op),
+                                                            std::vector<Index>(indices, indices + k)));
+  });
+}
+int orc_column_sampling_nystrom_rng(void* op, int64_t ell, void* rng, void** out) {
+  return guard([&] {
+    *out = new NystromApproximation(
+        column_sampling_nystrom(*static_cast<LinearOperator*>(op), ell, *static_cast<Rng*>(rng)));
+  });
+}
 int orc_nystrom_from_sketch(void* p, void** out) {
   return guard([&] { *out = new NystromApproximation(nystrom_from_sketch(*static_cast<SketchPair*>(p))); });
 }

@@ -501,6 +501,36 @@ def extend_sketch_with(pair, op: LinearOperator, fresh) -> SketchPair:
     return pair
 
 
+def extend_sketch_columns(pair, op: LinearOperator, extra: int, used: list, rng: Rng) -> SketchPair:
+    """extend_sketch_columns (nystrom.cpp:60-94): appends `extra` unused columns of A
+    drawn from `rng`; `used` is extended in place (the handle keeps its own copy)."""
+    if isinstance(pair, _PendingSketch):
+        if pair.n != op.dim():
+            raise InvalidArgument("extend_sketch_columns: dimension mismatch")
+        pair = make_empty_sketch(op)
+    _check(lib().npcg_nys_extend_columns(_vp(pair.h), _i64(extra), _vp(rng.h)))
+    cnt = _i64()
+    _check(lib().npcg_nys_used(_vp(pair.h), None, C.byref(cnt)))
+    buf = np.zeros(max(cnt.value, 1), dtype=np.int64)
+    _check(lib().npcg_nys_used(_vp(pair.h), buf.ctypes.data_as(_vp), C.byref(cnt)))
+    used[:] = [int(v) for v in buf[:cnt.value]]
+    return pair
+
+
+def column_sampling_nystrom(op: LinearOperator, ell_or_indices, rng: Rng | None = None) -> "NystromApproximation":
+    """column_sampling_nystrom (nystrom.cpp:150-184): `ell` columns drawn from
+    `rng`, or the caller's distinct indices."""
+    h = _vp()
+    if rng is not None:
+        _check(lib().npcg_column_sampling_nystrom(_vp(op.h), _i64(int(ell_or_indices)), None, _vp(rng.h),
+                                                  C.byref(h)))
+    else:
+        idx = np.ascontiguousarray(ell_or_indices, dtype=np.int64)
+        _check(lib().npcg_column_sampling_nystrom(_vp(op.h), _i64(idx.size), idx.ctypes.data_as(_vp), None,
+                                                  C.byref(h)))
+    return _approx_from(_Nys(h.value))
+
+
 def nystrom_from_sketch(pair: SketchPair) -> NystromApproximation:
     """nystrom_from_sketch (nystrom.cpp:96-140), factored on device."""
     _check(lib().npcg_nys_factor(_vp(pair.h)))

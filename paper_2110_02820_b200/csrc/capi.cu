@@ -632,6 +632,93 @@ int npcg_nys_extend_rng(npcg_nys* nys, int64_t extra, npcg_rng* rng) {
     nys->ctx->c->sync();
   });
 }
+namespace {
+// extend_sketch_columns' draw (nystrom.cpp:69-80): partial Fisher-Yates over the
+// unused indices in increasing order, rng.integer(remaining - i).
+std::vector<i64> draw_unused(HostRng& r, i64 n, const std::vector<i64>& used, i64 extra) {
+  std::vector<bool> taken(static_cast<size_t>(n), false);
+  for (const i64 j : used) taken[static_cast<size_t>(j)] = true;
+  std::vector<i64> remaining;
+  remaining.reserve(static_cast<size_t>(n) - used.size());
+  for (i64 j = 0; j < n; ++j)
+    if (!taken[static_cast<size_t>(j)]) remaining.push_back(j);
+  for (i64 i = 0; i < extra; ++i) {
+    const i64 pick = i + static_cast<i64>(r.integer(static_cast<uint64_t>(static_cast<i64>(remaining.size()) - i)));
+    std::swap(remaining[static_cast<size_t>(i)], remaining[static_cast<size_t>(pick)]);
+  }
+  remaining.resize(static_cast<size_t>(extra));
+  return remaining;
+}
+void extend_columns_rng(Nys& s, i64 extra, HostRng& r) {
+  if (!s.op || !s.op->has_column())
+    fail(NPCG_ERUNTIME, "extend_sketch_columns: operator has no column access");
+  if (extra < 1) invalid("extend_sketch_columns: extra must be >= 1");
+  if (static_cast<i64>(s.used.size()) + extra > s.n)
+    invalid("extend_sketch_columns: sketch size would exceed dimension");
+  const std::vector<i64> idx = draw_unused(r, s.n, s.used, extra);
+  nys_extend_columns(s, idx);
+  s.used.insert(s.used.end(), idx.begin(), idx.end());
+}
+}  // namespace
+
+int npcg_nys_extend_columns(npcg_nys* nys, int64_t extra, npcg_rng* rng) {
+  return guard([&] {
+    need(nys, "npcg_nys_extend_columns");
+    need(rng, "npcg_nys_extend_columns rng");
+    C(nys->ctx);
+    extend_columns_rng(nys->s, extra, rng->r);
+  });
+}
+
+int npcg_nys_used(const npcg_nys* nys, int64_t* out, int64_t* count) {
+  return guard([&] {
+    need(nys, "npcg_nys_used");
+    if (count) *count = static_cast<int64_t>(nys->s.used.size());
+    if (out) std::copy(nys->s.used.begin(), nys->s.used.end(), out);
+  });
+}
+
+int npcg_column_sampling_nystrom(npcg_op* op, int64_t ell, const int64_t* indices, npcg_rng* rng, npcg_nys** out) {
+  return guard([&] {
+    need(op, "npcg_column_sampling_nystrom");
+    Ctx& c = C(op->ctx);
+    const i64 n = op->op->n;
+    std::vector<i64> idx;
+    if (!indices) {  // nystrom.cpp:150-158
+      need(rng, "npcg_column_sampling_nystrom rng");
+      if (ell < 1 || ell > n) invalid("column_sampling_nystrom: need 1 <= ell <= dim");
+      if (!op->op->has_column()) fail(NPCG_ERUNTIME, "column_sampling_nystrom: operator has no column access");
+      std::vector<int64_t> pool(static_cast<size_t>(n));  // sample_without_replacement (random.cpp:44-56)
+      for (i64 i = 0; i < n; ++i) pool[static_cast<size_t>(i)] = i;
+      for (i64 i = 0; i < ell; ++i) {
+        const i64 j = i + static_cast<i64>(rng->r.integer(static_cast<uint64_t>(n - i)));
+        std::swap(pool[static_cast<size_t>(i)], pool[static_cast<size_t>(j)]);
+      }
+      idx.assign(pool.begin(), pool.begin() + ell);
+    } else {  // nystrom.cpp:160-184
+      if (ell < 1 || ell > n) invalid("column_sampling_nystrom: need 1 <= #indices <= dim");
+      if (!op->op->has_column()) fail(NPCG_ERUNTIME, "column_sampling_nystrom: operator has no column access");
+      std::vector<bool> seen(static_cast<size_t>(n), false);
+      for (i64 i = 0; i < ell; ++i) {
+        const i64 j = indices[i];
+        if (j < 0 || j >= n) invalid("column_sampling_nystrom: index out of range");
+        if (seen[static_cast<size_t>(j)]) invalid("column_sampling_nystrom: indices must be distinct");
+        seen[static_cast<size_t>(j)] = true;
+        idx.push_back(j);
+      }
+    }
+    auto h = std::make_unique<npcg_nys>();
+    h->ctx = op->ctx;
+    h->s.ctx = &c;
+    h->s.op = op->op.get();
+    h->s.n = n;
+    nys_extend_columns(h->s, idx);
+    h->s.used = idx;
+    nys_factor(h->s);
+    *out = h.release();
+  });
+}
+
 int npcg_nys_factor(npcg_nys* nys) {
   return guard([&] {
     need(nys, "npcg_nys_factor");
@@ -974,14 +1061,19 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
       if (!(cfg->tau > 0.0)) invalid("AdaptiveConfig: tau must be > 0");
       tau = cfg->tau;
     }
-    if (cfg->sketch != 0) fail(NPCG_ERUNTIME, "AdaptiveConfig: column sampling is not available in this build");
+    if (cfg->sketch != 0 && !op->op->has_column())  // adaptive.cpp:26-27
+      fail(NPCG_ERUNTIME, "AdaptiveConfig: column sampling needs column access");
     auto h = std::make_unique<npcg_nys>();
     h->ctx = op->ctx;
     Nys& s = h->s;
     s.ctx = &c;
     s.op = op->op.get();
     s.n = n;
-    auto grow = [&](i64 extra) {
+    auto grow = [&](i64 extra) {  // adaptive.cpp:30-35
+      if (cfg->sketch != 0) {
+        extend_columns_rng(s, extra, rng->r);
+        return;
+      }
       std::vector<double> raw(static_cast<size_t>(n * extra));
       rng->r.gaussian(n, extra, raw.data());
       nys_extend(s, raw.data(), n, extra, NPCG_HOST);

@@ -382,6 +382,37 @@ void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ld
   }
 }
 
+namespace {
+// columns idx of K with the difference formula of column() (operators.cpp:184-187)
+__global__ void kernel_idxcols_kernel(const double* __restrict__ pts, i64 ld, i64 n, i64 d,
+                                      const i64* __restrict__ idx, double c, double* __restrict__ out, i64 ldo) {
+  const i64 cc = blockIdx.y;
+  const i64 j = idx[cc];
+  for (i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (i64 k = 0; k < d; ++k) {
+      const double diff = pts[i + k * ld] - pts[j + k * ld];
+      s += diff * diff;
+    }
+    out[i + cc * ldo] = i == j ? 1.0 : exp(s * c);
+  }
+}
+}  // namespace
+
+void KernelFreeOp::columns(const i64* idx, i64 k, double* out, i64 ldo) {
+  DBuf<i64> di(k, ctx->stream);
+  NPCG_CUDA(cudaMemcpyAsync(di.p, idx, sizeof(i64) * k, cudaMemcpyHostToDevice, ctx->stream));
+  const double c = -1.0 / (2.0 * sigma * sigma);
+  for (i64 c0 = 0; c0 < k; c0 += 65535) {
+    const i64 kc = std::min<i64>(65535, k - c0);
+    NPCG_LAUNCH(*ctx, kernel_idxcols_kernel,
+                dim3(static_cast<unsigned>(std::min<i64>(cdiv(n, 256), 64)), static_cast<unsigned>(kc)), 256, 0,
+                pts.p(), pts.ld, n, d, di.p + c0, c, out + c0 * ldo, ldo);
+  }
+  ctx->sync();
+}
+
 void KernelFreeOp::column(i64 j, double* out) {
   const double c = -1.0 / (2.0 * sigma * sigma);
   NPCG_LAUNCH(*ctx, kernel_column_kernel, static_cast<unsigned>(cdiv(n, 256)), 256, 0, pts.p(), pts.ld, n, d, j, c,

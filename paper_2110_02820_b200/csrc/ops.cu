@@ -27,6 +27,34 @@ void Op::apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i6
 
 void Op::column(i64, double*) { fail(NPCG_ERUNTIME, "LinearOperator - column: operator has no column access"); }
 
+void Op::columns(const i64* idx, i64 k, double* out, i64 ldo) {
+  for (i64 c = 0; c < k; ++c) column(idx[c], out + c * ldo);
+}
+
+namespace {
+__global__ void gather_cols_kernel2(const double* __restrict__ a, i64 lda, i64 n, const i64* __restrict__ idx, i64 k,
+                                    double* __restrict__ out, i64 ldo) {
+  const i64 total = n * k;
+  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = t % n, c = t / n;
+    out[i + c * ldo] = a[i + idx[c] * lda];
+  }
+}
+__global__ void unit_cols_kernel(double* __restrict__ om, i64 ldo, const i64* __restrict__ idx, i64 k) {
+  const i64 c = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < k) om[idx[c] + c * ldo] = 1.0;
+}
+}  // namespace
+
+void DenseOp::columns(const i64* idx, i64 k, double* out, i64 ldo) {
+  DBuf<i64> d(k, ctx->stream);
+  NPCG_CUDA(cudaMemcpyAsync(d.p, idx, sizeof(i64) * k, cudaMemcpyHostToDevice, ctx->stream));
+  NPCG_LAUNCH(*ctx, gather_cols_kernel2, static_cast<unsigned>(std::min<i64>(cdiv(n * k, 256), 4096)), 256, 0,
+              a.p(), a.ld, n, d.p, k, out, ldo);
+  ctx->sync();  // the host index buffer is the caller's
+}
+
 // DenseOperator::do_matvec / do_apply_block (operators.cpp:72-78). A is
 // symmetric, so A V is computed as A^T V: each output entry is a dot of a
 // contiguous column with V (coldot for <= 8 columns; DMMA GEMM beyond).
@@ -91,6 +119,23 @@ void nys_extend(Nys& s, const double* raw, i64 ld, i64 extra, int where) {
   double* q_new = s.omega.col(old);
   orthonormalize(ctx, fresh.p(), fresh.ld, n, extra, q_new, s.omega.ld);
   s.op->apply(q_new, s.omega.ld, extra, s.y.col(old), s.y.ld);
+  s.size = old + extra;
+  s.factored = false;
+}
+
+void nys_extend_columns(Nys& s, const std::vector<i64>& idx) {
+  Ctx& ctx = *s.ctx;
+  const i64 old = s.size, extra = static_cast<i64>(idx.size());
+  if (extra == 0) return;
+  ensure_capacity(s, old + extra);
+  // omega columns: e_j (fresh capacity is zero; reused capacity is cleared first)
+  NPCG_CUDA(cudaMemset2DAsync(s.omega.col(old), s.omega.ld * 8, 0, s.n * 8, extra, ctx.stream));
+  DBuf<i64> d(extra, ctx.stream);
+  NPCG_CUDA(cudaMemcpyAsync(d.p, idx.data(), sizeof(i64) * extra, cudaMemcpyHostToDevice, ctx.stream));
+  NPCG_LAUNCH(ctx, unit_cols_kernel, static_cast<unsigned>(cdiv(extra, 256)), 256, 0, s.omega.col(old), s.omega.ld,
+              d.p, extra);
+  s.op->columns(idx.data(), extra, s.y.col(old), s.y.ld);
+  ctx.sync();
   s.size = old + extra;
   s.factored = false;
 }

@@ -27,10 +27,13 @@ struct Op {
   /// A product costs far more than a host round trip (matrix-free kernel):
   /// the PCG driver then keeps one iteration in flight instead of several.
   virtual bool costly() const { return false; }
+  /// out(:, c) = A(:, idx[c]) for c < k (host indices; ld ldo). Default: column() per index.
+  virtual void columns(const i64* idx, i64 k, double* out, i64 ldo);
 };
 
 struct DenseOp : Op {  // DenseOperator (operators.cpp:64-80); also the stored kernel
   DMat a;
+  void columns(const i64* idx, i64 k, double* out, i64 ldo) override;
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
   void apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) override;
   bool has_column() const override { return true; }
@@ -54,6 +57,8 @@ struct KernelFreeOp : Op {  // KernelOperator beyond dense_cap (operators.cpp:15
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
   bool has_column() const override { return true; }
   void column(i64 j, double* out) override;
+  void columns(const i64* idx, i64 k, double* out, i64 ldo) override;
+  bool costly() const override { return true; }
 };
 
 /// Exchange callback of a sharded operator (npcg_exchange_fn in the C-ABI):
@@ -104,8 +109,12 @@ struct Nys {
   double shift = 0.0;
   bool factored = false;
   std::vector<double> lambda_host;
+  std::vector<i64> used;  // column-sampling sketches: indices drawn so far (extend_sketch_columns)
 };
 void nys_extend(Nys& s, const double* raw, i64 ld, i64 extra, int where);
+/// Append unit columns e_j and A(:, j) for the given distinct indices
+/// (extend_sketch_columns / column_sampling_nystrom, nystrom.cpp:60-94,160-184).
+void nys_extend_columns(Nys& s, const std::vector<i64>& idx);
 void nys_factor(Nys& s);
 
 /// NystromPreconditioner (preconditioner.hpp:20-37).

@@ -51,6 +51,17 @@ int main() {
     CHECK(ap.lambda.size() == 3);
     for (Index i = 0; i < 3; ++i) CHECK(ap.lambda(i) == 0.0);
   }
+  // nystrom_test.cpp:84-103 — column sampling on diag(5, 0, 0) reconstructs exactly
+  {
+    Matrix d = Matrix::Zero(3, 3);
+    d(0, 0) = 5.0;
+    const DenseOperator dop(d);
+    const NystromApproximation ap = column_sampling_nystrom(dop, std::vector<Index>{0});
+    CHECK(ap.lambda.size() == 1 && std::abs(ap.lambda(0) - 5.0) < 1e-12);
+    threw = false;
+    try { column_sampling_nystrom(dop, std::vector<Index>{1, 1}); } catch (const std::invalid_argument&) { threw = true; }
+    CHECK(threw);
+  }
   // solvers_test.cpp:112-127 — known solution through Nyström PCG
   {
     const Index n = 60;

@@ -108,3 +108,18 @@ def test_configuration_validation(impl):  # :250-277
         kw.setdefault("tau", 10.0)
         with pytest.raises(ValueError):
             impl.adaptive(op, rng, mode="error", **kw)
+
+
+def test_column_sampling_drives_the_adaptive_loop(impl):  # adaptive_test.cpp:180-199
+    rng = impl.Rng(12)
+    pts = rng.gaussian_matrix(60, 3)
+    op = impl.KernelOperator(pts, 0.8)
+    out = impl.adaptive(op, rng, mode="ratio", ell0=5, ell_max=60, mu=1e-2, tau=10.0, sketch="column_sampling")
+    assert out.ell_final >= 5
+    if not out.hit_cap:
+        assert out.approximation.lambda_min <= 0.1
+    u = out.approximation.u
+    assert np.abs(u.T @ u - np.eye(out.ell_final)).max() < 1e-10
+    gram = impl.GramRidgeOperator(rng.gaussian_matrix(30, 10))
+    with pytest.raises(RuntimeError):
+        impl.adaptive(gram, rng, mode="ratio", ell0=2, ell_max=10, mu=1e-2, tau=10.0, sketch="column_sampling")

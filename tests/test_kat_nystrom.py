@@ -92,3 +92,65 @@ def test_stable_pipeline_survives_sixteen_decades(impl):  # :265-282
     assert min_eigenvalue(ahat) > -1e-14
     omega = impl.Rng(77).gaussian_matrix(n, ell)
     assert np.linalg.norm(ahat - nystrom_definitional(a, omega)) < 1e-6 * np.linalg.norm(a)
+
+
+# ---- column-sampling Nyström (nystrom.cpp:60-94,150-184) ----
+
+def test_column_sampling_on_diagonal_matrices(impl):  # nystrom_test.cpp:84-103
+    d = np.diag([5.0, 0, 0])
+    approx = impl.column_sampling_nystrom(impl.DenseOperator(d), [0])
+    assert np.abs(approx.materialize() - d).max() < 1e-12
+    approx = impl.column_sampling_nystrom(impl.DenseOperator(np.eye(4)), [0, 2])
+    assert np.abs(approx.materialize() - np.diag([1.0, 0, 1, 0])).max() < 1e-12
+    op = impl.DenseOperator(np.eye(4))
+    with pytest.raises(ValueError):
+        impl.column_sampling_nystrom(op, [1, 1])
+    with pytest.raises(ValueError):
+        impl.column_sampling_nystrom(op, [4])
+
+
+def test_column_sampling_matches_definitional_oracle(impl):  # :105-121
+    rng = impl.Rng(8)
+    pts = rng.gaussian_matrix(30, 3)
+    op = impl.KernelOperator(pts, 1.5)
+    k = op.dense()
+    approx = impl.column_sampling_nystrom(op, 10, impl.Rng(1234))
+    idx = impl.Rng(1234).sample_without_replacement(30, 10)
+    x = np.zeros((30, 10))
+    for i, j in enumerate(idx):
+        x[j, i] = 1.0
+    assert np.linalg.norm(approx.materialize() - nystrom_definitional(k, x)) < 1e-8 * np.linalg.norm(k)
+
+
+def test_column_sampling_requires_column_access(impl):  # :123-127
+    rng = impl.Rng(9)
+    op = impl.GramRidgeOperator(rng.gaussian_matrix(10, 6))
+    with pytest.raises(RuntimeError):
+        impl.column_sampling_nystrom(op, 2, rng)
+
+
+def test_extend_sketch_columns_draws_unused_indices(impl):  # :173-189
+    op = impl.DenseOperator(np.eye(6))
+    rng = impl.Rng(13)
+    used = []
+    pair = impl.extend_sketch_columns(impl.make_empty_sketch(6), op, 2, used, rng)
+    assert len(used) == 2
+    pair = impl.extend_sketch_columns(pair, op, 3, used, rng)
+    assert len(used) == 5 and len(set(used)) == 5
+    om, y = pair.arrays(6)
+    for i in range(5):
+        assert om[:, i].sum() == 1.0
+        assert np.array_equal(y[:, i], op.column(used[i]))
+    with pytest.raises(ValueError):
+        impl.extend_sketch_columns(pair, op, 2, used, rng)
+
+
+def test_column_sampling_draws_match_the_oracle(impl, orc):
+    # the same Rng stream picks the same columns in both implementations
+    op = impl.DenseOperator(np.diag(np.arange(1.0, 13.0)))
+    used = []
+    impl.extend_sketch_columns(impl.make_empty_sketch(12), op, 4, used, impl.Rng(21))
+    ref = []
+    orc.extend_sketch_columns(orc.make_empty_sketch(12), orc.DenseOperator(np.diag(np.arange(1.0, 13.0))), 4, ref,
+                              orc.Rng(21))
+    assert used == ref
