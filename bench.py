@@ -165,7 +165,7 @@ class DevicePath:
         n = w.n
         dev = torch.device("cuda", ctx.device)
         # column-major device buffers: torch (cols, rows) row-major == (rows, cols) col-major
-        self.omega = torch.from_numpy(np.ascontiguousarray(w.omega.T)).to(dev)
+        self.omega = torch.from_numpy(np.ascontiguousarray(w.omega.T)).to(dev) if w.omega is not None else None
         b = w.b.reshape(n, -1, order="F")
         self.s = b.shape[1]
         self.b = torch.from_numpy(np.ascontiguousarray(b.T)).to(dev)
@@ -175,34 +175,66 @@ class DevicePath:
         self.opts = npcg._SolveOpts(w.eta, w.max_iter, int(w.relative), 0)
 
     def step(self):
+        """One full solve: sketch (fixed Omega, or the adaptive rank search for
+        config 4), factorisation, preconditioner and PCG -- for the
+        regularisation-path workload (config 5) one sketch and a PCG solve per mu."""
         npcg, L, w, vp, i64 = self.npcg, self.L, self.w, C.c_void_p, C.c_int64
         nys, pre = vp(), vp()
-        npcg._check(L.npcg_nys_create(vp(self.op.h), C.byref(nys)))
         try:
-            npcg._check(L.npcg_nys_extend(nys, i64(w.ell), vp(self.omega.data_ptr()), i64(w.n), npcg.DEVICE))
-            npcg._check(L.npcg_nys_factor(nys))
-            npcg._check(L.npcg_pre_create(nys, C.c_double(w.mu), C.byref(pre)))
-            rc = L.npcg_pcg(vp(self.op.h), pre, C.c_double(w.mu), i64(self.s), vp(self.b.data_ptr()), i64(w.n), None,
-                            i64(w.n), C.byref(self.opts), vp(self.x.data_ptr()), i64(w.n), self.reports, None, None,
-                            npcg.DEVICE)
-            npcg._check(rc)
+            if w.adaptive:  # adaptive_nystrom (adaptive.cpp:111-123); b was drawn first from Rng(k)
+                a = w.adaptive
+                rng = npcg.Rng(int(w.name[3]))
+                rng.discard(2 * w.n)
+                cfg = npcg._AdaptiveCfg(a["ell0"], a["ell_max"], w.mu, 0, 1, a["tau"], a["q"], 1, 0)
+                out = npcg._AdaptiveOutcome()
+                npcg._check(L.npcg_adaptive(vp(self.op.h), C.byref(cfg), vp(rng.h), C.byref(nys), C.byref(out)))
+                self.adaptive_outcome = (out.ell_final, out.doublings, bool(out.hit_cap))
+            else:
+                npcg._check(L.npcg_nys_create(vp(self.op.h), C.byref(nys)))
+                npcg._check(L.npcg_nys_extend(nys, i64(w.ell), vp(self.omega.data_ptr()), i64(w.n), npcg.DEVICE))
+                npcg._check(L.npcg_nys_factor(nys))
+            iters = []
+            for mu in (w.mus or [w.mu]):
+                npcg._check(L.npcg_pre_create(nys, C.c_double(mu), C.byref(pre)))
+                rc = L.npcg_pcg(vp(self.op.h), pre, C.c_double(mu), i64(self.s), vp(self.b.data_ptr()), i64(w.n),
+                                None, i64(w.n), C.byref(self.opts), vp(self.x.data_ptr()), i64(w.n), self.reports,
+                                None, None, npcg.DEVICE)
+                if rc not in (0, 3):  # a diverged column is reported, not fatal, on the regularisation path
+                    npcg._check(rc)
+                iters.append([(r.iterations, bool(r.converged)) for r in self.reports])
+                L.npcg_pre_destroy(pre)
+                pre = vp()
         finally:
             if pre.value:
                 L.npcg_pre_destroy(pre)
-            L.npcg_nys_destroy(nys)
-        return [(r.iterations, bool(r.converged)) for r in self.reports]
+            if nys.value:
+                L.npcg_nys_destroy(nys)
+        return iters[0] if len(iters) == 1 else iters
 
 
 def e2e_step(npcg, w, ctx, host, exchange=None):
     """Public API with host buffers: every input crosses PCIe inside the step."""
     op = npcg.workloads.build_operator(npcg, host, ctx=ctx, exchange=exchange)
-    pair = npcg.make_empty_sketch(op)
-    pair = npcg.extend_sketch_with(pair, op, host.omega)
-    approx = npcg.nystrom_from_sketch(pair)
-    pre = npcg.build_preconditioner(approx, w.mu)
-    rep = npcg.nystrom_pcg(op, host.b, w.mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
-    x = rep.x if not isinstance(rep, list) else np.column_stack([r.x for r in rep])
-    return float(x.sum())
+    if w.adaptive:
+        a = w.adaptive
+        rng = npcg.Rng(int(w.name[3]))
+        rng.discard(2 * w.n)
+        approx = npcg.adaptive(op, rng, mode="error", ell0=a["ell0"], ell_max=a["ell_max"], mu=w.mu, tau=a["tau"],
+                               q=a["q"]).approximation
+    else:
+        pair = npcg.make_empty_sketch(op)
+        pair = npcg.extend_sketch_with(pair, op, host.omega)
+        approx = npcg.nystrom_from_sketch(pair)
+    total = 0.0
+    for mu in (w.mus or [w.mu]):
+        pre = npcg.build_preconditioner(approx, mu)
+        try:
+            rep = npcg.nystrom_pcg(op, host.b, mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
+        except npcg.SolveDivergenceError as e:  # reported per column on the regularisation path
+            rep = e.report
+        x = rep.x if not isinstance(rep, list) else np.column_stack([r.x for r in rep])
+        total += float(x.sum())
+    return total
 
 
 def input_bytes(w):
@@ -216,7 +248,7 @@ def input_bytes(w):
         op_bytes = w.data["a"].nbytes
     else:
         op_bytes = w.data["lambda"].nbytes
-    return op_bytes + w.omega.nbytes + w.b.nbytes
+    return op_bytes + (w.omega.nbytes if w.omega is not None else 0) + w.b.nbytes
 
 
 ALGO_NOTE = {
@@ -272,13 +304,24 @@ def cpu_baseline(w, steps=1):
     times, iters = [], []
     for _ in range(max(1, steps)):
         t0 = time.perf_counter()
-        pair = orc.extend_sketch_with(orc.make_empty_sketch(w.n), op, w.omega)
-        approx = orc.nystrom_from_sketch(pair)
-        pre = orc.build_preconditioner(approx, w.mu)
+        if w.adaptive:
+            a = w.adaptive
+            rng = orc.Rng(int(w.name[3]))
+            rng.gaussian_vector(w.n)  # b was drawn first
+            approx = orc.adaptive(op, rng, mode="error", ell0=a["ell0"], ell_max=a["ell_max"], mu=w.mu,
+                                  tau=a["tau"], q=a["q"]).approximation
+        else:
+            pair = orc.extend_sketch_with(orc.make_empty_sketch(w.n), op, w.omega)
+            approx = orc.nystrom_from_sketch(pair)
         b = w.b.reshape(w.n, -1, order="F")
-        for j in range(b.shape[1]):
-            rep = orc.nystrom_pcg(op, b[:, j], w.mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
-            iters.append(rep.iterations)
+        for mu in (w.mus or [w.mu]):
+            pre = orc.build_preconditioner(approx, mu)
+            for j in range(b.shape[1]):
+                try:
+                    rep = orc.nystrom_pcg(op, b[:, j], mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
+                except orc.SolveDivergenceError as e:
+                    rep = e.report
+                iters.append(rep.iterations)
         times.append(time.perf_counter() - t0)
     t = float(np.median(times))
     return {"value": 1.0 / t, "unit": "solves/s", "cores": ncores, "kind": "port",
@@ -374,13 +417,16 @@ def run_b200(args):
     prof = ctx.prof_report()
     ctx.prof_enable(False)
 
-    # end to end through the public API with host buffers
+    # end to end through the public API with host buffers (the device path's
+    # operator is released first: two copies of config 5's 80 GB A do not fit)
+    path.op = None
+    torch.cuda.synchronize()
     e2e = None
     if not args.no_e2e:
         pin = lambda a: _pinned(torch, a)
         host = workloads.Workload(**{**w.__dict__})
         host.data = {k: (pin(v) if isinstance(v, np.ndarray) and v.size > 1 else v) for k, v in w.data.items()}
-        host.omega, host.b = pin(w.omega), pin(w.b)
+        host.omega, host.b = (pin(w.omega) if w.omega is not None else None), pin(w.b)
         for _ in range(1):
             e2e_step(npcg, w, ctx, host, exchange)
         barrier()
@@ -400,7 +446,7 @@ def run_b200(args):
             el = float(t.item())
         h2d = input_bytes(w) - (w.data["x"].nbytes * (1 - 1 / world) if sharded and w.kind == "gram" else 0)
         e2e = {"value": (1 if sharded else world) * k2 / el, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(w.b.nbytes + 8 * w.ell), "steps": k2,
+               "d2h_bytes_per_step": int(w.b.nbytes * len(w.mus or [w.mu]) + 8 * w.ell), "steps": k2,
                "wall_s": time.perf_counter() - t0}
 
     if rank != 0:
@@ -426,7 +472,9 @@ def run_b200(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng mt19937_64+Box-Muller, seeded)",
         "config": {**w.describe(), "parallelism": f"rowshard{world}" if sharded else f"replicas{world}",
                    "l2": "inputs larger than L2 (X 640 MB)",
-                   "iterations": info[0][0], "converged": info[0][1]},
+                   **({"iterations_per_mu": [max(it for it, _ in rs) for rs in info], "mus": len(info)}
+                      if w.mus else {"iterations": info[0][0], "converged": info[0][1]}),
+                   **({"adaptive_ell_final_doublings_hitcap": list(path.adaptive_outcome)} if w.adaptive else {})},
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
         "clocks": clk.summary(), "input_generation_s": t_gen,
     }

@@ -284,6 +284,20 @@ __global__ void symmetrize_kernel(const double* __restrict__ a, i64 n, i64 lda, 
   }
 }
 
+// in place: each lower/upper pair is averaged by one thread (diagonal unchanged)
+__global__ void symmetrize_inplace_kernel(double* __restrict__ a, i64 n, i64 lda) {
+  const i64 total = n * n;
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = idx % n, j = idx / n;
+    if (i > j) {
+      const double v = (a[i + j * lda] + a[j + i * lda]) / 2.0;
+      a[i + j * lda] = v;
+      a[j + i * lda] = v;
+    }
+  }
+}
+
 __global__ void scale_cols_kernel(double* a, i64 rows, i64 cols, i64 lda, const double* __restrict__ d) {
   const i64 total = rows * cols;
   for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
@@ -390,6 +404,10 @@ void add2d(Ctx& ctx, i64 rows, i64 cols, const double* a, i64 lda, const double*
 }
 void symmetrize(Ctx& ctx, const double* a, i64 n, i64 lda, double* out, i64 ldo) {
   if (n <= 0) return;
+  if (a == out && lda == ldo) {
+    NPCG_LAUNCH(ctx, symmetrize_inplace_kernel, grid_for(ctx, n * n), 256, 0, out, n, ldo);
+    return;
+  }
   NPCG_LAUNCH(ctx, symmetrize_kernel, grid_for(ctx, n * n), 256, 0, a, n, lda, out, ldo);
 }
 void scale_cols(Ctx& ctx, double* a, i64 rows, i64 cols, i64 lda, const double* d) {

@@ -522,7 +522,7 @@ int npcg_op_lowrank_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g,
   return guard([&] {
     Ctx& c = C(ctx);
     if (n < 1 || r < 1) invalid("lowrank operator: need n >= 1 and r >= 1");
-    DMat G, GD, A, S;
+    DMat G, GD, A;
     upload(c, G, n, r, g, ldg, where);
     GD.alloc(n, r, c.stream, false);
     copy2d(c, n, r, G.p(), G.ld, GD.p(), GD.ld);
@@ -532,10 +532,9 @@ int npcg_op_lowrank_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g,
     A.alloc(n, n, c.stream, false);
     gemm(c, n, n, r, 1.0, Operand{GD.p(), GD.ld, false}, Operand{G.p(), G.ld, false}, 0.0, A.p(), A.ld);
     divide(c, n, n, A.p(), A.ld, static_cast<double>(r));
-    S.alloc(n, n, c.stream, true);
-    symmetrize(c, A.p(), n, A.ld, S.p(), S.ld);
+    symmetrize(c, A.p(), n, A.ld, A.p(), A.ld);  // in place: (A + A^T) / 2
     c.sync();
-    *out = make_dense(ctx, std::move(S), n, kDense);
+    *out = make_dense(ctx, std::move(A), n, kDense);
   });
 }
 
