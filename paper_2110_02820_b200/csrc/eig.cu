@@ -236,14 +236,25 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
   cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
+// Fast reciprocal (MUFU seed + Newton in the FP64 pipe, about 1 ulp): the
+// Sturm counts and inverse iteration only need it to a few ulps, and an IEEE
+// division on their sequential recurrences costs several times more.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+
 // number of eigenvalues of T strictly below x (Sturm sequence of LDL^T)
-__device__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
+__device__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2, int n, double x,
+                           double pivmin) {
   int cnt = 0;
   double q = d[0] - x;
   if (fabs(q) < pivmin) q = -pivmin;
   cnt += q < 0.0;
+#pragma unroll 8
   for (int i = 1; i < n; ++i) {
-    q = d[i] - x - e2[i - 1] / q;
+    q = (d[i] - x) - e2[i - 1] * fast_rcp(q);
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += q < 0.0;
   }
@@ -423,16 +434,17 @@ __global__ void invit_smem_kernel(const double* __restrict__ d, const double* __
       double nz;
       if (fabs(a) >= fabs(sub)) {
         const double piv = a == 0.0 ? tiny : a;
-        const double f = sub / piv;
-        u0[SX(i)] = piv;
+        const double pinv = fast_rcp(piv);
+        const double f = sub * pinv;
+        u0[SX(i)] = pinv;  // U's diagonal is kept as its reciprocal (back substitution multiplies)
         u1[SX(i)] = b;
         u2[SX(i)] = 0.0;
         nd -= f * b;
         z[SX(i)] = zi;
         nz = zi1 - f * zi;
       } else {
-        const double f = a / sub;
-        u0[SX(i)] = sub;
+        const double f = a * fast_rcp(sub);
+        u0[SX(i)] = fast_rcp(sub);
         u1[SX(i)] = nd;
         u2[SX(i)] = nb;
         const double nd2 = b - f * nd;
@@ -445,14 +457,14 @@ __global__ void invit_smem_kernel(const double* __restrict__ d, const double* __
       b = nb;
       zi = nz;
     }
-    u0[SX(n - 1)] = a == 0.0 ? tiny : a;
+    u0[SX(n - 1)] = fast_rcp(a == 0.0 ? tiny : a);
     z[SX(n - 1)] = zi;
-    // back substitution
-    double x2 = 0.0, x1 = z[SX(n - 1)] / u0[SX(n - 1)];
+    // back substitution (u0 holds reciprocals)
+    double x2 = 0.0, x1 = z[SX(n - 1)] * u0[SX(n - 1)];
     z[SX(n - 1)] = x1;
     double nrm = x1 * x1;
     for (int i = n - 2; i >= 0; --i) {
-      const double x = (z[SX(i)] - u1[SX(i)] * x1 - u2[SX(i)] * x2) / u0[SX(i)];
+      const double x = (z[SX(i)] - u1[SX(i)] * x1 - u2[SX(i)] * x2) * u0[SX(i)];
       z[SX(i)] = x;
       nrm += x * x;
       x2 = x1;
