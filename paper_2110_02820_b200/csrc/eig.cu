@@ -236,13 +236,14 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
   cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
-// Fast reciprocal (MUFU seed + Newton in the FP64 pipe, about 1 ulp): the
+// Fast reciprocal (MUFU seed + Newton steps in the FP64 pipe, about 1 ulp): the
 // Sturm counts and inverse iteration only need it to a few ulps, and an IEEE
 // division on their sequential recurrences costs several times more.
 __device__ __forceinline__ double fast_rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  return r;
+  const double e = fma(-x, r, 1.0);  // one more Newton step: the approximation alone is not full precision
+  return fma(r, e, r);
 }
 
 // number of eigenvalues of T strictly below x (Sturm sequence of LDL^T)
