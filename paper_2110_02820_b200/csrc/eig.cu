@@ -21,6 +21,7 @@
 #include <string>
 
 #include "eig.cuh"
+#include "gemm.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -551,6 +552,103 @@ __global__ void __launch_bounds__(256) backtransform_smem_kernel(const double* _
     for (int i = lane; i < n; i += 32) Z[i + static_cast<i64>(col) * ldz] = z[i];
 }
 
+// Compact-WY back-transformation: the reflectors k in block b = [32b, 32b+31]
+// multiply to P_b = H_{32b} ... H_{32b+31} = I - V_b T_b V_b^T (T_b upper
+// triangular, dlarft 'F','C'), and Z <- P_0 P_1 ... Z is applied block by block
+// (last block first) as Z -= V_b (T_b (V_b^T Z)): 32 independent dots per
+// column instead of 32 dependent reflector applications.
+constexpr int WY = 32;
+
+// T_b from the Gram S = H^T H (its 32x32 diagonal blocks) and tau; one warp per block.
+__global__ void wy_t_kernel(const double* __restrict__ S, i64 lds, const double* __restrict__ tau, int nref,
+                            double* __restrict__ T) {
+  __shared__ double Ts[WY][WY + 1];
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const int k0 = b * WY, kb = min(WY, nref - k0);
+  for (int idx = lane; idx < WY * (WY + 1); idx += 32) (&Ts[0][0])[idx] = 0.0;
+  __syncwarp();
+  for (int j = 0; j < kb; ++j) {
+    const double tj = tau[k0 + j];
+    // T[0:j, j] = -tau_j T[0:j, 0:j] (V^T v_j)[0:j]
+    double acc = 0.0;
+    if (lane < j)
+      for (int c = lane; c < j; ++c) acc += Ts[lane][c] * S[(k0 + c) + static_cast<i64>(k0 + j) * lds];
+    __syncwarp();
+    if (lane < j) Ts[lane][j] = -tj * acc;
+    if (lane == j) Ts[j][j] = tj;
+    __syncwarp();
+  }
+  for (int idx = lane; idx < WY * WY; idx += 32) {
+    const int r = idx % WY, c = idx / WY;
+    T[static_cast<i64>(b) * WY * WY + r + c * WY] = Ts[r][c];
+  }
+}
+
+// Z <- P_0 ... P_{nb-1} Z; CTA = 8 columns of Z (one warp each) kept in shared memory.
+__global__ void __launch_bounds__(256) wy_apply_kernel(const double* __restrict__ H, i64 ldh,
+                                                       const double* __restrict__ T, int nref, int n, double* Z,
+                                                       i64 ldz) {
+  extern __shared__ double wsm[];
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * nw + warp;
+  double* vb = wsm;                                    // [WY][n]
+  double* tb = vb + static_cast<i64>(WY) * n;          // [WY][WY] col-major
+  double* z = tb + WY * WY + static_cast<i64>(warp) * n;
+  if (col < n)
+    for (int i = lane; i < n; i += 32) z[i] = Z[i + static_cast<i64>(col) * ldz];
+  const int nblk = (nref + WY - 1) / WY;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int k0 = b * WY, kb = min(WY, nref - k0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < WY * n; idx += blockDim.x) {
+      const int c = idx / n, i = idx % n;
+      vb[idx] = c < kb ? H[i + static_cast<i64>(k0 + c) * ldh] : 0.0;
+    }
+    for (int idx = threadIdx.x; idx < WY * WY; idx += blockDim.x) tb[idx] = T[static_cast<i64>(b) * WY * WY + idx];
+    __syncthreads();
+    if (col >= n) continue;
+    // w = V^T z: per-lane partials of all 32 dots, then a reduce-scatter (lane j ends with w_j)
+    double acc[WY];
+#pragma unroll
+    for (int c = 0; c < WY; ++c) acc[c] = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double zi = z[i];
+#pragma unroll
+      for (int c = 0; c < WY; ++c) acc[c] += vb[c * n + i] * zi;
+    }
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+      const bool up = lane & sft;
+#pragma unroll
+      for (int c = 0; c < sft; ++c) {
+        const double send = up ? acc[c] : acc[sft + c];
+        const double keep = up ? acc[sft + c] : acc[c];
+        acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+      }
+    }
+    const double w = acc[0];
+    // u = T w (T upper triangular): lane j sums T[j][k] w_k, k >= j
+    double u = 0.0;
+#pragma unroll
+    for (int k = 0; k < WY; ++k) {
+      const double wk = __shfl_sync(0xffffffffu, w, k);
+      if (k >= lane) u += tb[lane + k * WY] * wk;
+    }
+    double ua[WY];
+#pragma unroll
+    for (int c = 0; c < WY; ++c) ua[c] = __shfl_sync(0xffffffffu, u, c);
+    // z -= V u
+    for (int i = lane; i < n; i += 32) {
+      double sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < WY; ++c) sum += vb[c * n + i] * ua[c];
+      z[i] -= sum;
+    }
+  }
+  if (col < n)
+    for (int i = lane; i < n; i += 32) Z[i + static_cast<i64>(col) * ldz] = z[i];
+}
+
 }  // namespace
 
 void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
@@ -645,11 +743,19 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
   }
   NPCG_LAUNCH(ctx, transpose_sq_kernel, dim3(static_cast<unsigned>(cdiv(n, 32)), static_cast<unsigned>(cdiv(n, 32))),
               dim3(32, 8), 0, zr.p, nn, Z, ldz);
-  if ((8 + BT_KB) * n * 8 <= 200 * 1024) {
-    const int smem = static_cast<int>((8 + BT_KB) * n * 8);
-    NPCG_CUDA(cudaFuncSetAttribute(backtransform_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    NPCG_LAUNCH(ctx, backtransform_smem_kernel, static_cast<unsigned>(cdiv(n, 8)), 256, smem, H.p(), H.ld, tau.p, nn,
-                Z, ldz);
+  const int nref = nn - 2;  // reflectors k = 0 .. n-3
+  if (nref >= 1 && (static_cast<i64>(WY + 8) * n + WY * WY) * 8 <= 200 * 1024) {
+    // compact WY: T blocks from the diagonal blocks of H^T H (one DMMA GEMM)
+    const int nblk = (nref + WY - 1) / WY;
+    DMat S;
+    S.alloc(n, n, ctx.stream, false);
+    gemm(ctx, n, n, n, 1.0, Operand{H.p(), H.ld, true}, Operand{H.p(), H.ld, true}, 0.0, S.p(), S.ld);
+    DBuf<double> Tw(static_cast<i64>(nblk) * WY * WY, ctx.stream);
+    NPCG_LAUNCH(ctx, wy_t_kernel, static_cast<unsigned>(nblk), 32, 0, S.p(), S.ld, tau.p, nref, Tw.p);
+    const int smem = static_cast<int>((static_cast<i64>(WY + 8) * n + WY * WY) * 8);
+    NPCG_CUDA(cudaFuncSetAttribute(wy_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    NPCG_LAUNCH(ctx, wy_apply_kernel, static_cast<unsigned>(cdiv(n, 8)), 256, smem, H.p(), H.ld, Tw.p, nref, nn, Z,
+                ldz);
   } else {
     NPCG_LAUNCH(ctx, backtransform_kernel, static_cast<unsigned>(cdiv(n * 32, 256)), 256, 0, H.p(), H.ld, tau.p, nn,
                 Z, ldz);
