@@ -16,6 +16,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <vector>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -29,6 +31,17 @@ namespace npcg {
 namespace {
 
 constexpr int TRI_THREADS = 256;
+
+// Fast reciprocal (MUFU seed + Newton steps in the FP64 pipe, about 1 ulp): the
+// Sturm counts and inverse iteration only need it to a few ulps, and an IEEE
+// division on their sequential recurrences costs several times more.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);  // one more Newton step: the approximation alone is not full precision
+  return fma(r, e, r);
+}
+
 
 // One grid-wide barrier per column: the rank-2 update of step k-1 is kept
 // pending (vp, wp) and applied on the fly -- redundantly by every CTA to
@@ -134,8 +147,38 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_kernel(double* M, i64 ld,
 // shared memory: CTA r of C owns columns c = r (mod C) whole (n <= ~620 at
 // C = 16). Column k and the matvec results p are read across the cluster
 // through DSMEM; one cluster barrier per column, no global-memory traffic.
+// One owned column of the fused pass: a_i -= vp[i+1] wc + wp[i+1] vc (written
+// back) and the lane's partial of sum_i a_i v_i, rows i = lane + 32 m < L.
+// restrict + loads grouped ahead of the stores let consecutive rows overlap.
+__device__ __forceinline__ double tri_lane_pass(double* __restrict__ col, const double* __restrict__ vp,
+                                                const double* __restrict__ wp, const double* __restrict__ v,
+                                                double vc, double wc, int L, int lane, bool pend) {
+  double acc = 0.0;
+  int i = lane;
+  if (pend) {
+    for (; i + 96 < L; i += 128) {
+      double a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = col[i + 32 * u] - (vp[i + 32 * u + 1] * wc + wp[i + 32 * u + 1] * vc);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) col[i + 32 * u] = a[u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += a[u] * v[i + 32 * u];
+    }
+    for (; i < L; i += 32) {
+      const double a = col[i] - (vp[i + 1] * wc + wp[i + 1] * vc);
+      col[i] = a;
+      acc += a * v[i];
+    }
+  } else {
+    for (; i < L; i += 32) acc += col[i] * v[i];
+  }
+  return acc;
+}
+
 __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const double* M, i64 ld, int n, double* d,
-                                                                       double* e, double* tau, double* H, i64 ldh) {
+                                                                       double* e, double* tau, double* H, i64 ldh,
+                                                                       unsigned long long* trace) {
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
   extern __shared__ double csm_t[];
@@ -146,8 +189,19 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
   double* wp = vp + n;
   double* pt = wp + n;
   double* pl = pt + n;             // [2][ncl] matvec results of the owned columns
-  __shared__ double red[32];
+  __shared__ double redA[TRI_THREADS / 32], redB[TRI_THREADS / 32];
+  __shared__ double alpha_sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // one-barrier block sum (fixed order, identical in every thread); buf is not reused before a later barrier
+  auto bsum1 = [&](double x, double* buf) {
+    x = warp_sum(x);
+    if (lane == 0) buf[warp] = x;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < TRI_THREADS / 32; ++w) t += buf[w];
+    return t;
+  };
   for (int lc = 0; lc < ncl; ++lc) {
     const int c = lc * C + rank;
     if (c >= n) break;
@@ -155,7 +209,15 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
   }
   cl.sync();
   bool pend = false;
+  auto tick = [&](int k, int ph) {
+    if (trace && rank == 0 && tid == 0 && k < 64) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      trace[k * 6 + ph] = t;
+    }
+  };
   for (int k = 0; k < n - 2; ++k) {
+    tick(k, 0);
     const int L = n - k - 1;
     const double* ck = cl.map_shared_rank(cols + static_cast<i64>(k / C) * n, k % C);
     double s = 0.0;
@@ -164,16 +226,17 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
       if (pend) x -= vp[j + 1] * wp[0] + wp[j + 1] * vp[0];
       v[j] = x;
       if (j > 0) s += x * x;
+      else alpha_sh = x;
     }
-    s = block_sum(s, red);
-    const double alpha = v[0];
+    s = bsum1(s, redA);  // (its barrier also publishes v and alpha)
+    tick(k, 1);
+    const double alpha = alpha_sh;
     double t = 0.0, beta = alpha, scal = 0.0;
     if (s > 0.0) {
       beta = -copysign(sqrt(alpha * alpha + s), alpha);
-      t = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
+      t = (beta - alpha) * fast_rcp(beta);
+      scal = fast_rcp(alpha - beta);
     }
-    __syncthreads();
     for (int j = tid; j < L; j += blockDim.x) v[j] = j == 0 ? 1.0 : v[j] * scal;
     if (rank == 0 && tid == 0) {
       d[k] = pend ? ck[k] - (vp[0] * wp[0] + wp[0] * vp[0]) : ck[k];
@@ -183,27 +246,52 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
     __syncthreads();
     if (rank == 0)
       for (int i = tid; i < L; i += blockDim.x) H[(k + 1 + i) + static_cast<i64>(k) * ldh] = v[i];
+    tick(k, 2);
     double* pk = pl + (k & 1) * ncl;
-    for (int lc = warp; lc < ncl; lc += nw) {
-      const int c = lc * C + rank;
-      if (c <= k || c >= n) continue;
-      const int ci = c - (k + 1);
-      double* col = cols + static_cast<i64>(lc) * n + (k + 1);
-      const double vc = pend ? vp[ci + 1] : 0.0, wc = pend ? wp[ci + 1] : 0.0;
-      double acc = 0.0;
-      if (pend) {
-        for (int i = lane; i < L; i += 32) {
-          const double a = col[i] - (vp[i + 1] * wc + wp[i + 1] * vc);
-          col[i] = a;
-          acc += a * v[i];
-        }
-      } else {
-        for (int i = lane; i < L; i += 32) acc += col[i] * v[i];
+    {
+      // this warp's owned trailing columns (lc = warp + nw q), processed together:
+      // vp/wp/v are read once per row and the column chains interleave
+      constexpr int QMAX = 4;
+      double* colq[QMAX];
+      double vcq[QMAX], wcq[QMAX], accq[QMAX];
+      int nq = 0;
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        const int lc = warp + nw * q;
+        const int c = lc * C + rank;
+        const bool live = lc < ncl && c > k && c < n;
+        const int ci = c - (k + 1);
+        colq[q] = live ? cols + static_cast<i64>(lc) * n + (k + 1) : nullptr;
+        vcq[q] = live && pend ? vp[ci + 1] : 0.0;
+        wcq[q] = live && pend ? wp[ci + 1] : 0.0;
+        accq[q] = 0.0;
+        nq += live;
       }
-      acc = warp_sum(acc);
-      if (lane == 0) pk[lc] = t * acc;
+      if (nq > 0) {
+        for (int i = lane; i < L; i += 32) {
+          const double vpi = pend ? vp[i + 1] : 0.0, wpi = pend ? wp[i + 1] : 0.0, vi = v[i];
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q) {
+            if (colq[q]) {
+              const double a = colq[q][i] - (vpi * wcq[q] + wpi * vcq[q]);
+              if (pend) colq[q][i] = a;
+              accq[q] += a * vi;
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q) accq[q] += __shfl_xor_sync(0xffffffffu, accq[q], o);
+        if (lane == 0)
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q)
+            if (colq[q]) pk[warp + nw * q] = t * accq[q];
+      }
     }
+    tick(k, 3);
     cl.sync();
+    tick(k, 4);
     double pv = 0.0;
     for (int i = tid; i < L; i += blockDim.x) {
       const int c = k + 1 + i;
@@ -211,7 +299,8 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
       pt[i] = pi;
       pv += pi * v[i];
     }
-    pv = block_sum(pv, red);
+    pv = bsum1(pv, redB);
+    tick(k, 5);
     const double K = 0.5 * t * pv;
     for (int i = tid; i < L; i += blockDim.x) {
       double w = pt[i];
@@ -235,16 +324,6 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
     }
   }
   cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
-}
-
-// Fast reciprocal (MUFU seed + Newton steps in the FP64 pipe, about 1 ulp): the
-// Sturm counts and inverse iteration only need it to a few ulps, and an IEEE
-// division on their sequential recurrences costs several times more.
-__device__ __forceinline__ double fast_rcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double e = fma(-x, r, 1.0);  // one more Newton step: the approximation alone is not full precision
-  return fma(r, e, r);
 }
 
 // number of eigenvalues of T strictly below x (Sturm sequence of LDL^T)
@@ -662,7 +741,7 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
     for (int C : {16, 8}) {  // cluster-resident variant when the matrix fits in C CTAs' shared memory
       const i64 ncl = cdiv(n, C);
       const i64 smem = (ncl * n + 4 * n + 2 * ncl) * 8;
-      if (smem > 220 * 1024) continue;
+      if (smem > 220 * 1024 || ncl > (TRI_THREADS / 32) * 4) continue;  // <= 4 owned columns per warp
       NPCG_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
       NPCG_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -684,8 +763,24 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
         continue;
       }
       ctx.prof_begin("tridiag_cluster_kernel");
+      static const bool tracing = std::getenv("NPCG_TRI_TRACE") != nullptr;  // diagnostics
+      DBuf<unsigned long long> tr;
+      if (tracing) {
+        tr.alloc(64 * 6, ctx.stream);
+        tr.zero();
+      }
       NPCG_CUDA(cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, static_cast<const double*>(M), ldm, nn, d.p, e.p,
-                                   tau.p, H.p(), H.ld));
+                                   tau.p, H.p(), H.ld, tracing ? tr.p : static_cast<unsigned long long*>(nullptr)));
+      if (tracing) {
+        ctx.sync();
+        std::vector<unsigned long long> h(64 * 6);
+        NPCG_CUDA(cudaMemcpy(h.data(), tr.p, 8 * h.size(), cudaMemcpyDeviceToHost));
+        for (int k = 1; k < 40 && k + 1 < n - 2; k += 8)
+          std::fprintf(stderr, "[tri n=%d] k=%d colred %.2f scal+fused? %.2f fused %.2f csync %.2f gather %.2f tail %.2f us\n",
+                       nn, k, (h[k * 6 + 1] - h[k * 6]) * 1e-3, (h[k * 6 + 2] - h[k * 6 + 1]) * 1e-3,
+                       (h[k * 6 + 3] - h[k * 6 + 2]) * 1e-3, (h[k * 6 + 4] - h[k * 6 + 3]) * 1e-3,
+                       (h[k * 6 + 5] - h[k * 6 + 4]) * 1e-3, (h[(k + 1) * 6] - h[k * 6 + 5]) * 1e-3);
+      }
       ctx.check_launch("tridiag_cluster_kernel");
       ctx.prof_end();
       done_tri = true;
