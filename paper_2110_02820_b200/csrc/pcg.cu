@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   __shared__ double sh[32];
   __shared__ double red[2][PT / 32], red2[2][PT / 32];
   __shared__ double zred[PT / 32][32];
+  __shared__ double wred[4 * S * (PT / 32)];  // P4: per-warp partials of up to 4 x S dots
   __shared__ ColState cs[S];
   __shared__ int running_sh;
   __shared__ uint64_t full_bar[NST];
@@ -574,16 +575,46 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
       if (running_sh == 0) break;
       if (!nys) continue;
       {
+        // this CTA's columns of U, up to UQ at a time: r is read once per row for all of them
+        // and the UQ x S dots are reduced together (one barrier)
+        constexpr int UQ = 4;
         const i64 u0 = min(a.ell, static_cast<i64>(c) * a.uslice), u1 = min(a.ell, u0 + a.uslice);
-        for (i64 j = u0; j < u1; ++j) {
-          const double* uc = a.U + j * a.ldu;
+        for (i64 j0 = u0; j0 < u1; j0 += UQ) {
+          double w[UQ][S];
 #pragma unroll
-          for (int s = 0; s < S; ++s) {
-            double w = 0.0;
-            for (i64 i = tid; i < n; i += PT) w += uc[i] * a.R[i + s * a.ldw];
-            w = block_sum(w, sh);
-            if (tid == 0) a.T[j + s * a.ell] = w * a.gain[j];
+          for (int q = 0; q < UQ; ++q)
+#pragma unroll
+            for (int s = 0; s < S; ++s) w[q][s] = 0.0;
+          for (i64 i = tid; i < n; i += PT) {
+            double ri[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) ri[s] = a.R[i + s * a.ldw];
+#pragma unroll
+            for (int q = 0; q < UQ; ++q) {
+              if (j0 + q < u1) {
+                const double uiq = a.U[i + (j0 + q) * a.ldu];
+#pragma unroll
+                for (int s = 0; s < S; ++s) w[q][s] += uiq * ri[s];
+              }
+            }
           }
+#pragma unroll
+          for (int q = 0; q < UQ; ++q)
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              const double tot = warp_sum(w[q][s]);
+              if (lane == 0) wred[(q * S + s) * (PT / 32) + warp] = tot;
+            }
+          __syncthreads();
+          if (tid < UQ * S) {
+            const int q = tid / S, s = tid % S;
+            if (j0 + q < u1) {
+              double tot = 0.0;
+              for (int ww = 0; ww < PT / 32; ++ww) tot += wred[tid * (PT / 32) + ww];  // fixed order
+              a.T[(j0 + q) + s * a.ell] = tot * a.gain[j0 + q];
+            }
+          }
+          __syncthreads();
         }
       }
       grid.sync();
