@@ -148,8 +148,9 @@ void free_apply_s(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, do
 // shared memory, K = d), the kernel epilogue (norms, clamp, exp, unit
 // diagonal) is applied to the accumulators in registers and multiplied into
 // the row sums with V -- K never touches HBM. Tiles are double-buffered with
-// cp.async. 8 warps, each a 64 x 32 slice of the tile.
-constexpr int KF_B = 128, KF_THREADS = 256;
+// cp.async. 8 warps per CTA, each a 32 x 32 slice of a 128 x 64 tile, two
+// CTAs per SM, so one CTA's DMMA phase overlaps the other's exp epilogue.
+constexpr int KF_BM = 128, KF_BN = 64, KF_WN = KF_BN / 32, KF_THREADS = 32 * (KF_BM / 32) * KF_WN;  // 8 warps, 32 x 32 tiles
 
 __device__ __forceinline__ void kf_dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -164,96 +165,131 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// Branch-free exp for x <= 0 (the kernel exponent c * max(s, 0), c < 0):
+// Cody-Waite reduction x = k ln2 + r, |r| <= ln2/2, degree-12 Taylor
+// polynomial, 2^k applied as two exact power-of-two factors (so k down to the
+// subnormal range is exact). About 1 ulp like CUDA's exp(), but without its
+// slow-path branch, so a warp's 16 to 32 exps per tile interleave freely.
+__device__ __forceinline__ double exp_nonpos(double x) {
+  x = fmax(x, -745.2);  // exp(-745.2) rounds to 0
+  const double kd = rint(x * 1.4426950408889634);
+  double r = fma(kd, -6.93147180369123816490e-01, x);
+  r = fma(kd, -1.90821492927058770002e-10, r);
+  double p = 1.0 / 479001600.0;  // 1/12!
+  p = fma(p, r, 1.0 / 39916800.0);
+  p = fma(p, r, 1.0 / 3628800.0);
+  p = fma(p, r, 1.0 / 362880.0);
+  p = fma(p, r, 1.0 / 40320.0);
+  p = fma(p, r, 1.0 / 5040.0);
+  p = fma(p, r, 1.0 / 720.0);
+  p = fma(p, r, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = static_cast<int>(kd);
+  const int k1 = k / 2, k2 = k - k1;  // each in [-538, 0]: normal powers of two
+  const double s1 = __longlong_as_double(static_cast<long long>(k1 + 1023) << 52);
+  const double s2 = __longlong_as_double(static_cast<long long>(k2 + 1023) << 52);
+  return p * s1 * s2;
+}
+
 template <int S>
-__global__ void __launch_bounds__(KF_THREADS, 1)
+__global__ void __launch_bounds__(KF_THREADS, 2)
     kfree_fused_kernel(const double* __restrict__ pts, i64 ldp, i64 n, int d, int dp,
                        const double* __restrict__ norms, double c, const double* __restrict__ V, i64 ldv,
-                       double* __restrict__ out, i64 ldo, const int* __restrict__ gate) {
+                       double* __restrict__ out, i64 ldo, i64 tiles_per_split, double* __restrict__ partial,
+                       const int* __restrict__ gate) {
   if (gate && *gate == 0) return;
   extern __shared__ double kfs[];
   const int lds = dp + 1;  // odd stride: the fragment reads hit distinct banks
   double* XI = kfs;                                   // [128][lds]
-  double* XJ = XI + KF_B * lds;                       // [2][128][lds]
-  double* NJ = XJ + 2 * KF_B * lds;                   // [2][128]
-  double* VJ = NJ + 2 * KF_B;                         // [2][S][128]
-  double* RED = VJ + 2 * S * KF_B;                    // [4][128][S]
+  double* XJ = XI + KF_BM * lds;                      // [2][KF_BN][lds]
+  double* NJ = XJ + 2 * KF_BN * lds;                  // [2][KF_BN]
+  double* VJ = NJ + 2 * KF_BN;                        // [2][S][KF_BN]
+  double* RED = VJ + 2 * S * KF_BN;                   // [KF_WN][KF_BM][S]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3, wm = warp >> 2, wn = warp & 3;
-  const i64 i0 = static_cast<i64>(blockIdx.x) * KF_B;
+  const int g = lane >> 2, t = lane & 3, wm = warp / KF_WN, wn = warp % KF_WN;  // 4 x KF_WN warps
+  const i64 i0 = static_cast<i64>(blockIdx.x) * KF_BM;
 
   auto load_tile = [&](i64 j0, int buf) {
-    double* xj = XJ + buf * KF_B * lds;
-    for (int idx = tid; idx < KF_B * dp; idx += KF_THREADS) {
-      const int r = idx % KF_B, k = idx / KF_B;
+    double* xj = XJ + buf * KF_BN * lds;
+    for (int idx = tid; idx < KF_BN * dp; idx += KF_THREADS) {
+      const int r = idx % KF_BN, k = idx / KF_BN;
       const bool ok = j0 + r < n && k < d;
       cp_async8(xj + r * lds + k, ok ? pts + (j0 + r) + static_cast<i64>(k) * ldp : pts, ok);
     }
-    for (int r = tid; r < KF_B; r += KF_THREADS) {
+    for (int r = tid; r < KF_BN; r += KF_THREADS) {
       const bool ok = j0 + r < n;
-      cp_async8(NJ + buf * KF_B + r, ok ? norms + j0 + r : norms, ok);
+      cp_async8(NJ + buf * KF_BN + r, ok ? norms + j0 + r : norms, ok);
 #pragma unroll
-      for (int s = 0; s < S; ++s) cp_async8(VJ + (buf * S + s) * KF_B + r, ok ? V + (j0 + r) + s * ldv : V, ok);
+      for (int s = 0; s < S; ++s) cp_async8(VJ + (buf * S + s) * KF_BN + r, ok ? V + (j0 + r) + s * ldv : V, ok);
     }
     cp_async_commit();
   };
 
-  for (int idx = tid; idx < KF_B * dp; idx += KF_THREADS) {
-    const int r = idx % KF_B, k = idx / KF_B;
+  for (int idx = tid; idx < KF_BM * dp; idx += KF_THREADS) {
+    const int r = idx % KF_BM, k = idx / KF_BM;
     XI[r * lds + k] = (i0 + r < n && k < d) ? pts[(i0 + r) + static_cast<i64>(k) * ldp] : 0.0;
   }
-  double ni[8];
+  double ni[4];
 #pragma unroll
-  for (int f = 0; f < 8; ++f) {
-    const i64 i = i0 + wm * 64 + f * 8 + g;
+  for (int f = 0; f < 4; ++f) {
+    const i64 i = i0 + wm * 32 + f * 8 + g;
     ni[f] = i < n ? norms[i] : 0.0;
   }
-  double racc[8][S];
+  double racc[4][S];
 #pragma unroll
-  for (int f = 0; f < 8; ++f)
+  for (int f = 0; f < 4; ++f)
 #pragma unroll
     for (int s = 0; s < S; ++s) racc[f][s] = 0.0;
 
-  load_tile(0, 0);
-  const i64 ntiles = (n + KF_B - 1) / KF_B;
-  for (i64 jt = 0; jt < ntiles; ++jt) {
-    const int buf = static_cast<int>(jt & 1);
+  // this CTA's column tiles [jt0, jt1) (blockIdx.y splits the columns so the
+  // grid fills whole waves; partial row sums are reduced in fixed order after)
+  const i64 ntiles_all = (n + KF_BN - 1) / KF_BN;
+  const i64 jt0 = static_cast<i64>(blockIdx.y) * tiles_per_split, jt1 = min(ntiles_all, jt0 + tiles_per_split);
+  if (jt0 < jt1) load_tile(jt0 * KF_BN, 0);
+  for (i64 jt = jt0; jt < jt1; ++jt) {
+    const int buf = static_cast<int>((jt - jt0) & 1);
     cp_async_wait_all();
     __syncthreads();  // tile jt resident; everyone is done with the other buffer
-    if (jt + 1 < ntiles) load_tile((jt + 1) * KF_B, buf ^ 1);
-    const double* xj = XJ + buf * KF_B * lds;
-    double acc[8][4][2];
+    if (jt + 1 < jt1) load_tile((jt + 1) * KF_BN, buf ^ 1);
+    const double* xj = XJ + buf * KF_BN * lds;
+    double acc[4][4][2];
 #pragma unroll
-    for (int f = 0; f < 8; ++f)
+    for (int f = 0; f < 4; ++f)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[f][q][0] = acc[f][q][1] = 0.0;
     for (int kk = 0; kk < dp; kk += 4) {
-      double a[8], b[4];
+      double a[4], b[4];
 #pragma unroll
-      for (int f = 0; f < 8; ++f) a[f] = XI[(wm * 64 + f * 8 + g) * lds + kk + t];
+      for (int f = 0; f < 4; ++f) a[f] = XI[(wm * 32 + f * 8 + g) * lds + kk + t];
 #pragma unroll
       for (int q = 0; q < 4; ++q) b[q] = xj[(wn * 32 + q * 8 + g) * lds + kk + t];
 #pragma unroll
-      for (int f = 0; f < 8; ++f)
+      for (int f = 0; f < 4; ++f)
 #pragma unroll
         for (int q = 0; q < 4; ++q) kf_dmma(acc[f][q][0], acc[f][q][1], a[f], b[q]);
     }
     // epilogue: K entries (operators.cpp:125-137 rounding order) times V into the row sums
-    const i64 j0 = jt * KF_B;
+    const i64 j0 = jt * KF_BN;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = wn * 32 + q * 8 + 2 * t + e;
-        const double nj = NJ[buf * KF_B + col];
+        const double nj = NJ[buf * KF_BN + col];
         double vj[S];
 #pragma unroll
-        for (int s = 0; s < S; ++s) vj[s] = VJ[(buf * S + s) * KF_B + col];
+        for (int s = 0; s < S; ++s) vj[s] = VJ[(buf * S + s) * KF_BN + col];
 #pragma unroll
-        for (int f = 0; f < 8; ++f) {
+        for (int f = 0; f < 4; ++f) {
           double sq = -2.0 * acc[f][q][e] + ni[f];
           sq = sq + nj;
-          const bool diag = i0 + wm * 64 + f * 8 + g == j0 + col;
-          const double kij = diag ? 1.0 : exp(fmax(sq, 0.0) * c);
+          const bool diag = i0 + wm * 32 + f * 8 + g == j0 + col;
+          const double ex = exp_nonpos(fmax(sq, 0.0) * c);  // unconditional: no per-element branch
+          const double kij = diag ? 1.0 : ex;
 #pragma unroll
           for (int s = 0; s < S; ++s) racc[f][s] += kij * vj[s];
         }
@@ -261,40 +297,72 @@ __global__ void __launch_bounds__(KF_THREADS, 1)
   }
   // row sums: over the 4 lanes of a row group, then over the 4 column warps (fixed order)
 #pragma unroll
-  for (int f = 0; f < 8; ++f)
+  for (int f = 0; f < 4; ++f)
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       double v = racc[f][s];
       v += __shfl_xor_sync(0xffffffffu, v, 1);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
-      if (t == 0) RED[(wn * KF_B + wm * 64 + f * 8 + g) * S + s] = v;
+      if (t == 0) RED[(wn * KF_BM + wm * 32 + f * 8 + g) * S + s] = v;
     }
   __syncthreads();
-  for (int idx = tid; idx < KF_B * S; idx += KF_THREADS) {
+  for (int idx = tid; idx < KF_BM * S; idx += KF_THREADS) {
     const int r = idx / S, s = idx % S;
     const i64 i = i0 + r;
     if (i < n) {
-      double v = RED[(0 * KF_B + r) * S + s];
-      v += RED[(1 * KF_B + r) * S + s];
-      v += RED[(2 * KF_B + r) * S + s];
-      v += RED[(3 * KF_B + r) * S + s];
-      out[i + s * ldo] = v;
+      double v = RED[(0 * KF_BM + r) * S + s];
+#pragma unroll
+      for (int w = 1; w < KF_WN; ++w) v += RED[(w * KF_BM + r) * S + s];
+      if (partial) partial[(static_cast<i64>(blockIdx.y) * S + s) * n + i] = v;
+      else out[i + s * ldo] = v;
     }
   }
+}
+
+__global__ void kfree_reduce_kernel(const double* __restrict__ partial, int splits, i64 n, int S,
+                                    double* __restrict__ out, i64 ldo, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
+  const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= n * S) return;
+  const i64 i = idx % n, s = idx / n;
+  double v = 0.0;
+  for (int b = 0; b < splits; ++b) v += partial[(static_cast<i64>(b) * S + s) * n + i];  // fixed order
+  out[i + s * ldo] = v;
 }
 
 template <int S>
 void kfree_fused(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, double* out, i64 ldo, const int* gate) {
   const int d = static_cast<int>(op.d), dp = (d + 3) / 4 * 4;
-  const i64 smem = (3 * KF_B * static_cast<i64>(dp + 1) + 2 * KF_B + 2 * S * KF_B + 4 * KF_B * S) * 8;
+  const i64 smem = ((KF_BM + 2 * KF_BN) * static_cast<i64>(dp + 1) + 2 * KF_BN + 2 * S * KF_BN + KF_WN * KF_BM * S) * 8;
   static bool attr = false;
   if (!attr) {
     NPCG_CUDA(cudaFuncSetAttribute(kfree_fused_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
   const double c = -1.0 / (2.0 * op.sigma * op.sigma);
-  NPCG_LAUNCH(ctx, kfree_fused_kernel<S>, static_cast<unsigned>(cdiv(op.n, KF_B)), KF_THREADS,
-              static_cast<int>(smem), op.pts.p(), op.pts.ld, op.n, d, dp, op.norms.p, c, V, ldv, out, ldo, gate);
+  // split the column tiles so that row blocks x splits fills whole waves (one CTA per SM)
+  const i64 rb = cdiv(op.n, KF_BM), nt = cdiv(op.n, KF_BN);
+  int best = 1;
+  double best_eff = 0.0;
+  for (int sp = 1; sp <= 16 && sp <= nt; ++sp) {
+    const i64 units = rb * sp;
+    const i64 slots = 2 * ctx.sm_count;  // two CTAs per SM
+    const double eff = static_cast<double>(units) / (cdiv(units, slots) * slots);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best = sp;
+    }
+  }
+  const i64 tps = cdiv(nt, best);
+  const int splits = static_cast<int>(cdiv(nt, tps));
+  DBuf<double> part;
+  if (splits > 1) part.alloc(static_cast<i64>(splits) * S * op.n, ctx.stream);
+  NPCG_LAUNCH(ctx, kfree_fused_kernel<S>, dim3(static_cast<unsigned>(rb), static_cast<unsigned>(splits)), KF_THREADS,
+              static_cast<int>(smem), op.pts.p(), op.pts.ld, op.n, d, dp, op.norms.p, c, V, ldv, out, ldo, tps,
+              splits > 1 ? part.p : static_cast<double*>(nullptr), gate);
+  if (splits > 1)
+    NPCG_LAUNCH(ctx, kfree_reduce_kernel, static_cast<unsigned>(cdiv(op.n * S, 256)), 256, 0, part.p, splits, op.n,
+                S, out, ldo, gate);
   ctx.prof_work(static_cast<double>(op.n) * op.n * (2.0 * dp + 2.0 * S), 8.0 * op.n * (d + 2 * S));
 }
 
