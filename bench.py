@@ -9,7 +9,9 @@ factorisation (shift, Cholesky, TRSM, thin SVD), preconditioner, PCG to 1e-10.
   value     solves/s with inputs (X, b, Omega) resident in HBM, device-timed
             with CUDA events on the library's stream, max over ranks
   e2e       solves/s through the public C-ABI with host buffers: X, Omega, b
-            copied host->device and x device->host inside every step
+            copied host->device and x device->host inside every step (the
+            ridge design through the streamed constructor: its row blocks
+            cross PCIe while the sketch already runs on the landed ones)
   roofline  the dominant kernel of the step (per-kernel CUDA-event timing in
             an instrumented step of the same run) against its roofline
   cpu_baseline  the CPU oracle (restatement of the reference) on this host
@@ -215,7 +217,7 @@ class DevicePath:
 
 def e2e_step(npcg, w, ctx, host, exchange=None):
     """Public API with host buffers: every input crosses PCIe inside the step."""
-    op = npcg.workloads.build_operator(npcg, host, ctx=ctx, exchange=exchange)
+    op = npcg.workloads.build_operator(npcg, host, ctx=ctx, exchange=exchange, streamed=True)
     if w.adaptive:
         a = w.adaptive
         rng = npcg.Rng(int(w.name[3]))

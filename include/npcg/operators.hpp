@@ -7,6 +7,8 @@
 #pragma once
 
 #include <memory>
+#include <stdexcept>
+#include <utility>
 
 #include "random.hpp"
 #include "types.hpp"
@@ -108,6 +110,30 @@ class GramRidgeOperator final : public DeviceOperator {
     return h;
   }
   Index rows_;
+};
+
+namespace detail {
+struct HostDesign {
+  Matrix design;
+};
+}  // namespace detail
+
+/// GramRidgeOperator that owns its design (taken by value, as the reference's
+/// constructor does) and streams it to the device: the upload overlaps the
+/// first product (npcg_op_gram_create_streamed). A non-finite design raises
+/// std::invalid_argument from that first product instead of the constructor.
+class StreamedGramRidgeOperator final : private detail::HostDesign, public DeviceOperator {
+ public:
+  explicit StreamedGramRidgeOperator(Matrix g) : detail::HostDesign{std::move(g)}, DeviceOperator(make(design)) {}
+  Index n_rows() const { return design.rows(); }
+
+ private:
+  static npcg_op* make(const Matrix& g) {
+    if (g.rows() < 1 || g.cols() < 1) throw std::invalid_argument("GramRidgeOperator: design matrix must be nonempty");
+    npcg_op* h = nullptr;
+    check_status(npcg_op_gram_create_streamed(default_context(), g.rows(), g.cols(), g.data(), g.rows(), &h));
+    return h;
+  }
 };
 
 /// KernelOperator(points, sigma, dense_cap) (operators.cpp:141-188).

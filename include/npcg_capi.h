@@ -92,6 +92,15 @@ int npcg_op_dense_create(npcg_ctx* ctx, int64_t rows, int64_t cols, const double
 /* GramRidgeOperator(Matrix design) = (1/m) G^T G, operators.cpp:105-121. */
 int npcg_op_gram_create(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, int64_t ldg,
                         int where, npcg_op** out);
+/* GramRidgeOperator(Matrix design) with a streamed upload (host buffer only).
+ * Replaces the same constructor (operators.cpp:105-110) for large designs:
+ * returns once the copy is enqueued, in ~80 MB row blocks on a side stream,
+ * and the first product (the sketch) starts on each block as it lands.
+ * Contract: `g` must stay valid and unchanged until the first call that
+ * applies the operator returns (or npcg_op_destroy); that call raises the
+ * constructor's non-finite error (NPCG_EINVAL, same message) in its place. */
+int npcg_op_gram_create_streamed(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, int64_t ldg,
+                                 npcg_op** out);
 /* KernelOperator(points n x d, sigma, dense_cap), operators.cpp:141-150:
  * stored (built on device) when n <= dense_cap, otherwise matrix-free. */
 int npcg_op_kernel_create(npcg_ctx* ctx, int64_t n, int64_t d, const double* pts, int64_t ldp,

@@ -361,11 +361,21 @@ def DenseOperator(a, ctx: Context | None = None) -> LinearOperator:
                    _i64(max(a.shape[0], 1)), HOST)
 
 
-def GramRidgeOperator(g, ctx: Context | None = None) -> LinearOperator:
+def GramRidgeOperator(g, ctx: Context | None = None, streamed: bool = False) -> LinearOperator:
+    """operators.cpp:105-121. `streamed=True` (npcg_op_gram_create_streamed):
+    the upload of X overlaps the first product (the sketch); the non-finite
+    check then raises from that first product instead of the constructor.
+    The operator keeps a reference to the host array, which must not be
+    modified until then."""
     ctx = ctx or default_context()
     g = _f64(g)
     if g.ndim != 2:
         raise InvalidArgument("GramRidgeOperator: design matrix must be nonempty")
+    if streamed:
+        op = _new_op(ctx, lib().npcg_op_gram_create_streamed, _vp(ctx.h), _i64(g.shape[0]), _i64(g.shape[1]),
+                     _ptr(g), _i64(max(g.shape[0], 1)))
+        op._host_ref = g
+        return op
     return _new_op(ctx, lib().npcg_op_gram_create, _vp(ctx.h), _i64(g.shape[0]), _i64(g.shape[1]), _ptr(g),
                    _i64(max(g.shape[0], 1)), HOST)
 

@@ -341,9 +341,14 @@ void copy2d(Ctx& ctx, i64 rows, i64 cols, const double* src, i64 lds, double* ds
 }
 
 void upload(Ctx& ctx, DMat& dst, i64 rows, i64 cols, const double* src, i64 lds, int where) {
-  dst.alloc(rows, cols, ctx.stream, true);
-  if (rows <= 0 || cols <= 0) return;
+  if (rows <= 0 || cols <= 0) {
+    dst.alloc(rows, cols, ctx.stream, true);
+    return;
+  }
   if (lds < rows) invalid("leading dimension smaller than the row count");
+  dst.alloc(rows, cols, ctx.stream, false);
+  if (dst.ld > rows)  // only the column pads need zeroing; the copy fills the rest
+    NPCG_CUDA(cudaMemset2DAsync(dst.p() + rows, dst.ld * 8, 0, (dst.ld - rows) * 8, cols, ctx.stream));
   NPCG_CUDA(cudaMemcpy2DAsync(dst.p(), dst.ld * 8, src, lds * 8, rows * 8, cols,
                               where == NPCG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx.stream));
 }
@@ -442,14 +447,17 @@ __global__ void scale_pow2_kernel(i64 rows, i64 cols, double* a, i64 ld, int e) 
 
 namespace {
 __global__ void transpose_tile_kernel(const double* __restrict__ src, i64 lds, i64 rows, i64 cols,
-                                      double* __restrict__ dst, i64 ldd) {
+                                      double* __restrict__ dst, i64 ldd, int* bad) {
   __shared__ double tile[32][33];
   const i64 r0 = static_cast<i64>(blockIdx.x) * 32, c0 = static_cast<i64>(blockIdx.y) * 32;
+  int nonfinite = 0;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const i64 r = r0 + threadIdx.x, c = c0 + k;
-    tile[k][threadIdx.x] = (r < rows && c < cols) ? src[r + c * lds] : 0.0;
+    const double x = (r < rows && c < cols) ? src[r + c * lds] : 0.0;
+    nonfinite |= !isfinite(x);
+    tile[k][threadIdx.x] = x;
   }
-  __syncthreads();
+  if (__syncthreads_or(nonfinite) && bad && threadIdx.x == 0 && threadIdx.y == 0) atomicOr(bad, 1);
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const i64 c = c0 + threadIdx.x, r = r0 + k;  // dst(c, r) = src(r, c)
     if (r < rows && c < cols) dst[c + r * ldd] = tile[threadIdx.x][k];
@@ -460,7 +468,15 @@ __global__ void transpose_tile_kernel(const double* __restrict__ src, i64 lds, i
 void transpose(Ctx& ctx, const double* src, i64 lds, i64 rows, i64 cols, double* dst, i64 ldd) {
   if (rows <= 0 || cols <= 0) return;
   NPCG_LAUNCH(ctx, transpose_tile_kernel, dim3(static_cast<unsigned>(cdiv(rows, 32)), static_cast<unsigned>(cdiv(cols, 32))),
-              dim3(32, 8), 0, src, lds, rows, cols, dst, ldd);
+              dim3(32, 8), 0, src, lds, rows, cols, dst, ldd, static_cast<int*>(nullptr));
+}
+
+void transpose_checked(Ctx& ctx, cudaStream_t s, const double* src, i64 lds, i64 rows, i64 cols, double* dst,
+                       i64 ldd, int* bad) {
+  if (rows <= 0 || cols <= 0) return;
+  transpose_tile_kernel<<<dim3(static_cast<unsigned>(cdiv(rows, 32)), static_cast<unsigned>(cdiv(cols, 32))),
+                          dim3(32, 8), 0, s>>>(src, lds, rows, cols, dst, ldd, bad);
+  ctx.check_launch("transpose_tile_kernel");
 }
 
 double max_abs(Ctx& ctx, const double* a, i64 rows, i64 cols, i64 ld) {

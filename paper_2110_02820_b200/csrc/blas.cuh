@@ -33,6 +33,9 @@ void symmetrize(Ctx& ctx, const double* a, i64 n, i64 lda, double* out, i64 ldo)
 void scale_cols(Ctx& ctx, double* a, i64 rows, i64 cols, i64 lda, const double* d);
 /// dst (cols x rows) = src^T (src rows x cols).
 void transpose(Ctx& ctx, const double* src, i64 lds, i64 rows, i64 cols, double* dst, i64 ldd);
+/// transpose() on stream `s`, OR-ing 1 into *bad (device) when src holds a non-finite entry.
+void transpose_checked(Ctx& ctx, cudaStream_t s, const double* src, i64 lds, i64 rows, i64 cols, double* dst,
+                       i64 ldd, int* bad);
 /// max |a_ij| of a block (synchronises).
 double max_abs(Ctx& ctx, const double* a, i64 rows, i64 cols, i64 ld);
 /// a *= 2^e exactly (ldexp).

@@ -128,8 +128,12 @@ Ctx::Ctx(int dev) : device(dev) {
   encode_tiled = reinterpret_cast<EncodeTiledFn>(fn);
 }
 Ctx::~Ctx() {
+  if (stream || aux) cudaSetDevice(device);
+  if (aux) {
+    cudaStreamSynchronize(aux);
+    cudaStreamDestroy(aux);
+  }
   if (stream) {
-    cudaSetDevice(device);
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
@@ -311,14 +315,24 @@ int npcg_op_gram_create(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, in
     op->m = m;
     op->div = static_cast<double>(m);
     op->kind = kGram;
-    {
-      DMat colmajor;  // caller layout, then the row-major copy the kernels stream
-      upload(c, colmajor, m, n, g, ldg, where);
-      if (!all_finite(c, colmajor.p(), m, n, colmajor.ld))
-        invalid("GramRidgeOperator: design matrix has non-finite entries");
-      op->xr.alloc(n, m, c.stream, true);
-      transpose(c, colmajor.p(), colmajor.ld, m, n, op->xr.p(), op->xr.ld);
-    }
+    gram_upload(c, *op, g, ldg, where);
+    *out = new npcg_op{ctx, std::move(op)};
+  });
+}
+
+int npcg_op_gram_create_streamed(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, int64_t ldg,
+                                 npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    if (m < 1 || n < 1) invalid("GramRidgeOperator: design matrix must be nonempty");  // operators.cpp:106-107
+    if (ldg < m) invalid("leading dimension smaller than the row count");
+    auto op = std::make_unique<GramOp>();
+    op->ctx = &c;
+    op->n = n;
+    op->m = m;
+    op->div = static_cast<double>(m);
+    op->kind = kGram;
+    gram_upload_streamed(c, *op, g, ldg);
     *out = new npcg_op{ctx, std::move(op)};
   });
 }
@@ -335,14 +349,7 @@ int npcg_op_gram_shard_create(npcg_ctx* ctx, int64_t m_local, int64_t n, const d
     local->m = m_local;
     local->div = static_cast<double>(m_total);
     local->kind = kGram;
-    {
-      DMat colmajor;
-      upload(c, colmajor, m_local, n, g, ldg, where);
-      if (!all_finite(c, colmajor.p(), m_local, n, colmajor.ld))
-        invalid("GramRidgeOperator: design matrix has non-finite entries");
-      local->xr.alloc(n, m_local, c.stream, true);
-      transpose(c, colmajor.p(), colmajor.ld, m_local, n, local->xr.p(), local->xr.ld);
-    }
+    gram_upload(c, *local, g, ldg, where);
     auto op = std::make_unique<ShardOp>();
     op->ctx = &c;
     op->n = n;

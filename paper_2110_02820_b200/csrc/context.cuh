@@ -34,6 +34,7 @@ struct Ctx {
   int sm_count = 148;
   int max_smem_optin = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;  // side stream for streamed host uploads (created on first use)
   std::atomic<int64_t> launches{0};
   EncodeTiledFn encode_tiled = nullptr;
   std::mutex mu;  // serialises public calls sharing this context
@@ -43,6 +44,10 @@ struct Ctx {
   explicit Ctx(int dev);
   ~Ctx();
   void sync() { NPCG_CUDA(cudaStreamSynchronize(stream)); }
+  cudaStream_t aux_stream() {
+    if (!aux) NPCG_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    return aux;
+  }
   void count(int k = 1) { launches.fetch_add(k, std::memory_order_relaxed); }
   void check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();

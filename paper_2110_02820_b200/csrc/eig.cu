@@ -221,12 +221,21 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
     const int L = n - k - 1;
     const double* ck = cl.map_shared_rank(cols + static_cast<i64>(k / C) * n, k % C);
     double s = 0.0;
-    for (int j = tid; j < L; j += blockDim.x) {
-      double x = ck[k + 1 + j];
-      if (pend) x -= vp[j + 1] * wp[0] + wp[j + 1] * vp[0];
-      v[j] = x;
-      if (j > 0) s += x * x;
-      else alpha_sh = x;
+    for (int j0 = tid; j0 < L; j0 += 2 * TRI_THREADS) {  // both remote loads in flight together
+      double xr[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) xr[u] = j0 + u * TRI_THREADS < L ? ck[k + 1 + j0 + u * TRI_THREADS] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = j0 + u * TRI_THREADS;
+        if (j < L) {
+          double x = xr[u];
+          if (pend) x -= vp[j + 1] * wp[0] + wp[j + 1] * vp[0];
+          v[j] = x;
+          if (j > 0) s += x * x;
+          else alpha_sh = x;
+        }
+      }
     }
     s = bsum1(s, redA);  // (its barrier also publishes v and alpha)
     tick(k, 1);
@@ -268,16 +277,49 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
         nq += live;
       }
       if (nq > 0) {
-        for (int i = lane; i < L; i += 32) {
-          const double vpi = pend ? vp[i + 1] : 0.0, wpi = pend ? wp[i + 1] : 0.0, vi = v[i];
+        // two rows per lane per step, every shared load issued before any store
+        // (the column stores could alias the loads as far as the compiler knows,
+        // which otherwise serialises load -> store -> load per column)
+        int i = lane;
+        for (; i + 32 < L; i += 64) {
+          double vpi[2], wpi[2], vi[2], a[2][QMAX];
 #pragma unroll
-          for (int q = 0; q < QMAX; ++q) {
-            if (colq[q]) {
-              const double a = colq[q][i] - (vpi * wcq[q] + wpi * vcq[q]);
-              if (pend) colq[q][i] = a;
-              accq[q] += a * vi;
-            }
+          for (int u = 0; u < 2; ++u) {
+            const int r = i + 32 * u;
+            vpi[u] = pend ? vp[r + 1] : 0.0;
+            wpi[u] = pend ? wp[r + 1] : 0.0;
+            vi[u] = v[r];
+#pragma unroll
+            for (int q = 0; q < QMAX; ++q) a[u][q] = colq[q] ? colq[q][r] : 0.0;
           }
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int q = 0; q < QMAX; ++q) a[u][q] -= vpi[u] * wcq[q] + wpi[u] * vcq[q];
+          if (pend)
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+              for (int q = 0; q < QMAX; ++q)
+                if (colq[q]) colq[q][i + 32 * u] = a[u][q];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int q = 0; q < QMAX; ++q) accq[q] += a[u][q] * vi[u];
+        }
+        if (i < L) {
+          const double vpi = pend ? vp[i + 1] : 0.0, wpi = pend ? wp[i + 1] : 0.0, vi = v[i];
+          double a[QMAX];
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q) a[q] = colq[q] ? colq[q][i] : 0.0;
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q) a[q] -= vpi * wcq[q] + wpi * vcq[q];
+          if (pend)
+#pragma unroll
+            for (int q = 0; q < QMAX; ++q)
+              if (colq[q]) colq[q][i] = a[q];
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q) accq[q] += a[q] * vi;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
@@ -293,11 +335,21 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
     cl.sync();
     tick(k, 4);
     double pv = 0.0;
-    for (int i = tid; i < L; i += blockDim.x) {
-      const int c = k + 1 + i;
-      const double pi = *cl.map_shared_rank(pk + c / C, c % C);
-      pt[i] = pi;
-      pv += pi * v[i];
+    for (int i0 = tid; i0 < L; i0 += 2 * TRI_THREADS) {  // both remote loads in flight together
+      double pr[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = k + 1 + i0 + u * TRI_THREADS;
+        pr[u] = i0 + u * TRI_THREADS < L ? *cl.map_shared_rank(pk + c / C, c % C) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = i0 + u * TRI_THREADS;
+        if (i < L) {
+          pt[i] = pr[u];
+          pv += pr[u] * v[i];
+        }
+      }
     }
     pv = bsum1(pv, redB);
     tick(k, 5);

@@ -9,6 +9,7 @@
 // sums the partials in fixed order and applies /m (+ mu v).
 // Algorithmic bytes: 8 m n per matvec (the reference's two GEMVs read X twice).
 #include <algorithm>
+#include <cstdlib>
 
 #include "blas.cuh"
 #include "gemm.cuh"
@@ -132,7 +133,94 @@ void gram_single_pass(Ctx& ctx, const GramOp& op, const double* V, i64 ldv, doub
 }  // namespace
 
 // GramRidgeOperator: out = X^T (X V) / m.
+void gram_upload(Ctx& c, GramOp& op, const double* g, i64 ldg, int where) {
+  const i64 m = op.m, n = op.n;
+  DMat colmajor;  // caller layout, then the row-major copy the kernels stream
+  upload(c, colmajor, m, n, g, ldg, where);
+  op.xr.alloc(n, m, c.stream, false);
+  if (op.xr.ld > n)
+    NPCG_CUDA(cudaMemset2DAsync(op.xr.p() + n, op.xr.ld * 8, 0, (op.xr.ld - n) * 8, m, c.stream));
+  DBuf<int> flag(1, c.stream);
+  flag.zero();
+  transpose_checked(c, c.stream, colmajor.p(), colmajor.ld, m, n, op.xr.p(), op.xr.ld, flag.p);
+  int h = 0;
+  NPCG_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (h) invalid("GramRidgeOperator: design matrix has non-finite entries");  // operators.cpp:108-109
+}
+
+void gram_upload_streamed(Ctx& c, GramOp& op, const double* g, i64 ldg) {
+  const i64 m = op.m, n = op.n;
+  cudaStream_t aux = c.aux_stream();
+  op.xr.alloc(n, m, c.stream, false);
+  if (op.xr.ld > n)  // pad rows of the row-major copy
+    NPCG_CUDA(cudaMemset2DAsync(op.xr.p() + n, op.xr.ld * 8, 0, (op.xr.ld - n) * 8, m, c.stream));
+  cudaEvent_t alloc_done;
+  NPCG_CUDA(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming));
+  NPCG_CUDA(cudaEventRecord(alloc_done, c.stream));
+  NPCG_CUDA(cudaStreamWaitEvent(aux, alloc_done, 0));
+  NPCG_CUDA(cudaEventDestroy(alloc_done));
+  op.bad.alloc(1, aux);
+  op.bad.zero();
+  // ~80 MB row blocks (multiples of 128 rows): the first block's sketch GEMMs
+  // start while the later blocks are still crossing PCIe
+  i64 rows = std::max<i64>(1024, (80ll << 20) / (8 * n) / 128 * 128);
+  if (const char* e = std::getenv("NPCG_STREAM_ROWS")) rows = std::max<i64>(16, std::atoll(e) / 16 * 16);  // tests
+  DMat staging;  // caller layout of the landing blocks
+  staging.alloc(m, n, aux, false);
+  for (i64 r0 = 0; r0 < m; r0 += rows) {
+    const i64 r1 = std::min(m, r0 + rows);
+    NPCG_CUDA(cudaMemcpy2DAsync(staging.p() + r0, staging.ld * 8, g + r0, ldg * 8, (r1 - r0) * 8, n,
+                                cudaMemcpyHostToDevice, aux));
+    transpose_checked(c, aux, staging.p() + r0, staging.ld, r1 - r0, n, op.xr.p() + r0 * op.xr.ld, op.xr.ld,
+                      op.bad.p);
+    GramOp::Chunk ch{r0, r1, nullptr};
+    NPCG_CUDA(cudaEventCreateWithFlags(&ch.ready, cudaEventDisableTiming));
+    NPCG_CUDA(cudaEventRecord(ch.ready, aux));
+    op.pending.push_back(ch);
+  }
+}
+
+void GramOp::settle() {
+  if (nonfinite) invalid("GramRidgeOperator: design matrix has non-finite entries");
+  if (pending.empty()) return;
+  for (auto& ch : pending) NPCG_CUDA(cudaStreamWaitEvent(ctx->stream, ch.ready, 0));
+  NPCG_CUDA(cudaEventSynchronize(pending.back().ready));
+  for (auto& ch : pending) cudaEventDestroy(ch.ready);
+  pending.clear();
+  NPCG_CUDA(cudaMemcpy(&nonfinite, bad.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (nonfinite) invalid("GramRidgeOperator: design matrix has non-finite entries");  // operators.cpp:108-109
+}
+
+GramOp::~GramOp() {
+  // the side stream may still write xr / read the caller's buffer
+  for (auto& ch : pending) {
+    cudaStreamWaitEvent(ctx->stream, ch.ready, 0);
+    cudaEventSynchronize(ch.ready);
+    cudaEventDestroy(ch.ready);
+  }
+}
+
 void GramOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
+  if (!pending.empty() && k > 8) {
+    // first product of a streamed operator (the sketch): block by block as
+    // the rows land, Z_b = X_b V and out (+)= X_b^T Z_b in fixed block order
+    DMat z;
+    z.alloc(m, k, ctx->stream, false);
+    for (size_t b = 0; b < pending.size(); ++b) {
+      const Chunk& ch = pending[b];
+      NPCG_CUDA(cudaStreamWaitEvent(ctx->stream, ch.ready, 0));
+      const i64 rb = ch.r1 - ch.r0;
+      const double* xb = xr.p() + ch.r0 * xr.ld;
+      gemm(*ctx, rb, k, n, 1.0, Operand{xb, xr.ld, true}, Operand{V, ldv, true}, 0.0, z.p() + ch.r0, z.ld);
+      gemm(*ctx, n, k, rb, 1.0, Operand{xb, xr.ld, false}, Operand{z.p() + ch.r0, z.ld, true}, b ? 1.0 : 0.0, out,
+           ldo);
+    }
+    settle();
+    divide(*ctx, n, k, out, ldo, div);
+    return;
+  }
+  settle();
   if (k == 1 && n <= 2 * GT * GV) {
     gram_single_pass<1>(*ctx, *this, V, ldv, 0.0, nullptr, 0, out, ldo, gate);
     return;
@@ -154,6 +242,7 @@ void GramOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const 
 }
 
 void GramOp::apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) {
+  settle();
   if (S == 1 && n <= 2 * GT * GV) {
     gram_single_pass<1>(*ctx, *this, P, ldp, mu, P, ldp, out, ldo, gate);
     return;

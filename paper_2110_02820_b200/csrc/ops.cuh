@@ -44,9 +44,31 @@ struct GramOp : Op {  // GramRidgeOperator (operators.cpp:105-121): (1/m) G^T (G
   DMat xr;            // design stored row-major: n x m col-major, data row a contiguous
   i64 m = 0;
   double div = 0.0;   // out /= div (operators.cpp:115); the global row count when X is a row shard
+  // Streamed construction (npcg_op_gram_create_streamed): row blocks of X
+  // still landing on the side stream; each is transposed into xr and checked
+  // for non-finite entries there, then `ready` fires.
+  struct Chunk {
+    i64 r0, r1;
+    cudaEvent_t ready;
+  };
+  std::vector<Chunk> pending;
+  DBuf<int> bad;  // non-finite flag of the streamed upload
+  int nonfinite = 0;  // latched: every later use raises the constructor's error
+  /// Order the context stream after every pending block, wait for the upload
+  /// (the caller's host buffer is free afterwards) and raise the constructor's
+  /// non-finite error (operators.cpp:108-109) if the flag is set.
+  void settle();
+  ~GramOp() override;
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
   void apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) override;
 };
+/// Upload the design `g` (m x n, ld ldg; host or device) into op.xr, checking
+/// for non-finite entries in the same pass (synchronous, raises the
+/// constructor's error).
+void gram_upload(Ctx& c, GramOp& op, const double* g, i64 ldg, int where);
+/// Enqueue the upload of the host design `g` (m x n, ld ldg) into op.xr in
+/// row blocks on the context's side stream; returns without waiting.
+void gram_upload_streamed(Ctx& c, GramOp& op, const double* g, i64 ldg);
 
 struct KernelFreeOp : Op {  // KernelOperator beyond dense_cap (operators.cpp:152-188)
   DMat pts;                 // n x d col-major (reference layout)

@@ -691,6 +691,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
                     DMat& V, State* st, double* hist, i64 hstride, i64 max_iter) {
   auto* gram = dynamic_cast<GramOp*>(&op);
   auto* dense = dynamic_cast<DenseOp*>(&op);
+  if (gram) gram->settle();
   const i64 n = op.n;
   const bool nys = pre != nullptr && pre->ell > 0;
   const int G = gram ? persistent_grid<1, true>(ctx)

@@ -119,12 +119,13 @@ def make(name: str, Rng, splitmix64, **kw) -> Workload:
     return CONFIGS[name](Rng, splitmix64, **kw)
 
 
-def build_operator(npcg, w: Workload, ctx=None, exchange=None):
+def build_operator(npcg, w: Workload, ctx=None, exchange=None, streamed=False):
     """The product operator for a workload (device-resident). With a
     dist.TorchExchange of world > 1 the ridge design is row-sharded: this rank
     uploads only its block of X and the products are completed by all-reduce;
     the stored kernel / low-rank operators are built per column block and
-    completed by all-gather."""
+    completed by all-gather. `streamed` overlaps the upload of a ridge design
+    with the sketch (npcg_op_gram_create_streamed)."""
     if exchange is not None:
         from . import dist as pd
         if w.kind == "gram":
@@ -141,7 +142,7 @@ def build_operator(npcg, w: Workload, ctx=None, exchange=None):
     if w.kind == "dense":
         return npcg.DenseOperator(w.data["a"], ctx=ctx)
     if w.kind == "gram":
-        return npcg.GramRidgeOperator(w.data["x"], ctx=ctx)
+        return npcg.GramRidgeOperator(w.data["x"], ctx=ctx, streamed=streamed)
     if w.kind == "kernel":
         return npcg.KernelOperator(w.data["points"], w.data["sigma"], w.data["dense_cap"], ctx=ctx)
     if w.kind == "lowrank":

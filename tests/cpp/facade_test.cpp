@@ -114,6 +114,31 @@ int main() {
     }
     CHECK(threw);
   }
+  // streamed Gram upload: same products as the synchronous constructor
+  {
+    Matrix g(300, 20);
+    for (Index j = 0; j < 20; ++j)
+      for (Index i = 0; i < 300; ++i) g(i, j) = std::sin(0.37 * i + 1.3 * j) / (1.0 + j);
+    const GramRidgeOperator sync(g);
+    const StreamedGramRidgeOperator streamed(g);
+    CHECK(streamed.n_rows() == 300 && streamed.dim() == 20);
+    Vector v(20);
+    for (Index j = 0; j < 20; ++j) v(j) = 1.0 / (1.0 + j);
+    const Vector a = sync.matvec(v), b = streamed.matvec(v);
+    double d = 0.0;
+    for (Index j = 0; j < 20; ++j) d = std::max(d, std::abs(a(j) - b(j)));
+    CHECK(d < 1e-14);
+    Matrix bad = g;
+    bad(7, 3) = std::nan("");
+    threw = false;
+    try {
+      const StreamedGramRidgeOperator s2(bad);
+      (void)s2.matvec(v);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   CHECK(iteration_bound(56.0, 1e-6) == 54);
   if (failures == 0) std::printf("facade ok\n");
   return failures == 0 ? 0 : 1;

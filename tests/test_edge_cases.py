@@ -140,3 +140,29 @@ def test_matrix_free_kernel_paths(npcg, n, d):
         assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max(), k
     j = n // 3
     assert np.allclose(free.column(j), stored.column(j), rtol=1e-13, atol=1e-15)
+
+
+def test_streamed_gram_upload(npcg, orc, monkeypatch):
+    """npcg_op_gram_create_streamed: the block-by-block sketch as X lands
+    matches the synchronous operator and the oracle; the non-finite check
+    moves from the constructor to the first product (same message)."""
+    monkeypatch.setenv("NPCG_STREAM_ROWS", "208")  # several row blocks, a ragged last one
+    rng = np.random.default_rng(17)
+    x = rng.standard_normal((1000, 90)) * (np.arange(1, 91) ** -0.5)
+    sync, streamed, oop = npcg.GramRidgeOperator(x), npcg.GramRidgeOperator(x, streamed=True), \
+        orc.GramRidgeOperator(x)
+    omega = npcg.Rng(4).gaussian_matrix(90, 24)
+    ap = npcg.nystrom_from_sketch(npcg.extend_sketch_with(npcg.make_empty_sketch(streamed), streamed, omega))
+    ao = orc.nystrom_from_sketch(orc.extend_sketch_with(orc.make_empty_sketch(90), oop, omega))
+    compare_approx(ap, ao)
+    v = rng.standard_normal(90)
+    assert np.array_equal(streamed.matvec(v), sync.matvec(v))
+    b = rng.standard_normal(90)
+    compare_solve(npcg.nystrom_pcg(streamed, b, 1e-3, npcg.build_preconditioner(ap, 1e-3), eta=1e-10, relative=True),
+                  orc.nystrom_pcg(oop, b, 1e-3, orc.build_preconditioner(ao, 1e-3), eta=1e-10, relative=True))
+    x[555, 7] = np.nan
+    bad = npcg.GramRidgeOperator(x, streamed=True)
+    with pytest.raises(ValueError, match="non-finite"):
+        bad.apply_block(rng.standard_normal((90, 24)))
+    with pytest.raises(ValueError, match="non-finite"):
+        bad.matvec(v)
