@@ -15,10 +15,12 @@
 #include <cooperative_groups.h>
 
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <sstream>
+#include <string>
 
 #include "async.cuh"
 #include "blas.cuh"
@@ -266,6 +268,7 @@ struct PersistArgs {
   State* st;
   double* hist;
   i64 hstride, max_iter, rows_per_cta, slice, uslice;
+  unsigned long long* trace;  // diagnostics (NPCG_PCG_TRACE): CTA 0 phase timestamps of iterations 2..9
 };
 
 template <int S, bool GRAM>
@@ -302,10 +305,20 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   const int G = gridDim.x, c = blockIdx.x;
   const i64 n = a.n;
   const i64 r0 = min(n, static_cast<i64>(c) * a.slice), r1 = min(n, r0 + a.slice);
+  auto tick = [&](i64 t, int ph) {
+    if (a.trace && c == 0 && tid == 0 && t >= 2 && t < 10) {
+      unsigned long long v;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+      a.trace[(t - 2) * 12 + ph] = v;
+    }
+  };
   const bool nys = a.ell > 0;
   const double* zsrc = nys ? a.Z : a.R;
 
   if (tid < S) cs[tid] = a.st->c[tid];
+  // this CTA's columns of U in P4 (shared memory is left to L1: a carve-out for
+  // U slows the X stream of P1 more than it saves in P4/P5)
+  const i64 u0 = nys ? min(a.ell, static_cast<i64>(c) * a.uslice) : 0, u1 = nys ? min(a.ell, u0 + a.uslice) : 0;
   __syncthreads();
   auto count_running = [&]() {
     int k = 0;
@@ -332,6 +345,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         return cs[s].status == 0 ? zsrc[i + s * a.ldw] + cs[s].beta * po : po;
       };
       // ---- P1
+      tick(t, 0);
       if (!first)
         for (i64 i = r0 + tid; i < r1; i += PT)
 #pragma unroll
@@ -409,23 +423,42 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
 #pragma unroll
         for (int k = 0; k < PV; ++k)
           if (ok[k]) reinterpret_cast<double2*>(dst)[tid + PT * k] = acc[k];
+        tick(t, 1);
         grid.sync();
-        // ---- P2: column slice of v, partial p.v
+        tick(t, 2);
+        // ---- P2: column slice of v, partial p.v. Lanes run over the slice's
+        // columns (coalesced rows of the partials), warps over the partials;
+        // every load of a lane is independent, so one L2 round trip covers them
         double pvl = 0.0;
-        for (i64 j = r0 + warp; j < r1; j += PT / 32) {
-          double s = 0.0;
-          for (int b = lane; b < G; b += 32) s += a.part[static_cast<i64>(b) * PW + j];
-          s = warp_sum(s);
-          const double pj = pcur[j];
-          double v = s / a.div;  // operators.cpp:115 (division), then out += mu p
-          v += a.mu * pj;
-          if (lane == 0) {
+        for (i64 jb = r0; jb < r1; jb += 32) {
+          const i64 j = jb + lane;
+          double s0 = 0.0, s1 = 0.0;
+          if (j < r1) {
+            int b = warp;
+#pragma unroll 4
+            for (; b + PT / 32 < G; b += 2 * (PT / 32)) {
+              s0 += a.part[static_cast<i64>(b) * PW + j];
+              s1 += a.part[static_cast<i64>(b + PT / 32) * PW + j];
+            }
+            if (b < G) s0 += a.part[static_cast<i64>(b) * PW + j];
+          }
+          zred[warp][lane] = s0 + s1;
+          __syncthreads();
+          if (warp == 0 && j < r1) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < PT / 32; ++w) s += zred[w][lane];  // fixed order
+            const double pj = pcur[j];
+            double v = s / a.div;  // operators.cpp:115 (division), then out += mu p
+            v += a.mu * pj;
             a.V[j] = v;
             pvl += pj * v;
           }
+          __syncthreads();
         }
         pvl = block_sum(pvl, sh);
         if (tid == 0) a.pv_part[c] = pvl;
+        tick(t, 3);
       } else {
         // dense: v = A p_t streamed column by column (axpy form, A col-major):
         // CTA (rb, cb) owns rows [rb*PW, +PW) x columns [cb*cpb, +cpb); each
@@ -523,6 +556,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         }
       }
       grid.sync();
+      tick(t, 4);
       // ---- P3: alpha (fin_dot kind 1), x and r updates, partial ||r||^2
 #pragma unroll
       for (int s = 0; s < S; ++s) {
@@ -551,41 +585,26 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         rr = block_sum(rr, sh);
         if (tid == 0) a.rr_part[c * S + s] = rr;
       }
+      tick(t, 5);
       grid.sync();
-      // ---- P4: residual norm, status (fin_res), then the preconditioner's U^T r
+      tick(t, 6);
+      // ---- P4: the preconditioner's U^T r first (independent of the convergence
+      // test, so its loads overlap the residual reduction), then ||r|| and status
+      double rr_pre[S];  // this thread's entry of the residual partials, loaded ahead of the U pass
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const double rr = all_sum(a.rr_part, s);
-        if (tid == 0 && cs[s].status == 0) {
-          const double res = sqrt(rr);
-          cs[s].res = res;
-          if (c == 0) a.hist[s * a.hstride + t] = res;
-          if (!isfinite(res)) cs[s].status = 3;      // solvers.cpp:88-93
-          else if (res <= cs[s].eta) cs[s].status = 1;  // :94-97
-          else if (t >= a.max_iter) cs[s].status = 5;
-          if (!nys && cs[s].status == 0) {  // z = r: r.z = ||r||^2 (fin_dot kind 2)
-            cs[s].beta = rr / cs[s].rz;
-            cs[s].rz = rr;
-          }
-        }
-      }
-      __syncthreads();
-      if (tid == 0) running_sh = count_running();
-      __syncthreads();
-      if (running_sh == 0) break;
-      if (!nys) continue;
-      {
+      for (int s = 0; s < S; ++s) rr_pre[s] = tid < G ? a.rr_part[tid * S + s] : 0.0;
+      if (nys) {
         // this CTA's columns of U, up to UQ at a time: r is read once per row for all of them
         // and the UQ x S dots are reduced together (one barrier)
         constexpr int UQ = 4;
-        const i64 u0 = min(a.ell, static_cast<i64>(c) * a.uslice), u1 = min(a.ell, u0 + a.uslice);
         for (i64 j0 = u0; j0 < u1; j0 += UQ) {
           double w[UQ][S];
 #pragma unroll
           for (int q = 0; q < UQ; ++q)
 #pragma unroll
             for (int s = 0; s < S; ++s) w[q][s] = 0.0;
-          for (i64 i = tid; i < n; i += PT) {
+#pragma unroll 4
+          for (i64 i = tid; i < n; i += PT) {  // unrolled: the rows' loads are in flight together
             double ri[S];
 #pragma unroll
             for (int s = 0; s < S; ++s) ri[s] = a.R[i + s * a.ldw];
@@ -617,16 +636,50 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
           __syncthreads();
         }
       }
+      // residual norm, status (fin_res)
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const double rr = G <= PT ? block_sum(rr_pre[s], sh) : all_sum(a.rr_part, s);  // same order as all_sum
+        if (tid == 0 && cs[s].status == 0) {
+          const double res = sqrt(rr);
+          cs[s].res = res;
+          if (c == 0) a.hist[s * a.hstride + t] = res;
+          if (!isfinite(res)) cs[s].status = 3;      // solvers.cpp:88-93
+          else if (res <= cs[s].eta) cs[s].status = 1;  // :94-97
+          else if (t >= a.max_iter) cs[s].status = 5;
+          if (!nys && cs[s].status == 0) {  // z = r: r.z = ||r||^2 (fin_dot kind 2)
+            cs[s].beta = rr / cs[s].rz;
+            cs[s].rz = rr;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) running_sh = count_running();
+      __syncthreads();
+      if (running_sh == 0) break;
+      if (!nys) continue;
+      tick(t, 7);
       grid.sync();
+      tick(t, 8);
       // ---- P5: z = r + U t on the slice (32 rows x 16 column groups), partial r.z
+      auto uat = [&](i64 i, i64 j) { return a.U[i + j * a.ldu]; };
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         double rz = 0.0;
         for (i64 i0 = r0; i0 < r1; i0 += 32) {
           const i64 i = i0 + lane;
           double acc = 0.0;
-          if (i < r1)
-            for (i64 j = warp; j < a.ell; j += PT / 32) acc += a.U[i + j * a.ldu] * a.T[j + s * a.ell];
+          if (i < r1) {
+            double acc1 = 0.0;  // two chains, loads several columns ahead
+            i64 j = warp;
+#pragma unroll 4
+            for (; j + PT / 32 < a.ell; j += 2 * (PT / 32)) {
+              acc += uat(i, j) * a.T[j + s * a.ell];
+              acc1 += uat(i, j + PT / 32) * a.T[j + PT / 32 + s * a.ell];
+            }
+            if (j < a.ell) acc += uat(i, j) * a.T[j + s * a.ell];
+            acc += acc1;
+          }
           zred[warp][lane] = acc;
           __syncthreads();
           if (warp == 0 && i < r1) {
@@ -643,7 +696,9 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         rz = block_sum(rz, sh);
         if (tid == 0) a.rz_part[c * S + s] = rz;
       }
+      tick(t, 9);
       grid.sync();
+      tick(t, 10);
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const double rz = all_sum(a.rz_part, s);
@@ -667,11 +722,12 @@ bool persistent_eligible(const Ctx& ctx, Op& op, i64 S) {
 }
 
 template <int S, bool GRAM>
-void launch_persistent(Ctx& ctx, PersistArgs& pa, int G) {
+void launch_persistent(Ctx& ctx, PersistArgs& pa, int G, int smem) {
   void* args[] = {&pa};
   ctx.prof_begin(GRAM ? "pcg_persistent_kernel<gram>" : "pcg_persistent_kernel<dense>");
+  // dynamic shared memory: the ring that streams A (dense), U's resident blocks (gram)
   NPCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(pcg_persistent_kernel<S, GRAM>), G, PT, args,
-                                        GRAM ? 0 : RING_BYTES, ctx.stream));  // the ring streams A (dense only)
+                                        smem, ctx.stream));
   ctx.check_launch("pcg_persistent_kernel");
   ctx.prof_end();
 }
@@ -756,12 +812,32 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   pa.max_iter = max_iter;
   pa.slice = cdiv(n, G);
   if (P.ld != R.ld || V.ld != R.ld || P1.ld != R.ld || (nys && Z.ld != R.ld)) fail(NPCG_ERUNTIME, "pcg: work layout");
-  if (gram) launch_persistent<1, true>(ctx, pa, G);
-  else if (S == 1) launch_persistent<1, false>(ctx, pa, G);
-  else if (S == 2) launch_persistent<2, false>(ctx, pa, G);
-  else if (S == 3) launch_persistent<3, false>(ctx, pa, G);
-  else launch_persistent<4, false>(ctx, pa, G);
+  static const bool tracing = std::getenv("NPCG_PCG_TRACE") != nullptr;  // diagnostics
+  DBuf<unsigned long long> tr;
+  if (tracing) {
+    tr.alloc(8 * 12, ctx.stream);
+    tr.zero();
+    pa.trace = tr.p;
+  }
+  const int smem = gram ? 0 : RING_BYTES;
+  if (gram) launch_persistent<1, true>(ctx, pa, G, smem);
+  else if (S == 1) launch_persistent<1, false>(ctx, pa, G, smem);
+  else if (S == 2) launch_persistent<2, false>(ctx, pa, G, smem);
+  else if (S == 3) launch_persistent<3, false>(ctx, pa, G, smem);
+  else launch_persistent<4, false>(ctx, pa, G, smem);
   ctx.sync();  // work buffers are released on return
+  if (tracing) {
+    unsigned long long h[8 * 12];
+    NPCG_CUDA(cudaMemcpy(h, tr.p, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int t = 0; t < 8; ++t) {
+      const unsigned long long* q = h + t * 12;
+      if (!q[0] || !q[10]) continue;
+      std::fprintf(stderr, "[pcg it %d] P1 %.2f s1 %.2f P2 %.2f s2 %.2f P3 %.2f s3 %.2f P4 %.2f s4 %.2f P5 %.2f s5 %.2f "
+                   "total %.2f us\n", t + 2, (q[1] - q[0]) * 1e-3, (q[2] - q[1]) * 1e-3, (q[3] - q[2]) * 1e-3,
+                   (q[4] - q[3]) * 1e-3, (q[5] - q[4]) * 1e-3, (q[6] - q[5]) * 1e-3, (q[7] - q[6]) * 1e-3,
+                   (q[8] - q[7]) * 1e-3, (q[9] - q[8]) * 1e-3, (q[10] - q[9]) * 1e-3, (q[10] - q[0]) * 1e-3);
+    }
+  }
   if (ctx.prof) {  // algorithmic traffic of the launch: per iteration A once, U twice, ~10 n-vectors
     State h;
     NPCG_CUDA(cudaMemcpy(&h, st, sizeof(State), cudaMemcpyDeviceToHost));
