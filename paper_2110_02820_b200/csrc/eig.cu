@@ -209,6 +209,11 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
   }
   cl.sync();
   bool pend = false;
+  if (trace && tid == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    trace[64 * 6 + rank] = sm;
+  }
   auto tick = [&](int k, int ph) {
     if (trace && rank == 0 && tid == 0 && k < 64) {
       unsigned long long t;
@@ -374,6 +379,215 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const doub
       e[n - 1] = 0.0;
       tau[n - 1] = 0.0;
     }
+  }
+  cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
+}
+
+// Register-resident variant of tridiag_cluster_kernel: warp w of CTA r keeps
+// its owned columns c = (w + 8q) C + r (q < 4) in registers, lane l holding
+// rows l + 32 m (m < MR), so the fused pass (pending rank-2 update + the
+// column's dot with v) touches shared memory only for the vectors. The next
+// step's column k+1 is taken as row k+1 (A is symmetric): every CTA publishes
+// the row's entries of its own columns next to their p values, and one
+// gather per step (half-warp h reads CTA h's 32 (p, row) pairs, contiguous)
+// moves both -- no CTA serves a whole column to the cluster (DSMEM bandwidth
+// per SM is ~21 B/clk; a 3.2 KB column to 15 peers costs ~1 us).
+template <int MR>
+__global__ void __launch_bounds__(TRI_THREADS, 1) tridiag_reg_kernel(const double* M, i64 ld, int n, double* d,
+                                                                      double* e, double* tau, double* H, i64 ldh,
+                                                                      unsigned long long* trace) {
+  constexpr int QMAX = 4, NW = TRI_THREADS / 32;
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
+  extern __shared__ double trs[];
+  double* v = trs;               // [n] reflector of the step (v[j] <-> row k+1+j)
+  double* vp = v + n;            // [n] previous step's v, w (vp[i] <-> row k+i)
+  double* wp = vp + n;
+  double* pt = wp + n;           // [n] gathered p (pt[i] <-> column k+1+i)
+  double* xcol = pt + n;         // [n] row k of the updated matrix (xcol[i] <-> column k+i)
+  __shared__ double2 pr[2][32];  // (p, row k+1 entry) of this CTA's owned columns
+  __shared__ double redA[NW], redB[NW];
+  __shared__ double alpha_sh, lastd;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ncl = (n + C - 1) / C;
+  auto bsum1 = [&](double x, double* buf) {
+    x = warp_sum(x);
+    if (lane == 0) buf[warp] = x;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += buf[w];
+    return t;
+  };
+  double a[QMAX][MR];
+  int cq[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int lc = warp + NW * q;
+    cq[q] = lc < ncl ? lc * C + rank : n;  // n = no column
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      const int r = lane + 32 * m;
+      a[q][m] = (cq[q] < n && r < n) ? M[r + static_cast<i64>(cq[q]) * ld] : 0.0;
+    }
+    if (lane == 0 && cq[q] < n) pr[1][lc].y = a[q][0];  // row 0 for the first step
+  }
+  if (trace && tid == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    trace[64 * 6 + rank] = sm;
+  }
+  // gather (p, row k+1) of step k-1 from every CTA: half-warp h <- CTA h
+  auto gather = [&](int k, int buf) {
+    const int src = tid >> 4, l0 = tid & 15;
+    if (src < C) {
+      const double2* rp = cl.map_shared_rank(&pr[buf][0], src);
+      const int c0 = l0 * C + src, c1 = (l0 + 16) * C + src;
+      const bool ok0 = l0 < ncl && c0 > k && c0 < n, ok1 = l0 + 16 < ncl && c1 > k && c1 < n;
+      const double2 g0 = ok0 ? rp[l0] : make_double2(0.0, 0.0), g1 = ok1 ? rp[l0 + 16] : make_double2(0.0, 0.0);
+      if (ok0) {
+        pt[c0 - k - 1] = g0.x;
+        xcol[c0 - k - 1] = g0.y;
+      }
+      if (ok1) {
+        pt[c1 - k - 1] = g1.x;
+        xcol[c1 - k - 1] = g1.y;
+      }
+    }
+  };
+  cl.sync();
+  gather(-1, 1);  // row 0 (its p entries are unused)
+  __syncthreads();
+  bool pend = false;
+  auto tick = [&](int k, int ph) {
+    if (trace && rank == 0 && tid == 0 && k < 64) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      trace[k * 6 + ph] = t;
+    }
+  };
+  for (int k = 0; k < n - 2; ++k) {
+    tick(k, 0);
+    const int L = n - k - 1;  // <= 511: rows k+1+tid and k+1+tid+256
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = tid + u * TRI_THREADS;
+      if (j < L) {
+        double x = xcol[j + 1];
+        if (pend) x -= vp[j + 1] * wp[0] + wp[j + 1] * vp[0];
+        v[j] = x;
+        if (j > 0) s += x * x;
+        else alpha_sh = x;
+      }
+    }
+    s = bsum1(s, redA);  // (its barrier also publishes v and alpha)
+    tick(k, 1);
+    const double alpha = alpha_sh;
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (s > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + s), alpha);
+      t = (beta - alpha) * fast_rcp(beta);
+      scal = fast_rcp(alpha - beta);
+    }
+    for (int j = tid; j < L; j += TRI_THREADS) v[j] = j == 0 ? 1.0 : v[j] * scal;  // this thread's own entries
+    if (rank == 0 && tid == 0) {
+      d[k] = pend ? xcol[0] - (vp[0] * wp[0] + wp[0] * vp[0]) : xcol[0];
+      e[k] = beta;
+      tau[k] = t;
+    }
+    __syncthreads();
+    if (rank == 0)
+      for (int i = tid; i < L; i += TRI_THREADS) H[(k + 1 + i) + static_cast<i64>(k) * ldh] = v[i];
+    tick(k, 2);
+    const int buf = k & 1;
+    {
+      double vcq[QMAX], wcq[QMAX], accq[QMAX], rowq[QMAX];
+      bool lq[QMAX];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        lq[q] = cq[q] > k && cq[q] < n;
+        vcq[q] = lq[q] && pend ? vp[cq[q] - k] : 0.0;
+        wcq[q] = lq[q] && pend ? wp[cq[q] - k] : 0.0;
+        accq[q] = 0.0;
+        rowq[q] = 0.0;
+      }
+      // Branch-free inside a group of 4 warp-rows (loads hoisted, 4 x QMAX
+      // independent chains): rows outside the trailing block and dead columns
+      // get zero coefficients, which leaves a unchanged and adds +0 to acc.
+#pragma unroll
+      for (int g = 0; g < MR / 4; ++g) {
+        if (32 * (4 * g + 3) + 31 <= k || 128 * g >= n) continue;  // whole group outside (uniform)
+        double vpi[4], wpi[4], vi[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = lane + 32 * (4 * g + u);
+          const bool rl = r > k && r < n;
+          const int ix = rl ? r - k : 1;
+          const double x0 = vp[ix], x1 = wp[ix], x2 = v[ix - 1];
+          vpi[u] = rl && pend ? x0 : 0.0;
+          wpi[u] = rl && pend ? x1 : 0.0;
+          vi[u] = rl ? x2 : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q) {
+            const double x = fma(-vpi[u], wcq[q], fma(-wpi[u], vcq[q], a[q][4 * g + u]));  // two FMAs
+            a[q][4 * g + u] = x;
+            accq[q] = fma(x, vi[u], accq[q]);
+          }
+      }
+      const int m1 = (k + 1) >> 5;  // warp-row holding row k+1 (uniform branch per m)
+#pragma unroll
+      for (int m = 0; m < MR; ++m)
+        if (m == m1)
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q) rowq[q] = a[q][m];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        if (lq[q] && lane == ((k + 1) & 31)) pr[buf][warp + NW * q].y = rowq[q];  // row k+1 of column cq
+        if (k == n - 3 && cq[q] == n - 1)  // a(n-1, n-1) after the last update, for the final 2 x 2 block
+#pragma unroll
+          for (int m = 0; m < MR; ++m)
+            if (lane + 32 * m == n - 1) lastd = a[q][m];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) accq[q] += __shfl_xor_sync(0xffffffffu, accq[q], o);
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q)
+          if (lq[q]) pr[buf][warp + NW * q].x = t * accq[q];
+    }
+    tick(k, 3);
+    cl.sync();
+    tick(k, 4);
+    gather(k, buf);
+    __syncthreads();
+    double pv = 0.0;
+    for (int i = tid; i < L; i += TRI_THREADS) pv += pt[i] * v[i];
+    pv = bsum1(pv, redB);
+    tick(k, 5);
+    const double K = 0.5 * t * pv;
+    for (int i = tid; i < L; i += TRI_THREADS) {
+      double w = pt[i];
+      w -= K * v[i];
+      wp[i] = w;
+      vp[i] = v[i];
+    }
+    pend = true;
+    __syncthreads();
+  }
+  if (rank == 0 && tid == 0) {
+    const double* ld1 = cl.map_shared_rank(&lastd, (n - 1) % C);
+    d[n - 2] = xcol[0] - (vp[0] * wp[0] + wp[0] * vp[0]);
+    e[n - 2] = xcol[1] - (vp[1] * wp[0] + wp[1] * vp[0]);
+    d[n - 1] = *ld1 - (vp[1] * wp[1] + wp[1] * vp[1]);
+    tau[n - 2] = 0.0;
+    e[n - 1] = 0.0;
+    tau[n - 1] = 0.0;
   }
   cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
@@ -789,7 +1003,58 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
   DMat H;
   H.alloc(n, n, ctx.stream, true);
   bool done_tri = false;
-  if (n >= 3 && !(std::getenv("NPCG_TRIDIAG") && std::string(std::getenv("NPCG_TRIDIAG")) == "global")) {
+  const char* tri_env = std::getenv("NPCG_TRIDIAG");  // diagnostics: "global" | "smem"
+  const std::string tri_mode = tri_env ? tri_env : "";
+  if (n >= 3 && n <= 512 && tri_mode.empty()) {
+    // register-resident cluster kernel: 8 CTAs up to n = 256, 16 up to 512
+    const int C = n <= 256 ? 8 : 16;
+    const size_t smem = static_cast<size_t>(5 * n * 8);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(TRI_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    auto kern = n <= 128 ? tridiag_reg_kernel<4> : n <= 256 ? tridiag_reg_kernel<8> : tridiag_reg_kernel<16>;
+    NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters >= 1) {
+      static const bool tracing = std::getenv("NPCG_TRI_TRACE") != nullptr;  // diagnostics
+      DBuf<unsigned long long> tr;
+      if (tracing) {
+        tr.alloc(64 * 6 + 16, ctx.stream);
+        tr.zero();
+      }
+      ctx.prof_begin("tridiag_reg_kernel");
+      NPCG_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<const double*>(M), ldm, nn, d.p, e.p, tau.p, H.p(), H.ld,
+                                   tracing ? tr.p : static_cast<unsigned long long*>(nullptr)));
+      ctx.check_launch("tridiag_reg_kernel");
+      ctx.prof_end();
+      if (tracing) {
+        ctx.sync();
+        std::vector<unsigned long long> h(64 * 6 + 16);
+        NPCG_CUDA(cudaMemcpy(h.data(), tr.p, 8 * h.size(), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[tri smid]");
+        for (int r = 0; r < 16; ++r) std::fprintf(stderr, " %llu", h[64 * 6 + r]);
+        std::fprintf(stderr, "\n");
+        for (int k = 1; k < 40 && k + 1 < n - 2; k += 8)
+          std::fprintf(stderr, "[tri-reg n=%d] k=%d colred %.2f scal %.2f fused %.2f csync %.2f gather %.2f tail %.2f us\n",
+                       nn, k, (h[k * 6 + 1] - h[k * 6]) * 1e-3, (h[k * 6 + 2] - h[k * 6 + 1]) * 1e-3,
+                       (h[k * 6 + 3] - h[k * 6 + 2]) * 1e-3, (h[k * 6 + 4] - h[k * 6 + 3]) * 1e-3,
+                       (h[k * 6 + 5] - h[k * 6 + 4]) * 1e-3, (h[(k + 1) * 6] - h[k * 6 + 5]) * 1e-3);
+      }
+      done_tri = true;
+    } else {
+      (void)cudaGetLastError();
+    }
+  }
+  if (n >= 3 && !done_tri && tri_mode != "global") {
     for (int C : {16, 8}) {  // cluster-resident variant when the matrix fits in C CTAs' shared memory
       const i64 ncl = cdiv(n, C);
       const i64 smem = (ncl * n + 4 * n + 2 * ncl) * 8;
@@ -818,15 +1083,18 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
       static const bool tracing = std::getenv("NPCG_TRI_TRACE") != nullptr;  // diagnostics
       DBuf<unsigned long long> tr;
       if (tracing) {
-        tr.alloc(64 * 6, ctx.stream);
+        tr.alloc(64 * 6 + 16, ctx.stream);
         tr.zero();
       }
       NPCG_CUDA(cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, static_cast<const double*>(M), ldm, nn, d.p, e.p,
                                    tau.p, H.p(), H.ld, tracing ? tr.p : static_cast<unsigned long long*>(nullptr)));
       if (tracing) {
         ctx.sync();
-        std::vector<unsigned long long> h(64 * 6);
+        std::vector<unsigned long long> h(64 * 6 + 16);
         NPCG_CUDA(cudaMemcpy(h.data(), tr.p, 8 * h.size(), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[tri smid]");
+        for (int r = 0; r < 16; ++r) std::fprintf(stderr, " %llu", h[64 * 6 + r]);
+        std::fprintf(stderr, "\n");
         for (int k = 1; k < 40 && k + 1 < n - 2; k += 8)
           std::fprintf(stderr, "[tri n=%d] k=%d colred %.2f scal+fused? %.2f fused %.2f csync %.2f gather %.2f tail %.2f us\n",
                        nn, k, (h[k * 6 + 1] - h[k * 6]) * 1e-3, (h[k * 6 + 2] - h[k * 6 + 1]) * 1e-3,
