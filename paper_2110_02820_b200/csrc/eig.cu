@@ -1,10 +1,12 @@
 // Symmetric eigenvectors of a small dense l x l matrix on device, for the
 // thin SVD of the Nyström pipeline (factor.cu).
 //
-//   1. Householder tridiagonalisation in one cooperative kernel: per column,
-//      every CTA forms the reflector redundantly; the previous step's rank-2
-//      update and this step's trailing symmetric matvec are fused in one pass
-//      split over CTAs by column (one grid-wide barrier per column).
+//   1. Householder tridiagonalisation: per column, every CTA forms the
+//      reflector redundantly; the previous step's rank-2 update and this
+//      step's trailing symmetric matvec are fused in one pass split over CTAs
+//      by column. n <= 512: one thread-block cluster with the matrix in
+//      registers (one cluster barrier per column); larger n: one cooperative
+//      kernel (one grid-wide barrier per column).
 //   2. Bisection with Sturm counts, one eigenvalue per thread.
 //   3. Inverse iteration on the tridiagonal (partial-pivoting LU), one
 //      eigenvector per thread, deterministic pseudo-random starts; exact
@@ -143,247 +145,8 @@ __global__ void __launch_bounds__(TRI_THREADS) tridiag_kernel(double* M, i64 ld,
   }
 }
 
-// Same algorithm inside one thread-block cluster with the matrix resident in
-// shared memory: CTA r of C owns columns c = r (mod C) whole (n <= ~620 at
-// C = 16). Column k and the matvec results p are read across the cluster
-// through DSMEM; one cluster barrier per column, no global-memory traffic.
-// One owned column of the fused pass: a_i -= vp[i+1] wc + wp[i+1] vc (written
-// back) and the lane's partial of sum_i a_i v_i, rows i = lane + 32 m < L.
-// restrict + loads grouped ahead of the stores let consecutive rows overlap.
-__device__ __forceinline__ double tri_lane_pass(double* __restrict__ col, const double* __restrict__ vp,
-                                                const double* __restrict__ wp, const double* __restrict__ v,
-                                                double vc, double wc, int L, int lane, bool pend) {
-  double acc = 0.0;
-  int i = lane;
-  if (pend) {
-    for (; i + 96 < L; i += 128) {
-      double a[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = col[i + 32 * u] - (vp[i + 32 * u + 1] * wc + wp[i + 32 * u + 1] * vc);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) col[i + 32 * u] = a[u];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc += a[u] * v[i + 32 * u];
-    }
-    for (; i < L; i += 32) {
-      const double a = col[i] - (vp[i + 1] * wc + wp[i + 1] * vc);
-      col[i] = a;
-      acc += a * v[i];
-    }
-  } else {
-    for (; i < L; i += 32) acc += col[i] * v[i];
-  }
-  return acc;
-}
-
-__global__ void __launch_bounds__(TRI_THREADS) tridiag_cluster_kernel(const double* M, i64 ld, int n, double* d,
-                                                                       double* e, double* tau, double* H, i64 ldh,
-                                                                       unsigned long long* trace) {
-  cg::cluster_group cl = cg::this_cluster();
-  const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
-  extern __shared__ double csm_t[];
-  const int ncl = (n + C - 1) / C;
-  double* cols = csm_t;            // [ncl][n]: local column lc is global column lc*C + rank
-  double* v = cols + static_cast<i64>(ncl) * n;
-  double* vp = v + n;
-  double* wp = vp + n;
-  double* pt = wp + n;
-  double* pl = pt + n;             // [2][ncl] matvec results of the owned columns
-  __shared__ double redA[TRI_THREADS / 32], redB[TRI_THREADS / 32];
-  __shared__ double alpha_sh;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  // one-barrier block sum (fixed order, identical in every thread); buf is not reused before a later barrier
-  auto bsum1 = [&](double x, double* buf) {
-    x = warp_sum(x);
-    if (lane == 0) buf[warp] = x;
-    __syncthreads();
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < TRI_THREADS / 32; ++w) t += buf[w];
-    return t;
-  };
-  for (int lc = 0; lc < ncl; ++lc) {
-    const int c = lc * C + rank;
-    if (c >= n) break;
-    for (int i = tid; i < n; i += blockDim.x) cols[static_cast<i64>(lc) * n + i] = M[i + static_cast<i64>(c) * ld];
-  }
-  cl.sync();
-  bool pend = false;
-  if (trace && tid == 0) {
-    unsigned sm;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
-    trace[64 * 6 + rank] = sm;
-  }
-  auto tick = [&](int k, int ph) {
-    if (trace && rank == 0 && tid == 0 && k < 64) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-      trace[k * 6 + ph] = t;
-    }
-  };
-  for (int k = 0; k < n - 2; ++k) {
-    tick(k, 0);
-    const int L = n - k - 1;
-    const double* ck = cl.map_shared_rank(cols + static_cast<i64>(k / C) * n, k % C);
-    double s = 0.0;
-    for (int j0 = tid; j0 < L; j0 += 2 * TRI_THREADS) {  // both remote loads in flight together
-      double xr[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) xr[u] = j0 + u * TRI_THREADS < L ? ck[k + 1 + j0 + u * TRI_THREADS] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int j = j0 + u * TRI_THREADS;
-        if (j < L) {
-          double x = xr[u];
-          if (pend) x -= vp[j + 1] * wp[0] + wp[j + 1] * vp[0];
-          v[j] = x;
-          if (j > 0) s += x * x;
-          else alpha_sh = x;
-        }
-      }
-    }
-    s = bsum1(s, redA);  // (its barrier also publishes v and alpha)
-    tick(k, 1);
-    const double alpha = alpha_sh;
-    double t = 0.0, beta = alpha, scal = 0.0;
-    if (s > 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + s), alpha);
-      t = (beta - alpha) * fast_rcp(beta);
-      scal = fast_rcp(alpha - beta);
-    }
-    for (int j = tid; j < L; j += blockDim.x) v[j] = j == 0 ? 1.0 : v[j] * scal;
-    if (rank == 0 && tid == 0) {
-      d[k] = pend ? ck[k] - (vp[0] * wp[0] + wp[0] * vp[0]) : ck[k];
-      e[k] = beta;
-      tau[k] = t;
-    }
-    __syncthreads();
-    if (rank == 0)
-      for (int i = tid; i < L; i += blockDim.x) H[(k + 1 + i) + static_cast<i64>(k) * ldh] = v[i];
-    tick(k, 2);
-    double* pk = pl + (k & 1) * ncl;
-    {
-      // this warp's owned trailing columns (lc = warp + nw q), processed together:
-      // vp/wp/v are read once per row and the column chains interleave
-      constexpr int QMAX = 4;
-      double* colq[QMAX];
-      double vcq[QMAX], wcq[QMAX], accq[QMAX];
-      int nq = 0;
-#pragma unroll
-      for (int q = 0; q < QMAX; ++q) {
-        const int lc = warp + nw * q;
-        const int c = lc * C + rank;
-        const bool live = lc < ncl && c > k && c < n;
-        const int ci = c - (k + 1);
-        colq[q] = live ? cols + static_cast<i64>(lc) * n + (k + 1) : nullptr;
-        vcq[q] = live && pend ? vp[ci + 1] : 0.0;
-        wcq[q] = live && pend ? wp[ci + 1] : 0.0;
-        accq[q] = 0.0;
-        nq += live;
-      }
-      if (nq > 0) {
-        // two rows per lane per step, every shared load issued before any store
-        // (the column stores could alias the loads as far as the compiler knows,
-        // which otherwise serialises load -> store -> load per column)
-        int i = lane;
-        for (; i + 32 < L; i += 64) {
-          double vpi[2], wpi[2], vi[2], a[2][QMAX];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int r = i + 32 * u;
-            vpi[u] = pend ? vp[r + 1] : 0.0;
-            wpi[u] = pend ? wp[r + 1] : 0.0;
-            vi[u] = v[r];
-#pragma unroll
-            for (int q = 0; q < QMAX; ++q) a[u][q] = colq[q] ? colq[q][r] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-#pragma unroll
-            for (int q = 0; q < QMAX; ++q) a[u][q] -= vpi[u] * wcq[q] + wpi[u] * vcq[q];
-          if (pend)
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-              for (int q = 0; q < QMAX; ++q)
-                if (colq[q]) colq[q][i + 32 * u] = a[u][q];
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-#pragma unroll
-            for (int q = 0; q < QMAX; ++q) accq[q] += a[u][q] * vi[u];
-        }
-        if (i < L) {
-          const double vpi = pend ? vp[i + 1] : 0.0, wpi = pend ? wp[i + 1] : 0.0, vi = v[i];
-          double a[QMAX];
-#pragma unroll
-          for (int q = 0; q < QMAX; ++q) a[q] = colq[q] ? colq[q][i] : 0.0;
-#pragma unroll
-          for (int q = 0; q < QMAX; ++q) a[q] -= vpi * wcq[q] + wpi * vcq[q];
-          if (pend)
-#pragma unroll
-            for (int q = 0; q < QMAX; ++q)
-              if (colq[q]) colq[q][i] = a[q];
-#pragma unroll
-          for (int q = 0; q < QMAX; ++q) accq[q] += a[q] * vi;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int q = 0; q < QMAX; ++q) accq[q] += __shfl_xor_sync(0xffffffffu, accq[q], o);
-        if (lane == 0)
-#pragma unroll
-          for (int q = 0; q < QMAX; ++q)
-            if (colq[q]) pk[warp + nw * q] = t * accq[q];
-      }
-    }
-    tick(k, 3);
-    cl.sync();
-    tick(k, 4);
-    double pv = 0.0;
-    for (int i0 = tid; i0 < L; i0 += 2 * TRI_THREADS) {  // both remote loads in flight together
-      double pr[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int c = k + 1 + i0 + u * TRI_THREADS;
-        pr[u] = i0 + u * TRI_THREADS < L ? *cl.map_shared_rank(pk + c / C, c % C) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int i = i0 + u * TRI_THREADS;
-        if (i < L) {
-          pt[i] = pr[u];
-          pv += pr[u] * v[i];
-        }
-      }
-    }
-    pv = bsum1(pv, redB);
-    tick(k, 5);
-    const double K = 0.5 * t * pv;
-    for (int i = tid; i < L; i += blockDim.x) {
-      double w = pt[i];
-      w -= K * v[i];
-      wp[i] = w;
-      vp[i] = v[i];
-    }
-    pend = true;
-    __syncthreads();
-  }
-  if (rank == 0 && tid == 0) {
-    if (n >= 3) {
-      const double* c2 = cl.map_shared_rank(cols + static_cast<i64>((n - 2) / C) * n, (n - 2) % C);
-      const double* c1 = cl.map_shared_rank(cols + static_cast<i64>((n - 1) / C) * n, (n - 1) % C);
-      d[n - 2] = c2[n - 2] - (vp[0] * wp[0] + wp[0] * vp[0]);
-      e[n - 2] = c2[n - 1] - (vp[1] * wp[0] + wp[1] * vp[0]);
-      d[n - 1] = c1[n - 1] - (vp[1] * wp[1] + wp[1] * vp[1]);
-      tau[n - 2] = 0.0;
-      e[n - 1] = 0.0;
-      tau[n - 1] = 0.0;
-    }
-  }
-  cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
-}
-
-// Register-resident variant of tridiag_cluster_kernel: warp w of CTA r keeps
+// The same algorithm inside one thread-block cluster (n <= 512, no global
+// memory traffic but the outputs). Warp w of CTA r keeps
 // its owned columns c = (w + 8q) C + r (q < 4) in registers, lane l holding
 // rows l + 32 m (m < MR), so the fused pass (pending rank-2 update + the
 // column's dot with v) touches shared memory only for the vectors. The next
@@ -1003,7 +766,7 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
   DMat H;
   H.alloc(n, n, ctx.stream, true);
   bool done_tri = false;
-  const char* tri_env = std::getenv("NPCG_TRIDIAG");  // diagnostics: "global" | "smem"
+  const char* tri_env = std::getenv("NPCG_TRIDIAG");  // diagnostics: "global"
   const std::string tri_mode = tri_env ? tri_env : "";
   if (n >= 3 && n <= 512 && tri_mode.empty()) {
     // register-resident cluster kernel: 8 CTAs up to n = 256, 16 up to 512
@@ -1052,59 +815,6 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
       done_tri = true;
     } else {
       (void)cudaGetLastError();
-    }
-  }
-  if (n >= 3 && !done_tri && tri_mode != "global") {
-    for (int C : {16, 8}) {  // cluster-resident variant when the matrix fits in C CTAs' shared memory
-      const i64 ncl = cdiv(n, C);
-      const i64 smem = (ncl * n + 4 * n + 2 * ncl) * 8;
-      if (smem > 220 * 1024 || ncl > (TRI_THREADS / 32) * 4) continue;  // <= 4 owned columns per warp
-      NPCG_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-      NPCG_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(C);
-      cfg.blockDim = dim3(TRI_THREADS);
-      cfg.dynamicSmemBytes = static_cast<size_t>(smem);
-      cfg.stream = ctx.stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = C;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      int nclusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclusters, tridiag_cluster_kernel, &cfg) != cudaSuccess || nclusters < 1) {
-        (void)cudaGetLastError();
-        continue;
-      }
-      ctx.prof_begin("tridiag_cluster_kernel");
-      static const bool tracing = std::getenv("NPCG_TRI_TRACE") != nullptr;  // diagnostics
-      DBuf<unsigned long long> tr;
-      if (tracing) {
-        tr.alloc(64 * 6 + 16, ctx.stream);
-        tr.zero();
-      }
-      NPCG_CUDA(cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, static_cast<const double*>(M), ldm, nn, d.p, e.p,
-                                   tau.p, H.p(), H.ld, tracing ? tr.p : static_cast<unsigned long long*>(nullptr)));
-      if (tracing) {
-        ctx.sync();
-        std::vector<unsigned long long> h(64 * 6 + 16);
-        NPCG_CUDA(cudaMemcpy(h.data(), tr.p, 8 * h.size(), cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "[tri smid]");
-        for (int r = 0; r < 16; ++r) std::fprintf(stderr, " %llu", h[64 * 6 + r]);
-        std::fprintf(stderr, "\n");
-        for (int k = 1; k < 40 && k + 1 < n - 2; k += 8)
-          std::fprintf(stderr, "[tri n=%d] k=%d colred %.2f scal+fused? %.2f fused %.2f csync %.2f gather %.2f tail %.2f us\n",
-                       nn, k, (h[k * 6 + 1] - h[k * 6]) * 1e-3, (h[k * 6 + 2] - h[k * 6 + 1]) * 1e-3,
-                       (h[k * 6 + 3] - h[k * 6 + 2]) * 1e-3, (h[k * 6 + 4] - h[k * 6 + 3]) * 1e-3,
-                       (h[k * 6 + 5] - h[k * 6 + 4]) * 1e-3, (h[(k + 1) * 6] - h[k * 6 + 5]) * 1e-3);
-      }
-      ctx.check_launch("tridiag_cluster_kernel");
-      ctx.prof_end();
-      done_tri = true;
-      break;
     }
   }
   if (n >= 3 && !done_tri) {
