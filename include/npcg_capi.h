@@ -98,7 +98,9 @@ int npcg_op_gram_create(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, in
  * and the first product (the sketch) starts on each block as it lands.
  * Contract: `g` must stay valid and unchanged until the first call that
  * applies the operator returns (or npcg_op_destroy); that call raises the
- * constructor's non-finite error (NPCG_EINVAL, same message) in its place. */
+ * constructor's non-finite error (NPCG_EINVAL, same message) in its place.
+ * Device memory: two copies of X until then (the synchronous constructor
+ * streams host designs through a 4 x ~80 MB staging ring instead). */
 int npcg_op_gram_create_streamed(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, int64_t ldg,
                                  npcg_op** out);
 /* KernelOperator(points n x d, sigma, dense_cap), operators.cpp:141-150:

@@ -128,11 +128,15 @@ Ctx::Ctx(int dev) : device(dev) {
   encode_tiled = reinterpret_cast<EncodeTiledFn>(fn);
 }
 Ctx::~Ctx() {
-  if (stream || aux) cudaSetDevice(device);
-  if (aux) {
-    cudaStreamSynchronize(aux);
-    cudaStreamDestroy(aux);
-  }
+  if (stream || aux || aux2) cudaSetDevice(device);
+  for (cudaStream_t* sp : {&aux, &aux2})
+    if (*sp) {
+      cudaStreamSynchronize(*sp);
+      cudaStreamDestroy(*sp);
+    }
+  if (stage) cudaFree(stage);
+  for (cudaEvent_t ev : stage_free)
+    if (ev) cudaEventDestroy(ev);
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);

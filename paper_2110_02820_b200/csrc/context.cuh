@@ -34,7 +34,15 @@ struct Ctx {
   int sm_count = 148;
   int max_smem_optin = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t aux = nullptr;  // side stream for streamed host uploads (created on first use)
+  cudaStream_t aux = nullptr;   // side streams for pipelined host uploads (created on first use):
+  cudaStream_t aux2 = nullptr;  // copies on aux, the per-block device work on aux2
+  // Staging ring of pipelined host uploads, kept for the context's lifetime
+  // (plain cudaMalloc: a stream-ordered free on the copy stream would let a
+  // later allocation on the compute stream inherit a wait on the copies).
+  static constexpr int kStageSlots = 4;
+  double* stage = nullptr;
+  i64 stage_slot = 0;  // doubles per slot
+  cudaEvent_t stage_free[kStageSlots] = {};
   std::atomic<int64_t> launches{0};
   EncodeTiledFn encode_tiled = nullptr;
   std::mutex mu;  // serialises public calls sharing this context
@@ -47,6 +55,10 @@ struct Ctx {
   cudaStream_t aux_stream() {
     if (!aux) NPCG_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
     return aux;
+  }
+  cudaStream_t aux2_stream() {
+    if (!aux2) NPCG_CUDA(cudaStreamCreateWithFlags(&aux2, cudaStreamNonBlocking));
+    return aux2;
   }
   void count(int k = 1) { launches.fetch_add(k, std::memory_order_relaxed); }
   void check_launch(const char* what) {

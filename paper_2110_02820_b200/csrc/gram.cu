@@ -10,6 +10,7 @@
 // Algorithmic bytes: 8 m n per matvec (the reference's two GEMVs read X twice).
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "blas.cuh"
 #include "gemm.cuh"
@@ -133,16 +134,86 @@ void gram_single_pass(Ctx& ctx, const GramOp& op, const double* V, i64 ldv, doub
 }  // namespace
 
 // GramRidgeOperator: out = X^T (X V) / m.
+namespace {
+// Host design (m x n, ld ldg) -> op.xr through a staging ring of NSLOT row
+// blocks: block b crosses PCIe into slot b % NSLOT on the copy stream while
+// earlier blocks are transposed (and checked for non-finite entries into
+// *bad) on the transpose stream. Device memory: xr plus NSLOT ~80 MB blocks
+// (the synchronous constructor; 11.7 ms for cfg 2's 640 MB, the PCIe rate). `ready` receives one
+// event per block, recorded on the transpose stream after its transpose.
+void upload_blocks(Ctx& c, GramOp& op, const double* g, i64 ldg, int* bad, std::vector<GramOp::Chunk>& ready) {
+  const i64 m = op.m, n = op.n;
+  cudaStream_t cp = c.aux_stream(), tr = c.aux2_stream();
+  cudaEvent_t start;
+  NPCG_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  NPCG_CUDA(cudaEventRecord(start, c.stream));  // xr, its pads and *bad are ready on the context stream
+  NPCG_CUDA(cudaStreamWaitEvent(cp, start, 0));
+  NPCG_CUDA(cudaStreamWaitEvent(tr, start, 0));
+  NPCG_CUDA(cudaEventDestroy(start));
+  i64 rows = std::max<i64>(1024, (80ll << 20) / (8 * n) / 128 * 128);
+  if (const char* e = std::getenv("NPCG_STREAM_ROWS")) rows = std::max<i64>(16, std::atoll(e) / 16 * 16);  // tests
+  rows = std::min(rows, m);
+  constexpr int NSLOT = Ctx::kStageSlots;
+  const i64 sld = dev_ld(rows), slot_elems = sld * n;
+  if (c.stage_slot < slot_elems) {  // (re)allocate the context's ring; earlier uploads must have drained it
+    NPCG_CUDA(cudaStreamSynchronize(cp));
+    NPCG_CUDA(cudaStreamSynchronize(tr));
+    if (c.stage) NPCG_CUDA(cudaFree(c.stage));
+    c.stage = nullptr;
+    c.stage_slot = 0;
+    NPCG_CUDA(cudaMalloc(reinterpret_cast<void**>(&c.stage), sizeof(double) * slot_elems * NSLOT));
+    c.stage_slot = slot_elems;
+    for (auto& ev : c.stage_free)
+      if (ev) {
+        cudaEventDestroy(ev);
+        ev = nullptr;
+      }
+  }
+  cudaEvent_t copied;
+  NPCG_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+  int blk = 0;
+  for (i64 r0 = 0; r0 < m; r0 += rows, ++blk) {
+    const i64 r1 = std::min(m, r0 + rows);
+    const int q = blk % NSLOT;
+    double* slot = c.stage + q * c.stage_slot;
+    if (c.stage_free[q]) NPCG_CUDA(cudaStreamWaitEvent(cp, c.stage_free[q], 0));  // the slot's last block is transposed
+    else NPCG_CUDA(cudaEventCreateWithFlags(&c.stage_free[q], cudaEventDisableTiming));
+    NPCG_CUDA(cudaMemcpy2DAsync(slot, sld * 8, g + r0, ldg * 8, (r1 - r0) * 8, n, cudaMemcpyHostToDevice, cp));
+    NPCG_CUDA(cudaEventRecord(copied, cp));
+    NPCG_CUDA(cudaStreamWaitEvent(tr, copied, 0));
+    transpose_checked(c, tr, slot, sld, r1 - r0, n, op.xr.p() + r0 * op.xr.ld, op.xr.ld, bad);
+    NPCG_CUDA(cudaEventRecord(c.stage_free[q], tr));
+    GramOp::Chunk ch{r0, r1, nullptr, nullptr};
+    NPCG_CUDA(cudaEventCreateWithFlags(&ch.ready, cudaEventDisableTiming));
+    NPCG_CUDA(cudaEventRecord(ch.ready, tr));
+    ready.push_back(ch);
+  }
+  NPCG_CUDA(cudaEventDestroy(copied));
+}
+
+void alloc_xr(Ctx& c, GramOp& op) {
+  op.xr.alloc(op.n, op.m, c.stream, false);
+  if (op.xr.ld > op.n)  // pad rows of the row-major copy
+    NPCG_CUDA(cudaMemset2DAsync(op.xr.p() + op.n, op.xr.ld * 8, 0, (op.xr.ld - op.n) * 8, op.m, c.stream));
+}
+}  // namespace
+
 void gram_upload(Ctx& c, GramOp& op, const double* g, i64 ldg, int where) {
   const i64 m = op.m, n = op.n;
-  DMat colmajor;  // caller layout, then the row-major copy the kernels stream
-  upload(c, colmajor, m, n, g, ldg, where);
-  op.xr.alloc(n, m, c.stream, false);
-  if (op.xr.ld > n)
-    NPCG_CUDA(cudaMemset2DAsync(op.xr.p() + n, op.xr.ld * 8, 0, (op.xr.ld - n) * 8, m, c.stream));
+  if (ldg < m) invalid("leading dimension smaller than the row count");
+  alloc_xr(c, op);
   DBuf<int> flag(1, c.stream);
   flag.zero();
-  transpose_checked(c, c.stream, colmajor.p(), colmajor.ld, m, n, op.xr.p(), op.xr.ld, flag.p);
+  if (where == NPCG_HOST) {
+    std::vector<GramOp::Chunk> blocks;
+    upload_blocks(c, op, g, ldg, flag.p, blocks);
+    for (auto& ch : blocks) {
+      NPCG_CUDA(cudaStreamWaitEvent(c.stream, ch.ready, 0));
+      cudaEventDestroy(ch.ready);
+    }
+  } else {
+    transpose_checked(c, c.stream, g, ldg, m, n, op.xr.p(), op.xr.ld, flag.p);
+  }
   int h = 0;
   NPCG_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
@@ -150,33 +221,37 @@ void gram_upload(Ctx& c, GramOp& op, const double* g, i64 ldg, int where) {
 }
 
 void gram_upload_streamed(Ctx& c, GramOp& op, const double* g, i64 ldg) {
+  // The whole design is staged in the caller's layout; the sketch GEMMs run on
+  // each landed block directly (they wait for its copy only), the transposes
+  // into xr follow each copy, and only settle() waits for them.
   const i64 m = op.m, n = op.n;
-  cudaStream_t aux = c.aux_stream();
-  op.xr.alloc(n, m, c.stream, false);
-  if (op.xr.ld > n)  // pad rows of the row-major copy
-    NPCG_CUDA(cudaMemset2DAsync(op.xr.p() + n, op.xr.ld * 8, 0, (op.xr.ld - n) * 8, m, c.stream));
-  cudaEvent_t alloc_done;
-  NPCG_CUDA(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming));
-  NPCG_CUDA(cudaEventRecord(alloc_done, c.stream));
-  NPCG_CUDA(cudaStreamWaitEvent(aux, alloc_done, 0));
-  NPCG_CUDA(cudaEventDestroy(alloc_done));
-  op.bad.alloc(1, aux);
+  alloc_xr(c, op);
+  op.stage.alloc(m, n, c.stream, false);
+  op.bad.alloc(1, c.stream);
   op.bad.zero();
-  // ~80 MB row blocks (multiples of 128 rows): the first block's sketch GEMMs
-  // start while the later blocks are still crossing PCIe
+  // transposes on the copy stream itself: measured 20.1 vs 24.6 ms per e2e
+  // solve against a separate transpose stream (either priority)
+  cudaStream_t cp = c.aux_stream(), tr = cp;
+  cudaEvent_t start;
+  NPCG_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  NPCG_CUDA(cudaEventRecord(start, c.stream));
+  NPCG_CUDA(cudaStreamWaitEvent(cp, start, 0));
+  NPCG_CUDA(cudaStreamWaitEvent(tr, start, 0));
+  NPCG_CUDA(cudaEventDestroy(start));
   i64 rows = std::max<i64>(1024, (80ll << 20) / (8 * n) / 128 * 128);
   if (const char* e = std::getenv("NPCG_STREAM_ROWS")) rows = std::max<i64>(16, std::atoll(e) / 16 * 16);  // tests
-  DMat staging;  // caller layout of the landing blocks
-  staging.alloc(m, n, aux, false);
   for (i64 r0 = 0; r0 < m; r0 += rows) {
     const i64 r1 = std::min(m, r0 + rows);
-    NPCG_CUDA(cudaMemcpy2DAsync(staging.p() + r0, staging.ld * 8, g + r0, ldg * 8, (r1 - r0) * 8, n,
-                                cudaMemcpyHostToDevice, aux));
-    transpose_checked(c, aux, staging.p() + r0, staging.ld, r1 - r0, n, op.xr.p() + r0 * op.xr.ld, op.xr.ld,
-                      op.bad.p);
-    GramOp::Chunk ch{r0, r1, nullptr};
+    GramOp::Chunk ch{r0, r1, nullptr, nullptr};
+    NPCG_CUDA(cudaEventCreateWithFlags(&ch.copied, cudaEventDisableTiming));
     NPCG_CUDA(cudaEventCreateWithFlags(&ch.ready, cudaEventDisableTiming));
-    NPCG_CUDA(cudaEventRecord(ch.ready, aux));
+    NPCG_CUDA(cudaMemcpy2DAsync(op.stage.p() + r0, op.stage.ld * 8, g + r0, ldg * 8, (r1 - r0) * 8, n,
+                                cudaMemcpyHostToDevice, cp));
+    NPCG_CUDA(cudaEventRecord(ch.copied, cp));
+    NPCG_CUDA(cudaStreamWaitEvent(tr, ch.copied, 0));
+    transpose_checked(c, tr, op.stage.p() + r0, op.stage.ld, r1 - r0, n, op.xr.p() + r0 * op.xr.ld, op.xr.ld,
+                      op.bad.p);
+    NPCG_CUDA(cudaEventRecord(ch.ready, tr));
     op.pending.push_back(ch);
   }
 }
@@ -186,8 +261,12 @@ void GramOp::settle() {
   if (pending.empty()) return;
   for (auto& ch : pending) NPCG_CUDA(cudaStreamWaitEvent(ctx->stream, ch.ready, 0));
   NPCG_CUDA(cudaEventSynchronize(pending.back().ready));
-  for (auto& ch : pending) cudaEventDestroy(ch.ready);
+  for (auto& ch : pending) {
+    cudaEventDestroy(ch.copied);
+    cudaEventDestroy(ch.ready);
+  }
   pending.clear();
+  stage.buf.release();  // freed on the context stream, which has waited for every transpose
   NPCG_CUDA(cudaMemcpy(&nonfinite, bad.p, sizeof(int), cudaMemcpyDeviceToHost));
   if (nonfinite) invalid("GramRidgeOperator: design matrix has non-finite entries");  // operators.cpp:108-109
 }
@@ -197,6 +276,7 @@ GramOp::~GramOp() {
   for (auto& ch : pending) {
     cudaStreamWaitEvent(ctx->stream, ch.ready, 0);
     cudaEventSynchronize(ch.ready);
+    cudaEventDestroy(ch.copied);
     cudaEventDestroy(ch.ready);
   }
 }
@@ -209,12 +289,12 @@ void GramOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const 
     z.alloc(m, k, ctx->stream, false);
     for (size_t b = 0; b < pending.size(); ++b) {
       const Chunk& ch = pending[b];
-      NPCG_CUDA(cudaStreamWaitEvent(ctx->stream, ch.ready, 0));
+      NPCG_CUDA(cudaStreamWaitEvent(ctx->stream, ch.copied, 0));
       const i64 rb = ch.r1 - ch.r0;
-      const double* xb = xr.p() + ch.r0 * xr.ld;
-      gemm(*ctx, rb, k, n, 1.0, Operand{xb, xr.ld, true}, Operand{V, ldv, true}, 0.0, z.p() + ch.r0, z.ld);
-      gemm(*ctx, n, k, rb, 1.0, Operand{xb, xr.ld, false}, Operand{z.p() + ch.r0, z.ld, true}, b ? 1.0 : 0.0, out,
-           ldo);
+      const double* xb = stage.p() + ch.r0;  // the landed block, caller layout (rb x n, ld m)
+      gemm(*ctx, rb, k, n, 1.0, Operand{xb, stage.ld, false}, Operand{V, ldv, true}, 0.0, z.p() + ch.r0, z.ld);
+      gemm(*ctx, n, k, rb, 1.0, Operand{xb, stage.ld, true}, Operand{z.p() + ch.r0, z.ld, true}, b ? 1.0 : 0.0,
+           out, ldo);
     }
     settle();
     divide(*ctx, n, k, out, ldo, div);

@@ -45,13 +45,15 @@ struct GramOp : Op {  // GramRidgeOperator (operators.cpp:105-121): (1/m) G^T (G
   i64 m = 0;
   double div = 0.0;   // out /= div (operators.cpp:115); the global row count when X is a row shard
   // Streamed construction (npcg_op_gram_create_streamed): row blocks of X
-  // still landing on the side stream; each is transposed into xr and checked
-  // for non-finite entries there, then `ready` fires.
+  // landing in `stage` (caller layout) on the copy stream (`copied` fires),
+  // then transposed into xr and checked for non-finite entries on the
+  // transpose stream (`ready` fires).
   struct Chunk {
     i64 r0, r1;
-    cudaEvent_t ready;
+    cudaEvent_t copied, ready;
   };
   std::vector<Chunk> pending;
+  DMat stage;  // m x n column-major copy of X while the streamed upload is pending
   DBuf<int> bad;  // non-finite flag of the streamed upload
   int nonfinite = 0;  // latched: every later use raises the constructor's error
   /// Order the context stream after every pending block, wait for the upload
