@@ -757,6 +757,123 @@ __global__ void __launch_bounds__(256) wy_apply_kernel(const double* __restrict_
     for (int i = lane; i < n; i += 32) Z[i + static_cast<i64>(col) * ldz] = z[i];
 }
 
+// The same back-transformation on the FP64 tensor pipe: CTA = 8 columns of Z
+// in shared memory; per block, W = V_b^T Z_t (k split over the 8 warps,
+// partials summed in fixed order), W' = T_b W, Z_t -= V_b W' (m-tiles over
+// the warps), all products mma.sync.m8n8k4.f64. V_b is read from L2 once per
+// CTA and block; shared rows padded to 33 doubles (conflict-free fragments).
+constexpr int WYC = 8;
+constexpr int VS = WY + 1;
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(256) wy_apply_dmma_kernel(const double* __restrict__ H, i64 ldh,
+                                                            const double* __restrict__ T, int nref, int n, double* Z,
+                                                            i64 ldz) {
+  extern __shared__ double wsm2[];
+  const int np = (n + 7) & ~7;
+  double* zt = wsm2;                             // [np][WYC]
+  double* vb = zt + static_cast<i64>(np) * WYC;  // [np][VS]
+  double* tb = vb + static_cast<i64>(np) * VS;   // [WY][WY] col-major
+  double* wpart = tb + WY * WY;                  // [8][WY][WYC]
+  double* wsh = wpart + 8 * WY * WYC;            // [WY][WYC]
+  double* wq = wsh + WY * WYC;                   // [WY][WYC]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int col0 = blockIdx.x * WYC;
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
+  for (int idx = tid; idx < np * WYC; idx += 256) {
+    const int i = idx / WYC, j = idx % WYC;
+    zt[idx] = (i < n && col0 + j < n) ? Z[i + static_cast<i64>(col0 + j) * ldz] : 0.0;
+  }
+  const int nblk = (nref + WY - 1) / WY;
+  const int ksteps = np / 4;
+  const int kw0 = warp * ksteps / 8, kw1 = (warp + 1) * ksteps / 8;
+  // V_b is prefetched into registers (thread: reflector tid / 8, rows tid % 8 + 8u)
+  // while the previous block computes
+  constexpr int NPRE = 64;  // np <= 512
+  double pre[NPRE], tpre[WY * WY / 256];
+  const int pc = tid >> 3, pr0 = tid & 7;
+  auto issue = [&](int b) {
+    const int k0 = b * WY, kb = min(WY, nref - k0);
+#pragma unroll
+    for (int u = 0; u < NPRE; ++u) {
+      const int i = pr0 + 8 * u;
+      pre[u] = (i < n && pc < kb) ? H[i + static_cast<i64>(k0 + pc) * ldh] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < WY * WY / 256; ++u) tpre[u] = T[static_cast<i64>(b) * WY * WY + tid + 256 * u];
+  };
+  issue(nblk - 1);
+  for (int b = nblk - 1; b >= 0; --b) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < NPRE; ++u)
+      if (pr0 + 8 * u < np) vb[(pr0 + 8 * u) * VS + pc] = pre[u];
+#pragma unroll
+    for (int u = 0; u < WY * WY / 256; ++u) tb[tid + 256 * u] = tpre[u];
+    __syncthreads();
+    if (b > 0) issue(b - 1);
+    // W = V_b^T Z_t: 4 m-tiles (reflectors) x 1 n-tile (columns), this warp's k-range
+    double c[4][2] = {};
+    for (int ks = kw0; ks < kw1; ++ks) {
+      const int kr = ks * 4 + fk;
+      const double bf = zt[kr * WYC + fr];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) dmma884(c[m][0], c[m][1], vb[kr * VS + m * 8 + fr], bf);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) wpart[(warp * WY + m * 8 + fr) * WYC + 2 * fk + e] = c[m][e];
+    __syncthreads();
+    {
+      const int r = tid / WYC, j = tid % WYC;
+      double sacc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc += wpart[(w * WY + r) * WYC + j];  // fixed order
+      wsh[r * WYC + j] = sacc;
+    }
+    __syncthreads();
+    {
+      const int r = tid / WYC, j = tid % WYC;  // W' = T W, T upper triangular
+      double sacc = 0.0;
+#pragma unroll
+      for (int k = 0; k < WY; ++k) sacc += k >= r ? tb[r + k * WY] * wsh[k * WYC + j] : 0.0;
+      wq[r * WYC + j] = sacc;
+    }
+    __syncthreads();
+    // Z_t -= V_b W': m-tiles of 8 rows over the warps, K = 32 (8 k-steps)
+    double bq[WY / 4];  // W' fragments, shared by every m-tile of the warp
+#pragma unroll
+    for (int ks = 0; ks < WY / 4; ++ks) bq[ks] = wq[(ks * 4 + fk) * WYC + fr];
+    for (int mt = warp; mt < np / 8; mt += 16) {  // two m-tiles per pass: independent chains
+      const int mt2 = mt + 8;
+      const bool two = mt2 < np / 8;
+      const int row = mt * 8 + fr, row2 = mt2 * 8 + fr;
+      double c0 = zt[row * WYC + 2 * fk], c1 = zt[row * WYC + 2 * fk + 1];
+      double d0 = two ? zt[row2 * WYC + 2 * fk] : 0.0, d1 = two ? zt[row2 * WYC + 2 * fk + 1] : 0.0;
+#pragma unroll
+      for (int ks = 0; ks < WY / 4; ++ks) {
+        dmma884(c0, c1, -vb[row * VS + ks * 4 + fk], bq[ks]);
+        if (two) dmma884(d0, d1, -vb[row2 * VS + ks * 4 + fk], bq[ks]);
+      }
+      zt[row * WYC + 2 * fk] = c0;
+      zt[row * WYC + 2 * fk + 1] = c1;
+      if (two) {
+        zt[row2 * WYC + 2 * fk] = d0;
+        zt[row2 * WYC + 2 * fk + 1] = d1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * WYC; idx += 256) {
+    const int j = idx / n, i = idx % n;
+    if (col0 + j < n) Z[i + static_cast<i64>(col0 + j) * ldz] = zt[i * WYC + j];
+  }
+}
+
 }  // namespace
 
 void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
@@ -877,10 +994,20 @@ void sym_eigvecs(Ctx& ctx, double* M, i64 ldm, i64 n, double* Z, i64 ldz) {
     gemm(ctx, n, n, n, 1.0, Operand{H.p(), H.ld, true}, Operand{H.p(), H.ld, true}, 0.0, S.p(), S.ld);
     DBuf<double> Tw(static_cast<i64>(nblk) * WY * WY, ctx.stream);
     NPCG_LAUNCH(ctx, wy_t_kernel, static_cast<unsigned>(nblk), 32, 0, S.p(), S.ld, tau.p, nref, Tw.p);
-    const int smem = static_cast<int>((static_cast<i64>(WY + 8) * n + WY * WY) * 8);
-    NPCG_CUDA(cudaFuncSetAttribute(wy_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    NPCG_LAUNCH(ctx, wy_apply_kernel, static_cast<unsigned>(cdiv(n, 8)), 256, smem, H.p(), H.ld, Tw.p, nref, nn, Z,
-                ldz);
+    const i64 np = round_up(n, 8);
+    const i64 smem2 = (np * (WYC + VS) + WY * WY + 10 * WY * WYC) * 8;  // (np <= 512: the register prefetch)
+    static const bool no_dmma = std::getenv("NPCG_WY") && std::string(std::getenv("NPCG_WY")) == "fma";  // diagnostics
+    if (np <= 512 && smem2 <= 220 * 1024 && !no_dmma) {
+      NPCG_CUDA(cudaFuncSetAttribute(wy_apply_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem2)));
+      NPCG_LAUNCH(ctx, wy_apply_dmma_kernel, static_cast<unsigned>(cdiv(n, WYC)), 256, static_cast<int>(smem2), H.p(),
+                  H.ld, Tw.p, nref, nn, Z, ldz);
+    } else {
+      const int smem = static_cast<int>((static_cast<i64>(WY + 8) * n + WY * WY) * 8);
+      NPCG_CUDA(cudaFuncSetAttribute(wy_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      NPCG_LAUNCH(ctx, wy_apply_kernel, static_cast<unsigned>(cdiv(n, 8)), 256, smem, H.p(), H.ld, Tw.p, nref, nn,
+                  Z, ldz);
+    }
   } else {
     NPCG_LAUNCH(ctx, backtransform_kernel, static_cast<unsigned>(cdiv(n * 32, 256)), 256, 0, H.p(), H.ld, tau.p, nn,
                 Z, ldz);
