@@ -11,6 +11,8 @@
 #include <cstdlib>
 #include <string>
 
+#include <cmath>
+#include <mutex>
 #include "blas.cuh"
 #include "gemm.cuh"
 #include "ops.cuh"
@@ -195,6 +197,34 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   return p * s1 * s2;
 }
 
+// Table-driven exp for the fused kernel (fewer FP64-pipe operations, which the
+// epilogue shares with the DMMA dot products): x = (1024 m + j) ln2/1024 + r,
+// |r| <= ln2/2048, exp(x) = 2^m * 2^(j/1024) * p(r) with p the degree-4
+// Taylor polynomial (truncation < 4e-20 relative), 2^(j/1024) from a
+// 1024-entry shared-memory table (correctly rounded, built on the host) and
+// 2^m added to the exponent field with integer instructions. x is clamped at
+// -707 (exp = 9e-308, the result stays normal): entries that small are
+// negligible next to K_ii = 1. About 1.5 ulp.
+constexpr int KF_TAB = 1024;
+__device__ double kf_exp2_tab_g[KF_TAB];
+__device__ __forceinline__ double exp_tab(double x, const double* __restrict__ tab) {
+  x = fmax(x, -707.0);
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52: the low mantissa bits of t hold rint(x 1024/ln2)
+  const double t = fma(x, 1477.3197218702985, magic);
+  const double kd = t - magic;
+  const int ki = __double2loint(t);
+  double r = fma(kd, -6.769015433292225e-04, x);  // ln2/1024 split in two (hi has 21 trailing zero bits)
+  r = fma(kd, -1.8634911418658083e-13, r);
+  double p = 1.0 / 24.0;
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double v = tab[ki & (KF_TAB - 1)] * p;  // in [0.9996, 2)
+  const int m = ki >> 10;                         // floor(ki / 1024), in [-1021, 0]
+  return __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
+}
+
 template <int S>
 __global__ void __launch_bounds__(KF_THREADS, 2)
     kfree_fused_kernel(const double* __restrict__ pts, i64 ldp, i64 n, int d, int dp,
@@ -209,6 +239,7 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
   double* NJ = XJ + 2 * KF_BN * lds;                  // [2][KF_BN]
   double* VJ = NJ + 2 * KF_BN;                        // [2][S][KF_BN]
   double* RED = VJ + 2 * S * KF_BN;                   // [KF_WN][KF_BM][S]
+  double* TAB = RED + KF_WN * KF_BM * S;              // [KF_TAB] 2^(j/KF_TAB)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3, wm = warp / KF_WN, wn = warp % KF_WN;  // 4 x KF_WN warps
   const i64 i0 = static_cast<i64>(blockIdx.x) * KF_BM;
@@ -233,6 +264,7 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
     const int r = idx % KF_BM, k = idx / KF_BM;
     XI[r * lds + k] = (i0 + r < n && k < d) ? pts[(i0 + r) + static_cast<i64>(k) * ldp] : 0.0;
   }
+  for (int idx = tid; idx < KF_TAB; idx += KF_THREADS) TAB[idx] = kf_exp2_tab_g[idx];
   double ni[4];
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
@@ -288,7 +320,7 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
           double sq = -2.0 * acc[f][q][e] + ni[f];
           sq = sq + nj;
           const bool diag = i0 + wm * 32 + f * 8 + g == j0 + col;
-          const double ex = exp_nonpos(fmax(sq, 0.0) * c);  // unconditional: no per-element branch
+          const double ex = exp_tab(fmax(sq, 0.0) * c, TAB);  // unconditional: no per-element branch
           const double kij = diag ? 1.0 : ex;
 #pragma unroll
           for (int s = 0; s < S; ++s) racc[f][s] += kij * vj[s];
@@ -333,8 +365,15 @@ __global__ void kfree_reduce_kernel(const double* __restrict__ partial, int spli
 template <int S>
 void kfree_fused(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, double* out, i64 ldo, const int* gate) {
   const int d = static_cast<int>(op.d), dp = (d + 3) / 4 * 4;
-  const i64 smem = ((KF_BM + 2 * KF_BN) * static_cast<i64>(dp + 1) + 2 * KF_BN + 2 * S * KF_BN + KF_WN * KF_BM * S) * 8;
+  const i64 smem =
+      ((KF_BM + 2 * KF_BN) * static_cast<i64>(dp + 1) + 2 * KF_BN + 2 * S * KF_BN + KF_WN * KF_BM * S + KF_TAB) * 8;
   static bool attr = false;
+  static std::once_flag tab_once;
+  std::call_once(tab_once, [] {
+    double h[KF_TAB];
+    for (int j = 0; j < KF_TAB; ++j) h[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / KF_TAB));
+    NPCG_CUDA(cudaMemcpyToSymbol(kf_exp2_tab_g, h, sizeof(h)));
+  });
   if (!attr) {
     NPCG_CUDA(cudaFuncSetAttribute(kfree_fused_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
