@@ -167,36 +167,6 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Branch-free exp for x <= 0 (the kernel exponent c * max(s, 0), c < 0):
-// Cody-Waite reduction x = k ln2 + r, |r| <= ln2/2, degree-12 Taylor
-// polynomial, 2^k applied as two exact power-of-two factors (so k down to the
-// subnormal range is exact). About 1 ulp like CUDA's exp(), but without its
-// slow-path branch, so a warp's 16 to 32 exps per tile interleave freely.
-__device__ __forceinline__ double exp_nonpos(double x) {
-  x = fmax(x, -745.2);  // exp(-745.2) rounds to 0
-  const double kd = rint(x * 1.4426950408889634);
-  double r = fma(kd, -6.93147180369123816490e-01, x);
-  r = fma(kd, -1.90821492927058770002e-10, r);
-  double p = 1.0 / 479001600.0;  // 1/12!
-  p = fma(p, r, 1.0 / 39916800.0);
-  p = fma(p, r, 1.0 / 3628800.0);
-  p = fma(p, r, 1.0 / 362880.0);
-  p = fma(p, r, 1.0 / 40320.0);
-  p = fma(p, r, 1.0 / 5040.0);
-  p = fma(p, r, 1.0 / 720.0);
-  p = fma(p, r, 1.0 / 120.0);
-  p = fma(p, r, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  const int k = static_cast<int>(kd);
-  const int k1 = k / 2, k2 = k - k1;  // each in [-538, 0]: normal powers of two
-  const double s1 = __longlong_as_double(static_cast<long long>(k1 + 1023) << 52);
-  const double s2 = __longlong_as_double(static_cast<long long>(k2 + 1023) << 52);
-  return p * s1 * s2;
-}
-
 // Table-driven exp for the fused kernel (fewer FP64-pipe operations, which the
 // epilogue shares with the DMMA dot products): x = (1024 m + j) ln2/1024 + r,
 // |r| <= ln2/2048, exp(x) = 2^m * 2^(j/1024) * p(r) with p the degree-4
