@@ -248,6 +248,12 @@ constexpr int PV = 4;    // double2 slots per thread in the gram row pass: n <= 
 constexpr int PW = 2 * PT * PV;
 constexpr int NST = 6;   // shared-memory ring stages of one PW-double segment (a row of X / a column segment of A)
 constexpr int RING_BYTES = NST * PW * 8;
+// dense path: row-block width per CTA (3-4 right-hand sides use half-width
+// blocks: 2 double2 slots per thread keep the accumulators in registers) and
+// ring depth (the same bytes in flight)
+constexpr int dense_pv(int S) { return S >= 3 ? 2 : PV; }
+constexpr int dense_pw(int S) { return 2 * PT * dense_pv(S); }
+constexpr int dense_nst(int S) { return RING_BYTES / (dense_pw(S) * 8); }
 
 struct PersistArgs {
   i64 n, m;
@@ -281,26 +287,27 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   __shared__ double wred[4 * S * (PT / 32)];  // P4: per-warp partials of up to 4 x S dots
   __shared__ ColState cs[S];
   __shared__ int running_sh;
-  __shared__ uint64_t full_bar[NST];
-  extern __shared__ __align__(128) double ring[];  // NST x PW doubles, fed by bulk copies (TMA)
+  constexpr int DPV = GRAM ? PV : dense_pv(S), DPW = 2 * PT * DPV, DNST = GRAM ? NST : dense_nst(S);
+  __shared__ uint64_t full_bar[DNST];
+  extern __shared__ __align__(128) double ring[];  // DNST x DPW doubles, fed by bulk copies (TMA)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t ring_head = 0, ring_tail = 0;  // segments consumed (all threads) / issued (thread 0)
   if (tid == 0) {
-    for (int q = 0; q < NST; ++q) mbarrier_init(&full_bar[q], 1);
+    for (int q = 0; q < DNST; ++q) mbarrier_init(&full_bar[q], 1);
     mbarrier_fence_init();
   }
   auto ring_issue = [&](const double* src, i64 count) {  // thread 0 only
-    const int slot = static_cast<int>(ring_tail % NST);
+    const int slot = static_cast<int>(ring_tail % DNST);
     const uint32_t bytes = static_cast<uint32_t>(round_up(count, 2) * 8);
     mbarrier_expect_tx(&full_bar[slot], bytes);
-    bulk_copy_g2s(ring + static_cast<i64>(slot) * PW, src, bytes, &full_bar[slot]);
+    bulk_copy_g2s(ring + static_cast<i64>(slot) * DPW, src, bytes, &full_bar[slot]);
     ++ring_tail;
   };
   auto ring_wait = [&]() -> const double* {  // next segment, in issue order
-    const int slot = static_cast<int>(ring_head % NST);
-    mbarrier_wait_parity(&full_bar[slot], (ring_head / NST) & 1u);
+    const int slot = static_cast<int>(ring_head % DNST);
+    mbarrier_wait_parity(&full_bar[slot], (ring_head / DNST) & 1u);
     ++ring_head;
-    return ring + static_cast<i64>(slot) * PW;
+    return ring + static_cast<i64>(slot) * DPW;
   };
   const int G = gridDim.x, c = blockIdx.x;
   const i64 n = a.n;
@@ -461,25 +468,25 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         tick(t, 3);
       } else {
         // dense: v = A p_t streamed column by column (axpy form, A col-major):
-        // CTA (rb, cb) owns rows [rb*PW, +PW) x columns [cb*cpb, +cpb); each
+        // CTA (rb, cb) owns rows [rb*DPW, +DPW) x columns [cb*cpb, +cpb); each
         // column segment is one contiguous bulk copy into the shared-memory
-        // ring (NST segments in flight); two columns per step, one block
+        // ring (DNST segments in flight); two columns per step, one block
         // barrier per step frees their slots. partial_cb = A[rows, cols_cb] p_t[cols_cb].
         const int nrb = static_cast<int>(a.nrb), ncb = static_cast<int>(a.ncb);
         if (c < nrb * ncb) {
           const int rb = c % nrb, cb = c / nrb;
-          const i64 rb0 = static_cast<i64>(rb) * PW, cnt = min(static_cast<i64>(PW), n - rb0);
+          const i64 rb0 = static_cast<i64>(rb) * DPW, cnt = min(static_cast<i64>(DPW), n - rb0);
           const i64 cb0 = static_cast<i64>(cb) * a.cpb, cb1 = min(n, cb0 + a.cpb);
-          double2 acc[S][PV];
-          bool ok[PV];
+          double2 acc[S][DPV];
+          bool ok[DPV];
 #pragma unroll
-          for (int k = 0; k < PV; ++k) {
+          for (int k = 0; k < DPV; ++k) {
             ok[k] = 2 * (tid + static_cast<i64>(PT) * k) < cnt;
 #pragma unroll
             for (int s = 0; s < S; ++s) acc[s][k] = make_double2(0.0, 0.0);
           }
           if (tid == 0)
-            for (i64 j = cb0; j < min(cb1, cb0 + NST); ++j) ring_issue(a.A + j * a.lda + rb0, cnt);
+            for (i64 j = cb0; j < min(cb1, cb0 + DNST); ++j) ring_issue(a.A + j * a.lda + rb0, cnt);
           // p_t of the whole vector is in pcur (slice owners wrote it before the barrier)
           auto load_p = [&](i64 j, double* dst) {
 #pragma unroll
@@ -492,22 +499,22 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             load_p(j + 1, q1);
             const double* s0 = ring_wait();
             const double* s1 = two ? ring_wait() : nullptr;
-            double2 c0[PV], c1[PV];
+            double2 c0[DPV], c1[DPV];
 #pragma unroll
-            for (int k = 0; k < PV; ++k) {
+            for (int k = 0; k < DPV; ++k) {
               c0[k] = ok[k] ? reinterpret_cast<const double2*>(s0)[tid + PT * k] : make_double2(0.0, 0.0);
               c1[k] = (ok[k] && two) ? reinterpret_cast<const double2*>(s1)[tid + PT * k] : make_double2(0.0, 0.0);
             }
             __syncthreads();  // every thread holds its values: the two slots may be refilled
             if (tid == 0) {
-              if (j + NST < cb1) ring_issue(a.A + (j + NST) * a.lda + rb0, cnt);
-              if (j + NST + 1 < cb1) ring_issue(a.A + (j + NST + 1) * a.lda + rb0, cnt);
+              if (j + DNST < cb1) ring_issue(a.A + (j + DNST) * a.lda + rb0, cnt);
+              if (j + DNST + 1 < cb1) ring_issue(a.A + (j + DNST + 1) * a.lda + rb0, cnt);
             }
 #pragma unroll
             for (int s = 0; s < S; ++s) {
               const double p0 = q0[s], p1 = q1[s];
 #pragma unroll
-              for (int k = 0; k < PV; ++k) {
+              for (int k = 0; k < DPV; ++k) {
                 acc[s][k].x += c0[k].x * p0;
                 acc[s][k].y += c0[k].y * p0;
                 acc[s][k].x += c1[k].x * p1;
@@ -519,7 +526,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
           for (int s = 0; s < S; ++s) {
             double* dst = a.part + (static_cast<i64>(cb) * S + s) * a.pstride + rb0;
 #pragma unroll
-            for (int k = 0; k < PV; ++k) {
+            for (int k = 0; k < DPV; ++k) {
               const i64 i = 2 * (tid + static_cast<i64>(PT) * k);
               if (i + 1 < cnt) {
                 reinterpret_cast<double2*>(dst)[tid + PT * k] = acc[s][k];
@@ -717,7 +724,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
 bool persistent_eligible(const Ctx& ctx, Op& op, i64 S) {
   (void)ctx;
   if (auto* g = dynamic_cast<GramOp*>(&op)) return S == 1 && g->n <= PW && g->m >= 1;
-  if (dynamic_cast<DenseOp*>(&op)) return S <= 4 && cdiv(op.n, PW) <= ctx.sm_count;
+  if (dynamic_cast<DenseOp*>(&op)) return S <= 4 && cdiv(op.n, dense_pw(static_cast<int>(S))) <= ctx.sm_count;
   return false;
 }
 
@@ -760,7 +767,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   if (gram) part.alloc(static_cast<i64>(G) * PW, ctx.stream);
   i64 nrb = 0, ncb = 0, cpb = 0, pstride = 0;
   if (dense) {
-    nrb = cdiv(n, PW);
+    nrb = cdiv(n, dense_pw(static_cast<int>(S)));
     ncb = std::max<i64>(1, G / nrb);
     cpb = cdiv(n, ncb);
     ncb = cdiv(n, cpb);
