@@ -10,7 +10,7 @@ import bench
 npcg.workloads = workloads
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 50000
 ctx = npcg.Context(0)
-w = workloads.make('cfg5', npcg.Rng, npcg.splitmix64, n=n, r=500, ell=100, nrhs=4, nmu=1)
+w = workloads.make('cfg5', npcg.Rng, npcg.splitmix64, n=n, r=500, ell=100, nrhs=4, nmu=2)
 path = bench.DevicePath(npcg, torch, w, ctx)
 L = npcg.lib(); vp = C.c_void_p; i64 = C.c_int64
 for s in (1, 2, 4):
