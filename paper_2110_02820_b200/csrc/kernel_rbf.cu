@@ -375,6 +375,285 @@ void kfree_fused(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, dou
   ctx.prof_work(static_cast<double>(op.n) * op.n * (2.0 * dp + 2.0 * S), 8.0 * op.n * (d + 2 * S));
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric fused matrix-free K V (k <= 2). K is symmetric, so each 128 x 128
+// block K_IJ with I < J is computed once (DMMA dots + exp epilogue, as above)
+// and used twice: row sums out_I += K_IJ v_J and column sums out_J += K_IJ^T v_I
+// -- half the dot products and half the exps of the row-streaming kernel.
+// The upper-triangle block pairs (I <= J, row-major) are split into equal
+// contiguous ranges over a persistent grid; CTA p adds its contributions into
+// its own length-n partial P_p (no other CTA touches it), and out = sum_p P_p
+// in fixed p order afterwards, so the result is deterministic. A given entry of
+// P_p is always updated by the same thread (slot r*S + s for block row r), so
+// the fire-and-forget adds to it are ordered by program order. Column sums of
+// a 128 x 64 half tile: each thread folds its 4 rows, a transposed butterfly
+// over the 8 row lanes leaves one column per lane (7 adds for 8 columns), and
+// the 4 row warps are summed through shared memory. Diagonal blocks are
+// evaluated whole (rows only, K_ii = 1).
+// Column flush of half tile h of column block J: sum the 4 row warps in order.
+// Thread tid owns partial slot tid = (block row)*S + s, for rows and columns alike.
+template <int S>
+__device__ __forceinline__ void kf_col_flush(const double* CRED, int h, i64 J, i64 n, double* mypart, int tid) {
+  const int slot = tid - h * KF_BN * S;
+  if (slot < 0 || slot >= KF_BN * S) return;
+  const int cc = slot / S, s = slot % S;
+  const double* cr = CRED + ((h * 4) * KF_BN + cc) * S + s;
+  const double v = ((cr[0] + cr[KF_BN * S]) + cr[2 * KF_BN * S]) + cr[3 * KF_BN * S];
+  const i64 j = J * KF_BM + h * KF_BN + cc;
+  if (j < n) atomicAdd(mypart + s * n + j, v);
+}
+
+template <int S>
+__global__ void __launch_bounds__(KF_THREADS, 2)
+    kfree_sym_kernel(const double* __restrict__ pts, i64 ldp, i64 n, int d, int dp, const double* __restrict__ norms,
+                     double c, const double* __restrict__ V, i64 ldv, i64 npairs, double* __restrict__ part,
+                     const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
+  extern __shared__ double kfs[];
+  const int lds = dp + 1;
+  double* XI = kfs;                       // [128][lds]
+  double* XJ = XI + KF_BM * lds;          // [2][64][lds]
+  double* NJ = XJ + 2 * KF_BN * lds;      // [2][64]
+  double* VJ = NJ + 2 * KF_BN;            // [2][S][64]
+  double* CRED = VJ + 2 * S * KF_BN;      // [2][4][64][S] column partials per row warp
+  double* RRED = CRED + 2 * 4 * KF_BN * S;  // [2][128][S] row partials per column warp
+  double* TAB = RRED + 2 * KF_BM * S;     // [KF_TAB]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3, wm = warp / KF_WN, wn = warp % KF_WN;
+  const i64 nb = (n + KF_BM - 1) / KF_BM;
+  double* mypart = part + static_cast<i64>(blockIdx.x) * S * n;
+
+  const i64 u0 = npairs * blockIdx.x / gridDim.x, u1 = npairs * (blockIdx.x + 1) / gridDim.x;
+  if (u0 >= u1) return;
+  // pair u -> (I, J): rows I' < I hold I*nb - I(I-1)/2 pairs
+  auto row_off = [&](i64 I) { return I * nb - I * (I - 1) / 2; };
+  i64 lo = 0, hi = nb - 1;
+  while (lo < hi) {
+    const i64 mid = (lo + hi + 1) / 2;
+    if (row_off(mid) <= u0) lo = mid;
+    else hi = mid - 1;
+  }
+  for (int idx = tid; idx < KF_TAB; idx += KF_THREADS) TAB[idx] = kf_exp2_tab_g[idx];
+
+  auto load_half = [&](i64 j0, int buf) {
+    double* xj = XJ + buf * KF_BN * lds;
+    for (int idx = tid; idx < KF_BN * dp; idx += KF_THREADS) {
+      const int r = idx % KF_BN, k = idx / KF_BN;
+      const bool ok = j0 + r < n && k < d;
+      cp_async8(xj + r * lds + k, ok ? pts + (j0 + r) + static_cast<i64>(k) * ldp : pts, ok);
+    }
+    for (int r = tid; r < KF_BN; r += KF_THREADS) {
+      const bool ok = j0 + r < n;
+      cp_async8(NJ + buf * KF_BN + r, ok ? norms + j0 + r : norms, ok);
+#pragma unroll
+      for (int s = 0; s < S; ++s) cp_async8(VJ + (buf * S + s) * KF_BN + r, ok ? V + (j0 + r) + s * ldv : V, ok);
+    }
+    cp_async_commit();
+  };
+
+  // half tile ht of this CTA: pair (I, J), half h (columns J*128 + h*64 ..)
+  i64 I = lo, J = lo + (u0 - row_off(lo));
+  const i64 nht = 2 * (u1 - u0);
+  load_half(J * KF_BM, 0);
+  i64 curI = -1;
+  double ni[4], vi[4][S], racc[4][S];
+  i64 pJ = -1;  // previous half tile's column block (for its column flush), -1 = none
+  int ph = 0;
+  for (i64 ht = 0; ht < nht; ++ht) {
+    const int h = static_cast<int>(ht & 1), buf = h;
+    cp_async_wait_all();
+    __syncthreads();  // half tile resident; previous epilogue done (CRED / XI free)
+    // column flush of the previous half tile (off-diagonal): sum the 4 row warps in order
+    if (pJ >= 0) kf_col_flush<S>(CRED, ph, pJ, n, mypart, tid);
+    if (I != curI) {
+      if (curI >= 0) {  // row flush of the finished row block
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            double v = racc[f][s];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            if (t == 0) RRED[(wn * KF_BM + wm * 32 + f * 8 + g) * S + s] = v;
+          }
+        __syncthreads();
+        if (tid < KF_BM * S) {
+          const int r = tid / S, s = tid % S;
+          const i64 i = curI * KF_BM + r;
+          if (i < n) atomicAdd(mypart + s * n + i, RRED[r * S + s] + RRED[(KF_BM + r) * S + s]);
+        }
+      }
+      for (int idx = tid; idx < KF_BM * dp; idx += KF_THREADS) {
+        const int r = idx % KF_BM, k = idx / KF_BM;
+        const i64 i = I * KF_BM + r;
+        XI[r * lds + k] = (i < n && k < d) ? pts[i + static_cast<i64>(k) * ldp] : 0.0;
+      }
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const i64 i = I * KF_BM + wm * 32 + f * 8 + g;
+        ni[f] = i < n ? norms[i] : 0.0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          vi[f][s] = i < n ? V[i + s * ldv] : 0.0;
+          racc[f][s] = 0.0;
+        }
+      }
+      curI = I;
+      __syncthreads();
+    }
+    // next half tile
+    i64 nI = I, nJ = J;
+    if (h == 1) {
+      if (++nJ == nb) nJ = ++nI;
+    }
+    if (ht + 1 < nht) load_half(nJ * KF_BM + (1 - h) * KF_BN, buf ^ 1);
+
+    const double* xj = XJ + buf * KF_BN * lds;
+    double acc[4][4][2];
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[f][q][0] = acc[f][q][1] = 0.0;
+    for (int kk = 0; kk < dp; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) a[f] = XI[(wm * 32 + f * 8 + g) * lds + kk + t];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) b[q] = xj[(wn * 32 + q * 8 + g) * lds + kk + t];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) kf_dmma(acc[f][q][0], acc[f][q][1], a[f], b[q]);
+    }
+    if (I == J) {  // diagonal block: rows only, unit diagonal
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = wn * 32 + q * 8 + 2 * t + e;
+          const double nj = NJ[buf * KF_BN + col];
+          double vj[S];
+#pragma unroll
+          for (int s = 0; s < S; ++s) vj[s] = VJ[(buf * S + s) * KF_BN + col];
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            double sq = -2.0 * acc[f][q][e] + ni[f];
+            sq = sq + nj;
+            const double ex = exp_tab(fmax(sq, 0.0) * c, TAB);
+            const double kij = (wm * 32 + f * 8 + g == h * KF_BN + col) ? 1.0 : ex;
+#pragma unroll
+            for (int s = 0; s < S; ++s) racc[f][s] += kij * vj[s];
+          }
+        }
+      pJ = -1;
+    } else {
+      double cs[8][S];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = wn * 32 + q * 8 + 2 * t + e;
+          const double nj = NJ[buf * KF_BN + col];
+          double vj[S];
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            vj[s] = VJ[(buf * S + s) * KF_BN + col];
+            cs[q * 2 + e][s] = 0.0;
+          }
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            double sq = -2.0 * acc[f][q][e] + ni[f];
+            sq = sq + nj;
+            const double kij = exp_tab(fmax(sq, 0.0) * c, TAB);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              racc[f][s] += kij * vj[s];
+              cs[q * 2 + e][s] += kij * vi[f][s];
+            }
+          }
+        }
+      // transposed butterfly over the 8 row lanes (lane bits 2..4): lane g ends with column slot g
+      const bool b2 = g & 4, b1 = g & 2, b0 = g & 1;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        double n4[4], n2[2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double send = b2 ? cs[j][s] : cs[j + 4][s];
+          const double keep = b2 ? cs[j + 4][s] : cs[j][s];
+          n4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const double send = b1 ? n4[j] : n4[j + 2];
+          const double keep = b1 ? n4[j + 2] : n4[j];
+          n2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        const double send = b0 ? n2[0] : n2[1];
+        const double keep = b0 ? n2[1] : n2[0];
+        const double v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        const int col = wn * 32 + (g >> 1) * 8 + 2 * t + (g & 1);
+        CRED[((h * 4 + wm) * KF_BN + col) * S + s] = v;
+      }
+      pJ = J;
+      ph = h;
+    }
+    I = nI;
+    J = nJ;
+  }
+  __syncthreads();
+  if (pJ >= 0) kf_col_flush<S>(CRED, ph, pJ, n, mypart, tid);
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      double v = racc[f][s];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (t == 0) RRED[(wn * KF_BM + wm * 32 + f * 8 + g) * S + s] = v;
+    }
+  __syncthreads();
+  if (tid < KF_BM * S) {
+    const int r = tid / S, s = tid % S;
+    const i64 i = curI * KF_BM + r;
+    if (i < n) atomicAdd(mypart + s * n + i, RRED[r * S + s] + RRED[(KF_BM + r) * S + s]);
+  }
+}
+
+template <int S>
+void kfree_sym(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, double* out, i64 ldo, const int* gate) {
+  const int d = static_cast<int>(op.d), dp = (d + 3) / 4 * 4;
+  const i64 smem = ((KF_BM + 2 * KF_BN) * static_cast<i64>(dp + 1) + 2 * KF_BN + 2 * S * KF_BN + 8 * KF_BN * S +
+                    2 * KF_BM * S + KF_TAB) *
+                   8;
+  static std::once_flag tab_once;
+  std::call_once(tab_once, [] {
+    double h[KF_TAB];
+    for (int j = 0; j < KF_TAB; ++j) h[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / KF_TAB));
+    NPCG_CUDA(cudaMemcpyToSymbol(kf_exp2_tab_g, h, sizeof(h)));
+  });
+  static int per_sm = 0;
+  static i64 per_sm_smem = -1;
+  if (per_sm_smem != smem) {
+    NPCG_CUDA(cudaFuncSetAttribute(kfree_sym_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    NPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfree_sym_kernel<S>, KF_THREADS,
+                                                            static_cast<size_t>(smem)));
+    per_sm = std::max(per_sm, 1);
+    per_sm_smem = smem;
+  }
+  const double c = -1.0 / (2.0 * op.sigma * op.sigma);
+  const i64 nb = cdiv(op.n, KF_BM), npairs = nb * (nb + 1) / 2;
+  const i64 grid = std::min<i64>(static_cast<i64>(per_sm) * ctx.sm_count, npairs);
+  DBuf<double> part(grid * S * op.n, ctx.stream);
+  NPCG_CUDA(cudaMemsetAsync(part.p, 0, sizeof(double) * grid * S * op.n, ctx.stream));
+  NPCG_LAUNCH(ctx, kfree_sym_kernel<S>, static_cast<unsigned>(grid), KF_THREADS, static_cast<int>(smem), op.pts.p(),
+              op.pts.ld, op.n, d, dp, op.norms.p, c, V, ldv, npairs, part.p, gate);
+  NPCG_LAUNCH(ctx, kfree_reduce_kernel, static_cast<unsigned>(cdiv(op.n * S, 256)), 256, 0, part.p,
+              static_cast<int>(grid), op.n, S, out, ldo, gate);
+  // reference work (every entry of K): the kernel evaluates the upper blocks only
+  ctx.prof_work(static_cast<double>(op.n) * op.n * (2.0 * d + 2.0 * S), 8.0 * op.n * (d + 2 * S));
+}
+
 }  // namespace
 
 void build_kernel_matrix(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma, DMat& K) {
@@ -413,9 +692,15 @@ void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ld
   static const char* mode = std::getenv("NPCG_KFREE");  // diagnostics: "blocked" / "scalar"
   const bool force_blocked = mode && std::string(mode) == "blocked";
   const bool force_scalar = mode && std::string(mode) == "scalar";
+  const bool rowwise = mode && std::string(mode) == "rowwise";  // diagnostics: non-symmetric fused kernel
   if (k <= 2 && op.d <= 64 && !force_blocked && !force_scalar) {
-    if (k == 1) kfree_fused<1>(ctx, op, V, ldv, out, ldo, gate);
-    else kfree_fused<2>(ctx, op, V, ldv, out, ldo, gate);
+    if (rowwise) {
+      if (k == 1) kfree_fused<1>(ctx, op, V, ldv, out, ldo, gate);
+      else kfree_fused<2>(ctx, op, V, ldv, out, ldo, gate);
+    } else {
+      if (k == 1) kfree_sym<1>(ctx, op, V, ldv, out, ldo, gate);
+      else kfree_sym<2>(ctx, op, V, ldv, out, ldo, gate);
+    }
     return;
   }
   if (k > 0 && !force_scalar) {

@@ -128,8 +128,11 @@ def test_persistent_and_multikernel_pcg_agree(tmp_path):
             assert np.linalg.norm(xp - xc) <= 1e-10 * np.linalg.norm(xc)
 
 
-@pytest.mark.parametrize("n,d", [(1300, 3), (700, 7), (257, 32)])
+@pytest.mark.parametrize("n,d", [(1300, 3), (700, 7), (257, 32), (5000, 32), (4099, 17)])
 def test_matrix_free_kernel_paths(npcg, n, d):
+    """Fused symmetric (k <= 2; n = 5000 / 4099 give several block pairs per
+    CTA and row-block changes inside a CTA), row-block (k > 2) and column paths
+    against the stored kernel; the fused product is deterministic."""
     rng = np.random.default_rng(n + d)
     pts = rng.random((n, d))
     free = npcg.KernelOperator(pts, 0.6, dense_cap=1)       # matrix-free
@@ -138,6 +141,8 @@ def test_matrix_free_kernel_paths(npcg, n, d):
         V = rng.standard_normal((n, k))
         got, want = free.apply_block(V), stored.apply_block(V)
         assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max(), k
+        if k <= 2:
+            assert np.array_equal(free.apply_block(V), got)
     j = n // 3
     assert np.allclose(free.column(j), stored.column(j), rtol=1e-13, atol=1e-15)
 
