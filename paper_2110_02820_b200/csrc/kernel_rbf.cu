@@ -13,6 +13,7 @@
 
 #include <cmath>
 #include <mutex>
+#include <vector>
 #include "blas.cuh"
 #include "gemm.cuh"
 #include "ops.cuh"
@@ -57,6 +58,17 @@ __global__ void kernel_colblock_epilogue_kernel(double* __restrict__ K, i64 ldk,
     double s = *p + norms[r0 + i];
     s = s + norms[j];
     *p = r0 + i == j ? 1.0 : exp(fmax(s, 0.0) * c);
+  }
+}
+
+__global__ void scale_points_kernel(const double* __restrict__ src, i64 lds, i64 n, i64 d, double f,
+                                    double* __restrict__ dst, i64 ldd, const double* __restrict__ norms, double c,
+                                    double* __restrict__ norms_s) {
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n * d;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = idx % n, k = idx / n;
+    dst[i + k * ldd] = src[i + k * lds] * f;
+    if (k == 0) norms_s[i] = c * norms[i];
   }
 }
 
@@ -192,6 +204,33 @@ __device__ __forceinline__ double exp_tab(double x, const double* __restrict__ t
   p = fma(p, r, 1.0);
   const double v = tab[ki & (KF_TAB - 1)] * p;  // in [0.9996, 2)
   const int m = ki >> 10;                         // floor(ki / 1024), in [-1021, 0]
+  return __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
+}
+
+// Bank-conflict-free variant for the symmetric kernel: 64-entry table
+// 2^(j/64) replicated 16 times (entry j of copy c at j*16 + c, lane l reads copy
+// l % 16, so a half warp touches 16 distinct banks whatever the indices), |r| <=
+// ln2/128 and a degree-5 Taylor polynomial (truncation < 4e-17 relative).
+// CLAMP = false when the caller has bounded |x| < 700 (no exponent underflow).
+constexpr int KF_TAB64 = 64, KF_TABREP = 16;
+__device__ double kf_exp2_tab64_g[KF_TAB64];
+template <bool CLAMP>
+__device__ __forceinline__ double exp_tab64(double x, const double* __restrict__ tab_lane) {
+  if (CLAMP) x = fmax(x, -707.0);
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = fma(x, 92.33248261689366, magic);
+  const double kd = t - magic;
+  const int ki = __double2loint(t);
+  double r = fma(kd, -0.010830424696223417, x);  // ln2/64 split: hi has 36 significant bits
+  r = fma(kd, -2.572804622327669e-14, r);
+  double p = 1.0 / 120.0;
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double v = tab_lane[(ki & (KF_TAB64 - 1)) * KF_TABREP] * p;
+  const int m = ki >> 6;
   return __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
 }
 
@@ -389,7 +428,10 @@ void kfree_fused(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, dou
 // a 128 x 64 half tile: each thread folds its 4 rows, a transposed butterfly
 // over the 8 row lanes leaves one column per lane (7 adds for 8 columns), and
 // the 4 row warps are summed through shared memory. Diagonal blocks are
-// evaluated whole (rows only, K_ii = 1).
+// evaluated whole (rows only, K_ii = 1). The scale and the norms ride on the
+// DMMA: points are pre-scaled by sqrt(-2c) (c = -1/(2 sigma^2)) and the
+// accumulator starts at c ||x_i||^2, so the exponent c (||x_i||^2 + ||x_j||^2 -
+// 2 x_i.x_j) is one add away (then min(., 0), the reference's max(0, d^2)).
 // Column flush of half tile h of column block J: sum the 4 row warps in order.
 // Thread tid owns partial slot tid = (block row)*S + s, for rows and columns alike.
 template <int S>
@@ -403,13 +445,14 @@ __device__ __forceinline__ void kf_col_flush(const double* CRED, int h, i64 J, i
   if (j < n) atomicAdd(mypart + s * n + j, v);
 }
 
-template <int S>
+template <int S, int DP, bool CLAMP>
 __global__ void __launch_bounds__(KF_THREADS, 2)
-    kfree_sym_kernel(const double* __restrict__ pts, i64 ldp, i64 n, int d, int dp, const double* __restrict__ norms,
+    kfree_sym_kernel(const double* __restrict__ pts, i64 ldp, i64 n, int d, int dp_rt, const double* __restrict__ norms,
                      double c, const double* __restrict__ V, i64 ldv, i64 npairs, double* __restrict__ part,
                      const int* __restrict__ gate) {
   if (gate && *gate == 0) return;
   extern __shared__ double kfs[];
+  const int dp = DP ? DP : dp_rt;
   const int lds = dp + 1;
   double* XI = kfs;                       // [128][lds]
   double* XJ = XI + KF_BM * lds;          // [2][64][lds]
@@ -417,7 +460,7 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
   double* VJ = NJ + 2 * KF_BN;            // [2][S][64]
   double* CRED = VJ + 2 * S * KF_BN;      // [2][4][64][S] column partials per row warp
   double* RRED = CRED + 2 * 4 * KF_BN * S;  // [2][128][S] row partials per column warp
-  double* TAB = RRED + 2 * KF_BM * S;     // [KF_TAB]
+  double* TAB = RRED + 2 * KF_BM * S;     // [KF_TAB64][KF_TABREP]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3, wm = warp / KF_WN, wn = warp % KF_WN;
   const i64 nb = (n + KF_BM - 1) / KF_BM;
@@ -433,7 +476,8 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
     if (row_off(mid) <= u0) lo = mid;
     else hi = mid - 1;
   }
-  for (int idx = tid; idx < KF_TAB; idx += KF_THREADS) TAB[idx] = kf_exp2_tab_g[idx];
+  for (int idx = tid; idx < KF_TAB64 * KF_TABREP; idx += KF_THREADS) TAB[idx] = kf_exp2_tab64_g[idx / KF_TABREP];
+  const double* tab_lane = TAB + (lane & (KF_TABREP - 1));
 
   auto load_half = [&](i64 j0, int buf) {
     double* xj = XJ + buf * KF_BN * lds;
@@ -513,7 +557,8 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
 #pragma unroll
     for (int f = 0; f < 4; ++f)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[f][q][0] = acc[f][q][1] = 0.0;
+      for (int q = 0; q < 4; ++q) acc[f][q][0] = acc[f][q][1] = ni[f];  // c ||x_i||^2 + (-2c x_i.x_j)
+#pragma unroll 8
     for (int kk = 0; kk < dp; kk += 4) {
       double a[4], b[4];
 #pragma unroll
@@ -537,9 +582,7 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
           for (int s = 0; s < S; ++s) vj[s] = VJ[(buf * S + s) * KF_BN + col];
 #pragma unroll
           for (int f = 0; f < 4; ++f) {
-            double sq = -2.0 * acc[f][q][e] + ni[f];
-            sq = sq + nj;
-            const double ex = exp_tab(fmax(sq, 0.0) * c, TAB);
+            const double ex = exp_tab64<CLAMP>(fmin(acc[f][q][e] + nj, 0.0), tab_lane);
             const double kij = (wm * 32 + f * 8 + g == h * KF_BN + col) ? 1.0 : ex;
 #pragma unroll
             for (int s = 0; s < S; ++s) racc[f][s] += kij * vj[s];
@@ -562,9 +605,7 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
           }
 #pragma unroll
           for (int f = 0; f < 4; ++f) {
-            double sq = -2.0 * acc[f][q][e] + ni[f];
-            sq = sq + nj;
-            const double kij = exp_tab(fmax(sq, 0.0) * c, TAB);
+            const double kij = exp_tab64<CLAMP>(fmin(acc[f][q][e] + nj, 0.0), tab_lane);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
               racc[f][s] += kij * vj[s];
@@ -620,34 +661,52 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
   }
 }
 
-template <int S>
-void kfree_sym(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, double* out, i64 ldo, const int* gate) {
-  const int d = static_cast<int>(op.d), dp = (d + 3) / 4 * 4;
-  const i64 smem = ((KF_BM + 2 * KF_BN) * static_cast<i64>(dp + 1) + 2 * KF_BN + 2 * S * KF_BN + 8 * KF_BN * S +
-                    2 * KF_BM * S + KF_TAB) *
-                   8;
-  static std::once_flag tab_once;
-  std::call_once(tab_once, [] {
-    double h[KF_TAB];
-    for (int j = 0; j < KF_TAB; ++j) h[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / KF_TAB));
-    NPCG_CUDA(cudaMemcpyToSymbol(kf_exp2_tab_g, h, sizeof(h)));
-  });
+template <int S, int DP, bool CLAMP>
+void kfree_sym_launch(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, i64 smem, i64 npairs, double c,
+                      double* part, const int* gate, i64& grid) {
   static int per_sm = 0;
   static i64 per_sm_smem = -1;
   if (per_sm_smem != smem) {
-    NPCG_CUDA(cudaFuncSetAttribute(kfree_sym_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    NPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfree_sym_kernel<S>, KF_THREADS,
+    NPCG_CUDA(cudaFuncSetAttribute(kfree_sym_kernel<S, DP, CLAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+    NPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfree_sym_kernel<S, DP, CLAMP>, KF_THREADS,
                                                             static_cast<size_t>(smem)));
     per_sm = std::max(per_sm, 1);
     per_sm_smem = smem;
   }
+  grid = std::min<i64>(static_cast<i64>(per_sm) * ctx.sm_count, npairs);
+  if (!part) return;  // sizing call
+  const int d = static_cast<int>(op.d);
+  NPCG_LAUNCH(ctx, (kfree_sym_kernel<S, DP, CLAMP>), static_cast<unsigned>(grid), KF_THREADS, static_cast<int>(smem),
+              op.pts_s.p(), op.pts_s.ld, op.n, d, (d + 3) / 4 * 4, op.norms_s.p, c, V, ldv, npairs, part, gate);
+}
+
+template <int S>
+void kfree_sym(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, double* out, i64 ldo, const int* gate) {
+  const int d = static_cast<int>(op.d), dp = (d + 3) / 4 * 4;
+  const i64 smem = ((KF_BM + 2 * KF_BN) * static_cast<i64>(dp + 1) + 2 * KF_BN + 2 * S * KF_BN + 8 * KF_BN * S +
+                    2 * KF_BM * S + KF_TAB64 * KF_TABREP) *
+                   8;
+  static std::once_flag tab_once;
+  std::call_once(tab_once, [] {
+    double h[KF_TAB64];
+    for (int j = 0; j < KF_TAB64; ++j) h[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / KF_TAB64));
+    NPCG_CUDA(cudaMemcpyToSymbol(kf_exp2_tab64_g, h, sizeof(h)));
+  });
   const double c = -1.0 / (2.0 * op.sigma * op.sigma);
+  // |exponent| <= |c| max ||x_i - x_j||^2 <= |c| 4 max ||x||^2: below 700 no clamp is needed
+  const bool clamp = !(std::fabs(c) * 4.0 * op.max_norm < 690.0);
   const i64 nb = cdiv(op.n, KF_BM), npairs = nb * (nb + 1) / 2;
-  const i64 grid = std::min<i64>(static_cast<i64>(per_sm) * ctx.sm_count, npairs);
+  auto launch = [&](double* part, i64& grid) {
+    if (dp == 32 && !clamp) kfree_sym_launch<S, 32, false>(ctx, op, V, ldv, smem, npairs, c, part, gate, grid);
+    else if (dp == 32) kfree_sym_launch<S, 32, true>(ctx, op, V, ldv, smem, npairs, c, part, gate, grid);
+    else kfree_sym_launch<S, 0, true>(ctx, op, V, ldv, smem, npairs, c, part, gate, grid);
+  };
+  i64 grid = 0;
+  launch(nullptr, grid);
   DBuf<double> part(grid * S * op.n, ctx.stream);
   NPCG_CUDA(cudaMemsetAsync(part.p, 0, sizeof(double) * grid * S * op.n, ctx.stream));
-  NPCG_LAUNCH(ctx, kfree_sym_kernel<S>, static_cast<unsigned>(grid), KF_THREADS, static_cast<int>(smem), op.pts.p(),
-              op.pts.ld, op.n, d, dp, op.norms.p, c, V, ldv, npairs, part.p, gate);
+  launch(part.p, grid);
   NPCG_LAUNCH(ctx, kfree_reduce_kernel, static_cast<unsigned>(cdiv(op.n * S, 256)), 256, 0, part.p,
               static_cast<int>(grid), op.n, S, out, ldo, gate);
   // reference work (every entry of K): the kernel evaluates the upper blocks only
@@ -682,6 +741,22 @@ void prepare_kernel_free(Ctx& ctx, KernelFreeOp& op) {
   op.norms.alloc(op.n, ctx.stream);
   NPCG_LAUNCH(ctx, row_norms_kernel, static_cast<unsigned>(cdiv(op.n, 256)), 256, 0, op.pts.p(), op.pts.ld, op.n,
               op.d, op.norms.p);
+  {
+    std::vector<double> h(static_cast<size_t>(op.n));
+    NPCG_CUDA(cudaMemcpyAsync(h.data(), op.norms.p, sizeof(double) * op.n, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    double mx = 0.0;
+    for (double v : h) mx = std::isnan(v) ? INFINITY : std::max(mx, v);
+    op.max_norm = mx;
+  }
+  {  // scaled copies for the symmetric fused kernel
+    const double c = -1.0 / (2.0 * op.sigma * op.sigma);
+    op.pts_s.alloc(op.n, op.d, ctx.stream, false);
+    op.norms_s.alloc(op.n, ctx.stream);
+    NPCG_LAUNCH(ctx, scale_points_kernel, static_cast<unsigned>(std::min<i64>(cdiv(op.n * op.d, 256), 4096)), 256, 0,
+                op.pts.p(), op.pts.ld, op.n, op.d, std::sqrt(-2.0 * c), op.pts_s.p(), op.pts_s.ld, op.norms.p, c,
+                op.norms_s.p);
+  }
   op.pts_rm.alloc(op.d, op.n, ctx.stream, true);
   NPCG_LAUNCH(ctx, transpose_kernel, static_cast<unsigned>(std::min<i64>(cdiv(op.n * op.d, 256), 4096)), 256, 0,
               op.pts.p(), op.pts.ld, op.n, op.d, op.pts_rm.p(), op.pts_rm.ld);
@@ -700,6 +775,35 @@ void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ld
     } else {
       if (k == 1) kfree_sym<1>(ctx, op, V, ldv, out, ldo, gate);
       else kfree_sym<2>(ctx, op, V, ldv, out, ldo, gate);
+    }
+    return;
+  }
+  if (k > 8 && !force_scalar && !force_blocked) {
+    // Many vectors (sketch blocks): recompute K by column blocks and use its
+    // symmetry. Block R = [r0, r0+rb) evaluates only K[r0:n, R] (DMMA -2 X X_R^T
+    // + kernel epilogue, n_R = norms), then
+    //   out_R      += K[r0:n, R]^T V[r0:n]        (the row block's upper part)
+    //   out[r0+rb:] += K[r0+rb:n, R] V_R           (its mirror below the diagonal)
+    // -- half the kernel entries and half the GEMM flops of the row-block
+    // recompute of do_apply_block (operators.cpp:166-177), same entry formula.
+    const i64 n = op.n;
+    const double c = -1.0 / (2.0 * op.sigma * op.sigma);
+    const i64 budget = i64{4} << 30;
+    const i64 R = std::min<i64>(n, std::max<i64>(128, budget / (8 * std::max<i64>(n, 1)) / 128 * 128));
+    DMat Kt;
+    Kt.alloc(n, R, ctx.stream, false);
+    NPCG_CUDA(cudaMemset2DAsync(out, sizeof(double) * ldo, 0, sizeof(double) * n, k, ctx.stream));
+    for (i64 r0 = 0; r0 < n; r0 += R) {
+      const i64 rb = std::min(R, n - r0), L = n - r0;
+      gemm(ctx, L, rb, op.d, -2.0, Operand{op.pts.p() + r0, op.pts.ld, false},
+           Operand{op.pts.p() + r0, op.pts.ld, false}, 0.0, Kt.p(), Kt.ld);
+      NPCG_LAUNCH(ctx, kernel_colblock_epilogue_kernel,
+                  static_cast<unsigned>(std::min<i64>(cdiv(rb * L, 256), ctx.sm_count * 16)), 256, 0, Kt.p(), Kt.ld, L,
+                  rb, i64{0}, op.norms.p + r0, c);
+      gemm(ctx, rb, k, L, 1.0, Operand{Kt.p(), Kt.ld, true}, Operand{V + r0, ldv, true}, 1.0, out + r0, ldo);
+      if (L > rb)
+        gemm(ctx, L - rb, k, rb, 1.0, Operand{Kt.p() + rb, Kt.ld, false}, Operand{V + r0, ldv, true}, 1.0,
+             out + r0 + rb, ldo);
     }
     return;
   }

@@ -76,6 +76,9 @@ struct KernelFreeOp : Op {  // KernelOperator beyond dense_cap (operators.cpp:15
   DMat pts;                 // n x d col-major (reference layout)
   DMat pts_rm;              // d x n col-major == points row-major (point-contiguous)
   DBuf<double> norms;       // ||x_i||^2
+  double max_norm = INFINITY;  // max_i ||x_i||^2 (bounds the kernel exponent)
+  DMat pts_s;               // points * sqrt(1/sigma^2) (symmetric fused kernel)
+  DBuf<double> norms_s;     // -||x_i||^2 / (2 sigma^2)
   i64 d = 0;
   double sigma = 1.0;
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
