@@ -207,30 +207,29 @@ __device__ __forceinline__ double exp_tab(double x, const double* __restrict__ t
   return __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
 }
 
-// Bank-conflict-free variant for the symmetric kernel: 64-entry table
-// 2^(j/64) replicated 16 times (entry j of copy c at j*16 + c, lane l reads copy
-// l % 16, so a half warp touches 16 distinct banks whatever the indices), |r| <=
-// ln2/128 and a degree-5 Taylor polynomial (truncation < 4e-17 relative).
-// CLAMP = false when the caller has bounded |x| < 700 (no exponent underflow).
-constexpr int KF_TAB64 = 64, KF_TABREP = 16;
+// Variant for the symmetric kernel: 256-entry table 2^(j/256) replicated 4
+// times (entry j of copy c at j*4 + c, lane l reads copy l % 4: 4x fewer bank
+// conflicts on the data-dependent index), |r| <= ln2/512 and a degree-4 Taylor
+// polynomial (truncation < 4e-17 relative). CLAMP = false when the caller has
+// bounded |x| < 700 (no exponent underflow).
+constexpr int KF_TAB64 = 256, KF_TABREP = 4;
 __device__ double kf_exp2_tab64_g[KF_TAB64];
 template <bool CLAMP>
 __device__ __forceinline__ double exp_tab64(double x, const double* __restrict__ tab_lane) {
   if (CLAMP) x = fmax(x, -707.0);
   const double magic = 6755399441055744.0;  // 1.5 * 2^52
-  const double t = fma(x, 92.33248261689366, magic);
+  const double t = fma(x, 369.3299304675746, magic);
   const double kd = t - magic;
   const int ki = __double2loint(t);
-  double r = fma(kd, -0.010830424696223417, x);  // ln2/64 split: hi has 36 significant bits
-  r = fma(kd, -2.572804622327669e-14, r);
-  double p = 1.0 / 120.0;
-  p = fma(p, r, 1.0 / 24.0);
+  double r = fma(kd, -0.0027076061741126978, x);  // ln2/256 split: hi has 35 significant bits
+  r = fma(kd, 5.0411407304988844e-14, r);
+  double p = 1.0 / 24.0;
   p = fma(p, r, 1.0 / 6.0);
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const double v = tab_lane[(ki & (KF_TAB64 - 1)) * KF_TABREP] * p;
-  const int m = ki >> 6;
+  const int m = ki >> 8;
   return __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
 }
 
