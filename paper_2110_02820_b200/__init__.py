@@ -171,8 +171,14 @@ class Context:
     def prof_report(self) -> dict:
         """{kernel name: (launches, total_ms, algorithmic flops, algorithmic bytes)}
         since prof_enable(True)."""
-        buf = C.create_string_buffer(1 << 20)
-        _check(lib().npcg_prof_report(_vp(self.h), buf, _i64(1 << 20)))
+        cap = 1 << 20
+        while True:
+            buf = C.create_string_buffer(cap)
+            rc = lib().npcg_prof_report(_vp(self.h), buf, _i64(cap))
+            if rc == 0 or cap >= 1 << 28:
+                _check(rc)
+                break
+            cap <<= 2  # many distinct launch labels (e.g. per-shape GEMMs of a long run)
         out = {}
         for line in buf.value.decode().splitlines():
             name, cnt, ms, fl, by = line.split("\t")

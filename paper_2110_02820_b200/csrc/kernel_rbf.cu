@@ -787,7 +787,13 @@ void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ld
     // recompute of do_apply_block (operators.cpp:166-177), same entry formula.
     const i64 n = op.n;
     const double c = -1.0 / (2.0 * op.sigma * op.sigma);
-    const i64 budget = i64{4} << 30;
+    // column block of K: up to 16 GB or a quarter of the free memory (wide
+    // blocks keep the GEMMs large: M = R for K^T V, contraction R for the mirror)
+    i64 budget = i64{16} << 30;
+    if (const char* e = std::getenv("NPCG_KBLOCK_BYTES")) budget = std::atoll(e);
+    size_t free_b = 0, total_b = 0;
+    NPCG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    budget = std::max<i64>(i64{1} << 30, std::min<i64>(budget, static_cast<i64>(free_b / 4)));
     const i64 R = std::min<i64>(n, std::max<i64>(128, budget / (8 * std::max<i64>(n, 1)) / 128 * 128));
     DMat Kt;
     Kt.alloc(n, R, ctx.stream, false);

@@ -17,6 +17,7 @@ ctx.sync()
 dt = time.perf_counter() - t
 rep = ctx.prof_report()
 ctx.prof_enable(False)
-print("n=%d d=%d k=%d wall %.4f s" % (n, d, k, dt))
+print("n=%d d=%d k=%d wall %.4f s, kernels %.3f ms, %d launches" % (n, d, k, dt, sum(v[1] for v in rep.values()),
+                                                                  sum(v[0] for v in rep.values())))
 for name, v in sorted(rep.items(), key=lambda kv: -kv[1][1]):
     print("  %-50s %4d launches %9.3f ms" % (name, v[0], v[1]))
