@@ -26,6 +26,8 @@ namespace {
 constexpr int CPW = 4;            // columns per warp (coldot)
 constexpr int CD_WARPS = 8;       // warps per CTA (coldot)
 constexpr int CD_COLS = CPW * CD_WARPS;
+constexpr int RD_THREADS = 256;   // rowdot: 2 rows per thread, c staged in shared memory
+constexpr int RD_SMEM_MAX = 48 * 1024;
 
 template <int S>
 __global__ void __launch_bounds__(256) coldot_kernel(const double* __restrict__ M, i64 ldm, i64 nrows, i64 ncols,
@@ -49,18 +51,20 @@ __global__ void __launch_bounds__(256) coldot_kernel(const double* __restrict__ 
   for (int c = 0; c < CPW; ++c) col[c] = M + min(j0 + c, ncols - 1) * ldm;
 
   i64 i = r0 + 2 * lane;
-  // main loop: 4 row-pairs per lane per trip
-  for (; i + 3 * 64 + 1 < r1; i += 4 * 64) {
-    double2 a[4][CPW], x[4][S];
+  // main loop: UN row-pairs per lane per trip (fewer for many right-hand
+  // sides: the x registers would cap occupancy)
+  constexpr int UN = S <= 2 ? 4 : 2;
+  for (; i + (UN - 1) * 64 + 1 < r1; i += UN * 64) {
+    double2 a[UN][CPW], x[UN][S];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < UN; ++u) {
 #pragma unroll
       for (int c = 0; c < CPW; ++c) a[u][c] = __ldg(reinterpret_cast<const double2*>(col[c] + i + u * 64));
 #pragma unroll
       for (int s = 0; s < S; ++s) x[u][s] = __ldg(reinterpret_cast<const double2*>(X + s * ldx + i + u * 64));
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < UN; ++u)
 #pragma unroll
       for (int c = 0; c < CPW; ++c)
 #pragma unroll
@@ -115,40 +119,49 @@ __global__ void coldot_reduce_kernel(const double* __restrict__ partial, int spl
 }
 
 template <int S>
-__global__ void __launch_bounds__(128) rowdot_kernel(const double* __restrict__ M, i64 ldm, i64 nrows, i64 ncols,
-                                                     const double* __restrict__ c, i64 ldc, i64 cols_per_split,
-                                                     const double* __restrict__ base, i64 ldb,
-                                                     double* __restrict__ out, i64 ldo,
-                                                     double* __restrict__ partial, const int* __restrict__ gate) {
+__global__ void __launch_bounds__(RD_THREADS) rowdot_kernel(const double* __restrict__ M, i64 ldm, i64 nrows,
+                                                            i64 ncols, const double* __restrict__ c, i64 ldc,
+                                                            i64 cols_per_split, const double* __restrict__ base,
+                                                            i64 ldb, double* __restrict__ out, i64 ldo,
+                                                            double* __restrict__ partial,
+                                                            const int* __restrict__ gate) {
   if (gate && *gate == 0) return;
-  const i64 i = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) * 2;
-  if (i >= nrows) return;
+  extern __shared__ double cs[];  // c[k0:k1, :] as [k][S]
   const i64 k0 = static_cast<i64>(blockIdx.y) * cols_per_split;
   const i64 k1 = min(ncols, k0 + cols_per_split);
+  const int kc = static_cast<int>(k1 - k0);
+  for (int idx = threadIdx.x; idx < kc * S; idx += RD_THREADS) {
+    const int kk = idx / S, s = idx % S;
+    cs[idx] = c[s * ldc + k0 + kk];
+  }
+  __syncthreads();
+  const i64 i = (static_cast<i64>(blockIdx.x) * RD_THREADS + threadIdx.x) * 2;
+  if (i >= nrows) return;
   const bool two = i + 1 < nrows;
   double acc0[S], acc1[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) acc0[s] = acc1[s] = 0.0;
-  i64 k = k0;
+  const double* mp = M + k0 * ldm + i;
+  int k = 0;
   constexpr int U = 8;  // 8 x 16 B loads in flight per thread
-  for (; k + U - 1 < k1; k += U) {
+  for (; k + U - 1 < kc; k += U) {
     double2 a[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) a[u] = __ldg(reinterpret_cast<const double2*>(M + (k + u) * ldm + i));
+    for (int u = 0; u < U; ++u) a[u] = __ldg(reinterpret_cast<const double2*>(mp + (k + u) * ldm));
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const double cv = __ldg(c + s * ldc + k + u);
+        const double cv = cs[(k + u) * S + s];
         acc0[s] += a[u].x * cv;
         acc1[s] += a[u].y * cv;
       }
   }
-  for (; k < k1; ++k) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(M + k * ldm + i));
+  for (; k < kc; ++k) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(mp + k * ldm));
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      const double cv = __ldg(c + s * ldc + k);
+      const double cv = cs[k * S + s];
       acc0[s] += a.x * cv;
       acc1[s] += a.y * cv;
     }
@@ -529,21 +542,25 @@ void coldot_s(Ctx& ctx, const double* M, i64 ldm, i64 nrows, i64 ncols, const do
 template <int S>
 void rowdot_s(Ctx& ctx, const double* M, i64 ldm, i64 nrows, i64 ncols, const double* c, i64 ldc,
               const double* base, i64 ldb, double* out, i64 ldo, const int* gate) {
-  const i64 rblocks = cdiv(nrows, 256);
+  const i64 rblocks = cdiv(nrows, 2 * RD_THREADS);
+  // enough CTAs for the bytes in flight (~8 per SM), at least 16 columns each,
+  // and the CTA's slice of c in 48 KB of shared memory
   i64 splits = 1;
-  const i64 target = 2 * ctx.sm_count;
-  if (rblocks < target) splits = std::max<i64>(1, std::min<i64>(cdiv(target, rblocks), ncols / 32));
+  const i64 target = 8 * ctx.sm_count;
+  if (rblocks < target) splits = std::max<i64>(1, std::min<i64>(cdiv(target, rblocks), ncols / 16));
+  splits = std::max<i64>(splits, cdiv(ncols * S * 8, RD_SMEM_MAX));
   i64 cps = cdiv(ncols, splits);
   splits = cdiv(ncols, std::max<i64>(cps, 1));
+  const int smem = static_cast<int>(std::max<i64>(cps, 1) * S * 8);
   if (splits <= 1) {
-    NPCG_LAUNCH(ctx, rowdot_kernel<S>, dim3(static_cast<unsigned>(rblocks), 1), 128, 0, M, ldm, nrows, ncols, c, ldc,
-                std::max<i64>(ncols, 1), base, ldb, out, ldo, static_cast<double*>(nullptr), gate);
+    NPCG_LAUNCH(ctx, rowdot_kernel<S>, dim3(static_cast<unsigned>(rblocks), 1), RD_THREADS, smem, M, ldm, nrows,
+                ncols, c, ldc, std::max<i64>(ncols, 1), base, ldb, out, ldo, static_cast<double*>(nullptr), gate);
     ctx.prof_work(2.0 * nrows * ncols * S, 8.0 * (nrows * ncols + S * (2 * nrows + ncols)));
     return;
   }
   DBuf<double> part(splits * S * nrows, ctx.stream);
-  NPCG_LAUNCH(ctx, rowdot_kernel<S>, dim3(static_cast<unsigned>(rblocks), static_cast<unsigned>(splits)), 128, 0, M,
-              ldm, nrows, ncols, c, ldc, cps, base, ldb, out, ldo, part.p, gate);
+  NPCG_LAUNCH(ctx, rowdot_kernel<S>, dim3(static_cast<unsigned>(rblocks), static_cast<unsigned>(splits)), RD_THREADS,
+              smem, M, ldm, nrows, ncols, c, ldc, cps, base, ldb, out, ldo, part.p, gate);
   ctx.prof_work(2.0 * nrows * ncols * S, 8.0 * (nrows * ncols + S * (2 * nrows + ncols)));
   NPCG_LAUNCH(ctx, rowdot_reduce_kernel, static_cast<unsigned>(cdiv(nrows * S, 256)), 256, 0, part.p,
               static_cast<int>(splits), nrows, S, base, ldb, out, ldo, gate);
