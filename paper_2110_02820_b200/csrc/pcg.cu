@@ -14,7 +14,9 @@
 // read it first), so overshoot costs only empty launches.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <chrono>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -270,6 +272,14 @@ struct PersistArgs {
   double* T;
   double* part;                       // gram: G x PW; dense: ncb x S x pstride
   i64 nrb, ncb, cpb, pstride;         // dense: row blocks of PW rows, column blocks of cpb columns
+  // dense, symmetric use of A (sym != 0): CTA c streams row block unit_rb[c],
+  // columns [unit_j0[c], unit_j1[c]) of the block-upper part; row sums go to
+  // part[(c*S + s)*DPW + local row], column dots to colpart[(rb*S + s)*pstride + j]
+  int sym;
+  const i64* unit;                    // segments x 3: rb, j0, j1 (row-major order)
+  const int* cseg;                    // G + 1: first segment of each CTA
+  const int* ustart;                  // nrb + 1: first segment of each row block
+  double* colpart;
   double *pv_part, *rr_part, *rz_part;  // G x S
   State* st;
   double* hist;
@@ -472,11 +482,23 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         // column segment is one contiguous bulk copy into the shared-memory
         // ring (DNST segments in flight); two columns per step, one block
         // barrier per step frees their slots. partial_cb = A[rows, cols_cb] p_t[cols_cb].
+        // Symmetric use (a.sym): CTA c owns row block rb and columns [j0, j1) of
+        // the block-upper part (j >= rb*DPW). A column segment beyond the
+        // diagonal block is used twice: axpy into the rows of rb (A[R, j] p_j)
+        // and a dot with p over those rows, which is (A p)_j's share from the
+        // rows of rb (A[j, R] = A[R, j]^T): half of A is read per iteration.
         const int nrb = static_cast<int>(a.nrb), ncb = static_cast<int>(a.ncb);
-        if (c < nrb * ncb) {
-          const int rb = c % nrb, cb = c / nrb;
+        // symmetric: CTA c's equal-byte range of the block-upper work list, as
+        // segments kseg in [cseg[c], cseg[c+1]) of (row block, column range)
+        const int kbeg = a.sym ? a.cseg[c] : c, kend = a.sym ? a.cseg[c + 1] : (c < nrb * ncb ? c + 1 : c);
+        for (int kseg = kbeg; kseg < kend; ++kseg) {
+          const int rb = a.sym ? static_cast<int>(a.unit[3 * kseg]) : c % nrb, cb = a.sym ? kseg : c / nrb;
           const i64 rb0 = static_cast<i64>(rb) * DPW, cnt = min(static_cast<i64>(DPW), n - rb0);
-          const i64 cb0 = static_cast<i64>(cb) * a.cpb, cb1 = min(n, cb0 + a.cpb);
+          const i64 cb0 = a.sym ? a.unit[3 * kseg + 1] : static_cast<i64>(cb) * a.cpb;
+          const i64 cb1 = a.sym ? a.unit[3 * kseg + 2] : min(n, cb0 + a.cpb);
+          const i64 offd = rb0 + DPW;  // first column beyond the diagonal block
+          __shared__ double wdot[2][PT / 32][2 * S];
+          double2 pr[S][DPV];  // p_t on this thread's rows (symmetric dots)
           double2 acc[S][DPV];
           bool ok[DPV];
 #pragma unroll
@@ -485,6 +507,28 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
 #pragma unroll
             for (int s = 0; s < S; ++s) acc[s][k] = make_double2(0.0, 0.0);
           }
+          if (a.sym) {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+              for (int k = 0; k < DPV; ++k) {
+                const i64 i = rb0 + 2 * (tid + static_cast<i64>(PT) * k);
+                pr[s][k] = make_double2(i < n ? pcur[i + s * a.ldw] : 0.0, i + 1 < n ? pcur[i + 1 + s * a.ldw] : 0.0);
+              }
+          }
+          // column dots of the previous step: 16 warp partials summed in fixed order
+          auto flush_dots = [&](i64 jp, int buf) {
+            if (tid < 2 * S) {
+              const int e = tid / S, s = tid % S;
+              if (jp + e < cb1) {
+                double v = 0.0;
+                for (int w = 0; w < PT / 32; ++w) v += wdot[buf][w][e * S + s];
+                a.colpart[(static_cast<i64>(rb) * S + s) * a.pstride + jp + e] = v;
+              }
+            }
+          };
+          i64 jprev = -1;
+          int step = 0;
           if (tid == 0)
             for (i64 j = cb0; j < min(cb1, cb0 + DNST); ++j) ring_issue(a.A + j * a.lda + rb0, cnt);
           // p_t of the whole vector is in pcur (slice owners wrote it before the barrier)
@@ -510,6 +554,43 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
               if (j + DNST < cb1) ring_issue(a.A + (j + DNST) * a.lda + rb0, cnt);
               if (j + DNST + 1 < cb1) ring_issue(a.A + (j + DNST + 1) * a.lda + rb0, cnt);
             }
+            if (a.sym) {
+              if (jprev >= 0) flush_dots(jprev, (step - 1) & 1);
+              jprev = -1;
+              if (j >= offd) {  // both columns are beyond the diagonal block (offd is even)
+                // the 2S dots (slot e*S + s), padded to a power of two, reduced over
+                // the warp by a transposed butterfly: lane group g ends with slot g
+                constexpr int NV = 2 * S <= 2 ? 2 : 2 * S <= 4 ? 4 : 8;
+                constexpr int LG = NV == 2 ? 1 : NV == 4 ? 2 : 3;
+                double d[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) d[v] = 0.0;
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+#pragma unroll
+                  for (int k = 0; k < DPV; ++k) {
+                    d[s] += c0[k].x * pr[s][k].x + c0[k].y * pr[s][k].y;
+                    d[S + s] += c1[k].x * pr[s][k].x + c1[k].y * pr[s][k].y;
+                  }
+#pragma unroll
+                for (int st = 0; st < LG; ++st) {
+                  const int m = 16 >> st, half = NV >> (st + 1);
+                  const bool hi = lane & m;
+#pragma unroll
+                  for (int v = 0; v < half; ++v) {
+                    const double send = hi ? d[v] : d[v + half];
+                    const double keep = hi ? d[v + half] : d[v];
+                    d[v] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                  }
+                }
+#pragma unroll
+                for (int m = 16 >> LG; m >= 1; m >>= 1) d[0] += __shfl_xor_sync(0xffffffffu, d[0], m);
+                const int slot = lane >> (5 - LG);
+                if ((lane & ((32 >> LG) - 1)) == 0 && slot < 2 * S) wdot[step & 1][warp][slot] = d[0];
+                jprev = j;
+              }
+              ++step;
+            }
 #pragma unroll
             for (int s = 0; s < S; ++s) {
               const double p0 = q0[s], p1 = q1[s];
@@ -522,9 +603,14 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
               }
             }
           }
+          if (a.sym) {
+            __syncthreads();
+            if (jprev >= 0) flush_dots(jprev, (step - 1) & 1);
+          }
 #pragma unroll
           for (int s = 0; s < S; ++s) {
-            double* dst = a.part + (static_cast<i64>(cb) * S + s) * a.pstride + rb0;
+            double* dst = a.sym ? a.part + (static_cast<i64>(kseg) * S + s) * DPW
+                                : a.part + (static_cast<i64>(cb) * S + s) * a.pstride + rb0;
 #pragma unroll
             for (int k = 0; k < DPV; ++k) {
               const i64 i = 2 * (tid + static_cast<i64>(PT) * k);
@@ -536,12 +622,36 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             }
           }
         }
+        tick(t, 1);
         grid.sync();
+        tick(t, 2);
         // ---- P2 (dense): v = (sum_cb partial_cb) + mu p for the slice, partial p.v
         double pvl[S];
 #pragma unroll
         for (int s = 0; s < S; ++s) pvl[s] = 0.0;
-        for (i64 j = r0 + warp; j < r1; j += PT / 32) {
+        if (a.sym) {
+          // symmetric: thread per row (coalesced over the warp); row sums of the
+          // units of j's row block, then the column dots of the row blocks above,
+          // in that fixed order
+          for (i64 j = r0 + tid; j < r1; j += PT) {
+            const int rbj = static_cast<int>(j / DPW);
+            const int us = a.ustart[rbj], nu = a.ustart[rbj + 1] - us;
+            const i64 loc = j - static_cast<i64>(rbj) * DPW;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              double sum = 0.0;
+              for (int b = 0; b < nu; ++b) sum += a.part[(static_cast<i64>(us + b) * S + s) * DPW + loc];
+#pragma unroll 4
+              for (int b = 0; b < rbj; ++b) sum += a.colpart[(static_cast<i64>(b) * S + s) * a.pstride + j];
+              const double pj = pcur[j + s * a.ldw];
+              double v = sum;  // operators.cpp:72-78 then solvers.cpp:137-141: out = A p; out += mu p
+              v += a.mu * pj;
+              a.V[j + s * a.ldw] = v;
+              pvl[s] += pj * v;
+            }
+          }
+        }
+        for (i64 j = r0 + warp; j < r1 && !a.sym; j += PT / 32) {
 #pragma unroll
           for (int s = 0; s < S; ++s) {
             double sum = 0.0;
@@ -561,6 +671,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
           const double tot = block_sum(pvl[s], sh);
           if (tid == 0) a.pv_part[c * S + s] = tot;
         }
+        tick(t, 3);
       }
       grid.sync();
       tick(t, 4);
@@ -766,13 +877,70 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   DBuf<double> part, T, scal(3 * static_cast<i64>(G) * S, ctx.stream);
   if (gram) part.alloc(static_cast<i64>(G) * PW, ctx.stream);
   i64 nrb = 0, ncb = 0, cpb = 0, pstride = 0;
+  DBuf<i64> units;
+  DBuf<int> cseg, ustart;
+  DBuf<double> colpart;
+  int sym = 0;
   if (dense) {
-    nrb = cdiv(n, dense_pw(static_cast<int>(S)));
-    ncb = std::max<i64>(1, G / nrb);
-    cpb = cdiv(n, ncb);
-    ncb = cdiv(n, cpb);
+    const i64 dpw = dense_pw(static_cast<int>(S));
+    nrb = cdiv(n, dpw);
     pstride = round_up(n, 2);
-    part.alloc(ncb * S * pstride, ctx.stream);
+    static const bool full = std::getenv("NPCG_DENSE_FULL") != nullptr;  // diagnostics: read all of A
+    sym = (!full && nrb > 1 && nrb <= G) ? 1 : 0;
+    if (sym) {
+      // block-upper part: row block rb streams columns [rb*dpw, n) of cnt_rb
+      // rows; CTA c takes the byte range [c W / G, (c+1) W / G) of that work
+      // list in row-major order (one segment per row block it touches;
+      // boundaries on even columns so a step's two columns share a side of the
+      // diagonal block)
+      std::vector<double> cum(static_cast<size_t>(nrb + 1), 0.0);
+      for (i64 rb = 0; rb < nrb; ++rb) {
+        const i64 cnt = std::min(dpw, n - rb * dpw);
+        cum[static_cast<size_t>(rb + 1)] = cum[static_cast<size_t>(rb)] + static_cast<double>(n - rb * dpw) * cnt;
+      }
+      const double W = cum[static_cast<size_t>(nrb)];
+      auto pos = [&](i64 c) -> std::pair<i64, i64> {  // (row block, column) where CTA c starts
+        if (c >= G) return {nrb - 1, n};
+        const double wc = W * static_cast<double>(c) / static_cast<double>(G);
+        i64 rb = std::upper_bound(cum.begin(), cum.end(), wc) - cum.begin() - 1;
+        rb = std::min<i64>(std::max<i64>(rb, 0), nrb - 1);
+        const i64 cnt = std::min(dpw, n - rb * dpw);
+        const i64 off = static_cast<i64>(std::ceil((wc - cum[static_cast<size_t>(rb)]) / static_cast<double>(cnt)));
+        return {rb, std::min(n, rb * dpw + round_up(off, 2))};
+      };
+      std::vector<i64> hu;
+      std::vector<int> hc(static_cast<size_t>(G + 1)), hs(static_cast<size_t>(nrb + 1), -1);
+      for (i64 c = 0; c < G; ++c) {
+        hc[static_cast<size_t>(c)] = static_cast<int>(hu.size() / 3);
+        const auto [ra, ja] = pos(c);
+        const auto [rz, jz] = pos(c + 1);
+        for (i64 rb = ra; rb <= rz; ++rb) {
+          const i64 j0 = rb == ra ? ja : rb * dpw, j1 = rb == rz ? jz : n;
+          if (j0 >= j1) continue;
+          if (hs[static_cast<size_t>(rb)] < 0) hs[static_cast<size_t>(rb)] = static_cast<int>(hu.size() / 3);
+          hu.insert(hu.end(), {rb, j0, j1});
+        }
+      }
+      const int nseg = static_cast<int>(hu.size() / 3);
+      hc[static_cast<size_t>(G)] = nseg;
+      hs[static_cast<size_t>(nrb)] = nseg;
+      for (i64 rb = nrb - 1; rb >= 0; --rb)
+        if (hs[static_cast<size_t>(rb)] < 0) hs[static_cast<size_t>(rb)] = hs[static_cast<size_t>(rb + 1)];
+      units.alloc(3 * static_cast<i64>(nseg), ctx.stream);
+      cseg.alloc(G + 1, ctx.stream);
+      ustart.alloc(nrb + 1, ctx.stream);
+      NPCG_CUDA(cudaMemcpyAsync(units.p, hu.data(), sizeof(i64) * hu.size(), cudaMemcpyHostToDevice, ctx.stream));
+      NPCG_CUDA(cudaMemcpyAsync(cseg.p, hc.data(), sizeof(int) * hc.size(), cudaMemcpyHostToDevice, ctx.stream));
+      NPCG_CUDA(cudaMemcpyAsync(ustart.p, hs.data(), sizeof(int) * hs.size(), cudaMemcpyHostToDevice, ctx.stream));
+      part.alloc(static_cast<i64>(nseg) * S * dpw, ctx.stream);
+      colpart.alloc(nrb * S * pstride, ctx.stream);
+      ctx.sync();  // host staging vectors go out of scope
+    } else {
+      ncb = std::max<i64>(1, G / nrb);
+      cpb = cdiv(n, ncb);
+      ncb = cdiv(n, cpb);
+      part.alloc(ncb * S * pstride, ctx.stream);
+    }
   }
   if (nys) T.alloc(pre->ell * S, ctx.stream);
   PersistArgs pa{};
@@ -810,6 +978,11 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   pa.ncb = ncb;
   pa.cpb = cpb;
   pa.pstride = pstride;
+  pa.sym = sym;
+  pa.unit = units.p;
+  pa.cseg = cseg.p;
+  pa.ustart = ustart.p;
+  pa.colpart = colpart.p;
   pa.pv_part = scal.p;
   pa.rr_part = scal.p + G * S;
   pa.rz_part = scal.p + 2 * G * S;
@@ -838,7 +1011,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
     NPCG_CUDA(cudaMemcpy(h, tr.p, sizeof(h), cudaMemcpyDeviceToHost));
     for (int t = 0; t < 8; ++t) {
       const unsigned long long* q = h + t * 12;
-      if (!q[0] || !q[10]) continue;
+      if (!q[0] || !q[4]) continue;
       std::fprintf(stderr, "[pcg it %d] P1 %.2f s1 %.2f P2 %.2f s2 %.2f P3 %.2f s3 %.2f P4 %.2f s4 %.2f P5 %.2f s5 %.2f "
                    "total %.2f us\n", t + 2, (q[1] - q[0]) * 1e-3, (q[2] - q[1]) * 1e-3, (q[3] - q[2]) * 1e-3,
                    (q[4] - q[3]) * 1e-3, (q[5] - q[4]) * 1e-3, (q[6] - q[5]) * 1e-3, (q[7] - q[6]) * 1e-3,
@@ -850,7 +1023,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
     NPCG_CUDA(cudaMemcpy(&h, st, sizeof(State), cudaMemcpyDeviceToHost));
     i64 iters = 0;
     for (i64 s = 0; s < S; ++s) iters = std::max<i64>(iters, h.c[s].iters);
-    const double a_bytes = gram ? 8.0 * gram->m * n : 8.0 * n * n;
+    const double a_bytes = gram ? 8.0 * gram->m * n : 8.0 * n * n;  // the reference's bytes (sym reads ~half)
     const double a_flops = gram ? 4.0 * gram->m * n * S : 2.0 * n * n * S;
     const double u_bytes = nys ? 2.0 * 8.0 * n * pre->ell : 0.0;
     const double u_flops = nys ? 4.0 * n * pre->ell * S : 0.0;
