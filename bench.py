@@ -258,9 +258,17 @@ ALGO_NOTE = {
     "gemm_dmma_kernel": ("tensor", "2*M*N*K flops per launch (sketch X*Omega, X^T*Z, Gram/TRSM/CholeskyQR GEMMs)"),
     "coldot_kernel": ("hbm", "8*rows*cols matrix bytes + vectors per launch (X^T z, U^T r)"),
     "rowdot_kernel": ("hbm", "8*rows*cols matrix bytes + vectors per launch (X v, U t)"),
-    "pcg_persistent_kernel": ("hbm", "per PCG iteration: X once (8*m*n B; dense: 8*n^2), U twice (2*8*n*l B) "
-                                     "and ~10 n-vectors (80*n B); x iterations of the launch"),
+    "pcg_persistent_kernel": ("hbm", "per PCG iteration: X once (8*m*n B; dense: the block-upper part of A that "
+                                     "the symmetric kernel streams, ~4*n^2 + 4*n*rowblock B, vs the reference's "
+                                     "8*n^2), U twice (2*8*n*l B) and ~10 n-vectors (80*n B); x iterations"),
+    "kfree_sym_kernel": ("tensor", "reference count n^2*(2d+2k) flops per launch (the kernel evaluates the upper "
+                                   "block pairs only: half of that on the pipe)"),
 }
+
+
+L2_NOTE = {"cfg1": "A 32 MB is L2-resident (no flush; latency-bound config)",
+           "cfg2": "inputs larger than L2 (X 640 MB)", "cfg3": "inputs larger than L2 (K 20 GB)",
+           "cfg4": "points 256 MB > L2; K recomputed", "cfg5": "inputs larger than L2 (A 80 GB)"}
 
 
 def roofline_from_profile(prof, peaks, dgemm_peak, ncu_traffic):
@@ -479,7 +487,7 @@ def run_b200(args):
         "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng mt19937_64+Box-Muller, seeded)",
         "config": {**w.describe(), "parallelism": f"rowshard{world}" if sharded else f"replicas{world}",
-                   "l2": "inputs larger than L2 (X 640 MB)",
+                   "l2": L2_NOTE.get(args.config, "inputs larger than L2"),
                    **({"iterations_per_mu": [max(it for it, _ in rs) for rs in info], "mus": len(info)}
                       if w.mus else {"iterations": info[0][0], "converged": info[0][1]}),
                    **({"adaptive_ell_final_doublings_hitcap": list(path.adaptive_outcome)} if w.adaptive else {})},

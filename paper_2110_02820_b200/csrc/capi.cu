@@ -6,6 +6,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
+#include <future>
+#include <random>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -1079,18 +1083,79 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
     s.ctx = &c;
     s.op = op->op.get();
     s.n = n;
+    // Draw-ahead (error strategy, Gaussian sketch): the stream after an Omega
+    // block is always the power vector g, then -- if the loop continues -- the
+    // next block, whose size the doubling rule fixes in advance. A host thread
+    // draws both from a copy of the engine while the GPU sketches and
+    // factors; the caller's engine is advanced only by what the loop consumes
+    // (g, then the block if used), so the stream is exactly the reference's.
+    struct DrawAhead {
+      std::thread th;
+      std::promise<void> g_ready;
+      std::future<void> g_fut;
+      std::vector<double> g, raw;
+      std::mt19937_64 after_g, after_raw;
+      i64 extra = 0;
+      bool active = false, g_taken = false;
+      void finish() {
+        if (th.joinable()) th.join();
+        active = false;
+      }
+      ~DrawAhead() { finish(); }
+    } ahead;
+    const bool draw_ahead = cfg->tol_mode == 0 && cfg->sketch == 0 && std::getenv("NPCG_NO_DRAW_AHEAD") == nullptr;
+    auto start_ahead = [&](i64 size_after) {
+      if (!draw_ahead) return;
+      const i64 ex = size_after >= cfg->ell_max ? 0
+                     : 2 * size_after <= cfg->ell_max ? size_after : cfg->ell_max - size_after;
+      ahead.extra = (ex > 0 && n * ex <= (i64{2} << 30)) ? ex : 0;  // <= 16 GB of host staging
+      ahead.g_ready = std::promise<void>();
+      ahead.g_fut = ahead.g_ready.get_future();
+      ahead.g_taken = false;
+      ahead.active = true;
+      ahead.th = std::thread([&ahead = ahead, eng = rng->r, n]() mutable {
+        ahead.g.resize(static_cast<size_t>(n));
+        eng.gaussian(n, 1, ahead.g.data());
+        ahead.after_g = eng.engine;
+        ahead.g_ready.set_value();
+        if (ahead.extra > 0) {
+          ahead.raw.resize(static_cast<size_t>(n * ahead.extra));
+          eng.gaussian(n, ahead.extra, ahead.raw.data());
+          ahead.after_raw = eng.engine;
+        }
+      });
+    };
     auto grow = [&](i64 extra) {  // adaptive.cpp:30-35
       if (cfg->sketch != 0) {
         extend_columns_rng(s, extra, rng->r);
         return;
       }
-      std::vector<double> raw(static_cast<size_t>(n * extra));
-      rng->r.gaussian(n, extra, raw.data());
+      std::vector<double> raw;
+      if (ahead.active) {
+        ahead.finish();
+        if (ahead.g_taken && ahead.extra == extra) {
+          raw.swap(ahead.raw);
+          rng->r.engine = ahead.after_raw;
+        }
+      }
+      if (raw.empty()) {
+        raw.resize(static_cast<size_t>(n * extra));
+        rng->r.gaussian(n, extra, raw.data());
+      }
+      start_ahead(s.size + extra);
       nys_extend(s, raw.data(), n, extra, NPCG_HOST);
     };
     auto estimate = [&]() {
-      std::vector<double> g(static_cast<size_t>(n));
-      rng->r.gaussian(n, 1, g.data());
+      std::vector<double> g;
+      if (ahead.active && !ahead.g_taken) {
+        ahead.g_fut.wait();
+        g = ahead.g;
+        rng->r.engine = ahead.after_g;
+        ahead.g_taken = true;
+      } else {
+        g.resize(static_cast<size_t>(n));
+        rng->r.gaussian(n, 1, g.data());
+      }
       View gv = view_in(c, g.data(), n, 1, n, NPCG_HOST);
       return power_estimate(c, *op->op, s, cfg->q, gv.p);
     };
@@ -1130,6 +1195,7 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
         }
       }
     }
+    ahead.finish();  // an unused draw-ahead block is discarded (the engine never saw it)
     const double lmin = s.ell == 0 ? 0.0 : s.lambda_host.back();
     const double e0 = err ? std::max(0.0, *err) : 0.0;
     outcome->ell_final = s.ell;

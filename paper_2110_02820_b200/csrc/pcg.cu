@@ -879,6 +879,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   i64 nrb = 0, ncb = 0, cpb = 0, pstride = 0;
   DBuf<i64> units;
   DBuf<int> cseg, ustart;
+  double sym_entries = 0.0;  // entries of A streamed per iteration in symmetric use
   DBuf<double> colpart;
   int sym = 0;
   if (dense) {
@@ -899,6 +900,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
         cum[static_cast<size_t>(rb + 1)] = cum[static_cast<size_t>(rb)] + static_cast<double>(n - rb * dpw) * cnt;
       }
       const double W = cum[static_cast<size_t>(nrb)];
+      sym_entries = W;
       auto pos = [&](i64 c) -> std::pair<i64, i64> {  // (row block, column) where CTA c starts
         if (c >= G) return {nrb - 1, n};
         const double wc = W * static_cast<double>(c) / static_cast<double>(G);
@@ -1023,7 +1025,8 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
     NPCG_CUDA(cudaMemcpy(&h, st, sizeof(State), cudaMemcpyDeviceToHost));
     i64 iters = 0;
     for (i64 s = 0; s < S; ++s) iters = std::max<i64>(iters, h.c[s].iters);
-    const double a_bytes = gram ? 8.0 * gram->m * n : 8.0 * n * n;  // the reference's bytes (sym reads ~half)
+    // bytes the kernel's algorithm streams: X, all of A, or A's block-upper part
+    const double a_bytes = gram ? 8.0 * gram->m * n : sym ? 8.0 * sym_entries : 8.0 * n * n;
     const double a_flops = gram ? 4.0 * gram->m * n * S : 2.0 * n * n * S;
     const double u_bytes = nys ? 2.0 * 8.0 * n * pre->ell : 0.0;
     const double u_flops = nys ? 4.0 * n * pre->ell * S : 0.0;

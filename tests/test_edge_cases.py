@@ -128,6 +128,50 @@ def test_persistent_and_multikernel_pcg_agree(tmp_path):
             assert np.linalg.norm(xp - xc) <= 1e-10 * np.linalg.norm(xc)
 
 
+_SYM_DRIVER = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2110_02820_b200 as npcg
+rng = np.random.default_rng(11)
+n = 9001  # several row blocks of the symmetric persistent path (4096 / 2048 rows), ragged last block
+g = rng.standard_normal((n, 300))
+a = (g * np.exp(-np.arange(300) / 40.0)) @ g.T / 300.0
+a = 0.5 * (a + a.T)
+op = npcg.DenseOperator(a)
+omega = npcg.Rng(7).gaussian_matrix(n, 200)
+ap = npcg.nystrom_from_sketch(npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, omega))
+out = {}
+for s in (1, 2, 3, 4):
+    b = rng.standard_normal((n, s)) if s > 1 else rng.standard_normal(n)
+    r = npcg.nystrom_pcg(op, b, 1e-3, npcg.build_preconditioner(ap, 1e-3), eta=1e-10, relative=True)
+    r = r if isinstance(r, list) else [r]
+    out[s] = [(rr.iterations, rr.x) for rr in r]
+np.save(sys.argv[2], np.array([out], dtype=object), allow_pickle=True)
+"""
+
+
+@pytest.mark.gpu
+def test_symmetric_dense_pcg_matches_multikernel(tmp_path):
+    """The persistent dense PCG reads only the block-upper part of A (row axpy
+    + mirrored column dots); it must agree with the multi-kernel loop, which
+    reads all of A (coldot), for 1-4 right-hand sides over several row blocks."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("persistent", "classic"):
+        env = dict(os.environ)
+        if mode == "classic":
+            env["NPCG_PCG"] = "classic"
+        f = tmp_path / f"{mode}.npy"
+        r = subprocess.run([sys.executable, "-c", _SYM_DRIVER, root, str(f)], env=env, capture_output=True,
+                           text=True, timeout=900)
+        assert r.returncode == 0, r.stderr
+        res[mode] = np.load(f, allow_pickle=True)[0]
+    for s in (1, 2, 3, 4):
+        for (ip, xp), (ic, xc) in zip(res["persistent"][s], res["classic"][s]):
+            assert ip > 5 and abs(ip - ic) <= 1, (s, ip, ic)
+            assert np.linalg.norm(xp - xc) <= 1e-9 * np.linalg.norm(xc), s
+
+
 @pytest.mark.parametrize("n,d", [(1300, 3), (700, 7), (257, 32), (5000, 32), (4099, 17)])
 def test_matrix_free_kernel_paths(npcg, n, d):
     """Fused symmetric (k <= 2; n = 5000 / 4099 give several block pairs per

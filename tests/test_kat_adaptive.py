@@ -123,3 +123,26 @@ def test_column_sampling_drives_the_adaptive_loop(impl):  # adaptive_test.cpp:18
     gram = impl.GramRidgeOperator(rng.gaussian_matrix(30, 10))
     with pytest.raises(RuntimeError):
         impl.adaptive(gram, rng, mode="ratio", ell0=2, ell_max=10, mu=1e-2, tau=10.0, sketch="column_sampling")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ell0,ell_max,diag", [(4, 16, "flat"), (5, 12, "flat"), (10, 100, "tail"), (3, 40, "poly")])
+def test_adaptive_stream_position_matches_reference(orc, ell0, ell_max, diag):
+    """The library's draw-ahead (next Omega block and power vector drawn on a
+    host thread while the GPU works) must leave the caller's Rng exactly where
+    the reference's sequential draws leave it (random.hpp:11-20), whether the
+    loop stops on the estimate, on the cap after an estimate, or on the top-up."""
+    import paper_2110_02820_b200 as npcg
+    n = 100
+    d = {"flat": np.ones(n), "tail": np.r_[1.0, np.full(n - 1, 1e-12)],
+         "poly": np.arange(1, n + 1, dtype=float) ** -2.0}[diag]
+    outs, rngs = [], []
+    for impl in (npcg, orc):
+        rng = impl.Rng(21)
+        outs.append(impl.adaptive(impl.DenseOperator(np.diag(d)), rng, mode="error", ell0=ell0, ell_max=ell_max,
+                                  mu=1e-3, tau=10.0))
+        rngs.append(rng)
+    assert (outs[0].ell_final, outs[0].doublings, outs[0].hit_cap) == (outs[1].ell_final, outs[1].doublings,
+                                                                       outs[1].hit_cap)
+    assert rngs[0].normal() == rngs[1].normal()
+    assert np.array_equal(rngs[0].gaussian_vector(5), rngs[1].gaussian_vector(5))
