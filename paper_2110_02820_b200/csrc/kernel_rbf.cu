@@ -407,10 +407,10 @@ void kfree_fused(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, dou
   NPCG_LAUNCH(ctx, kfree_fused_kernel<S>, dim3(static_cast<unsigned>(rb), static_cast<unsigned>(splits)), KF_THREADS,
               static_cast<int>(smem), op.pts.p(), op.pts.ld, op.n, d, dp, op.norms.p, c, V, ldv, out, ldo, tps,
               splits > 1 ? part.p : static_cast<double*>(nullptr), gate);
+  ctx.prof_work(static_cast<double>(op.n) * op.n * (2.0 * dp + 2.0 * S), 8.0 * op.n * (d + 2 * S));
   if (splits > 1)
     NPCG_LAUNCH(ctx, kfree_reduce_kernel, static_cast<unsigned>(cdiv(op.n * S, 256)), 256, 0, part.p, splits, op.n,
                 S, out, ldo, gate);
-  ctx.prof_work(static_cast<double>(op.n) * op.n * (2.0 * dp + 2.0 * S), 8.0 * op.n * (d + 2 * S));
 }
 
 // ---------------------------------------------------------------------------
@@ -660,6 +660,127 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
   }
 }
 
+void init_exp_table64() {
+  static std::once_flag tab_once;
+  std::call_once(tab_once, [] {
+    double h[KF_TAB64];
+    for (int j = 0; j < KF_TAB64; ++j) h[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / KF_TAB64));
+    NPCG_CUDA(cudaMemcpyToSymbol(kf_exp2_tab64_g, h, sizeof(h)));
+  });
+}
+
+// One pass per kernel block: K[a + b*ldk] = k(x_{row0+a}, x_{col0+b}) for a <
+// rows, b < cols (unit diagonal), a 128 x 64 tile per CTA -- the DMMA dots of
+// the scaled points seeded with c||x_i||^2, + c||x_j||^2, min(., 0), the table
+// exp, one store. Replaces the -2 X X^T GEMM + the epilogue's read-modify-write.
+constexpr int KB_TPC = 8;  // column tiles per CTA (row block, table and prologue reused)
+template <int DP, bool CLAMP>
+__global__ void __launch_bounds__(KF_THREADS, 2)
+    kblock_kernel(const double* __restrict__ pts, i64 ldp, int d, int dp_rt, const double* __restrict__ nrm,
+                  i64 row0, i64 rows, i64 col0, i64 cols, double* __restrict__ K, i64 ldk) {
+  extern __shared__ double kfs[];
+  const int dp = DP ? DP : dp_rt;
+  const int lds = dp + 1;
+  double* XI = kfs;                   // [128][lds]
+  double* XJ = XI + KF_BM * lds;      // [2][64][lds]
+  double* NJ = XJ + 2 * KF_BN * lds;  // [2][64]
+  double* TAB = NJ + 2 * KF_BN;       // [KF_TAB64][KF_TABREP]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3, wm = warp / KF_WN, wn = warp % KF_WN;
+  const i64 a0 = static_cast<i64>(blockIdx.x) * KF_BM;
+  const i64 nct = (cols + KF_BN - 1) / KF_BN;
+  const i64 ct0 = static_cast<i64>(blockIdx.y) * KB_TPC, ct1 = min(nct, ct0 + KB_TPC);
+  auto load_cols = [&](i64 b0, int buf) {
+    double* xj = XJ + buf * KF_BN * lds;
+    for (int idx = tid; idx < KF_BN * dp; idx += KF_THREADS) {
+      const int r = idx % KF_BN, k = idx / KF_BN;
+      const bool ok = b0 + r < cols && k < d;
+      cp_async8(xj + r * lds + k, ok ? pts + (col0 + b0 + r) + static_cast<i64>(k) * ldp : pts, ok);
+    }
+    for (int r = tid; r < KF_BN; r += KF_THREADS) {
+      const bool ok = b0 + r < cols;
+      cp_async8(NJ + buf * KF_BN + r, ok ? nrm + col0 + b0 + r : nrm, ok);
+    }
+    cp_async_commit();
+  };
+  if (ct0 < ct1) load_cols(ct0 * KF_BN, 0);
+  for (int idx = tid; idx < KF_BM * dp; idx += KF_THREADS) {
+    const int r = idx % KF_BM, k = idx / KF_BM;
+    XI[r * lds + k] = (a0 + r < rows && k < d) ? pts[(row0 + a0 + r) + static_cast<i64>(k) * ldp] : 0.0;
+  }
+  for (int idx = tid; idx < KF_TAB64 * KF_TABREP; idx += KF_THREADS) TAB[idx] = kf_exp2_tab64_g[idx / KF_TABREP];
+  const double* tab_lane = TAB + (lane & (KF_TABREP - 1));
+  double ni[4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const i64 a = a0 + wm * 32 + f * 8 + g;
+    ni[f] = a < rows ? nrm[row0 + a] : 0.0;
+  }
+  for (i64 ct = ct0; ct < ct1; ++ct) {
+    const int buf = static_cast<int>((ct - ct0) & 1);
+    cp_async_wait_all();
+    __syncthreads();
+    if (ct + 1 < ct1) load_cols((ct + 1) * KF_BN, buf ^ 1);
+    const double* xj = XJ + buf * KF_BN * lds;
+    double acc[4][4][2];
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[f][q][0] = acc[f][q][1] = ni[f];
+#pragma unroll 8
+    for (int kk = 0; kk < dp; kk += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) av[f] = XI[(wm * 32 + f * 8 + g) * lds + kk + t];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bv[q] = xj[(wn * 32 + q * 8 + g) * lds + kk + t];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) kf_dmma(acc[f][q][0], acc[f][q][1], av[f], bv[q]);
+    }
+    const i64 b0 = ct * KF_BN;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * 32 + q * 8 + 2 * t + e;
+        const i64 b = b0 + col;
+        const double nj = NJ[buf * KF_BN + col];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const i64 a = a0 + wm * 32 + f * 8 + g;
+          const double ex = exp_tab64<CLAMP>(fmin(acc[f][q][e] + nj, 0.0), tab_lane);
+          if (a < rows && b < cols) K[a + b * ldk] = row0 + a == col0 + b ? 1.0 : ex;
+        }
+      }
+  }
+}
+
+template <int DP, bool CLAMP>
+void kblock_launch(Ctx& ctx, const KernelFreeOp& op, i64 row0, i64 rows, i64 col0, i64 cols, double* K, i64 ldk) {
+  const int d = static_cast<int>(op.d), dp = (d + 3) / 4 * 4;
+  const i64 smem = ((KF_BM + 2 * KF_BN) * static_cast<i64>(dp + 1) + 2 * KF_BN + KF_TAB64 * KF_TABREP) * 8;
+  static bool attr = false;
+  if (!attr) {
+    NPCG_CUDA(cudaFuncSetAttribute(kblock_kernel<DP, CLAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  NPCG_LAUNCH(ctx, (kblock_kernel<DP, CLAMP>),
+              dim3(static_cast<unsigned>(cdiv(rows, KF_BM)), static_cast<unsigned>(cdiv(cdiv(cols, KF_BN), KB_TPC))),
+              KF_THREADS,
+              static_cast<int>(smem), op.pts_s.p(), op.pts_s.ld, d, dp, op.norms_s.p, row0, rows, col0, cols, K, ldk);
+  ctx.prof_work(2.0 * rows * cols * dp, 8.0 * rows * cols);
+}
+
+void kernel_block(Ctx& ctx, const KernelFreeOp& op, i64 row0, i64 rows, i64 col0, i64 cols, double* K, i64 ldk) {
+  init_exp_table64();
+  const int dp = (static_cast<int>(op.d) + 3) / 4 * 4;
+  const bool clamp = !(std::fabs(-1.0 / (2.0 * op.sigma * op.sigma)) * 4.0 * op.max_norm < 690.0);
+  if (dp == 32 && !clamp) kblock_launch<32, false>(ctx, op, row0, rows, col0, cols, K, ldk);
+  else kblock_launch<0, true>(ctx, op, row0, rows, col0, cols, K, ldk);
+}
+
 template <int S, int DP, bool CLAMP>
 void kfree_sym_launch(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, i64 smem, i64 npairs, double c,
                       double* part, const int* gate, i64& grid) {
@@ -686,12 +807,7 @@ void kfree_sym(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, doubl
   const i64 smem = ((KF_BM + 2 * KF_BN) * static_cast<i64>(dp + 1) + 2 * KF_BN + 2 * S * KF_BN + 8 * KF_BN * S +
                     2 * KF_BM * S + KF_TAB64 * KF_TABREP) *
                    8;
-  static std::once_flag tab_once;
-  std::call_once(tab_once, [] {
-    double h[KF_TAB64];
-    for (int j = 0; j < KF_TAB64; ++j) h[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / KF_TAB64));
-    NPCG_CUDA(cudaMemcpyToSymbol(kf_exp2_tab64_g, h, sizeof(h)));
-  });
+  init_exp_table64();
   const double c = -1.0 / (2.0 * op.sigma * op.sigma);
   // |exponent| <= |c| max ||x_i - x_j||^2 <= |c| 4 max ||x||^2: below 700 no clamp is needed
   const bool clamp = !(std::fabs(c) * 4.0 * op.max_norm < 690.0);
@@ -706,10 +822,10 @@ void kfree_sym(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, doubl
   DBuf<double> part(grid * S * op.n, ctx.stream);
   NPCG_CUDA(cudaMemsetAsync(part.p, 0, sizeof(double) * grid * S * op.n, ctx.stream));
   launch(part.p, grid);
-  NPCG_LAUNCH(ctx, kfree_reduce_kernel, static_cast<unsigned>(cdiv(op.n * S, 256)), 256, 0, part.p,
-              static_cast<int>(grid), op.n, S, out, ldo, gate);
   // reference work (every entry of K): the kernel evaluates the upper blocks only
   ctx.prof_work(static_cast<double>(op.n) * op.n * (2.0 * d + 2.0 * S), 8.0 * op.n * (d + 2 * S));
+  NPCG_LAUNCH(ctx, kfree_reduce_kernel, static_cast<unsigned>(cdiv(op.n * S, 256)), 256, 0, part.p,
+              static_cast<int>(grid), op.n, S, out, ldo, gate);
 }
 
 }  // namespace
@@ -800,11 +916,15 @@ void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ld
     NPCG_CUDA(cudaMemset2DAsync(out, sizeof(double) * ldo, 0, sizeof(double) * n, k, ctx.stream));
     for (i64 r0 = 0; r0 < n; r0 += R) {
       const i64 rb = std::min(R, n - r0), L = n - r0;
-      gemm(ctx, L, rb, op.d, -2.0, Operand{op.pts.p() + r0, op.pts.ld, false},
-           Operand{op.pts.p() + r0, op.pts.ld, false}, 0.0, Kt.p(), Kt.ld);
-      NPCG_LAUNCH(ctx, kernel_colblock_epilogue_kernel,
-                  static_cast<unsigned>(std::min<i64>(cdiv(rb * L, 256), ctx.sm_count * 16)), 256, 0, Kt.p(), Kt.ld, L,
-                  rb, i64{0}, op.norms.p + r0, c);
+      if (op.d <= 64) {  // one fused pass (DMMA dots + exp + store)
+        kernel_block(ctx, op, r0, L, r0, rb, Kt.p(), Kt.ld);
+      } else {
+        gemm(ctx, L, rb, op.d, -2.0, Operand{op.pts.p() + r0, op.pts.ld, false},
+             Operand{op.pts.p() + r0, op.pts.ld, false}, 0.0, Kt.p(), Kt.ld);
+        NPCG_LAUNCH(ctx, kernel_colblock_epilogue_kernel,
+                    static_cast<unsigned>(std::min<i64>(cdiv(rb * L, 256), ctx.sm_count * 16)), 256, 0, Kt.p(), Kt.ld,
+                    L, rb, i64{0}, op.norms.p + r0, c);
+      }
       gemm(ctx, rb, k, L, 1.0, Operand{Kt.p(), Kt.ld, true}, Operand{V + r0, ldv, true}, 1.0, out + r0, ldo);
       if (L > rb)
         gemm(ctx, L - rb, k, rb, 1.0, Operand{Kt.p() + rb, Kt.ld, false}, Operand{V + r0, ldv, true}, 1.0,
