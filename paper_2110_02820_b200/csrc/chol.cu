@@ -121,10 +121,16 @@ __device__ __noinline__ bool diag_factor(Tile& T, Tile& Xs, int nr) {
     if (lane == 0) rs[j] = r;
     const double l = lane == j ? d * r : row[j] * r;
     if (lane >= j) row[j] = l;
+    // the next pivot's column first: its multiplier comes by one shuffle, so
+    // the chain to the next step is shfl -> rsqrt -> mul -> shfl -> fma
+    if (j + 1 < CB) {
+      const double ln = __shfl_sync(0xffffffffu, l, j + 1);
+      if (lane >= j + 1) row[j + 1] -= l * ln;
+    }
     lv[j & 1][lane] = l;
     __syncwarp();
 #pragma unroll
-    for (int c = j + 1; c < CB; ++c) {
+    for (int c = j + 2; c < CB; ++c) {  // off the critical path
       const double lc = lv[j & 1][c];
       if (lane >= c) row[c] -= l * lc;
     }
