@@ -26,7 +26,9 @@ struct NystromApproximation {  // nystrom.hpp:19-33
   double lambda_min() const { return lambda.size() == 0 ? 0.0 : lambda(lambda.size() - 1); }
 };
 
-/// Cached test matrix and sketch (nystrom.hpp:42-48), on device and grown in place.
+/// Cached test matrix and sketch (nystrom.hpp:42-48), on device. A value:
+/// extending returns a new pair that shares the device storage copy-on-append
+/// (npcg_nys_clone), so the input pair never changes.
 struct SketchPair {
   std::shared_ptr<npcg_nys> device;
   Index n = 0;
@@ -42,6 +44,11 @@ namespace detail {
 inline std::shared_ptr<npcg_nys> own(npcg_nys* h) {
   return std::shared_ptr<npcg_nys>(h, [](npcg_nys* p) { npcg_nys_destroy(p); });
 }
+inline std::shared_ptr<npcg_nys> clone(const std::shared_ptr<npcg_nys>& h, bool factors_only) {
+  npcg_nys* c = nullptr;
+  check_status(npcg_nys_clone(h.get(), factors_only ? 1 : 0, &c));
+  return own(c);
+}
 inline NystromApproximation fetch(const std::shared_ptr<npcg_nys>& nys) {
   std::int64_t n = 0, size = 0, ell = 0;
   double shift = 0.0;
@@ -52,7 +59,7 @@ inline NystromApproximation fetch(const std::shared_ptr<npcg_nys>& nys) {
   a.shift_used = shift;
   check_status(npcg_nys_get(nys.get(), a.lambda.data(), ell ? a.u.data() : nullptr, std::max<std::int64_t>(n, 1),
                             NPCG_HOST));
-  a.device = nys;
+  a.device = clone(nys, true);  // the approximation is a value: later refactors of the pair leave it alone
   return a;
 }
 }  // namespace detail
@@ -68,8 +75,9 @@ inline SketchPair make_empty_sketch(const LinearOperator& op) {
 /// the reference's stream order; Gram-Schmidt, QR and Y = A Omega on device.
 inline SketchPair extend_sketch(const SketchPair& pair, const LinearOperator& op, Index extra, Rng& rng) {
   if (pair.dim() != op.dim()) throw std::invalid_argument("extend_sketch: dimension mismatch");
-  check_status(npcg_nys_extend_rng(pair.device.get(), extra, rng.handle()));
-  return pair;
+  SketchPair out{detail::clone(pair.device, false), pair.n};
+  check_status(npcg_nys_extend_rng(out.device.get(), extra, rng.handle()));
+  return out;
 }
 
 /// nystrom_from_sketch (nystrom.cpp:96-140).
@@ -89,13 +97,14 @@ inline NystromApproximation randomized_nystrom(const LinearOperator& op, Index e
 inline SketchPair extend_sketch_columns(const SketchPair& pair, const LinearOperator& op, Index extra,
                                         std::vector<Index>& used, Rng& rng) {
   if (pair.dim() != op.dim()) throw std::invalid_argument("extend_sketch_columns: dimension mismatch");
-  check_status(npcg_nys_extend_columns(pair.device.get(), extra, rng.handle()));
+  SketchPair out{detail::clone(pair.device, false), pair.n};
+  check_status(npcg_nys_extend_columns(out.device.get(), extra, rng.handle()));
   int64_t count = 0;
-  check_status(npcg_nys_used(pair.device.get(), nullptr, &count));
+  check_status(npcg_nys_used(out.device.get(), nullptr, &count));
   std::vector<int64_t> idx(static_cast<size_t>(count));
-  check_status(npcg_nys_used(pair.device.get(), idx.data(), &count));
+  check_status(npcg_nys_used(out.device.get(), idx.data(), &count));
   used.assign(idx.begin(), idx.end());
-  return pair;
+  return out;
 }
 
 /// column_sampling_nystrom (nystrom.cpp:150-158): ell distinct columns from rng.

@@ -180,10 +180,21 @@ int npcg_nys_info(const npcg_nys* nys, int64_t* n, int64_t* sketch_cols, int64_t
 int npcg_nys_get(npcg_nys* nys, double* lambda, double* u, int64_t ldu, int where);
 /* The cached sketch pair (omega, y: n x size), nullable outputs. */
 int npcg_nys_get_sketch(npcg_nys* nys, double* omega, double* y, int64_t ld, int where);
+/* A second handle on the same sketch pair and factored approximation, O(1):
+ * the sketch storage is shared copy-on-append (appending through one handle
+ * never changes what the other sees), the factors are immutable and shared.
+ * This gives the reference's value semantics -- extend_sketch returns a new
+ * SketchPair and leaves its input unchanged (nystrom.cpp:36-58), and a
+ * NystromApproximation / preconditioner is unaffected by later extends or
+ * refactors of the pair it came from. factors_only != 0: the clone holds only
+ * the approximation (no sketch, no operator). */
+int npcg_nys_clone(const npcg_nys* nys, int factors_only, npcg_nys** out);
 int npcg_nys_destroy(npcg_nys* nys);
 
 /* ---- preconditioner (preconditioner.hpp:20-65) --------------------------- */
-/* build_preconditioner(approx, mu), preconditioner.cpp:80-89 (mu > 0). */
+/* build_preconditioner(approx, mu), preconditioner.cpp:80-89 (mu > 0). The
+ * preconditioner keeps its own reference to the factors: later extends /
+ * refactors of `nys` (or destroying it) do not affect it. */
 int npcg_pre_create(npcg_nys* nys, double mu, npcg_pre** out);
 /* apply_inverse / apply_inverse_block (preconditioner.cpp:27-45), R n x s. */
 int npcg_pre_apply_inverse(npcg_pre* pre, int64_t s, const double* r, int64_t ldr, double* z,
@@ -215,7 +226,8 @@ typedef struct {
  * share one pass over A per iteration (column j == nystrom_pcg on column j).
  * pre == NULL -> identity (cg on A + mu I, solvers.cpp:111-120).
  * history: s x (max_iter+1) col-major residual norms (nullable).
- * iterates: (max_iter+1) x n x s (nullable; needs record_iterates).
+ * iterates: (max_iter+1) x n x s (nullable; needs record_iterates); only the
+ * rows t < max history_len are written (device memory grows with the loop).
  * Returns NPCG_EDIVERGED if any column diverged (its report says which). */
 int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, int64_t ldb,
              const double* x0, int64_t ldx0, const npcg_solve_opts* opts, double* x, int64_t ldx,

@@ -421,17 +421,34 @@ class _Nys:
             self.h = None
 
 
-@dataclass
 class NystromApproximation:
-    """reference NystromApproximation (nystrom.hpp:19-33); U/lambda fetched from device."""
-    u: np.ndarray
-    lam: np.ndarray
-    shift_used: float
-    h: object = field(default=None, repr=False)
+    """reference NystromApproximation (nystrom.hpp:19-33). The factors live on
+    the device (a factors-only npcg_nys handle, immutable); `lam` is mirrored
+    on construction, `u` is downloaded on first access only."""
+
+    def __init__(self, u, lam, shift_used, h=None, n=None):
+        self._u, self.lam, self.shift_used, self.h = u, lam, shift_used, h
+        self._n = n if n is not None else (u.shape[0] if u is not None else 0)
+
+    @property
+    def u(self) -> np.ndarray:
+        if self._u is None:
+            e = self.lam.size
+            u = np.empty((self._n, e), order="F")
+            if e:
+                _check(lib().npcg_nys_get(_vp(self.h.h), None, _ptr(u), _i64(max(self._n, 1)), HOST))
+            self._u = u
+        return self._u
 
     @property
     def lambda_min(self):
         return float(self.lam[-1]) if self.lam.size else 0.0
+
+    def dim(self):
+        return self._n
+
+    def size(self):
+        return int(self.lam.size)
 
     def rank(self):
         return int(np.count_nonzero(self.lam > 0))
@@ -440,14 +457,22 @@ class NystromApproximation:
         return (self.u * self.lam) @ self.u.T
 
 
-def _approx_from(nys: _Nys, with_u: bool = True) -> NystromApproximation:
+def _clone(nys: "_Nys", factors_only: bool) -> "_Nys":
+    h = _vp()
+    _check(lib().npcg_nys_clone(_vp(nys.h), int(factors_only), C.byref(h)))
+    return _Nys(h.value)
+
+
+def _approx_from(nys: _Nys) -> NystromApproximation:
+    """The factored approximation of `nys` as an independent value: a
+    factors-only handle (later extends / refactors of the pair leave it
+    unchanged); U stays on the device until `.u` is read."""
     n, size, ell, shift = _i64(), _i64(), _i64(), C.c_double()
     _check(lib().npcg_nys_info(_vp(nys.h), C.byref(n), C.byref(size), C.byref(ell), C.byref(shift)))
     e = max(ell.value, 0)
     lam = np.empty(e)
-    u = np.empty((n.value, e), order="F") if with_u else None
-    _check(lib().npcg_nys_get(_vp(nys.h), _ptr(lam), _ptr(u), _i64(max(n.value, 1)), HOST))
-    return NystromApproximation(u if u is not None else np.empty((n.value, 0)), lam, shift.value, nys)
+    _check(lib().npcg_nys_get(_vp(nys.h), _ptr(lam), None, _i64(max(n.value, 1)), HOST))
+    return NystromApproximation(None, lam, shift.value, _clone(nys, True), n.value)
 
 
 class SketchPair:
@@ -497,33 +522,40 @@ class _PendingSketch:
         return 0
 
 
-def extend_sketch(pair, op: LinearOperator, extra: int, rng: Rng) -> SketchPair:
-    """extend_sketch (nystrom.cpp:36-58); the device pair is grown in place
-    (old columns untouched) and returned."""
+def _fresh_pair(pair, op, what):
+    """The pair a non-mutating extend writes into: an empty sketch bound to
+    `op`, or an O(1) copy-on-append clone of `pair` (the input stays as it was,
+    as the reference's extend_sketch returns a new SketchPair)."""
     if isinstance(pair, _PendingSketch):
         if pair.n != op.dim():
-            raise InvalidArgument("extend_sketch: dimension mismatch")
-        pair = make_empty_sketch(op)
-    _check(lib().npcg_nys_extend_rng(_vp(pair.h), _i64(extra), _vp(rng.h)))
-    return pair
+            raise InvalidArgument(f"{what}: dimension mismatch")
+        return make_empty_sketch(op)
+    if pair.op.dim() != op.dim():
+        raise InvalidArgument(f"{what}: dimension mismatch")
+    return SketchPair(_clone(pair._nys, False), pair.op)
+
+
+def extend_sketch(pair, op: LinearOperator, extra: int, rng: Rng) -> SketchPair:
+    """extend_sketch (nystrom.cpp:36-58): returns a new pair; `pair` is left
+    unchanged (device storage is shared copy-on-append)."""
+    out = _fresh_pair(pair, op, "extend_sketch")
+    _check(lib().npcg_nys_extend_rng(_vp(out.h), _i64(extra), _vp(rng.h)))
+    return out
 
 
 def extend_sketch_with(pair, op: LinearOperator, fresh) -> SketchPair:
     """extend_sketch with a caller-drawn raw Gaussian block (n x extra)."""
-    if isinstance(pair, _PendingSketch):
-        pair = make_empty_sketch(op)
+    out = _fresh_pair(pair, op, "extend_sketch")
     fresh = _f64(fresh)
-    _check(lib().npcg_nys_extend(_vp(pair.h), _i64(fresh.shape[1]), _ptr(fresh), _i64(fresh.shape[0]), HOST))
-    return pair
+    _check(lib().npcg_nys_extend(_vp(out.h), _i64(fresh.shape[1]), _ptr(fresh), _i64(fresh.shape[0]), HOST))
+    return out
 
 
 def extend_sketch_columns(pair, op: LinearOperator, extra: int, used: list, rng: Rng) -> SketchPair:
     """extend_sketch_columns (nystrom.cpp:60-94): appends `extra` unused columns of A
-    drawn from `rng`; `used` is extended in place (the handle keeps its own copy)."""
-    if isinstance(pair, _PendingSketch):
-        if pair.n != op.dim():
-            raise InvalidArgument("extend_sketch_columns: dimension mismatch")
-        pair = make_empty_sketch(op)
+    drawn from `rng`; `used` is extended in place (the handle keeps its own copy).
+    Returns a new pair; `pair` is left unchanged."""
+    pair = _fresh_pair(pair, op, "extend_sketch_columns")
     _check(lib().npcg_nys_extend_columns(_vp(pair.h), _i64(extra), _vp(rng.h)))
     cnt = _i64()
     _check(lib().npcg_nys_used(_vp(pair.h), None, C.byref(cnt)))
@@ -570,7 +602,7 @@ def make_approximation(u, lam, shift_used=0.0, ctx: Context | None = None) -> Ny
     h = _vp()
     _check(lib().npcg_nys_from_factors(_vp(ctx.h), _i64(n), _i64(ell), _ptr(u) if ell else None, _i64(max(n, 1)),
                                        _ptr(lam) if ell else None, C.c_double(shift_used), HOST, C.byref(h)))
-    return NystromApproximation(u.reshape(n, ell), lam, shift_used, _Nys(h.value))
+    return NystromApproximation(u.reshape(n, ell), lam, shift_used, _Nys(h.value), n)
 
 
 # ------------------------------------------------------------------ preconditioner
@@ -579,7 +611,7 @@ class NystromPreconditioner:
 
     def __init__(self, h, approx: NystromApproximation, mu: float):
         self.h, self.approx, self.mu = h, approx, mu
-        self.n = approx.u.shape[0]
+        self.n = approx.dim()
         self.lambda_ell = approx.lambda_min
 
     def __del__(self):

@@ -44,7 +44,6 @@ struct npcg_nys {
 };
 struct npcg_pre {
   npcg_ctx* ctx;
-  npcg_nys* nys;
   Pre p;
 };
 
@@ -749,21 +748,22 @@ int npcg_nys_from_factors(npcg_ctx* ctx, int64_t n, int64_t ell, const double* u
     Nys& s = h->s;
     s.ctx = &c;
     s.n = n;
-    s.ell = ell;
-    s.shift = shift_used;
-    s.factored = true;
+    auto f = std::make_shared<Factors>();
+    f->ell = ell;
+    f->shift = shift_used;
     if (ell > 0) {
-      upload(c, s.u, n, ell, u, ldu, where);
-      s.lambda.alloc(ell, c.stream);
-      NPCG_CUDA(cudaMemcpyAsync(s.lambda.p, lambda, sizeof(double) * ell,
+      upload(c, f->u, n, ell, u, ldu, where);
+      f->lambda.alloc(ell, c.stream);
+      NPCG_CUDA(cudaMemcpyAsync(f->lambda.p, lambda, sizeof(double) * ell,
                                 where == NPCG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c.stream));
-      s.lambda_host.resize(static_cast<size_t>(ell));
-      NPCG_CUDA(cudaMemcpyAsync(s.lambda_host.data(), s.lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToHost,
+      f->lambda_host.resize(static_cast<size_t>(ell));
+      NPCG_CUDA(cudaMemcpyAsync(f->lambda_host.data(), f->lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToHost,
                                 c.stream));
     } else {
-      s.u.alloc(n, 0, c.stream, false);
+      f->u.alloc(n, 0, c.stream, false);
     }
     c.sync();
+    s.fac = std::move(f);
     *out = h.release();
   });
 }
@@ -772,21 +772,22 @@ int npcg_nys_info(const npcg_nys* nys, int64_t* n, int64_t* sketch_cols, int64_t
     need(nys, "npcg_nys_info");
     if (n) *n = nys->s.n;
     if (sketch_cols) *sketch_cols = nys->s.size;
-    if (ell_factored) *ell_factored = nys->s.factored ? nys->s.ell : -1;
-    if (shift) *shift = nys->s.shift;
+    if (ell_factored) *ell_factored = nys->s.factored() ? nys->s.fac->ell : -1;
+    if (shift) *shift = nys->s.factored() ? nys->s.fac->shift : 0.0;
   });
 }
 int npcg_nys_get(npcg_nys* nys, double* lambda, double* u, int64_t ldu, int where) {
   return guard([&] {
     need(nys, "npcg_nys_get");
     Ctx& c = C(nys->ctx);
-    if (!nys->s.factored) fail(NPCG_ERUNTIME, "npcg_nys_get: approximation not factored (call npcg_nys_factor)");
-    const i64 ell = nys->s.ell;
+    if (!nys->s.factored()) fail(NPCG_ERUNTIME, "npcg_nys_get: approximation not factored (call npcg_nys_factor)");
+    const Factors& f = *nys->s.fac;
+    const i64 ell = f.ell;
     if (lambda && ell > 0) {
-      if (where == NPCG_HOST) std::memcpy(lambda, nys->s.lambda_host.data(), sizeof(double) * ell);
-      else NPCG_CUDA(cudaMemcpyAsync(lambda, nys->s.lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToDevice, c.stream));
+      if (where == NPCG_HOST) std::memcpy(lambda, f.lambda_host.data(), sizeof(double) * ell);
+      else NPCG_CUDA(cudaMemcpyAsync(lambda, f.lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToDevice, c.stream));
     }
-    if (u && ell > 0) download(c, nys->s.u.p(), nys->s.u.ld, nys->s.n, ell, u, ldu, where);
+    if (u && ell > 0) download(c, f.u.p(), f.u.ld, nys->s.n, ell, u, ldu, where);
     c.sync();
   });
 }
@@ -795,9 +796,27 @@ int npcg_nys_get_sketch(npcg_nys* nys, double* omega, double* y, int64_t ld, int
     need(nys, "npcg_nys_get_sketch");
     Ctx& c = C(nys->ctx);
     if (nys->s.size == 0) return;
-    if (omega) download(c, nys->s.omega.p(), nys->s.omega.ld, nys->s.n, nys->s.size, omega, ld, where);
-    if (y) download(c, nys->s.y.p(), nys->s.y.ld, nys->s.n, nys->s.size, y, ld, where);
+    if (omega) download(c, nys->s.omega().p(), nys->s.omega().ld, nys->s.n, nys->s.size, omega, ld, where);
+    if (y) download(c, nys->s.y().p(), nys->s.y().ld, nys->s.n, nys->s.size, y, ld, where);
     c.sync();
+  });
+}
+int npcg_nys_clone(const npcg_nys* nys, int factors_only, npcg_nys** out) {
+  return guard([&] {
+    need(nys, "npcg_nys_clone");
+    need(out, "npcg_nys_clone");
+    auto h = std::make_unique<npcg_nys>();
+    h->ctx = nys->ctx;
+    h->s.ctx = nys->s.ctx;
+    h->s.n = nys->s.n;
+    h->s.fac = nys->s.fac;
+    if (!factors_only) {  // shares the sketch store; the first append by either handle past the other copies
+      h->s.op = nys->s.op;
+      h->s.sk = nys->s.sk;
+      h->s.size = nys->s.size;
+      h->s.used = nys->s.used;
+    }
+    *out = h.release();
   });
 }
 int npcg_nys_destroy(npcg_nys* nys) {
@@ -815,10 +834,8 @@ int npcg_pre_create(npcg_nys* nys, double mu, npcg_pre** out) {
   return guard([&] {
     need(nys, "npcg_pre_create");
     C(nys->ctx);
-    if (!nys->s.factored) fail(NPCG_ERUNTIME, "build_preconditioner: approximation not factored");
     auto h = std::make_unique<npcg_pre>();
     h->ctx = nys->ctx;
-    h->nys = nys;
     pre_build(h->p, nys->s, mu);
     *out = h.release();
   });
@@ -885,16 +902,14 @@ int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, 
     }
     DMat X;
     X.alloc(n, s, c.stream, false);
-    DBuf<double> its;
-    if (iterates && po.record_iterates) {
-      its.alloc((po.max_iter + 1) * n * std::min<i64>(s, 8), c.stream);
-      its.zero();
-    }
+    const bool rec = iterates && po.record_iterates;
     for (i64 s0 = 0; s0 < s; s0 += 8) {
       const i64 sb = std::min<i64>(8, s - s0);
+      IterateRec its;
       PcgResult r = pcg_solve(c, *op->op, pre ? &pre->p : nullptr, mu, sb, B.p + s0 * B.ld, B.ld,
                               x0 ? X0.p + s0 * X0.ld : nullptr, X0.ld, po, X.p() + s0 * X.ld, X.ld,
-                              its.p ? its.p : nullptr, context);
+                              rec ? &its : nullptr, context);
+      i64 rows = 0;  // iterations recorded by any column of the batch
       for (i64 j = 0; j < sb; ++j) {
         const PcgColumnReport& cr = r.cols[static_cast<size_t>(j)];
         npcg_solve_report& rep = reports[s0 + j];
@@ -905,16 +920,18 @@ int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, 
         rep.eta_used = cr.eta_used;
         rep.wall_time = r.wall_time;
         rep.history_len = static_cast<int64_t>(cr.history.size());
+        rows = std::max<i64>(rows, rep.history_len);
         if (history)
           std::copy(cr.history.begin(), cr.history.end(), history + (s0 + j) * (po.max_iter + 1));
       }
-      if (its.p) {  // layout to caller: [t][col][n] for the whole s
-        std::vector<double> h(static_cast<size_t>((po.max_iter + 1) * n * sb));
-        NPCG_CUDA(cudaMemcpy(h.data(), its.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
-        for (i64 t = 0; t <= po.max_iter; ++t)
-          for (i64 j = 0; j < sb; ++j)
-            std::copy(h.begin() + (t * sb + j) * n, h.begin() + (t * sb + j + 1) * n,
-                      iterates + (t * s + s0 + j) * n);
+      if (rec) {  // layout to caller: [t][col][n] for the whole s; only the rows the loop reached
+        rows = std::min(rows, its.cap);
+        for (i64 t = 0; t < rows; ++t) {
+          const cudaMemcpyKind k = where == NPCG_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+          NPCG_CUDA(cudaMemcpyAsync(iterates + (t * s + s0) * n, its.buf.p + t * n * sb, sizeof(double) * n * sb, k,
+                                    c.stream));
+        }
+        c.sync();
       }
       if (r.diverged) {
         diverged = true;
@@ -993,7 +1010,7 @@ double dot_dev(Ctx& c, const double* a, const double* b, i64 n) {
 
 // estimate_error_power (adaptive.cpp:83-109) from the raw start vector g.
 double power_estimate(Ctx& c, Op& op, const Nys& s, i64 q, const double* g_dev) {
-  const i64 n = op.n, ell = s.factored ? s.ell : 0;
+  const i64 n = op.n, ell = s.factored() ? s.fac->ell : 0;
   DMat v, w, t;
   v.alloc(n, 1, c.stream, true);
   w.alloc(n, 1, c.stream, true);
@@ -1006,10 +1023,10 @@ double power_estimate(Ctx& c, Op& op, const Nys& s, i64 q, const double* g_dev) 
   for (i64 i = 0; i < q; ++i) {
     op.apply(v.p(), v.ld, 1, w.p(), w.ld);
     if (ell > 0) {  // w -= U (lambda .* (U^T v))
-      coldot(c, s.u.p(), s.u.ld, n, ell, v.p(), v.ld, 1, t.p(), t.ld);
-      scale_cols(c, t.p(), 1, ell, 1, s.lambda.p);  // t_j *= lambda_j (as a 1 x ell row)
+      coldot(c, s.fac->u.p(), s.fac->u.ld, n, ell, v.p(), v.ld, 1, t.p(), t.ld);
+      scale_cols(c, t.p(), 1, ell, 1, s.fac->lambda.p);  // t_j *= lambda_j (as a 1 x ell row)
       axpby(c, ell, 1, 0.0, t.p(), -1.0, t.p(), t.ld);  // t = -t (exact)
-      rowdot(c, s.u.p(), s.u.ld, n, ell, t.p(), t.ld, 1, w.p(), w.ld, w.p(), w.ld);
+      rowdot(c, s.fac->u.p(), s.fac->u.ld, n, ell, t.p(), t.ld, 1, w.p(), w.ld, w.p(), w.ld);
     }
     estimate = dot_dev(c, v.p(), w.p(), n);
     const double nrm = std::sqrt(sum_squares(c, w.p(), n, 1, w.ld));
@@ -1027,7 +1044,7 @@ int npcg_power_estimate(npcg_op* op, npcg_nys* nys, int64_t q, const double* g_r
     need(nys, "npcg_power_estimate");
     Ctx& c = C(op->ctx);
     if (q < 1) invalid("estimate_error_power: q must be >= 1");  // adaptive.cpp:86
-    if (nys->s.factored && nys->s.ell > 0 && nys->s.n != op->op->n)
+    if (nys->s.factored() && nys->s.fac->ell > 0 && nys->s.n != op->op->n)
       invalid("estimate_error_power: factor shape mismatch");
     View g = view_in(c, g_raw, op->op->n, 1, op->op->n, where);
     *est = power_estimate(c, *op->op, nys->s, q, g.p);
@@ -1039,7 +1056,7 @@ int npcg_power_estimate_rng(npcg_op* op, npcg_nys* nys, int64_t q, npcg_rng* rng
     need(nys, "npcg_power_estimate_rng");
     Ctx& c = C(op->ctx);
     if (q < 1) invalid("estimate_error_power: q must be >= 1");
-    if (nys->s.factored && nys->s.ell > 0 && nys->s.n != op->op->n)
+    if (nys->s.factored() && nys->s.fac->ell > 0 && nys->s.n != op->op->n)
       invalid("estimate_error_power: factor shape mismatch");
     std::vector<double> g(static_cast<size_t>(op->op->n));
     rng->r.gaussian(op->op->n, 1, g.data());  // gaussian_vector (adaptive.cpp:90)
@@ -1169,7 +1186,7 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
     } else {  // doubling_loop (adaptive.cpp:50-79)
       const double tol = tau * cfg->mu;
       auto should_stop = [&]() -> bool {
-        const double lmin = s.ell == 0 ? 0.0 : s.lambda_host.back();
+        const double lmin = s.fac->lambda_min();
         if (cfg->tol_mode == 1) return lmin <= tau * cfg->mu;  // adaptive.cpp:129-132
         const double e = estimate();                           // adaptive.cpp:115-121
         err = e;
@@ -1196,9 +1213,9 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
       }
     }
     ahead.finish();  // an unused draw-ahead block is discarded (the engine never saw it)
-    const double lmin = s.ell == 0 ? 0.0 : s.lambda_host.back();
+    const double lmin = s.fac->lambda_min();
     const double e0 = err ? std::max(0.0, *err) : 0.0;
-    outcome->ell_final = s.ell;
+    outcome->ell_final = s.fac->ell;
     outcome->doublings = doublings;
     outcome->hit_cap = hit_cap ? 1 : 0;
     outcome->has_error_estimate = err ? 1 : 0;

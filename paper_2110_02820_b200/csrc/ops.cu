@@ -80,18 +80,22 @@ void KernelFreeOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, 
 
 // ================================ Nyström ====================================
 namespace {
+/// Make columns [0, cols) of s's sketch writable by s: in place when s owns
+/// the written end of its store and the capacity suffices, otherwise a fresh
+/// store (doubling growth) with s's `size` columns copied over.
 void ensure_capacity(Nys& s, i64 cols) {
-  if (s.omega.cols >= cols) return;
-  const i64 cap = std::min<i64>(s.n, std::max<i64>(cols, 2 * s.omega.cols));
-  DMat om, y;
-  om.alloc(s.n, cap, s.ctx->stream, true);
-  y.alloc(s.n, cap, s.ctx->stream, true);
+  if (s.sk && s.sk->omega.cols >= cols && s.sk->filled == s.size) return;
+  const i64 have = s.sk ? s.sk->omega.cols : 0;
+  const i64 cap = std::min<i64>(s.n, std::max<i64>(cols, 2 * have));
+  auto st = std::make_shared<SketchStore>();
+  st->omega.alloc(s.n, cap, s.ctx->stream, true);
+  st->y.alloc(s.n, cap, s.ctx->stream, true);
   if (s.size > 0) {
-    copy2d(*s.ctx, s.n, s.size, s.omega.p(), s.omega.ld, om.p(), om.ld);
-    copy2d(*s.ctx, s.n, s.size, s.y.p(), s.y.ld, y.p(), y.ld);
+    copy2d(*s.ctx, s.n, s.size, s.sk->omega.p(), s.sk->omega.ld, st->omega.p(), st->omega.ld);
+    copy2d(*s.ctx, s.n, s.size, s.sk->y.p(), s.sk->y.ld, st->y.p(), st->y.ld);
   }
-  s.omega = std::move(om);
-  s.y = std::move(y);
+  st->filled = s.size;
+  s.sk = std::move(st);
 }
 }  // namespace
 
@@ -104,23 +108,24 @@ void nys_extend(Nys& s, const double* raw, i64 ld, i64 extra, int where) {
   const i64 n = s.n, old = s.size;
   DMat fresh;
   upload(ctx, fresh, n, extra, raw, ld, where);
+  ensure_capacity(s, old + extra);
+  SketchStore& st = *s.sk;
   // Two passes of block Gram-Schmidt against the existing columns.
   if (old > 0) {
     DMat coef;
     coef.alloc(old, extra, ctx.stream, false);
     for (int pass = 0; pass < 2; ++pass) {
-      gemm(ctx, old, extra, n, 1.0, Operand{s.omega.p(), s.omega.ld, true}, Operand{fresh.p(), fresh.ld, true}, 0.0,
+      gemm(ctx, old, extra, n, 1.0, Operand{st.omega.p(), st.omega.ld, true}, Operand{fresh.p(), fresh.ld, true}, 0.0,
            coef.p(), coef.ld);
-      gemm(ctx, n, extra, old, -1.0, Operand{s.omega.p(), s.omega.ld, false}, Operand{coef.p(), coef.ld, true}, 1.0,
+      gemm(ctx, n, extra, old, -1.0, Operand{st.omega.p(), st.omega.ld, false}, Operand{coef.p(), coef.ld, true}, 1.0,
            fresh.p(), fresh.ld);
     }
   }
-  ensure_capacity(s, old + extra);
-  double* q_new = s.omega.col(old);
-  orthonormalize(ctx, fresh.p(), fresh.ld, n, extra, q_new, s.omega.ld);
-  s.op->apply(q_new, s.omega.ld, extra, s.y.col(old), s.y.ld);
-  s.size = old + extra;
-  s.factored = false;
+  double* q_new = st.omega.col(old);
+  orthonormalize(ctx, fresh.p(), fresh.ld, n, extra, q_new, st.omega.ld);
+  s.op->apply(q_new, st.omega.ld, extra, st.y.col(old), st.y.ld);
+  s.size = st.filled = old + extra;
+  s.fac.reset();  // the handle now holds an unfactored, larger sketch
 }
 
 void nys_extend_columns(Nys& s, const std::vector<i64>& idx) {
@@ -128,16 +133,17 @@ void nys_extend_columns(Nys& s, const std::vector<i64>& idx) {
   const i64 old = s.size, extra = static_cast<i64>(idx.size());
   if (extra == 0) return;
   ensure_capacity(s, old + extra);
+  SketchStore& st = *s.sk;
   // omega columns: e_j (fresh capacity is zero; reused capacity is cleared first)
-  NPCG_CUDA(cudaMemset2DAsync(s.omega.col(old), s.omega.ld * 8, 0, s.n * 8, extra, ctx.stream));
+  NPCG_CUDA(cudaMemset2DAsync(st.omega.col(old), st.omega.ld * 8, 0, s.n * 8, extra, ctx.stream));
   DBuf<i64> d(extra, ctx.stream);
   NPCG_CUDA(cudaMemcpyAsync(d.p, idx.data(), sizeof(i64) * extra, cudaMemcpyHostToDevice, ctx.stream));
-  NPCG_LAUNCH(ctx, unit_cols_kernel, static_cast<unsigned>(cdiv(extra, 256)), 256, 0, s.omega.col(old), s.omega.ld,
+  NPCG_LAUNCH(ctx, unit_cols_kernel, static_cast<unsigned>(cdiv(extra, 256)), 256, 0, st.omega.col(old), st.omega.ld,
               d.p, extra);
-  s.op->columns(idx.data(), extra, s.y.col(old), s.y.ld);
+  s.op->columns(idx.data(), extra, st.y.col(old), st.y.ld);
   ctx.sync();
-  s.size = old + extra;
-  s.factored = false;
+  s.size = st.filled = old + extra;
+  s.fac.reset();
 }
 
 namespace {
@@ -151,22 +157,23 @@ double ulp_spacing(double x) {
 }
 }  // namespace
 
-// nystrom_from_sketch (nystrom.cpp:96-140).
+// nystrom_from_sketch (nystrom.cpp:96-140). The result is built in a fresh
+// Factors and published only after every check passed.
 void nys_factor(Nys& s) {
   Ctx& ctx = *s.ctx;
   const i64 n = s.n, ell = s.size;
-  s.ell = ell;
-  s.factored = true;
-  s.lambda_host.assign(static_cast<size_t>(ell), 0.0);
+  auto f = std::make_shared<Factors>();
+  f->ell = ell;
   if (ell == 0) {
-    s.u.alloc(n, 0, ctx.stream, false);
-    s.lambda.release();
-    s.shift = 0.0;
+    f->u.alloc(n, 0, ctx.stream, false);
+    s.fac = std::move(f);
     return;
   }
-  if (!all_finite(ctx, s.y.p(), n, ell, s.y.ld))
+  const DMat& om = s.omega();
+  const DMat& y = s.y();
+  if (!all_finite(ctx, y.p(), n, ell, y.ld))
     fail(NPCG_ERUNTIME, "nystrom_from_sketch: sketch has non-finite entries");
-  const double ynorm = std::sqrt(sum_squares(ctx, s.y.p(), n, ell, s.y.ld));
+  const double ynorm = std::sqrt(sum_squares(ctx, y.p(), n, ell, y.ld));
   const double nu0 = ulp_spacing(ynorm);
   double nu = nu0;
   DMat ynu, core, b;
@@ -175,14 +182,14 @@ void nys_factor(Nys& s) {
   b.alloc(n, ell, ctx.stream, false);
   bool factored = false;
   for (int attempt = 0; attempt <= 3; ++attempt, nu *= 10.0) {
-    add_scaled(ctx, n, ell, s.y.p(), nu, s.omega.p(), ynu.p(), ynu.ld);  // Y + nu Omega (shared ld)
-    gemm(ctx, ell, ell, n, 1.0, Operand{s.omega.p(), s.omega.ld, true}, Operand{ynu.p(), ynu.ld, true}, 0.0,
+    add_scaled(ctx, n, ell, y.p(), nu, om.p(), ynu.p(), ynu.ld);  // Y + nu Omega (shared ld)
+    gemm(ctx, ell, ell, n, 1.0, Operand{om.p(), om.ld, true}, Operand{ynu.p(), ynu.ld, true}, 0.0,
          core.p(), core.ld);
-    CholFactor f;
-    if (!cholesky(ctx, core.p(), ell, core.ld, f)) continue;
-    trsm_right_lt(ctx, n, ell, ynu.p(), ynu.ld, core.p(), core.ld, f, b.p(), b.ld);
+    CholFactor cf;
+    if (!cholesky(ctx, core.p(), ell, core.ld, cf)) continue;
+    trsm_right_lt(ctx, n, ell, ynu.p(), ynu.ld, core.p(), core.ld, cf, b.p(), b.ld);
     if (!all_finite(ctx, b.p(), n, ell, b.ld)) continue;
-    s.shift = nu;
+    f->shift = nu;
     factored = true;
     break;
   }
@@ -195,18 +202,20 @@ void nys_factor(Nys& s) {
   }
   ynu.buf.release();
   core.buf.release();
-  s.u.alloc(n, ell, ctx.stream, false);
+  f->u.alloc(n, ell, ctx.stream, false);
   DBuf<double> sigma(ell, ctx.stream);
-  thin_svd(ctx, b.p(), b.ld, n, ell, s.u.p(), s.u.ld, sigma.p);
-  s.lambda.alloc(ell, ctx.stream);
-  NPCG_LAUNCH(ctx, clamp_lambda_kernel, static_cast<unsigned>(cdiv(ell, 256)), 256, 0, sigma.p, ell, s.shift,
-              s.lambda.p);
-  NPCG_CUDA(cudaMemcpyAsync(s.lambda_host.data(), s.lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToHost,
+  thin_svd(ctx, b.p(), b.ld, n, ell, f->u.p(), f->u.ld, sigma.p);
+  f->lambda.alloc(ell, ctx.stream);
+  NPCG_LAUNCH(ctx, clamp_lambda_kernel, static_cast<unsigned>(cdiv(ell, 256)), 256, 0, sigma.p, ell, f->shift,
+              f->lambda.p);
+  f->lambda_host.assign(static_cast<size_t>(ell), 0.0);
+  NPCG_CUDA(cudaMemcpyAsync(f->lambda_host.data(), f->lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToHost,
                             ctx.stream));
   ctx.sync();
   for (i64 i = 1; i < ell; ++i)
-    if (s.lambda_host[i] > s.lambda_host[i - 1])
+    if (f->lambda_host[i] > f->lambda_host[i - 1])
       fail(NPCG_ERUNTIME, "nystrom_from_sketch: eigenvalue estimates out of order");
+  s.fac = std::move(f);
 }
 
 // ============================ preconditioner =================================
@@ -229,16 +238,17 @@ __global__ void scale_rows_kernel(double* T, i64 ell, i64 S, i64 ldt, const doub
 // build_preconditioner (preconditioner.cpp:80-89).
 void pre_build(Pre& p, const Nys& s, double mu) {
   if (!(mu > 0.0)) invalid("build_preconditioner: mu must be > 0");
+  if (!s.factored()) fail(NPCG_ERUNTIME, "build_preconditioner: approximation not factored");
   p.ctx = s.ctx;
-  p.nys = &s;
+  p.fac = s.fac;
   p.n = s.n;
-  p.ell = s.ell;
+  p.ell = s.fac->ell;
   p.mu = mu;
-  p.lambda_ell = s.ell == 0 ? 0.0 : s.lambda_host.back();
+  p.lambda_ell = s.fac->lambda_min();
   if (p.ell > 0) {
     p.gain_inv.alloc(p.ell, s.ctx->stream);
     p.gain_fwd.alloc(p.ell, s.ctx->stream);
-    NPCG_LAUNCH(*s.ctx, gains_kernel, static_cast<unsigned>(cdiv(p.ell, 256)), 256, 0, s.lambda.p, p.ell,
+    NPCG_LAUNCH(*s.ctx, gains_kernel, static_cast<unsigned>(cdiv(p.ell, 256)), 256, 0, s.fac->lambda.p, p.ell,
                 p.lambda_ell, mu, p.gain_inv.p, p.gain_fwd.p);
   }
 }
@@ -248,11 +258,11 @@ namespace {
 void lowrank_update(Pre& p, const double* g, const double* V, i64 ldv, i64 S, double* out, i64 ldo,
                     const int* gate) {
   Ctx& ctx = *p.ctx;
-  const Nys& s = *p.nys;
   if (p.ell == 0) {
     copy2d(ctx, p.n, S, V, ldv, out, ldo);
     return;
   }
+  const Factors& s = *p.fac;
   DMat T;
   T.alloc(p.ell, S, ctx.stream, false);
   if (S <= 8) {

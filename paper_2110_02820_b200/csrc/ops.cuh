@@ -123,31 +123,56 @@ void build_kernel_colblock(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma
 void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, i64 k, double* out, i64 ldo,
                        const int* gate);
 
+/// Device storage of a sketch pair (Omega, Y), capacity-managed. Several
+/// Nys handles may share one store (npcg_nys_clone, the facade's value-
+/// semantics extend_sketch): a handle of size s views the first s columns,
+/// and appending writes only columns >= s, so the store records how many
+/// columns have been written; a handle extending behind that mark (a branch)
+/// or past the capacity copies its own columns to a fresh store first.
+struct SketchStore {
+  DMat omega, y;
+  i64 filled = 0;
+};
+
+/// The factored approximation (nystrom.hpp:19-33): U, lambda, shift. It is
+/// immutable once published -- a Nys handle and every preconditioner built
+/// from it share it, so extending or refactoring the handle later never
+/// changes an existing preconditioner (the reference's value semantics).
+struct Factors {
+  DMat u;                         // n x ell
+  DBuf<double> lambda;            // ell, nonincreasing
+  std::vector<double> lambda_host;
+  i64 ell = 0;
+  double shift = 0.0;
+  double lambda_min() const { return ell == 0 ? 0.0 : lambda_host.back(); }
+};
+
 /// Cached sketch + factored approximation (nystrom.hpp:19-48).
 struct Nys {
   Ctx* ctx = nullptr;
   Op* op = nullptr;  // not owned; nullptr for from_factors
   i64 n = 0;
-  DMat omega, y;     // capacity-managed; first `size` columns valid
+  std::shared_ptr<SketchStore> sk;  // first `size` columns are this handle's pair
   i64 size = 0;
-  DMat u;            // n x ell
-  DBuf<double> lambda;
-  i64 ell = 0;
-  double shift = 0.0;
-  bool factored = false;
-  std::vector<double> lambda_host;
+  std::shared_ptr<const Factors> fac;  // null until factored; replaced only by a successful nys_factor
   std::vector<i64> used;  // column-sampling sketches: indices drawn so far (extend_sketch_columns)
+  bool factored() const { return static_cast<bool>(fac); }
+  const DMat& omega() const { return sk->omega; }
+  const DMat& y() const { return sk->y; }
 };
 void nys_extend(Nys& s, const double* raw, i64 ld, i64 extra, int where);
 /// Append unit columns e_j and A(:, j) for the given distinct indices
 /// (extend_sketch_columns / column_sampling_nystrom, nystrom.cpp:60-94,160-184).
 void nys_extend_columns(Nys& s, const std::vector<i64>& idx);
+/// nystrom_from_sketch: publishes a new Factors on success; on failure the
+/// handle keeps what it had (nothing is half-updated).
 void nys_factor(Nys& s);
 
-/// NystromPreconditioner (preconditioner.hpp:20-37).
+/// NystromPreconditioner (preconditioner.hpp:20-37). Holds its own reference
+/// to the factors it was built from.
 struct Pre {
   Ctx* ctx = nullptr;
-  const Nys* nys = nullptr;  // U, lambda (device); not owned
+  std::shared_ptr<const Factors> fac;  // U, lambda (device)
   i64 n = 0, ell = 0;
   double mu = 0.0, lambda_ell = 0.0;
   DBuf<double> gain_inv;  // (lambda_ell + mu)/(lambda + mu) - 1

@@ -960,8 +960,8 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
     pa.div = 1.0;
   }
   if (nys) {
-    pa.U = pre->nys->u.p();
-    pa.ldu = pre->nys->u.ld;
+    pa.U = pre->fac->u.p();
+    pa.ldu = pre->fac->u.ld;
     pa.ell = pre->ell;
     pa.gain = pre->gain_inv.p;
     pa.T = T.p;
@@ -1037,7 +1037,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
 }  // namespace
 
 PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* B, i64 ldb, const double* X0,
-                    i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, double* iterates, const char* context) {
+                    i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, IterateRec* iterates, const char* context) {
   using Clock = std::chrono::steady_clock;
   const auto t0 = Clock::now();
   if (S < 1 || S > kMaxS) fail(NPCG_EINVAL, "pcg_solve: 1..8 right-hand sides per batch");
@@ -1071,9 +1071,23 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
   NPCG_LAUNCH(ctx, fin0_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, opt.eta, opt.relative ? 1 : 0,
               hist.p, hstride);
   DBuf<int> run_flags;
+  // iterate record: room for iteration t (doubling growth, zero-filled)
+  auto reserve_iterate = [&](i64 t) -> double* {
+    if (t >= iterates->cap) {
+      const i64 cap = std::min<i64>(opt.max_iter + 1, std::max<i64>({t + 1, 2 * iterates->cap, 16}));
+      DBuf<double> nb(cap * n * S, ctx.stream);
+      nb.zero();
+      if (iterates->cap > 0)
+        NPCG_CUDA(cudaMemcpyAsync(nb.p, iterates->buf.p, sizeof(double) * iterates->cap * n * S,
+                                  cudaMemcpyDeviceToDevice, ctx.stream));
+      iterates->buf = std::move(nb);
+      iterates->cap = cap;
+    }
+    return iterates->buf.p + t * n * S;
+  };
   if (iterates) {
     run_flags.alloc(S, ctx.stream);
-    NPCG_LAUNCH(ctx, record_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, iterates, st.p,
+    NPCG_LAUNCH(ctx, record_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, reserve_iterate(0), st.p,
                 static_cast<const int*>(nullptr));
   }
   // z = P^{-1} r; p = z; rz = r.z
@@ -1122,7 +1136,7 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
       NPCG_LAUNCH(ctx, fin_res_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, static_cast<int>(t),
                   opt.max_iter, hist.p, hstride);
       if (iterates)
-        NPCG_LAUNCH(ctx, record_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, iterates + t * n * S, st.p,
+        NPCG_LAUNCH(ctx, record_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, reserve_iterate(t), st.p,
                     run_flags.p);
       if (!identity) pre_apply_inverse(*pre, R.p(), R.ld, S, Z.p(), Z.ld, gate);
       NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), R.p(), R.ld, Zp, ldz,

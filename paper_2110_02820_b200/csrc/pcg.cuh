@@ -32,11 +32,19 @@ struct PcgResult {
   std::string message;
 };
 
+/// Device record of the iterates (record_iterates, solvers.hpp:24): layout
+/// [t][s][n] for t < cap, zero where a column did not run; grown by doubling
+/// as the loop advances (not sized for max_iter up front).
+struct IterateRec {
+  DBuf<double> buf;
+  i64 cap = 0;  // iterations the buffer holds
+};
+
 /// Solves (A + mu I) X = B column by column with P^{-1} from `pre`
 /// (nullptr = identity, i.e. cg() on A + mu I). B, X0, X are device n x S
-/// (X0 nullable = 0). `iterates` (device, nullable): (max_iter+1) x n x S.
+/// (X0 nullable = 0). `iterates` (nullable): filled with x_0 .. x_t.
 PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* B, i64 ldb, const double* X0,
-                    i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, double* iterates,
+                    i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, IterateRec* iterates,
                     const char* context = "nystrom_pcg");
 
 struct BlockPcgResult {

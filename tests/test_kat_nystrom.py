@@ -154,3 +154,35 @@ def test_column_sampling_draws_match_the_oracle(impl, orc):
     orc.extend_sketch_columns(orc.make_empty_sketch(12), orc.DenseOperator(np.diag(np.arange(1.0, 13.0))), 4, ref,
                               orc.Rng(21))
     assert used == ref
+
+
+def test_extend_sketch_leaves_its_input_unchanged(impl):
+    """extend_sketch returns a new SketchPair (nystrom.cpp:36-58): extending the
+    same pair twice (a branch) must not disturb either result, and an
+    approximation / preconditioner built earlier is unaffected by later
+    extends and refactors (value semantics of nystrom.hpp:19-48)."""
+    a = random_psd(impl, impl.Rng(20), 30, 1e2)
+    op = impl.DenseOperator(a)
+    base = impl.extend_sketch(impl.make_empty_sketch(30), op, 4, impl.Rng(21))
+    om4, y4 = base.arrays(30)
+    approx4 = impl.nystrom_from_sketch(base)
+    pre = impl.build_preconditioner(approx4, 0.1)
+    r = impl.Rng(22).gaussian_vector(30)
+    z_before = pre.apply_inverse(r)
+    lam4 = approx4.lam.copy()
+    longer = impl.extend_sketch(base, op, 3, impl.Rng(23))
+    om7, y7 = longer.arrays(30)
+    branch = impl.extend_sketch(base, op, 2, impl.Rng(24))  # appends behind `longer`'s columns
+    assert base.size() == 4 and longer.size() == 7 and branch.size() == 6
+    om4b, y4b = base.arrays(30)
+    assert np.array_equal(om4b, om4) and np.array_equal(y4b, y4)
+    om7b, y7b = longer.arrays(30)
+    assert np.array_equal(om7b, om7) and np.array_equal(y7b, y7)
+    om6, _ = branch.arrays(30)
+    assert np.array_equal(om6[:, :4], om4)
+    impl.nystrom_from_sketch(longer)
+    impl.nystrom_from_sketch(branch)
+    assert np.array_equal(approx4.lam, lam4)
+    assert np.array_equal(pre.apply_inverse(r), z_before)
+    again = impl.nystrom_from_sketch(base)
+    assert np.array_equal(again.lam, lam4)
