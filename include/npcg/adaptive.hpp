@@ -43,7 +43,8 @@ struct AdaptiveOutcome {  // adaptive.hpp:40-47
 /// estimate_error_power (adaptive.cpp:83-109).
 inline double estimate_error_power(const LinearOperator& op, const NystromApproximation& approx, Index q, Rng& rng) {
   double est = 0.0;
-  check_status(npcg_power_estimate_rng(device_handle(op), approx.device.get(), q, rng.handle(), &est));
+  const OpRef ref = device_handle(op);
+  ref.check(npcg_power_estimate_rng(ref, approx.device.get(), q, rng.handle(), &est));
   return est;
 }
 
@@ -54,7 +55,8 @@ inline AdaptiveOutcome adaptive_call(const LinearOperator& op, const AdaptiveCon
                         c.secondary_criterion ? 1 : 0, c.sketch == SketchKind::gaussian ? 0 : 1};
   npcg_nys* h = nullptr;
   npcg_adaptive_outcome o{};
-  check_status(npcg_adaptive(device_handle(op), &cfg, rng.handle(), &h, &o));
+  const OpRef ref = device_handle(op);
+  ref.check(npcg_adaptive(ref, &cfg, rng.handle(), &h, &o));
   AdaptiveOutcome out;
   out.approximation = fetch(own(h));
   if (o.has_error_estimate) out.error_estimate = o.error_estimate;

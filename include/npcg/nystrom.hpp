@@ -67,7 +67,8 @@ inline NystromApproximation fetch(const std::shared_ptr<npcg_nys>& nys) {
 /// make_empty_sketch (nystrom.cpp:28-34), bound to its operator on device.
 inline SketchPair make_empty_sketch(const LinearOperator& op) {
   npcg_nys* h = nullptr;
-  check_status(npcg_nys_create(device_handle(op), &h));
+  const OpRef ref = device_handle(op);
+  check_status(npcg_nys_create(ref, &h));
   return SketchPair{detail::own(h), op.dim()};
 }
 
@@ -76,7 +77,9 @@ inline SketchPair make_empty_sketch(const LinearOperator& op) {
 inline SketchPair extend_sketch(const SketchPair& pair, const LinearOperator& op, Index extra, Rng& rng) {
   if (pair.dim() != op.dim()) throw std::invalid_argument("extend_sketch: dimension mismatch");
   SketchPair out{detail::clone(pair.device, false), pair.n};
-  check_status(npcg_nys_extend_rng(out.device.get(), extra, rng.handle()));
+  const OpRef h = device_handle(op);  // the operator of this call (a user operator is bound for the call)
+  check_status(npcg_nys_bind(out.device.get(), h));
+  h.check(npcg_nys_extend_rng(out.device.get(), extra, rng.handle()));
   return out;
 }
 
@@ -98,7 +101,9 @@ inline SketchPair extend_sketch_columns(const SketchPair& pair, const LinearOper
                                         std::vector<Index>& used, Rng& rng) {
   if (pair.dim() != op.dim()) throw std::invalid_argument("extend_sketch_columns: dimension mismatch");
   SketchPair out{detail::clone(pair.device, false), pair.n};
-  check_status(npcg_nys_extend_columns(out.device.get(), extra, rng.handle()));
+  const OpRef h = device_handle(op);
+  check_status(npcg_nys_bind(out.device.get(), h));
+  h.check(npcg_nys_extend_columns(out.device.get(), extra, rng.handle()));
   int64_t count = 0;
   check_status(npcg_nys_used(out.device.get(), nullptr, &count));
   std::vector<int64_t> idx(static_cast<size_t>(count));
@@ -110,7 +115,8 @@ inline SketchPair extend_sketch_columns(const SketchPair& pair, const LinearOper
 /// column_sampling_nystrom (nystrom.cpp:150-158): ell distinct columns from rng.
 inline NystromApproximation column_sampling_nystrom(const LinearOperator& op, Index ell, Rng& rng) {
   npcg_nys* h = nullptr;
-  check_status(npcg_column_sampling_nystrom(device_handle(op), ell, nullptr, rng.handle(), &h));
+  const OpRef ref = device_handle(op);
+  ref.check(npcg_column_sampling_nystrom(ref, ell, nullptr, rng.handle(), &h));
   return detail::fetch(detail::own(h));
 }
 
@@ -118,8 +124,8 @@ inline NystromApproximation column_sampling_nystrom(const LinearOperator& op, In
 inline NystromApproximation column_sampling_nystrom(const LinearOperator& op, const std::vector<Index>& indices) {
   std::vector<int64_t> idx(indices.begin(), indices.end());
   npcg_nys* h = nullptr;
-  check_status(npcg_column_sampling_nystrom(device_handle(op), static_cast<int64_t>(idx.size()), idx.data(),
-                                            nullptr, &h));
+  const OpRef ref = device_handle(op);
+  ref.check(npcg_column_sampling_nystrom(ref, static_cast<int64_t>(idx.size()), idx.data(), nullptr, &h));
   return detail::fetch(detail::own(h));
 }
 

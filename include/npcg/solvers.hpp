@@ -31,7 +31,7 @@ struct SolveReport {  // solvers.hpp:28-37
 struct BlockSolveReport {  // solvers.hpp:40-49
   Matrix x;
   Index iterations = 0;
-  std::vector<std::vector<double>> residual_history;  // final residual per column only
+  std::vector<std::vector<double>> residual_history;  // per column, one entry per iteration (+ the initial)
   std::vector<bool> converged;
   std::vector<Index> deflated;
   Index fallback_count = 0;
@@ -59,7 +59,8 @@ inline SolveReport pcg_call(const LinearOperator& op, npcg_pre* pre, double mu, 
   const Index hl = std::max<Index>(opt.max_iter, 0) + 1;
   std::vector<double> hist(static_cast<size_t>(hl));
   std::vector<double> its(opt.record_iterates ? static_cast<size_t>(hl * n) : 0);
-  const int rc = npcg_pcg(device_handle(op), pre, mu, 1, b.data(), std::max<Index>(n, 1), x0 ? x0->data() : nullptr,
+  const OpRef ref = device_handle(op);
+  const int rc = npcg_pcg(ref, pre, mu, 1, b.data(), std::max<Index>(n, 1), x0 ? x0->data() : nullptr,
                           std::max<Index>(n, 1), &o, rep.x.data(), std::max<Index>(n, 1), &r, hist.data(),
                           opt.record_iterates ? its.data() : nullptr, NPCG_HOST);
   rep.iterations = r.iterations;
@@ -74,13 +75,21 @@ inline SolveReport pcg_call(const LinearOperator& op, npcg_pre* pre, double mu, 
     rep.iterates.push_back(std::move(xi));
   }
   if (rc == NPCG_EDIVERGED) throw SolveDivergenceError(npcg_last_error(), std::move(rep));
-  check_status(rc);
+  ref.check(rc);
   return rep;
 }
 }  // namespace detail
 
-/// cg on A_mu (solvers.cpp:111-120): the regularised operator is the device
-/// operator plus the literal shift mu.
+/// cg (solvers.cpp:111-120): textbook CG on an spd operator, typically
+/// regularize(op, mu) (the reference's bench calls cg(RegularizedOperator(op,
+/// shift), b, options), bench.cpp:218-220).
+inline SolveReport cg(const LinearOperator& op_mu, const Vector& b, const SolveOptions& opt = {}) {
+  return detail::pcg_call(op_mu, nullptr, 0.0, b, nullptr, opt);
+}
+inline SolveReport cg(const LinearOperator& op_mu, const Vector& b, const Vector& x0, const SolveOptions& opt = {}) {
+  return detail::pcg_call(op_mu, nullptr, 0.0, b, &x0, opt);
+}
+/// Extension: cg on op + mu I without building the regularized operator.
 inline SolveReport cg(const LinearOperator& op, double mu, const Vector& b, const SolveOptions& opt = {}) {
   return detail::pcg_call(op, nullptr, mu, b, nullptr, opt);
 }
@@ -107,16 +116,20 @@ inline BlockSolveReport block_nystrom_pcg(const LinearOperator& op, const Matrix
   std::vector<int> conv(static_cast<size_t>(s));
   std::vector<std::int64_t> defl(static_cast<size_t>(s));
   std::vector<double> fres(static_cast<size_t>(s));
-  check_status(npcg_block_pcg(device_handle(op), precond.device.get(), mu, s, b.data(), std::max<Index>(n, 1), &o,
-                              rep.x.data(), std::max<Index>(n, 1), &r, conv.data(), defl.data(), fres.data(),
-                              NPCG_HOST));
+  const Index hl = std::max<Index>(opt.max_iter, 0) + 1;
+  std::vector<double> hist(static_cast<size_t>(hl * s));
+  std::vector<std::int64_t> hlen(static_cast<size_t>(s));
+  const OpRef ref = device_handle(op);
+  ref.check(npcg_block_pcg(ref, precond.device.get(), mu, s, b.data(), std::max<Index>(n, 1), &o, rep.x.data(),
+                           std::max<Index>(n, 1), &r, conv.data(), defl.data(), fres.data(), hist.data(), hlen.data(),
+                           NPCG_HOST));
   rep.iterations = r.iterations;
   rep.fallback_count = r.fallback_count;
   rep.eta_used = r.eta_used;
   rep.wall_time = r.wall_time;
   for (Index j = 0; j < s; ++j) {
     rep.converged.push_back(conv[static_cast<size_t>(j)] != 0);
-    rep.residual_history.push_back({fres[static_cast<size_t>(j)]});
+    rep.residual_history.emplace_back(hist.begin() + j * hl, hist.begin() + j * hl + hlen[static_cast<size_t>(j)]);
   }
   rep.deflated.assign(defl.begin(), defl.begin() + r.n_deflated);
   return rep;

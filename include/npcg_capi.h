@@ -139,9 +139,36 @@ int npcg_op_kernel_shard_create(npcg_ctx* ctx, int64_t n, int64_t d, const doubl
 int npcg_op_lowrank_shard_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g, int64_t ldg,
                                  const double* lambda, int64_t nranks, int64_t rank, int where, npcg_exchange_fn fn,
                                  void* user, npcg_op** out);
+/* The reference's plug-in point: a user subclass of LinearOperator
+ * (operators.hpp:25-47, NVI do_matvec / do_apply_block / do_column) as a
+ * device operator every entry point accepts (sketch, power method, PCG,
+ * block PCG). `apply` computes out = A V for k columns (n x k, col-major):
+ *   where = NPCG_HOST:   host buffers; the library synchronises its stream,
+ *                        copies V out, calls `apply`, copies out back in;
+ *   where = NPCG_DEVICE: device pointers of the context's GPU; `stream` is the
+ *                        library's cudaStream_t and the callback must order
+ *                        its work on it (no host synchronisation needed).
+ * `column` (nullable: no column access, operators.cpp:42-50) writes A(:, j).
+ * A non-zero return from a callback fails the calling entry point with
+ * NPCG_ERUNTIME ("LinearOperator callback failed ..."). `user` is borrowed
+ * and must outlive the operator. */
+typedef int (*npcg_apply_fn)(void* user, int64_t n, int64_t k, const double* v, int64_t ldv, double* out,
+                             int64_t ldo, void* stream);
+typedef int (*npcg_column_fn)(void* user, int64_t j, double* out, void* stream);
+int npcg_op_callback_create(npcg_ctx* ctx, int64_t n, npcg_apply_fn apply, npcg_column_fn column, void* user,
+                            int where, npcg_op** out);
+/* RegularizedOperator(base, mu) / regularize (operators.hpp:69-94,153;
+ * operators.cpp:82-103,201-203): A_mu v = base v; += mu v (the reference's
+ * rounding order). mu >= 0 (invalid_argument otherwise). Non-owning view of
+ * `base`, which must outlive the result (the reference's reference
+ * constructor; the C++ facade holds a shared_ptr for the owning one). No
+ * column access, as in the reference. cg on it (npcg_pcg with pre = NULL,
+ * mu = 0) runs the same fused kernels as nystrom_pcg on base with mu. */
+int npcg_op_regularize(npcg_op* base, double mu, npcg_op** out);
 int npcg_op_destroy(npcg_op* op);
 int npcg_op_dim(const npcg_op* op, int64_t* n);
-int npcg_op_kind(const npcg_op* op); /* 0 dense, 1 gram, 2 kernel stored, 3 kernel matrix-free */
+int npcg_op_kind(const npcg_op* op); /* 0 dense, 1 gram, 2 kernel stored, 3 kernel matrix-free, 4 user callback,
+                                        5 regularized */
 int npcg_op_has_column_access(const npcg_op* op);
 /* LinearOperator::matvec / apply_block (operators.cpp:25-40): dim + finiteness
  * checks, then A V. V and out are rows x k col-major. */
@@ -153,6 +180,10 @@ int npcg_op_column(npcg_op* op, int64_t j, double* out, int where);
 /* ---- Nyström (nystrom.hpp:19-89) ---------------------------------------- */
 /* make_empty_sketch(n) bound to op (nystrom.cpp:28-34). */
 int npcg_nys_create(npcg_op* op, npcg_nys** out);
+/* Rebind the sketch pair to `op` (same dimension) for the next extend: the
+ * reference passes the operator to every extend_sketch call
+ * (nystrom.cpp:36-58) rather than storing it in the SketchPair. */
+int npcg_nys_bind(npcg_nys* nys, npcg_op* op);
 /* extend_sketch (nystrom.cpp:36-58) with the raw n x extra Gaussian block the
  * reference Rng would draw (gaussian_matrix); block Gram-Schmidt x2 against
  * the existing columns, orthonormalisation and Y_new = A Q_new on device. */
@@ -233,7 +264,11 @@ int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, 
              const double* x0, int64_t ldx0, const npcg_solve_opts* opts, double* x, int64_t ldx,
              npcg_solve_report* reports, double* history, double* iterates, int where);
 
-/* block_nystrom_pcg (solvers.cpp:150-279), O'Leary block PCG. */
+/* block_nystrom_pcg (solvers.cpp:150-279), O'Leary block PCG, 1 <= s <= 32
+ * (one joint Krylov space; not separable into batches).
+ * history: s x (max_iter+1) col-major per-column residual norms of every
+ * iteration (BlockSolveReport::residual_history, solvers.hpp:40-49), with
+ * history_len[j] entries valid (both nullable). */
 typedef struct {
   int64_t iterations;
   int64_t fallback_count;
@@ -243,7 +278,8 @@ typedef struct {
 } npcg_block_report;
 int npcg_block_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, int64_t ldb,
                    const npcg_solve_opts* opts, double* x, int64_t ldx, npcg_block_report* rep,
-                   int* converged, int64_t* deflated, double* final_residual, int where);
+                   int* converged, int64_t* deflated, double* final_residual, double* history,
+                   int64_t* history_len, int where);
 
 /* iteration_bound (solvers.cpp:281-291). */
 int npcg_iteration_bound(double kappa, double epsilon, int64_t* out);

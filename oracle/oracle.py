@@ -499,7 +499,50 @@ def nystrom_pcg(op: LinearOperator, b, mu: float, precond: NystromPreconditioner
     return rep
 
 
-def cg(op: LinearOperator, mu: float, b, eta=1e-10, max_iter=500, relative=False, x0=None) -> SolveReport:
+class RegularizedOperator:
+    """RegularizedOperator(base, mu) (operators.cpp:82-103): matvec = base.matvec(v); out += mu v."""
+
+    def __init__(self, base, mu: float):
+        if base is None:
+            raise InvalidArgument("RegularizedOperator: base operator is null")
+        if not mu >= 0.0:
+            raise InvalidArgument("RegularizedOperator: mu must be >= 0")
+        self.base, self.mu = base, float(mu)
+
+    def dim(self) -> int:
+        return self.base.dim()
+
+    def has_column_access(self) -> bool:
+        return False
+
+    def matvec(self, v) -> np.ndarray:
+        out = self.base.matvec(v)
+        out += self.mu * np.asarray(v, dtype=np.float64)
+        return out
+
+    def apply_block(self, V) -> np.ndarray:
+        out = self.base.apply_block(V)
+        out += self.mu * np.asarray(V, dtype=np.float64)
+        return out
+
+
+def regularize(op, mu: float) -> RegularizedOperator:
+    return RegularizedOperator(op, mu)
+
+
+def cg(op, *args, eta=1e-10, max_iter=500, relative=False, x0=None) -> SolveReport:
+    """cg(op_mu, b[, x0]) (solvers.cpp:111-120), or the shorthand cg(op, mu, b)."""
+    if len(args) >= 1 and np.ndim(args[0]) == 0:
+        mu, rest = float(args[0]), args[1:]
+    else:
+        mu, rest = 0.0, args
+    b = rest[0]
+    if len(rest) > 1:
+        x0 = rest[1]
+    if isinstance(op, RegularizedOperator):  # the C++ restatement's Regularized wrapper does the same arithmetic
+        if mu != 0.0:
+            raise InvalidArgument("cg: shift given twice")
+        op, mu = op.base, op.mu
     n = op.dim()
     b = _f64(b).ravel()
     x0 = None if x0 is None else _f64(x0).ravel()
@@ -521,6 +564,7 @@ class BlockSolveReport:
     deflated: list
     fallback_count: int
     final_residual: np.ndarray
+    residual_history: list | None = None  # per column, every iteration (solvers.hpp:40-49)
 
 
 def block_nystrom_pcg(op, B, mu, precond, eta=1e-10, max_iter=500, relative=False) -> BlockSolveReport:
@@ -531,11 +575,14 @@ def block_nystrom_pcg(op, B, mu, precond, eta=1e-10, max_iter=500, relative=Fals
     conv = (C.c_int * s)()
     defl = (_i64 * s)()
     fres = np.empty(s)
+    hist = np.zeros((max_iter + 1, s), order="F")
+    hlen = np.zeros(s, dtype=np.int64)
     _check(lib().orc_block_pcg(C.c_void_p(op.h), _i64(s), _ptr(B), C.c_double(mu),
                                None if precond is None else C.c_void_p(precond.h), C.c_double(eta),
                                _i64(max_iter), C.c_int(int(relative)), _ptr(x), C.byref(it), conv, defl,
-                               C.byref(nd), C.byref(fb), _ptr(fres)))
-    return BlockSolveReport(x, it.value, [bool(c) for c in conv], list(defl[: nd.value]), fb.value, fres)
+                               C.byref(nd), C.byref(fb), _ptr(fres), _ptr(hist), hlen.ctypes.data_as(C.c_void_p)))
+    return BlockSolveReport(x, it.value, [bool(c) for c in conv], list(defl[: nd.value]), fb.value, fres,
+                            [hist[: hlen[j], j].copy() for j in range(s)])
 
 
 def iteration_bound(kappa: float, eps: float) -> int:

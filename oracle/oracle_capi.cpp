@@ -350,7 +350,8 @@ int orc_cg(void* op, double mu, const double* b, const double* x0, double eta, i
 }
 int orc_block_pcg(void* op, int64_t s, const double* b, double mu, void* pre, double eta,
                   int64_t max_iter, int relative, double* x, int64_t* iterations, int* converged,
-                  int64_t* deflated, int64_t* n_deflated, int64_t* fallback_count, double* final_res) {
+                  int64_t* deflated, int64_t* n_deflated, int64_t* fallback_count, double* final_res,
+                  double* history, int64_t* history_len) {
   return guard([&] {
     auto* o = static_cast<LinearOperator*>(op);
     const Index n = o->dim();
@@ -363,7 +364,10 @@ int orc_block_pcg(void* op, int64_t s, const double* b, double mu, void* pre, do
     *iterations = r.iterations;
     for (Index j = 0; j < s; ++j) {
       converged[j] = r.converged[static_cast<size_t>(j)] ? 1 : 0;
-      final_res[j] = r.residual_history[static_cast<size_t>(j)].back();
+      const auto& h = r.residual_history[static_cast<size_t>(j)];
+      final_res[j] = h.back();
+      if (history_len) history_len[j] = static_cast<int64_t>(h.size());
+      if (history) std::memcpy(history + j * (max_iter + 1), h.data(), sizeof(double) * h.size());
     }
     *n_deflated = static_cast<int64_t>(r.deflated.size());
     for (size_t i = 0; i < r.deflated.size(); ++i) deflated[i] = r.deflated[i];

@@ -26,6 +26,7 @@ if the library or a B200 is missing, calls raise.
 from __future__ import annotations
 
 import ctypes as C
+from contextlib import contextmanager
 import os
 import threading
 from dataclasses import dataclass, field
@@ -410,6 +411,181 @@ def LowRankOperator(g, lam, ctx: Context | None = None) -> LinearOperator:
                    _i64(g.shape[0]), _ptr(lam), HOST)
 
 
+APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                       C.c_void_p)
+COLUMN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
+class UserOperator:
+    """The reference's plug-in point (operators.hpp:25-47, NVI): subclass and
+    implement ``do_dim`` and ``do_matvec`` (optionally ``do_apply_block``,
+    ``has_column_access`` + ``do_column``). Every solver entry point accepts
+    it; the library calls back into it through npcg_op_callback_create."""
+
+    def dim(self) -> int:
+        return int(self.do_dim())
+
+    def matvec(self, v) -> np.ndarray:  # operators.cpp:25-30
+        v = np.asarray(v, dtype=np.float64)
+        if v.shape != (self.dim(),):
+            raise InvalidArgument(f"LinearOperator - matvec: dimension mismatch (got {v.size}, operator dim "
+                                  f"{self.dim()})")
+        if not np.all(np.isfinite(v)):
+            raise InvalidArgument("LinearOperator - matvec: input has non-finite entries")
+        return np.asarray(self.do_matvec(v), dtype=np.float64)
+
+    def apply_block(self, V) -> np.ndarray:  # operators.cpp:32-40
+        V = np.asarray(V, dtype=np.float64)
+        if V.ndim != 2 or V.shape[0] != self.dim():
+            raise InvalidArgument("LinearOperator - apply_block: dimension mismatch")
+        if not np.all(np.isfinite(V)):
+            raise InvalidArgument("LinearOperator - apply_block: input has non-finite entries")
+        return np.asarray(self.do_apply_block(V), dtype=np.float64)
+
+    def has_column_access(self) -> bool:
+        return False
+
+    def column(self, j: int) -> np.ndarray:  # operators.cpp:42-50
+        if not self.has_column_access():
+            raise NpcgRuntimeError("LinearOperator - column: operator has no column access")
+        if not 0 <= j < self.dim():
+            raise InvalidArgument("LinearOperator - column: index out of range")
+        return np.asarray(self.do_column(j), dtype=np.float64)
+
+    def do_apply_block(self, V):  # operators.cpp:52-58: one do_matvec per column
+        return np.column_stack([self.do_matvec(V[:, j]) for j in range(V.shape[1])]) if V.shape[1] else \
+            np.empty((self.dim(), 0))
+
+    def do_column(self, j):
+        raise NpcgRuntimeError("LinearOperator - column: operator has no column access")
+
+
+class _CallbackBinding:
+    """A user operator bound to the C-ABI for one library call (host buffers).
+    An exception raised by the operator is kept and re-raised by _bound()."""
+
+    def __init__(self, op, ctx=None):
+        self.op, self.error = op, None
+        ctx = ctx or default_context()
+        self._apply = APPLY_FN(self._apply_cb)
+        self._column = COLUMN_FN(self._column_cb) if op.has_column_access() else None
+        h = _vp()
+        _check(lib().npcg_op_callback_create(_vp(ctx.h), _i64(op.dim()), self._apply,
+                                             self._column if self._column else COLUMN_FN(), None, HOST, C.byref(h)))
+        self.h = h.value
+
+    def _apply_cb(self, user, n, k, v, ldv, out, ldo, stream):
+        try:
+            V = np.ctypeslib.as_array(C.cast(v, C.POINTER(C.c_double)), shape=(k, ldv)).T[:n, :]
+            O = np.ctypeslib.as_array(C.cast(out, C.POINTER(C.c_double)), shape=(k, ldo)).T[:n, :]
+            if k == 1:
+                O[:, 0] = self.op.matvec(V[:, 0].copy())
+            else:
+                O[:, :] = self.op.apply_block(np.asfortranarray(V))
+            return 0
+        except BaseException as e:  # noqa: BLE001 - carried across the C boundary
+            self.error = e
+            return 1
+
+    def _column_cb(self, user, j, out, stream):
+        try:
+            n = self.op.dim()
+            np.ctypeslib.as_array(C.cast(out, C.POINTER(C.c_double)), shape=(n,))[:] = self.op.column(int(j))
+            return 0
+        except BaseException as e:  # noqa: BLE001
+            self.error = e
+            return 1
+
+    def close(self):
+        if self.h:
+            lib().npcg_op_destroy(_vp(self.h))
+            self.h = None
+
+
+@contextmanager
+def _bound(op):
+    """The device handle a library call runs on: the operator's own, or a
+    callback operator around a user operator for the duration of the call."""
+    if isinstance(op, LinearOperator):
+        yield op.h
+        return
+    if not hasattr(op, "matvec") or not hasattr(op, "dim"):
+        raise InvalidArgument("npcg: operator must be a LinearOperator or provide dim()/matvec()")
+    b = _CallbackBinding(op)
+    try:
+        yield b.h
+    except (NpcgRuntimeError, InvalidArgument, CudaError, SolveDivergenceError):
+        if b.error is not None:
+            raise b.error from None
+        raise
+    finally:
+        b.close()
+
+
+class RegularizedOperator(LinearOperator):
+    """RegularizedOperator(base, mu) (operators.hpp:69-94; operators.cpp:82-103):
+    A_mu v = base v; += mu v. Over a device operator this is a device operator
+    (npcg_op_regularize): cg(regularize(op, mu), b) runs the same fused kernels
+    as nystrom_pcg(op, b, mu, None). Over a user operator it evaluates on the
+    host through the base's NVI (and is bound by callback like any user op)."""
+
+    def __init__(self, base, mu: float):
+        if base is None:
+            raise InvalidArgument("RegularizedOperator: base operator is null")
+        if not mu >= 0.0:
+            raise InvalidArgument("RegularizedOperator: mu must be >= 0")
+        self.base, self.mu = base, float(mu)
+        if isinstance(base, LinearOperator):
+            h = _vp()
+            _check(lib().npcg_op_regularize(_vp(base.h), C.c_double(mu), C.byref(h)))
+            super().__init__(h.value, base.ctx)
+        else:
+            self.h, self.ctx = None, None
+            self._user = _RegularizedUser(base, self.mu)
+
+    def dim(self) -> int:
+        return self.base.dim()
+
+    def has_column_access(self) -> bool:
+        return False
+
+    def matvec(self, v):
+        return super().matvec(v) if self.h else self._user.matvec(v)
+
+    def apply_block(self, V):
+        return super().apply_block(V) if self.h else self._user.apply_block(V)
+
+
+class _RegularizedUser(UserOperator):
+    def __init__(self, base, mu):
+        self.base, self.mu = base, mu
+
+    def do_dim(self):
+        return self.base.dim()
+
+    def do_matvec(self, v):
+        out = np.array(self.base.matvec(v), dtype=np.float64)
+        out += self.mu * v
+        return out
+
+    def do_apply_block(self, V):
+        out = np.array(self.base.apply_block(V), dtype=np.float64)
+        out += self.mu * V
+        return out
+
+
+def regularize(op, mu: float) -> RegularizedOperator:
+    """regularize(op, mu) (operators.hpp:153; operators.cpp:201-203)."""
+    return RegularizedOperator(op, mu)
+
+
+def _unwrap(op):
+    """RegularizedOperator over a user operator binds as that user operator."""
+    if isinstance(op, RegularizedOperator) and op.h is None:
+        return op._user
+    return op
+
+
 # ------------------------------------------------------------------ Nyström
 class _Nys:
     def __init__(self, h):
@@ -502,11 +678,12 @@ class SketchPair:
 def make_empty_sketch(n_or_op, op: LinearOperator | None = None) -> "SketchPair | _PendingSketch":
     """make_empty_sketch(n) (nystrom.cpp:28-34). The device sketch binds to its
     operator at the first extend_sketch call."""
-    if isinstance(n_or_op, LinearOperator):
+    if not np.isscalar(n_or_op):  # an operator (device, regularized or user)
         op = n_or_op
     if op is not None:
         h = _vp()
-        _check(lib().npcg_nys_create(_vp(op.h), C.byref(h)))
+        with _bound(_unwrap(op)) as oh:
+            _check(lib().npcg_nys_create(_vp(oh), C.byref(h)))
         return SketchPair(_Nys(h.value), op)
     n = int(n_or_op)
     if n < 1:
@@ -532,14 +709,16 @@ def _fresh_pair(pair, op, what):
         return make_empty_sketch(op)
     if pair.op.dim() != op.dim():
         raise InvalidArgument(f"{what}: dimension mismatch")
-    return SketchPair(_clone(pair._nys, False), pair.op)
+    return SketchPair(_clone(pair._nys, False), op)
 
 
 def extend_sketch(pair, op: LinearOperator, extra: int, rng: Rng) -> SketchPair:
     """extend_sketch (nystrom.cpp:36-58): returns a new pair; `pair` is left
     unchanged (device storage is shared copy-on-append)."""
     out = _fresh_pair(pair, op, "extend_sketch")
-    _check(lib().npcg_nys_extend_rng(_vp(out.h), _i64(extra), _vp(rng.h)))
+    with _bound(_unwrap(op)) as oh:  # the reference passes op to every extend (nystrom.cpp:36)
+        _check(lib().npcg_nys_bind(_vp(out.h), _vp(oh)))
+        _check(lib().npcg_nys_extend_rng(_vp(out.h), _i64(extra), _vp(rng.h)))
     return out
 
 
@@ -547,7 +726,9 @@ def extend_sketch_with(pair, op: LinearOperator, fresh) -> SketchPair:
     """extend_sketch with a caller-drawn raw Gaussian block (n x extra)."""
     out = _fresh_pair(pair, op, "extend_sketch")
     fresh = _f64(fresh)
-    _check(lib().npcg_nys_extend(_vp(out.h), _i64(fresh.shape[1]), _ptr(fresh), _i64(fresh.shape[0]), HOST))
+    with _bound(_unwrap(op)) as oh:
+        _check(lib().npcg_nys_bind(_vp(out.h), _vp(oh)))
+        _check(lib().npcg_nys_extend(_vp(out.h), _i64(fresh.shape[1]), _ptr(fresh), _i64(fresh.shape[0]), HOST))
     return out
 
 
@@ -556,7 +737,9 @@ def extend_sketch_columns(pair, op: LinearOperator, extra: int, used: list, rng:
     drawn from `rng`; `used` is extended in place (the handle keeps its own copy).
     Returns a new pair; `pair` is left unchanged."""
     pair = _fresh_pair(pair, op, "extend_sketch_columns")
-    _check(lib().npcg_nys_extend_columns(_vp(pair.h), _i64(extra), _vp(rng.h)))
+    with _bound(_unwrap(op)) as oh:
+        _check(lib().npcg_nys_bind(_vp(pair.h), _vp(oh)))
+        _check(lib().npcg_nys_extend_columns(_vp(pair.h), _i64(extra), _vp(rng.h)))
     cnt = _i64()
     _check(lib().npcg_nys_used(_vp(pair.h), None, C.byref(cnt)))
     buf = np.zeros(max(cnt.value, 1), dtype=np.int64)
@@ -569,13 +752,14 @@ def column_sampling_nystrom(op: LinearOperator, ell_or_indices, rng: Rng | None 
     """column_sampling_nystrom (nystrom.cpp:150-184): `ell` columns drawn from
     `rng`, or the caller's distinct indices."""
     h = _vp()
-    if rng is not None:
-        _check(lib().npcg_column_sampling_nystrom(_vp(op.h), _i64(int(ell_or_indices)), None, _vp(rng.h),
-                                                  C.byref(h)))
-    else:
-        idx = np.ascontiguousarray(ell_or_indices, dtype=np.int64)
-        _check(lib().npcg_column_sampling_nystrom(_vp(op.h), _i64(idx.size), idx.ctypes.data_as(_vp), None,
-                                                  C.byref(h)))
+    with _bound(_unwrap(op)) as oh:
+        if rng is not None:
+            _check(lib().npcg_column_sampling_nystrom(_vp(oh), _i64(int(ell_or_indices)), None, _vp(rng.h),
+                                                      C.byref(h)))
+        else:
+            idx = np.ascontiguousarray(ell_or_indices, dtype=np.int64)
+            _check(lib().npcg_column_sampling_nystrom(_vp(oh), _i64(idx.size), idx.ctypes.data_as(_vp), None,
+                                                      C.byref(h)))
     return _approx_from(_Nys(h.value))
 
 
@@ -677,8 +861,12 @@ def _pcg(op, pre, mu, B, eta, max_iter, relative, record_iterates, x0):
     hist = np.zeros((max(max_iter, 0) + 1, s), order="F")
     its = np.zeros(((max_iter + 1) * n * s,)) if record_iterates else None
     opts = _SolveOpts(float(eta), int(max_iter), int(bool(relative)), int(bool(record_iterates)))
-    rc = lib().npcg_pcg(_vp(op.h), None if pre is None else _vp(pre.h), C.c_double(mu), _i64(s), _ptr(B), _i64(n),
-                        _ptr(x0), _i64(n), C.byref(opts), _ptr(X), _i64(n), reps, _ptr(hist), _ptr(its), HOST)
+    with _bound(_unwrap(op)) as oh:
+        rc = lib().npcg_pcg(_vp(oh), None if pre is None else _vp(pre.h), C.c_double(mu), _i64(s), _ptr(B),
+                            _i64(n), _ptr(x0), _i64(n), C.byref(opts), _ptr(X), _i64(n), reps, _ptr(hist), _ptr(its),
+                            HOST)
+        if rc not in (0, 3):
+            _check(rc)
     out = []
     for j in range(s):
         r = reps[j]
@@ -703,8 +891,19 @@ def nystrom_pcg(op: LinearOperator, b, mu: float, precond: NystromPreconditioner
     return _pcg(op, precond, mu, b, eta, max_iter, relative, record_iterates, x0)
 
 
-def cg(op: LinearOperator, mu: float, b, eta=1e-10, max_iter=500, relative=False, x0=None):
-    """cg on A + mu I (solvers.cpp:111-120)."""
+def cg(op, *args, eta=1e-10, max_iter=500, relative=False, x0=None):
+    """cg (solvers.cpp:111-120): ``cg(op_mu, b[, x0])`` on an spd operator --
+    typically regularize(op, mu), as the reference bench calls it
+    (bench.cpp:218-220) -- or the shorthand ``cg(op, mu, b)`` on op + mu I."""
+    if len(args) >= 1 and np.ndim(args[0]) == 0:
+        mu, rest = float(args[0]), args[1:]
+    else:
+        mu, rest = 0.0, args
+    if not rest:
+        raise InvalidArgument("cg: right-hand side missing")
+    b = rest[0]
+    if len(rest) > 1:
+        x0 = rest[1]
     return _pcg(op, None, mu, b, eta, max_iter, relative, False, x0)
 
 
@@ -716,10 +915,11 @@ class BlockSolveReport:
     deflated: list
     fallback_count: int
     final_residual: np.ndarray
+    residual_history: list | None = None  # per column, every iteration (solvers.hpp:40-49)
 
 
 def block_nystrom_pcg(op, B, mu, precond, eta=1e-10, max_iter=500, relative=False) -> BlockSolveReport:
-    """block_nystrom_pcg (solvers.cpp:150-279)."""
+    """block_nystrom_pcg (solvers.cpp:150-279), 1 <= s <= 32 columns."""
     B = _f64(B)
     n, s = B.shape
     X = np.empty((n, s), order="F")
@@ -727,12 +927,15 @@ def block_nystrom_pcg(op, B, mu, precond, eta=1e-10, max_iter=500, relative=Fals
     conv = (C.c_int * s)()
     defl = (_i64 * s)()
     fres = np.empty(s)
+    hist = np.zeros((max_iter + 1, s), order="F")
+    hlen = np.zeros(s, dtype=np.int64)
     opts = _SolveOpts(float(eta), int(max_iter), int(bool(relative)), 0)
-    _check(lib().npcg_block_pcg(_vp(op.h), None if precond is None else _vp(precond.h), C.c_double(mu), _i64(s),
-                                _ptr(B), _i64(n), C.byref(opts), _ptr(X), _i64(n), C.byref(rep), conv, defl,
-                                _ptr(fres), HOST))
+    with _bound(_unwrap(op)) as h:
+        _check(lib().npcg_block_pcg(_vp(h), None if precond is None else _vp(precond.h), C.c_double(mu), _i64(s),
+                                    _ptr(B), _i64(n), C.byref(opts), _ptr(X), _i64(n), C.byref(rep), conv, defl,
+                                    _ptr(fres), _ptr(hist), hlen.ctypes.data_as(_vp), HOST))
     return BlockSolveReport(X, rep.iterations, [bool(c) for c in conv], list(defl[: rep.n_deflated]),
-                            rep.fallback_count, fres)
+                            rep.fallback_count, fres, [hist[: hlen[j], j].copy() for j in range(s)])
 
 
 def iteration_bound(kappa: float, eps: float) -> int:
@@ -745,7 +948,8 @@ def iteration_bound(kappa: float, eps: float) -> int:
 def estimate_error_power(op: LinearOperator, approx: NystromApproximation, q: int, rng: Rng) -> float:
     """estimate_error_power (adaptive.cpp:83-109)."""
     out = C.c_double()
-    _check(lib().npcg_power_estimate_rng(_vp(op.h), _vp(approx.h.h), _i64(q), _vp(rng.h), C.byref(out)))
+    with _bound(_unwrap(op)) as oh:
+        _check(lib().npcg_power_estimate_rng(_vp(oh), _vp(approx.h.h), _i64(q), _vp(rng.h), C.byref(out)))
     return out.value
 
 
@@ -768,7 +972,8 @@ def adaptive(op, rng: Rng, *, mode="error", ell0=10, ell_max=0, mu=0.0, tau=None
                        int(q), int(bool(secondary_criterion)), 0 if sketch == "gaussian" else 1)
     out = _AdaptiveOutcome()
     h = _vp()
-    _check(lib().npcg_adaptive(_vp(op.h), C.byref(cfg), _vp(rng.h), C.byref(h), C.byref(out)))
+    with _bound(_unwrap(op)) as oh:
+        _check(lib().npcg_adaptive(_vp(oh), C.byref(cfg), _vp(rng.h), C.byref(h), C.byref(out)))
     approx = _approx_from(_Nys(h.value))
     return AdaptiveOutcome(approx, out.error_estimate if out.has_error_estimate else None, out.doublings,
                            bool(out.hit_cap), out.posterior_condition, out.ell_final)

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) coldot_kernel(const double* __restrict__ 
           partial[(static_cast<i64>(blockIdx.y) * S + s) * ncols + j] = acc[c][s];
         } else {
           double v = acc[c][s];
-          if (shift) v += mu * shift[j + s * ldsh];
+          if (shift) v = __dadd_rn(v, __dmul_rn(mu, shift[j + s * ldsh]));  // out += mu v, unfused (operators.cpp:97)
           out[j + s * ldo] = v;
         }
       }
@@ -114,7 +114,7 @@ __global__ void coldot_reduce_kernel(const double* __restrict__ partial, int spl
   const i64 j = idx % ncols, s = idx / ncols;
   double v = 0.0;
   for (int k = 0; k < splits; ++k) v += partial[(static_cast<i64>(k) * S + s) * ncols + j];
-  if (shift) v += mu * shift[j + s * ldsh];
+  if (shift) v = __dadd_rn(v, __dmul_rn(mu, shift[j + s * ldsh]));  // out += mu v, unfused (operators.cpp:97)
   out[j + s * ldo] = v;
 }
 
@@ -264,7 +264,7 @@ __global__ void axpby_kernel(i64 rows, i64 cols, double a, const double* __restr
   for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += static_cast<i64>(gridDim.x) * blockDim.x) {
     const i64 o = idx % rows + idx / rows * ld;
-    y[o] = a * x[o] + b * y[o];
+    y[o] = __dadd_rn(__dmul_rn(a, x[o]), __dmul_rn(b, y[o]));  // unfused, as Eigen evaluates it
   }
 }
 
@@ -274,7 +274,7 @@ __global__ void add_scaled_kernel(i64 rows, i64 cols, const double* __restrict__
   for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += static_cast<i64>(gridDim.x) * blockDim.x) {
     const i64 o = idx % rows + idx / rows * ld;
-    out[o] = a[o] + nu * b[o];
+    out[o] = __dadd_rn(a[o], __dmul_rn(nu, b[o]));  // Y + nu Omega unfused (nystrom.cpp:113)
   }
 }
 

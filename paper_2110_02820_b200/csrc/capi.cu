@@ -552,6 +552,42 @@ int npcg_op_lowrank_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g,
   });
 }
 
+int npcg_op_callback_create(npcg_ctx* ctx, int64_t n, npcg_apply_fn apply, npcg_column_fn column, void* user,
+                            int where, npcg_op** out) {
+  return guard([&] {
+    Ctx& c = C(ctx);
+    need(out, "npcg_op_callback_create");
+    if (!apply) invalid("npcg_op_callback_create: apply callback is null");
+    if (n < 1) invalid("LinearOperator: dimension must be positive");
+    if (where != NPCG_HOST && where != NPCG_DEVICE) invalid("npcg_op_callback_create: where must be host or device");
+    auto op = std::make_unique<CallbackOp>();
+    op->ctx = &c;
+    op->n = n;
+    op->kind = kCallback;
+    op->fn = apply;
+    op->col = column;
+    op->user = user;
+    op->where = where;
+    *out = new npcg_op{ctx, std::move(op)};
+  });
+}
+
+int npcg_op_regularize(npcg_op* base, double mu, npcg_op** out) {
+  return guard([&] {
+    need(base, "RegularizedOperator: base operator is null");  // operators.cpp:84-85
+    need(out, "npcg_op_regularize");
+    Ctx& c = C(base->ctx);
+    if (!(mu >= 0.0)) invalid("RegularizedOperator: mu must be >= 0");  // operators.cpp:86
+    auto op = std::make_unique<RegOp>();
+    op->ctx = &c;
+    op->n = base->op->n;
+    op->kind = kRegularized;
+    op->base = base->op.get();
+    op->mu = mu;
+    *out = new npcg_op{base->ctx, std::move(op)};
+  });
+}
+
 int npcg_op_destroy(npcg_op* op) {
   return guard([&] {
     if (op) {
@@ -622,6 +658,14 @@ int npcg_nys_create(npcg_op* op, npcg_nys** out) {
     h->s.op = op->op.get();
     h->s.n = op->op->n;
     *out = h.release();
+  });
+}
+int npcg_nys_bind(npcg_nys* nys, npcg_op* op) {
+  return guard([&] {
+    need(nys, "npcg_nys_bind");
+    need(op, "npcg_nys_bind operator");
+    if (op->op->n != nys->s.n) invalid("extend_sketch: dimension mismatch");
+    nys->s.op = op->op.get();
   });
 }
 int npcg_nys_extend(npcg_nys* nys, int64_t extra, const double* omega_raw, int64_t ld, int where) {
@@ -950,7 +994,7 @@ int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, 
 
 int npcg_block_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, int64_t ldb,
                    const npcg_solve_opts* opts, double* x, int64_t ldx, npcg_block_report* rep, int* converged,
-                   int64_t* deflated, double* final_residual, int where) {
+                   int64_t* deflated, double* final_residual, double* history, int64_t* history_len, int where) {
   return guard([&] {
     need(op, "npcg_block_pcg");
     need(opts, "npcg_block_pcg options");
@@ -958,7 +1002,7 @@ int npcg_block_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const doubl
     const i64 n = op->op->n;
     // solvers.cpp:156-165
     if (s < 1) invalid("block_nystrom_pcg: need at least one column");
-    if (s > 8) invalid("block_nystrom_pcg: at most 8 right-hand sides per block in this build");
+    if (s > 32) invalid("block_nystrom_pcg: at most 32 right-hand sides per block in this build");
     if (!(opts->eta > 0.0)) invalid("block_nystrom_pcg: eta must be > 0");
     if (!(mu >= 0.0)) invalid("block_nystrom_pcg: mu must be >= 0");
     if (pre && pre->p.ell > 0 && pre->p.n != n) invalid("block_nystrom_pcg: preconditioner dimension mismatch");
@@ -975,7 +1019,11 @@ int npcg_block_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const doubl
     rep->wall_time = r.wall_time;
     for (i64 j = 0; j < s; ++j) {
       converged[j] = r.converged[static_cast<size_t>(j)] ? 1 : 0;
-      final_residual[j] = r.history[static_cast<size_t>(j)].back();
+      const std::vector<double>& hj = r.history[static_cast<size_t>(j)];
+      final_residual[j] = hj.back();
+      const i64 len = std::min<i64>(static_cast<i64>(hj.size()), po.max_iter + 1);
+      if (history_len) history_len[j] = len;
+      if (history) std::copy(hj.begin(), hj.begin() + len, history + j * (po.max_iter + 1));
     }
     for (size_t i = 0; i < r.deflated.size(); ++i) deflated[i] = r.deflated[i];
   });

@@ -108,7 +108,7 @@ __global__ void gram_finish_kernel(const double* __restrict__ partial, int npart
   double t = 0.0;
   for (int b = 0; b < nparts; ++b) t += partial[(static_cast<i64>(b) * S + s) * width + c];
   double o = t / inv_m_div;  // out /= n_rows (operators.cpp:115: division)
-  if (P) o += mu * P[j + s * ldp];
+  if (P) o = __dadd_rn(o, __dmul_rn(mu, P[j + s * ldp]));  // out += mu v, unfused
   out[j + s * ldo] = o;
 }
 

@@ -5,6 +5,8 @@
 #include <cmath>
 #include <limits>
 #include <sstream>
+#include <string>
+#include <vector>
 
 #include "blas.cuh"
 #include "factor.cuh"
@@ -76,6 +78,69 @@ void DenseOp::column(i64 j, double* out) { copy2d(*ctx, n, 1, a.col(j), a.ld, ou
 
 void KernelFreeOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
   kernel_apply_free(*ctx, *this, V, ldv, k, out, ldo, gate);
+}
+
+// User operator callbacks (npcg_op_callback_create). The gate is the PCG
+// loop's "any column running" flag: a product of a finished solve is skipped,
+// so the user's operator sees exactly the products the reference would make.
+void CallbackOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
+  Ctx& c = *ctx;
+  if (gate) {
+    int h = 1;
+    NPCG_CUDA(cudaMemcpyAsync(&h, gate, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (h == 0) return;
+  }
+  int rc = 0;
+  if (where == NPCG_DEVICE) {
+    rc = fn(user, n, k, V, ldv, out, ldo, c.stream);
+  } else {
+    std::vector<double> hv(static_cast<size_t>(n * k)), ho(static_cast<size_t>(n * k));
+    NPCG_CUDA(cudaMemcpy2DAsync(hv.data(), n * 8, V, ldv * 8, n * 8, k, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    rc = fn(user, n, k, hv.data(), n, ho.data(), n, nullptr);
+    if (rc == 0) {
+      NPCG_CUDA(cudaMemcpy2DAsync(out, ldo * 8, ho.data(), n * 8, n * 8, k, cudaMemcpyHostToDevice, c.stream));
+      c.sync();  // ho is released on return
+    }
+  }
+  if (rc != 0) fail(NPCG_ERUNTIME, "LinearOperator callback failed (apply returned " + std::to_string(rc) + ")");
+}
+
+void CallbackOp::column(i64 j, double* out) {
+  Ctx& c = *ctx;
+  if (!col) Op::column(j, out);
+  int rc = 0;
+  if (where == NPCG_DEVICE) {
+    rc = col(user, j, out, c.stream);
+  } else {
+    std::vector<double> h(static_cast<size_t>(n));
+    c.sync();
+    rc = col(user, j, h.data(), nullptr);
+    if (rc == 0) {
+      NPCG_CUDA(cudaMemcpyAsync(out, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      c.sync();
+    }
+  }
+  if (rc != 0) fail(NPCG_ERUNTIME, "LinearOperator callback failed (column returned " + std::to_string(rc) + ")");
+}
+
+// RegularizedOperator::do_matvec / do_apply_block (operators.cpp:95-103):
+// out = base V; out += mu V -- the base's fused shift epilogue has exactly
+// this rounding order.
+void RegOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
+  if (k <= 8) {
+    base->apply_shift(V, ldv, static_cast<int>(k), mu, out, ldo, gate);
+  } else {
+    base->apply(V, ldv, k, out, ldo, gate);
+    for (i64 s = 0; s < k; ++s) axpby(*ctx, n, 1, mu, V + s * ldv, 1.0, out + s * ldo, ldo);
+  }
+}
+void RegOp::apply_shift(const double* P, i64 ldp, int S, double mu2, double* out, i64 ldo, const int* gate) {
+  apply(P, ldp, S, out, ldo, gate);
+  if (mu2 != 0.0) {  // (A_mu p) += mu2 p (nystrom_pcg on a regularized operator, solvers.cpp:137-141)
+    for (int s = 0; s < S; ++s) axpby(*ctx, n, 1, mu2, P + s * ldp, 1.0, out + s * ldo, ldo);
+  }
 }
 
 // ================================ Nyström ====================================

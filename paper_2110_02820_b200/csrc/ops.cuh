@@ -9,7 +9,7 @@
 
 namespace npcg {
 
-enum OpKind { kDense = 0, kGram = 1, kKernelStored = 2, kKernelFree = 3 };
+enum OpKind { kDense = 0, kGram = 1, kKernelStored = 2, kKernelFree = 3, kCallback = 4, kRegularized = 5 };
 
 /// LinearOperator (operators.hpp:25-47) on device. apply() is the unchecked
 /// do_apply_block(); the C-ABI layer does the reference's dim/finite checks.
@@ -86,6 +86,28 @@ struct KernelFreeOp : Op {  // KernelOperator beyond dense_cap (operators.cpp:15
   void column(i64 j, double* out) override;
   void columns(const i64* idx, i64 k, double* out, i64 ldo) override;
   bool costly() const override { return true; }
+};
+
+/// A user operator behind C callbacks (npcg_op_callback_create): the
+/// reference's LinearOperator plug-in point (operators.hpp:25-47).
+struct CallbackOp : Op {
+  npcg_apply_fn fn = nullptr;
+  npcg_column_fn col = nullptr;
+  void* user = nullptr;
+  int where = NPCG_HOST;
+  void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
+  bool has_column() const override { return col != nullptr; }
+  void column(i64 j, double* out) override;
+  bool costly() const override { return true; }  // unknown cost: keep one PCG iteration in flight
+};
+
+/// RegularizedOperator (operators.cpp:82-103): out = base V; out += mu V.
+struct RegOp : Op {
+  Op* base = nullptr;  // not owned (the reference's non-owning view)
+  double mu = 0.0;
+  void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
+  void apply_shift(const double* P, i64 ldp, int S, double mu2, double* out, i64 ldo, const int* gate) override;
+  bool costly() const override { return base->costly(); }
 };
 
 /// Exchange callback of a sharded operator (npcg_exchange_fn in the C-ABI):

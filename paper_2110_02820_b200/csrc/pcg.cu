@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             for (int w = 0; w < PT / 32; ++w) s += zred[w][lane];  // fixed order
             const double pj = pcur[j];
             double v = s / a.div;  // operators.cpp:115 (division), then out += mu p
-            v += a.mu * pj;
+            v = __dadd_rn(v, __dmul_rn(a.mu, pj));  // out += mu p, unfused (solvers.cpp:139)
             a.V[j] = v;
             pvl += pj * v;
           }
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
               for (int b = 0; b < rbj; ++b) sum += a.colpart[(static_cast<i64>(b) * S + s) * a.pstride + j];
               const double pj = pcur[j + s * a.ldw];
               double v = sum;  // operators.cpp:72-78 then solvers.cpp:137-141: out = A p; out += mu p
-              v += a.mu * pj;
+              v = __dadd_rn(v, __dmul_rn(a.mu, pj));  // out += mu p, unfused (solvers.cpp:139)
               a.V[j + s * a.ldw] = v;
               pvl[s] += pj * v;
             }
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             sum = warp_sum(sum);
             const double pj = pcur[j + s * a.ldw];
             double v = sum;  // operators.cpp:72-78 then solvers.cpp:137-141: out = A p; out += mu p
-            v += a.mu * pj;
+            v = __dadd_rn(v, __dmul_rn(a.mu, pj));  // out += mu p, unfused (solvers.cpp:139)
             if (lane == 0) {
               a.V[j + s * a.ldw] = v;
               pvl[s] += pj * v;
@@ -1038,6 +1038,11 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
 
 PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* B, i64 ldb, const double* X0,
                     i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, IterateRec* iterates, const char* context) {
+  // cg on RegularizedOperator(base, a) (solvers.cpp:111-120 + operators.cpp:95-98)
+  // is nystrom_pcg's loop on base with shift a: the same products, the same
+  // rounding (out = base p; out += a p), so the fused kernels apply.
+  if (auto* reg = dynamic_cast<RegOp*>(&op); reg && mu == 0.0)
+    return pcg_solve(ctx, *reg->base, pre, reg->mu, S, B, ldb, X0, ldx0, opt, X, ldx, iterates, context);
   using Clock = std::chrono::steady_clock;
   const auto t0 = Clock::now();
   if (S < 1 || S > kMaxS) fail(NPCG_EINVAL, "pcg_solve: 1..8 right-hand sides per batch");

@@ -4,6 +4,7 @@
 // operators/preconditioner/solvers/nystrom tests. Exit code 0 = all passed.
 #include <cmath>
 #include <cstdio>
+#include <memory>
 #include <stdexcept>
 
 #include "npcg/npcg.hpp"
@@ -19,7 +20,46 @@ static int failures = 0;
     }                                                                 \
   } while (0)
 
-int main() {
+// A user-defined operator: the reference's plug-in point (operators.hpp:25-47).
+// 1-D Laplacian-like tridiagonal SPD matrix, diag 2 + i/n, off-diagonals -1;
+// only do_dim / do_matvec are implemented (do_apply_block is the NVI default).
+class TridiagOperator final : public LinearOperator {
+ public:
+  explicit TridiagOperator(Index n) : n_(n) {}
+  mutable Index calls = 0;
+  static double diag(Index i, Index n) { return 2.0 + static_cast<double>(i) / static_cast<double>(n); }
+
+ protected:
+  Index do_dim() const override { return n_; }
+  void do_matvec(const Vector& v, Vector& out) const override {
+    ++calls;
+    for (Index i = 0; i < n_; ++i) {
+      double s = diag(i, n_) * v(i);
+      if (i > 0) s -= v(i - 1);
+      if (i + 1 < n_) s -= v(i + 1);
+      out(i) = s;
+    }
+  }
+
+ private:
+  Index n_;
+};
+
+class ThrowingOperator final : public LinearOperator {
+ protected:
+  Index do_dim() const override { return 4; }
+  void do_matvec(const Vector&, Vector&) const override { throw std::domain_error("user operator failed"); }
+};
+
+static void dump(FILE* f, const char* name, Index iters, const Vector& x) {
+  if (!f) return;
+  std::fprintf(f, "%s %td", name, iters);
+  for (Index i = 0; i < x.size(); ++i) std::fprintf(f, " %.17g", x(i));
+  std::fprintf(f, "\n");
+}
+
+int main(int argc, char** argv) {
+  FILE* out = argc > 1 ? std::fopen(argv[1], "w") : nullptr;
   // operators_test.cpp:55-62 — dense matvec on a 2x2 example
   Matrix a(2, 2);
   a(0, 0) = 2; a(0, 1) = 1; a(1, 0) = 1; a(1, 1) = 2;
@@ -140,6 +180,73 @@ int main() {
     CHECK(threw);
   }
   CHECK(iteration_bound(56.0, 1e-6) == 54);
+  // The plug-in point: a user LinearOperator subclass through every solver
+  // entry point, and cg(regularize(op, mu), b) -- the reference bench's call
+  // (bench.cpp:218-220). The pytest side compares these against the oracle.
+  {
+    const Index n = 200;
+    auto user = std::make_shared<TridiagOperator>(n);
+    Vector b(n);
+    for (Index i = 0; i < n; ++i) b(i) = std::cos(0.1 * i);
+    const double mu = 0.05;
+    SolveOptions opt;
+    opt.relative = true;
+    const RegularizedOperator reg = regularize(user, mu);
+    CHECK(reg.handle() == nullptr);  // host-side user operator
+    const SolveReport r1 = cg(reg, b, opt);
+    CHECK(r1.converged && r1.matvec_count == r1.iterations + 1);
+    CHECK(user->calls >= r1.iterations);
+    dump(out, "user_cg_regularized", r1.iterations, r1.x);
+    Rng rng(11);
+    const NystromApproximation ap = randomized_nystrom(*user, 20, rng);
+    CHECK(ap.lambda.size() == 20);
+    const NystromPreconditioner pre = build_preconditioner(ap, mu);
+    const SolveReport r2 = nystrom_pcg(*user, b, mu, pre, opt);
+    CHECK(r2.converged);
+    dump(out, "user_nystrom_pcg", r2.iterations, r2.x);
+    Vector lam_dump(ap.lambda.size());
+    for (Index i = 0; i < ap.lambda.size(); ++i) lam_dump(i) = ap.lambda(i);
+    dump(out, "user_lambda", 0, lam_dump);
+    Matrix B2(n, 3);
+    for (Index j = 0; j < 3; ++j)
+      for (Index i = 0; i < n; ++i) B2(i, j) = std::sin(0.05 * (i + 1) * (j + 1));
+    const BlockSolveReport br = block_nystrom_pcg(*user, B2, mu, pre, opt);
+    for (Index j = 0; j < 3; ++j) {
+      CHECK(br.converged[static_cast<size_t>(j)]);
+      CHECK(static_cast<Index>(br.residual_history[static_cast<size_t>(j)].size()) == br.iterations + 1);
+    }
+    Vector bx(n);
+    for (Index i = 0; i < n; ++i) bx(i) = br.x(i, 1);
+    dump(out, "user_block_col1", br.iterations, bx);
+    // a device operator regularized on device: the same kernels as nystrom_pcg(op, b, mu, empty)
+    Vector lam(n);
+    for (Index j = 0; j < n; ++j) lam(j) = std::pow(j + 1.0, -2.0);
+    auto A = std::make_shared<DenseOperator>(synthesize_operator(SpectrumProfile(lam), 9));
+    const RegularizedOperator dreg = regularize(A, 1e-3);
+    CHECK(dreg.handle() != nullptr && !dreg.has_column_access());
+    const SolveReport r3 = cg(dreg, b, opt);
+    const SolveReport r4 = cg(*A, 1e-3, b, opt);
+    CHECK(r3.iterations == r4.iterations);
+    double d = 0.0;
+    for (Index i = 0; i < n; ++i) d = std::max(d, std::abs(r3.x(i) - r4.x(i)));
+    CHECK(d == 0.0);
+    const Vector m1 = dreg.matvec(b), m2 = A->matvec(b);
+    d = 0.0;
+    for (Index i = 0; i < n; ++i) d = std::max(d, std::abs(m1(i) - (m2(i) + 1e-3 * b(i))));
+    CHECK(d == 0.0);
+    threw = false;
+    try { regularize(A, -1.0); } catch (const std::invalid_argument&) { threw = true; }
+    CHECK(threw);
+    // a user operator's own exception crosses the library unchanged
+    threw = false;
+    try {
+      cg(ThrowingOperator(), Vector{1.0, 2.0, 3.0, 4.0}, opt);
+    } catch (const std::domain_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  if (out) std::fclose(out);
   if (failures == 0) std::printf("facade ok\n");
   return failures == 0 ? 0 : 1;
 }
