@@ -1,32 +1,36 @@
 #!/usr/bin/env python
 """Benchmark of the B200 Nyström-PCG hot path (BASELINE.json metric).
 
-One step = one full solve of BASELINE config 2 (configs[1]; ridge regression,
-X 20000 x 4000, ell = 400, mu = 1e-3, relative tol 1e-10): Nyström sketch of the
-raw Gaussian Omega (orthonormalise + Y = A Omega on DMMA), on-device
+Default workload: BASELINE config 3 (configs[2]) -- Gaussian kernel ridge
+regression with the kernel matrix stored in HBM (n = 50 000 points in d = 64,
+K 20 GB, ell = 1000, mu = 0.05, relative tol 1e-10), the largest config whose
+operator fits one GPU and the north star's >= 70 %-of-HBM target. One step =
+one full solve as the reference's run_benchmark times it (bench.cpp:214-275:
+sketch + preconditioner + PCG, the operator already built): Nyström sketch of
+the raw Gaussian Omega (orthonormalise + Y = K Omega on DMMA), on-device
 factorisation (shift, Cholesky, TRSM, thin SVD), preconditioner, PCG to 1e-10.
+`--config cfg1|cfg2|cfg4|cfg5` selects the other BASELINE configs.
 
-  value     solves/s with inputs (X, b, Omega) resident in HBM, device-timed
-            with CUDA events on the library's stream, max over ranks
-  e2e       solves/s through the public C-ABI with host buffers: X, Omega, b
-            copied host->device and x device->host inside every step (the
-            ridge design through the streamed constructor: its row blocks
-            cross PCIe while the sketch already runs on the landed ones)
-  roofline  the dominant kernel of the step (per-kernel CUDA-event timing in
-            an instrumented step of the same run) against its roofline
-  cpu_baseline  the CPU oracle (restatement of the reference) on this host
+  value     solves/s with the operator (K) and Omega, b resident in HBM,
+            device-timed with CUDA events on the library's stream, max over ranks
+  e2e       solves/s through the public API from pageable host numpy arrays,
+            as a user holds them: the points, Omega and b cross PCIe and K is
+            built on the device inside every step; x comes back to the host
+  roofline  the dominant kernel of the step (per-kernel CUDA-event timing in an
+            instrumented step of the same run): achieved = bytes the kernel's
+            algorithm streams / its time; `sec8d` restates it with SURVEY
+            §8(d)'s per-iteration bytes (8n^2 + 16 n ell + 80 n)
+  cpu_baseline  the CPU oracle (line-by-line restatement of the reference) on
+            this host: one full solve on all cores, and the faithful
+            single-thread time (the reference's Eigen has no OpenMP) from a
+            sampled, extrapolated run
 
 `--impl reference` times the reference's CPU path (the oracle port; the
 reference itself cannot be built here: Eigen3/LAPACKE are absent) on all host
 cores, rank 0 only. Under torchrun (N > 1) the stored-kernel (cfg 3) and
-low-rank (cfg 5) operators are row-sharded with replicated
-vectors: rank g builds the column block A[:, R_g] and every product is
-completed by an NCCL all-gather enqueued on the library stream through
-paper_2110_02820_b200/dist.py -- one solve split over N GPUs ("strong"
-scaling). The ridge config 2 runs one independent solve per GPU by default
-("weak"; its replicated factorisation caps strong scaling), and `--shard`
-splits it too: rank g holds rows R_g of X and products are completed by an
-NCCL all-reduce of n doubles per PCG iteration (n x ell for the sketch).
+low-rank (cfg 5) operators are row-sharded: one solve split over
+N GPUs ("strong" scaling); the ridge config 2 runs one independent solve per
+GPU by default ("weak"), `--shard` splits it too.
 """
 from __future__ import annotations
 
@@ -54,7 +58,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="cfg2")
+    p.add_argument("--config", default="cfg3")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--small", action="store_true", help="reduced sizes (smoke runs)")
@@ -67,6 +71,18 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def parallelism(args, world, w=None):
+    """The same string in both arms (the driver compares the config dicts)."""
+    kind = {"cfg1": "synth", "cfg2": "gram", "cfg3": "kernel", "cfg4": "kernel-free", "cfg5": "lowrank"}[args.config]
+    sharded = kind in ("gram", "kernel", "lowrank") and (args.shard or (world > 1 and kind != "gram"))
+    return (f"rowshard{world}" if sharded else f"replicas{world}"), sharded
+
+
+def config_dict(args, w, world):
+    par, _ = parallelism(args, world)
+    return {**w.describe(), "parallelism": par, "l2": L2_NOTE.get(args.config, "inputs larger than L2")}
 
 
 def workload_kwargs(args):
@@ -295,7 +311,7 @@ def roofline_from_profile(prof, peaks, dgemm_peak, ncu_traffic):
     traffic = None
     if ncu_traffic and name in ncu_traffic:
         traffic = ncu_traffic[name]
-    return {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+    return {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "ms": ms,
             "frac": achieved / peak if peak else None, "traffic": traffic, "launches": cnt,
             "share_of_step": ms / total if total else None, "peak_source": src, "work_per_launch": note,
             "kernels": {k: {"launches": v[0], "ms": round(v[1], 4),
@@ -305,61 +321,168 @@ def roofline_from_profile(prof, peaks, dgemm_peak, ncu_traffic):
                         for k, v in sorted(named.items(), key=lambda kv: -kv[1][1])[:10]}}
 
 
-def cpu_baseline(w, steps=1):
-    """The oracle (CPU restatement of the reference path) on this host, all cores."""
+def sec8d_bytes_per_iteration(w):
+    """SURVEY §8(d)'s algorithmic bytes of one PCG iteration (all RHS together)."""
+    n, ell = w.n, w.ell
+    s = w.b.reshape(n, -1, order="F").shape[1]
+    if w.kind == "gram":
+        return 8.0 * w.data["x"].shape[0] * n + 16.0 * n * ell + 80.0 * n
+    if w.kind in ("kernel", "synth", "dense", "lowrank") and not w.adaptive:
+        return 8.0 * n * n + 16.0 * n * ell + 80.0 * n * s
+    return None
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_solve(orc, op, w, phases=None):
+    """One full solve with the oracle, as run_benchmark times it (bench.cpp:214-275)."""
+    t0 = time.perf_counter()
+    if w.adaptive:
+        a = w.adaptive
+        rng = orc.Rng(int(w.name[3]))
+        rng.gaussian_vector(w.n)  # b was drawn first
+        approx = orc.adaptive(op, rng, mode="error", ell0=a["ell0"], ell_max=a["ell_max"], mu=w.mu,
+                              tau=a["tau"], q=a["q"]).approximation
+        t1 = t2 = time.perf_counter()
+    else:
+        pair = orc.extend_sketch_with(orc.make_empty_sketch(w.n), op, w.omega)
+        t1 = time.perf_counter()
+        approx = orc.nystrom_from_sketch(pair)
+        t2 = time.perf_counter()
+    b = w.b.reshape(w.n, -1, order="F")
+    iters, pre = [], None
+    for mu in (w.mus or [w.mu]):
+        pre = orc.build_preconditioner(approx, mu)
+        for j in range(b.shape[1]):
+            try:
+                rep = orc.nystrom_pcg(op, b[:, j], mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
+            except orc.SolveDivergenceError as e:
+                rep = e.report
+            iters.append(rep.iterations)
+    t3 = time.perf_counter()
+    if phases is not None:
+        phases.update(sketch=t1 - t0, factor=t2 - t1, pcg=t3 - t2, total=t3 - t0, iterations=iters, pre=pre)
+    return t3 - t0, iters
+
+
+def single_thread_estimate(orc, op, w, ph, ncores):
+    """The faithful reference configuration is single-threaded (its Eigen has
+    no OpenMP). A full single-thread solve of a large config takes
+    minutes, so it is sampled: one sketch block A Omega[:, :c], one product A b
+    and one preconditioner apply are timed at 1 thread; the sketch scales by
+    ell / c, the PCG by the iteration count of the all-core run, and the
+    factorisation (and the sketch's non-GEMM remainder) by the measured
+    1-thread / all-core ratio of the same sketch block."""
+    if w.adaptive or w.omega is None:
+        return None
+    c = min(w.ell, 32)
+    blk = np.asfortranarray(w.omega[:, :c])
+    b = np.ascontiguousarray(w.b.reshape(w.n, -1, order="F")[:, 0])
+    orc.set_threads(ncores)
+    t = time.perf_counter()
+    op.apply_block(blk)
+    t_blk_all = time.perf_counter() - t
+    orc.set_threads(1)
+    try:
+        t = time.perf_counter()
+        op.apply_block(blk)
+        t_blk = time.perf_counter() - t
+        t = time.perf_counter()
+        op.matvec(b)
+        t_mv = time.perf_counter() - t
+        t = time.perf_counter()
+        ph["pre"].apply_inverse(b)
+        t_pre = time.perf_counter() - t
+    finally:
+        orc.set_threads(ncores)
+    ratio = t_blk / max(t_blk_all, 1e-9)
+    gemm_all = t_blk_all * w.ell / c
+    sketch = t_blk * w.ell / c + max(ph["sketch"] - gemm_all, 0.0) * ratio
+    factor = ph["factor"] * ratio
+    nsolve = sum(ph["iterations"])
+    pcg = nsolve * (t_mv + t_pre) + len(ph["iterations"]) * t_mv
+    total = sketch + factor + pcg
+    return {"value": 1.0 / total, "unit": "solves/s", "cores": 1, "seconds_per_solve": total,
+            "sample": f"1 thread, sampled + extrapolated: A Omega[:, :{c}] {t_blk:.2f} s (x {w.ell / c:.1f}), "
+                      f"A b {t_mv:.3f} s + P^-1 r {t_pre:.3f} s (x {nsolve} iterations), factorisation = all-core "
+                      f"{ph['factor']:.2f} s x the 1-thread/all-core ratio {ratio:.2f} of the sketch block",
+            "phases_s": {"sketch": sketch, "factor": factor, "pcg": pcg}}
+
+
+def cpu_baseline(w, steps=1, single=True):
+    """The oracle (CPU restatement of the reference path) on this host: full
+    solves on all cores, plus the sampled single-thread estimate."""
     from oracle import oracle as orc
     from oracle.workload_ops import build_oracle_operator
     ncores = os.cpu_count() or 1
     orc.set_threads(ncores)
     op = build_oracle_operator(orc, w)
-    times, iters = [], []
+    times, ph = [], {}
     for _ in range(max(1, steps)):
-        t0 = time.perf_counter()
-        if w.adaptive:
-            a = w.adaptive
-            rng = orc.Rng(int(w.name[3]))
-            rng.gaussian_vector(w.n)  # b was drawn first
-            approx = orc.adaptive(op, rng, mode="error", ell0=a["ell0"], ell_max=a["ell_max"], mu=w.mu,
-                                  tau=a["tau"], q=a["q"]).approximation
-        else:
-            pair = orc.extend_sketch_with(orc.make_empty_sketch(w.n), op, w.omega)
-            approx = orc.nystrom_from_sketch(pair)
-        b = w.b.reshape(w.n, -1, order="F")
-        for mu in (w.mus or [w.mu]):
-            pre = orc.build_preconditioner(approx, mu)
-            for j in range(b.shape[1]):
-                try:
-                    rep = orc.nystrom_pcg(op, b[:, j], mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
-                except orc.SolveDivergenceError as e:
-                    rep = e.report
-                iters.append(rep.iterations)
-        times.append(time.perf_counter() - t0)
+        t, iters = _oracle_solve(orc, op, w, ph)
+        times.append(t)
     t = float(np.median(times))
-    return {"value": 1.0 / t, "unit": "solves/s", "cores": ncores, "kind": "port",
-            "sample": f"{len(times)} full solve(s) of {w.name} (sketch+factor+PCG), OpenBLAS {orc.corename()} "
-                      f"x{orc.get_threads()} threads", "seconds_per_solve": t, "iterations": iters[-1]}
+    out = {"value": 1.0 / t, "unit": "solves/s", "cores": ncores, "kind": "port",
+           "sample": f"{len(times)} full solve(s) of {w.name} (sketch+factor+PCG), OpenBLAS {orc.corename()} "
+                     f"x{orc.get_threads()} threads", "seconds_per_solve": t, "iterations": ph["iterations"][-1],
+           "phases_s": {k: ph[k] for k in ("sketch", "factor", "pcg")},
+           "nproc": ncores, "cpu_model": cpu_model(), "openblas_core": orc.corename()}
+    if single:
+        st = single_thread_estimate(orc, op, w, ph, ncores)
+        if st:
+            out["single_thread"] = st
+    return out
 
 
 def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return 0
-    import paper_2110_02820_b200 as npcg_mod  # for the input generators only (host Rng)
     from paper_2110_02820_b200 import workloads
     from oracle import oracle as orc
+    from oracle.workload_ops import build_oracle_operator
     w = workloads.make(args.config, orc.Rng, orc.splitmix64, **workload_kwargs(args))
-    del npcg_mod
-    if args.warmup > 0:
-        cpu_baseline(w, steps=min(args.warmup, 1))  # untimed warm-up (OpenBLAS thread pool, page-in)
+    ncores = os.cpu_count() or 1
+    orc.set_threads(ncores)
+    op = build_oracle_operator(orc, w)
+    t_est = None
+    for _ in range(min(args.warmup, 1)):  # untimed warm-up (OpenBLAS thread pool, page-in); sizes the sample
+        t_est, _ = _oracle_solve(orc, op, w)
+    # Each step is one full solve. A solve of the large configs takes tens of
+    # seconds on the CPU, so the timed sample is bounded to ~150 s: the first
+    # `timed` of the K steps are run (all K when they fit).
+    budget = 150.0
+    timed = args.steps if not t_est else max(1, min(args.steps, int(budget // max(t_est, 1e-9))))
     t0 = time.perf_counter()
-    base = cpu_baseline(w, steps=args.steps)
-    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "solves/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / base["value"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng, seeded)",
-            "config": {**w.describe(), "rhs": "data" if args.config == "cfg2" else "Rng"},
-            "cpu_baseline": base, "e2e": {"value": base["value"], "unit": "solves/s", "h2d_bytes_per_step": 0,
-                                          "d2h_bytes_per_step": 0},
-            "wall_s": time.perf_counter() - t0}
+    ph = {}
+    its = []
+    for _ in range(timed):
+        _, its = _oracle_solve(orc, op, w, ph)
+    el = time.perf_counter() - t0
+    value = timed / el
+    base = {"value": value, "unit": "solves/s", "cores": ncores, "kind": "port",
+            "sample": f"{timed} of {args.steps} steps timed, each one full solve of {w.name} (sketch+factor+PCG) "
+                      f"through the oracle port on all {ncores} host cores (OpenBLAS {orc.corename()})",
+            "nproc": ncores, "cpu_model": cpu_model(), "openblas_core": orc.corename(),
+            "phases_s": {k: ph[k] for k in ("sketch", "factor", "pcg")}}
+    st = single_thread_estimate(orc, op, w, ph, ncores)
+    if st:
+        base["single_thread"] = st
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": args.gpus,
+            "steps": args.steps, "steps_timed": timed, "warmup": args.warmup, "ms_per_step": 1e3 / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference Rng mt19937_64+Box-Muller, seeded)",
+            "config": config_dict(args, w, world), "solve": {"iterations": its},
+            "cpu_baseline": base, "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -392,8 +515,7 @@ def run_b200(args):
     # ridge config 2 replicates by default: its factorisation (3.6 of 11.5 ms)
     # is replicated under sharding, so independent solves per GPU are the
     # throughput-optimal deployment; --shard splits it as well.
-    shardable = w.kind in ("gram", "lowrank") or (w.kind == "kernel" and w.n <= w.data.get("dense_cap", 0))
-    sharded = shardable and (args.shard or (world > 1 and w.kind != "gram"))
+    _, sharded = parallelism(args, world)
     if sharded:
         from paper_2110_02820_b200 import dist as pd
         exchange = pd.TorchExchange()
@@ -439,10 +561,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     e2e = None
     if not args.no_e2e:
-        pin = lambda a: _pinned(torch, a)
-        host = workloads.Workload(**{**w.__dict__})
-        host.data = {k: (pin(v) if isinstance(v, np.ndarray) and v.size > 1 else v) for k, v in w.data.items()}
-        host.omega, host.b = (pin(w.omega) if w.omega is not None else None), pin(w.b)
+        host = w  # the user's pageable numpy arrays (no pinned staging prepared outside the timed region)
         for _ in range(1):
             e2e_step(npcg, w, ctx, host, exchange)
         barrier()
@@ -463,7 +582,9 @@ def run_b200(args):
         h2d = input_bytes(w) - (w.data["x"].nbytes * (1 - 1 / world) if sharded and w.kind == "gram" else 0)
         e2e = {"value": (1 if sharded else world) * k2 / el, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(w.b.nbytes * len(w.mus or [w.mu]) + 8 * w.ell), "steps": k2,
-               "wall_s": time.perf_counter() - t0}
+               "wall_s": time.perf_counter() - t0,
+               "host_buffers": "pageable numpy arrays (operator inputs, Omega, b); the operator (e.g. K) is built "
+                               "on the device inside every step"}
 
     if rank != 0:
         return 0
@@ -474,6 +595,15 @@ def run_b200(args):
     if tf.exists():
         ncu_traffic = json.loads(tf.read_text()).get(args.config)
     roof = roofline_from_profile(prof, peaks, dg, ncu_traffic)
+    sec8d = sec8d_bytes_per_iteration(w)
+    if roof["kernel"].startswith("pcg_persistent_kernel") and sec8d:
+        # the persistent kernel runs as many iterations as its slowest column, once per mu
+        iters = sum(max(it for it, _ in rs) for rs in info) if w.mus else max(it for it, _ in info)
+        ach = sec8d * iters / (roof["ms"] / 1e3) / 1e9
+        roof["sec8d"] = {"bytes_per_iteration": sec8d, "iterations": iters, "achieved": ach, "unit": "GB/s",
+                         "frac": ach / roof["peak"],
+                         "note": "SURVEY 8(d) counts the reference's full pass over A (8 n^2); the symmetric "
+                                 "kernel streams the block-upper half, so this exceeds 1 by design"}
     cpu = None
     if not args.no_cpu and world == 1:
         from oracle import oracle as orc
@@ -486,27 +616,19 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng mt19937_64+Box-Muller, seeded)",
-        "config": {**w.describe(), "parallelism": f"rowshard{world}" if sharded else f"replicas{world}",
-                   "l2": L2_NOTE.get(args.config, "inputs larger than L2"),
-                   **({"iterations_per_mu": [max(it for it, _ in rs) for rs in info], "mus": len(info)}
-                      if w.mus else {"iterations": info[0][0], "converged": info[0][1]}),
-                   **({"adaptive_ell_final_doublings_hitcap": list(path.adaptive_outcome)} if w.adaptive else {})},
+        "config": config_dict(args, w, world),
+        "solve": {**({"iterations_per_mu": [max(it for it, _ in rs) for rs in info], "mus": len(info)}
+                     if w.mus else {"iterations": info[0][0], "converged": info[0][1]}),
+                  **({"adaptive_ell_final_doublings_hitcap": list(path.adaptive_outcome)} if w.adaptive else {})},
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
+        "fp64_peak": {"dgemm_tflops": dg, "source": "cuBLAS DGEMM 8192^3 best of 5, this GPU, this run "
+                                                     "(MEASURED_PEAKS.json has no FP64 figure)"},
         "clocks": clk.summary(), "input_generation_s": t_gen,
     }
     print(json.dumps(line), flush=True)
     if world > 1 or args.shard:
         torch.distributed.destroy_process_group()
     return 0
-
-
-def _pinned(torch, a):
-    t = torch.empty(a.shape[::-1] if a.ndim == 2 else a.shape, dtype=torch.float64, pin_memory=True)
-    arr = t.numpy()
-    if a.ndim == 2:
-        arr = arr.T  # Fortran view
-    arr[...] = a
-    return arr
 
 
 def main():

@@ -71,3 +71,35 @@ def nystrom_definitional(a, x):
 
 def energy_norm(m, v):
     return float(np.sqrt(v @ (m @ v)))
+
+
+def effective_dimension(lam, mu):
+    # diagnostics.cpp:12-18
+    return float(sum(l / (l + mu) for l in lam))
+
+
+def recommended_sketch_size(lam, mu):
+    # diagnostics.cpp:31-35
+    import math
+    deff = effective_dimension(lam, mu)
+    return min(2 * int(math.ceil(1.5 * deff)) + 1, len(lam))
+
+
+def preconditioner_matrix(approx, mu):
+    # NystromPreconditioner::materialize (preconditioner.cpp:47-54)
+    u, lam = approx.u, approx.lam
+    n = u.shape[0]
+    p = np.eye(n)
+    if lam.size == 0:
+        return p
+    gain = (lam + mu) / (lam[-1] + mu) - 1.0
+    return p + (u * gain) @ u.T
+
+
+def exact_condition_number(p, a_mu):
+    # diagnostics.cpp:64-88 (dense O(n^3) oracle): cond(P^-1/2 A_mu P^-1/2)
+    w, v = np.linalg.eigh((p + p.T) / 2)
+    inv_sqrt = (v / np.sqrt(w)) @ v.T
+    m = inv_sqrt @ a_mu @ inv_sqrt
+    eig = np.linalg.eigvalsh((m + m.T) / 2)
+    return float(eig[-1] / eig[0])

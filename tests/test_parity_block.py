@@ -1,0 +1,83 @@
+"""block_nystrom_pcg (solvers.cpp:150-279) on the B200 against the oracle's
+block PCG on identical inputs: iterations within +-1, the same deflated
+columns and fallback count, X within 1e-8, and the per-column residual
+history of every iteration (BlockSolveReport::residual_history,
+solvers.hpp:40-49) within rounding drift."""
+import numpy as np
+import pytest
+
+from support import geo_spectrum, psd_from_spectrum
+
+pytestmark = pytest.mark.gpu
+
+
+def compare_block(rb, ob):
+    assert abs(rb.iterations - ob.iterations) <= 1, (rb.iterations, ob.iterations)
+    assert rb.deflated == ob.deflated
+    assert rb.fallback_count == ob.fallback_count
+    assert rb.converged == ob.converged
+    err = np.linalg.norm(rb.x - ob.x) / np.linalg.norm(ob.x)
+    assert err <= 1e-8, f"X rel err {err:.3e}"
+    drift = 0.0
+    for hg, ho in zip(rb.residual_history, ob.residual_history):
+        assert abs(len(hg) - len(ho)) <= 1
+        k = min(len(hg), len(ho))
+        d = np.abs(hg[:k] - ho[:k])
+        # rounding drift grows as the residual shrinks: bounded relative to the
+        # column's own entry plus a floor at the initial residual's eps scale
+        assert np.all(d <= 1e-6 * ho[:k] + 1e-12 * ho[0]), d.max()
+        drift = max(drift, float(np.max(d / np.maximum(ho[:k], 1e-300))))
+    return err, drift
+
+
+@pytest.fixture(scope="module")
+def npcg():
+    import paper_2110_02820_b200 as m
+    return m
+
+
+def test_block_pcg_matches_oracle_with_histories(npcg, orc):
+    n, mu = 400, 1e-2
+    a = psd_from_spectrum(orc, geo_spectrum(n, 0.9), orc.Rng(7))
+    op, oop = npcg.DenseOperator(a), orc.DenseOperator(a)
+    omega = orc.Rng(8).gaussian_matrix(n, 40)
+    ap = npcg.nystrom_from_sketch(npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, omega))
+    ao = orc.nystrom_from_sketch(orc.extend_sketch_with(orc.make_empty_sketch(n), oop, omega))
+    pre, opre = npcg.build_preconditioner(ap, mu), orc.build_preconditioner(ao, mu)
+    b = orc.Rng(9).gaussian_matrix(n, 5)
+    for relative in (True, False):
+        rb = npcg.block_nystrom_pcg(op, b, mu, pre, eta=1e-10, relative=relative)
+        ob = orc.block_nystrom_pcg(oop, b, mu, opre, eta=1e-10, relative=relative)
+        compare_block(rb, ob)
+        assert all(len(h) == rb.iterations + 1 for h in rb.residual_history)
+
+
+def test_block_pcg_deflation_matches_oracle(npcg, orc):
+    # columns 2 = col0 + col1 and 4 = 0 are deflated by the rank-revealing QR
+    n, mu = 300, 1e-2
+    a = psd_from_spectrum(orc, geo_spectrum(n, 0.85), orc.Rng(17))
+    op, oop = npcg.DenseOperator(a), orc.DenseOperator(a)
+    b = orc.Rng(18).gaussian_matrix(n, 5)
+    b[:, 2] = b[:, 0] + b[:, 1]
+    b[:, 4] = 0.0
+    rb = npcg.block_nystrom_pcg(op, b, mu, None, eta=1e-10, relative=False)
+    ob = orc.block_nystrom_pcg(oop, b, mu, None, eta=1e-10, relative=False)
+    assert ob.deflated == [2, 4] or len(ob.deflated) == 2
+    compare_block(rb, ob)
+
+
+def test_block_pcg_regularisation_path_cfg5_reduced(npcg, orc):
+    """Config 5's 4 right-hand sides solved as one block on the low-rank
+    operator, at each mu of a shortened path (one sketch)."""
+    from paper_2110_02820_b200 import workloads
+    from oracle.workload_ops import build_oracle_operator
+    w = workloads.make("cfg5", orc.Rng, orc.splitmix64, n=2000, r=200, ell=100, nmu=3)
+    op = npcg.LowRankOperator(w.data["g"], w.data["lambda"])
+    oop = build_oracle_operator(orc, w)
+    ap = npcg.nystrom_from_sketch(npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, w.omega))
+    ao = orc.nystrom_from_sketch(orc.extend_sketch_with(orc.make_empty_sketch(w.n), oop, w.omega))
+    for mu in w.mus:
+        pre, opre = npcg.build_preconditioner(ap, mu), orc.build_preconditioner(ao, mu)
+        rb = npcg.block_nystrom_pcg(op, w.b, mu, pre, eta=w.eta, relative=True, max_iter=w.max_iter)
+        ob = orc.block_nystrom_pcg(oop, w.b, mu, opre, eta=w.eta, relative=True, max_iter=w.max_iter)
+        compare_block(rb, ob)

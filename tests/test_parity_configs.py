@@ -47,9 +47,11 @@ def operators(npcg, orc, w):
         p, s, cap = w.data["points"], w.data["sigma"], w.data["dense_cap"]
         return npcg.KernelOperator(p, s, cap), orc.KernelOperator(p, s, cap)
     if w.kind == "lowrank":
+        # the oracle's A = G diag(lambda) G^T / r is built on the CPU from G
+        # (oracle/workload_ops.py), independently of the device generator
+        from oracle.workload_ops import build_oracle_operator
         g, lam = w.data["g"], w.data["lambda"]
-        op = npcg.LowRankOperator(g, lam)
-        return op, orc.DenseOperator(op.dense())
+        return npcg.LowRankOperator(g, lam), build_oracle_operator(orc, w)
     raise ValueError(w.kind)
 
 
@@ -124,8 +126,11 @@ def test_cfg3_kernel_stored_full(npcg, orc):
 
 
 def test_cfg4_kernel_matrix_free_adaptive_reduced(npcg, orc):
-    w = shared_inputs(npcg, orc, "cfg4", n=3000, ell_max=300)
-    w.data["dense_cap"] = 1000  # n > dense_cap: both sides take the matrix-free path
+    run_adaptive_free(npcg, orc, shared_inputs(npcg, orc, "cfg4", n=3000, ell_max=300))
+
+
+def run_adaptive_free(npcg, orc, w):
+    w.data["dense_cap"] = min(w.data["dense_cap"], w.n // 3)  # n > dense_cap: both sides take the matrix-free path
     op, oop = operators(npcg, orc, w)
     assert op.kind == 3  # matrix-free path (n > dense_cap is forced below)
     cfg = dict(mode="error", ell0=w.adaptive["ell0"], ell_max=w.adaptive["ell_max"], mu=w.mu,
@@ -145,8 +150,16 @@ def test_cfg4_kernel_matrix_free_adaptive_reduced(npcg, orc):
     compare_solve(rp, ro)
 
 
-def test_cfg5_regularization_path_reduced(npcg, orc):
-    w = shared_inputs(npcg, orc, "cfg5", n=3000, r=300, ell=150, nmu=4)
+def test_cfg5_lowrank_operator_matches_oracle_build(npcg, orc):
+    """The device-built A = G diag(lambda) G^T / r against the CPU build from G."""
+    from oracle.workload_ops import build_oracle_operator
+    w = shared_inputs(npcg, orc, "cfg5", n=2500, r=400, ell=100, nmu=2)
+    a_gpu = npcg.LowRankOperator(w.data["g"], w.data["lambda"]).dense()
+    a_cpu = build_oracle_operator(orc, w).dense()
+    assert np.abs(a_gpu - a_cpu).max() <= 1e-13 * np.abs(a_cpu).max()
+
+
+def run_regpath(npcg, orc, w):
     op, oop = operators(npcg, orc, w)
     pair = npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, w.omega)
     ap = npcg.nystrom_from_sketch(pair)
@@ -158,3 +171,21 @@ def test_cfg5_regularization_path_reduced(npcg, orc):
         for j, rp in enumerate(reps):
             ro = orc.nystrom_pcg(oop, w.b[:, j], mu, opre, eta=w.eta, relative=True)
             compare_solve(rp, ro)
+
+
+def test_cfg5_regularization_path_reduced(npcg, orc):
+    run_regpath(npcg, orc, shared_inputs(npcg, orc, "cfg5", n=3000, r=300, ell=150, nmu=4))
+
+
+@pytest.mark.slow
+def test_cfg5_regularization_path_n20000(npcg, orc):
+    """config 5 at n = 20 000 (r = 1000, ell = 400), the same
+    construction; four mu of the path (10^-6 .. 10^-1, all 4 RHS each)."""
+    run_regpath(npcg, orc, shared_inputs(npcg, orc, "cfg5", n=20000, r=1000, ell=400, nmu=4))
+
+
+@pytest.mark.slow
+def test_cfg4_kernel_matrix_free_adaptive_n20000(npcg, orc):
+    """SURVEY §8(c): config 4 at n = 20 000 (same d, sigma, mu/n, ell0;
+    ell_max = n/10 = 2000), matrix-free on both sides."""
+    run_adaptive_free(npcg, orc, shared_inputs(npcg, orc, "cfg4", n=20000, ell_max=2000))
