@@ -74,9 +74,10 @@ def dist_env():
 
 
 def parallelism(args, world, w=None):
-    """The same string in both arms (the driver compares the config dicts)."""
-    kind = {"cfg1": "synth", "cfg2": "gram", "cfg3": "kernel", "cfg4": "kernel-free", "cfg5": "lowrank"}[args.config]
-    sharded = kind in ("gram", "kernel", "lowrank") and (args.shard or (world > 1 and kind != "gram"))
+    """The same string in both arms (the driver compares the config dicts).
+    Under torchrun every config but the 2000-dimensional config 1 (replicas,
+    SURVEY §8e) is row-sharded: one solve split over the N GPUs."""
+    sharded = args.config != "cfg1" and (args.shard or world > 1)
     return (f"rowshard{world}" if sharded else f"replicas{world}"), sharded
 
 
@@ -176,19 +177,22 @@ def dgemm_peak_tflops(torch):
 class DevicePath:
     """Drives the C-ABI with device-resident inputs (NPCG_DEVICE pointers)."""
 
-    def __init__(self, npcg, torch, w, ctx, exchange=None):
+    def __init__(self, npcg, torch, w, ctx):
         self.npcg, self.torch, self.w, self.ctx = npcg, torch, w, ctx
         L = npcg.lib()
         self.L = L
-        self.op = npcg.workloads.build_operator(npcg, w, ctx=ctx, exchange=exchange)
-        n = w.n
+        self.op = npcg.workloads.build_operator(npcg, w, ctx=ctx)
+        # this rank's row block of every n-vector (all rows unsharded)
+        self.off, self.nl = self.op.rows()
+        n, off, nl = w.n, self.off, self.nl
         dev = torch.device("cuda", ctx.device)
         # column-major device buffers: torch (cols, rows) row-major == (rows, cols) col-major
-        self.omega = torch.from_numpy(np.ascontiguousarray(w.omega.T)).to(dev) if w.omega is not None else None
-        b = w.b.reshape(n, -1, order="F")
+        self.omega = (torch.from_numpy(np.ascontiguousarray(w.omega[off:off + nl].T)).to(dev)
+                      if w.omega is not None else None)
+        b = w.b.reshape(n, -1, order="F")[off:off + nl]
         self.s = b.shape[1]
         self.b = torch.from_numpy(np.ascontiguousarray(b.T)).to(dev)
-        self.x = torch.empty((self.s, n), dtype=torch.float64, device=dev)
+        self.x = torch.empty((self.s, nl), dtype=torch.float64, device=dev)
         torch.cuda.synchronize()
         self.reports = (npcg._SolveReport * self.s)()
         self.opts = npcg._SolveOpts(w.eta, w.max_iter, int(w.relative), 0)
@@ -210,14 +214,14 @@ class DevicePath:
                 self.adaptive_outcome = (out.ell_final, out.doublings, bool(out.hit_cap))
             else:
                 npcg._check(L.npcg_nys_create(vp(self.op.h), C.byref(nys)))
-                npcg._check(L.npcg_nys_extend(nys, i64(w.ell), vp(self.omega.data_ptr()), i64(w.n), npcg.DEVICE))
+                npcg._check(L.npcg_nys_extend(nys, i64(w.ell), vp(self.omega.data_ptr()), i64(self.nl), npcg.DEVICE))
                 npcg._check(L.npcg_nys_factor(nys))
             iters = []
             for mu in (w.mus or [w.mu]):
                 npcg._check(L.npcg_pre_create(nys, C.c_double(mu), C.byref(pre)))
-                rc = L.npcg_pcg(vp(self.op.h), pre, C.c_double(mu), i64(self.s), vp(self.b.data_ptr()), i64(w.n),
-                                None, i64(w.n), C.byref(self.opts), vp(self.x.data_ptr()), i64(w.n), self.reports,
-                                None, None, npcg.DEVICE)
+                rc = L.npcg_pcg(vp(self.op.h), pre, C.c_double(mu), i64(self.s), vp(self.b.data_ptr()), i64(self.nl),
+                                None, i64(self.nl), C.byref(self.opts), vp(self.x.data_ptr()), i64(self.nl),
+                                self.reports, None, None, npcg.DEVICE)
                 if rc not in (0, 3):  # a diverged column is reported, not fatal, on the regularisation path
                     npcg._check(rc)
                 iters.append([(r.iterations, bool(r.converged)) for r in self.reports])
@@ -231,9 +235,11 @@ class DevicePath:
         return iters[0] if len(iters) == 1 else iters
 
 
-def e2e_step(npcg, w, ctx, host, exchange=None):
-    """Public API with host buffers: every input crosses PCIe inside the step."""
-    op = npcg.workloads.build_operator(npcg, host, ctx=ctx, exchange=exchange, streamed=True)
+def e2e_step(npcg, w, ctx, host):
+    """Public API with host buffers: every input crosses PCIe inside the step
+    (on a row-sharded context each rank passes its rows of Omega and b)."""
+    op = npcg.workloads.build_operator(npcg, host, ctx=ctx, streamed=True)
+    off, nl = op.rows()
     if w.adaptive:
         a = w.adaptive
         rng = npcg.Rng(int(w.name[3]))
@@ -242,13 +248,14 @@ def e2e_step(npcg, w, ctx, host, exchange=None):
                                q=a["q"]).approximation
     else:
         pair = npcg.make_empty_sketch(op)
-        pair = npcg.extend_sketch_with(pair, op, host.omega)
+        pair = npcg.extend_sketch_with(pair, op, host.omega[off:off + nl])
         approx = npcg.nystrom_from_sketch(pair)
     total = 0.0
     for mu in (w.mus or [w.mu]):
         pre = npcg.build_preconditioner(approx, mu)
         try:
-            rep = npcg.nystrom_pcg(op, host.b, mu, pre, eta=w.eta, max_iter=w.max_iter, relative=w.relative)
+            rep = npcg.nystrom_pcg(op, host.b[off:off + nl], mu, pre, eta=w.eta, max_iter=w.max_iter,
+                                   relative=w.relative)
         except npcg.SolveDivergenceError as e:  # reported per column on the regularisation path
             rep = e.report
         x = rep.x if not isinstance(rep, list) else np.column_stack([r.x for r in rep])
@@ -504,22 +511,19 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(local)
-    ctx = npcg.Context(local)
+    _, sharded = parallelism(args, world)
+    if sharded:  # NCCL data plane inside the library (the unique id travels over torch.distributed once)
+        from paper_2110_02820_b200 import dist as pd
+        ctx = pd.nccl_context(local)
+    else:
+        ctx = npcg.Context(local)
     t_gen = time.perf_counter()
     w = workloads.make(args.config, npcg.Rng, npcg.splitmix64,
                        gemm=lambda a, b, transa=False: npcg.gemm(a, b, transa=transa, ctx=ctx), **workload_kwargs(args))
     t_gen = time.perf_counter() - t_gen
-    exchange = None
-    # Multi-GPU: the operator-bound configs (stored kernel cfg 3, low-rank cfg 5)
-    # are row-sharded -- one solve split over the GPUs (strong scaling). The
-    # ridge config 2 replicates by default: its factorisation (3.6 of 11.5 ms)
-    # is replicated under sharding, so independent solves per GPU are the
-    # throughput-optimal deployment; --shard splits it as well.
-    _, sharded = parallelism(args, world)
-    if sharded:
-        from paper_2110_02820_b200 import dist as pd
-        exchange = pd.TorchExchange()
-    path = DevicePath(npcg, torch, w, ctx, exchange)
+    # Multi-GPU: every n-vector is row-sharded and the library
+    # issues the all-gathers / all-reduces / reduce-scatters itself (NCCL).
+    path = DevicePath(npcg, torch, w, ctx)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 
     def barrier():
@@ -563,7 +567,7 @@ def run_b200(args):
     if not args.no_e2e:
         host = w  # the user's pageable numpy arrays (no pinned staging prepared outside the timed region)
         for _ in range(1):
-            e2e_step(npcg, w, ctx, host, exchange)
+            e2e_step(npcg, w, ctx, host)
         barrier()
         t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -571,7 +575,7 @@ def run_b200(args):
         e0.record(stream)
         k2 = max(1, min(args.steps, 3))
         for _ in range(k2):
-            e2e_step(npcg, w, ctx, host, exchange)
+            e2e_step(npcg, w, ctx, host)
         e1.record(stream)
         e1.synchronize()
         el = max(e0.elapsed_time(e1) / 1e3, 1e-9)
@@ -579,7 +583,10 @@ def run_b200(args):
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             el = float(t.item())
-        h2d = input_bytes(w) - (w.data["x"].nbytes * (1 - 1 / world) if sharded and w.kind == "gram" else 0)
+        h2d = input_bytes(w)
+        if sharded:  # each rank uploads its rows of X (ridge), of Omega and of b; points / G are replicated
+            h2d -= (w.data["x"].nbytes if w.kind == "gram" else 0) * (1 - 1 / world)
+            h2d -= ((w.omega.nbytes if w.omega is not None else 0) + w.b.nbytes) * (1 - 1 / world)
         e2e = {"value": (1 if sharded else world) * k2 / el, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(w.b.nbytes * len(w.mus or [w.mu]) + 8 * w.ell), "steps": k2,
                "wall_s": time.perf_counter() - t0,

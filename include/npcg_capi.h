@@ -52,6 +52,28 @@ const char* npcg_version(void);
 int npcg_ctx_create(int device, npcg_ctx** out);
 int npcg_ctx_destroy(npcg_ctx* ctx);
 int npcg_ctx_sync(npcg_ctx* ctx);
+/* ---- row-sharded contexts: one process per GPU --------------
+ * No reference counterpart (the reference is single-process). On a sharded
+ * context every dimension n of an operator is split into balanced contiguous
+ * row blocks R_g (npcg_ctx_layout) and every n-length argument of every entry
+ * point -- right-hand sides, solutions, raw Omega blocks, U, power vectors,
+ * columns -- is this rank's row block (count rows, ld >= count). Rng-drawn
+ * blocks are drawn whole on every rank (the reference's stream) and each rank
+ * keeps its rows. The exchanges -- all-gather of p / sketch blocks, sum
+ * all-reduce of the row reductions (Omega^T Y, Grams, dots, U^T r),
+ * reduce-scatter of partial products -- are issued by the library from C++
+ * on its stream: NCCL (npcg_ctx_create_sharded), or a host callback
+ * (npcg_ctx_create_exchange; kind 0 in-place sum all-reduce of `count`
+ * doubles, 1 all-gather of `count` doubles per rank into recv rank-major,
+ * 2 reduce-scatter: recv (count) = sum over ranks of send[rank*count ..]). */
+typedef int (*npcg_exchange_fn)(void* user, int kind, double* send, double* recv, int64_t count, void* stream);
+/* 128-byte ncclUniqueId (rank 0 creates it, the host distributes it). */
+int npcg_nccl_unique_id(void* out128);
+int npcg_ctx_create_sharded(int device, int rank, int world, const void* nccl_id128, npcg_ctx** out);
+int npcg_ctx_create_exchange(int device, int rank, int world, npcg_exchange_fn fn, void* user, npcg_ctx** out);
+/* rank, world and this rank's row block [offset, offset + count) of dimension n. */
+int npcg_ctx_layout(const npcg_ctx* ctx, int64_t n, int* rank, int* world, int64_t* offset, int64_t* count);
+
 /* The CUDA stream all of this context's work is ordered on (cudaStream_t). */
 void* npcg_ctx_stream(npcg_ctx* ctx);
 /* Device memory owned by the context's allocator (for NPCG_DEVICE inputs). */
@@ -114,31 +136,17 @@ int npcg_op_synthesize(npcg_ctx* ctx, int64_t n, const double* lambda, uint64_t 
 /* A = G diag(lambda) G^T / r (low-rank synthetic psd; BASELINE config 5). */
 int npcg_op_lowrank_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g, int64_t ldg,
                            const double* lambda, int where, npcg_op** out);
-/* Row-sharded operators for one-process-per-GPU runs (no
- * reference counterpart: the reference is single-process). Vectors stay
- * replicated; `fn` completes each local product on the library stream:
- *   kind 0: in-place sum all-reduce of `count` doubles (send == recv);
- *   kind 1: all-gather of `count` doubles per rank into recv, rank-major.
- * The host binds it to NCCL (paper_2110_02820_b200/dist.py, torch.distributed). */
-typedef int (*npcg_exchange_fn)(void* user, int kind, double* send, double* recv, int64_t count, void* stream);
-/* GramRidgeOperator over the row block X_g (m_local x n) of a design with
- * m_total rows: A v = all-reduce_g X_g^T (X_g v) / m_total. */
+/* Row-sharded operators for an explicit local block (sharded contexts, see
+ * npcg_ctx_create_sharded): the column block A[:, R_g] (n x count(rank)) of a
+ * symmetric A, and the row block X_g (m_local x n) of a ridge design with
+ * m_total rows. The regular constructors above take the full data on a
+ * sharded context and keep this rank's share themselves (dense: A[:, R_g];
+ * Gram: the rows of X; kernel: K[:, R_g] built from all points, or a share
+ * of the matrix-free work; low-rank: G diag(lambda) G[R_g]^T / r). */
+int npcg_op_dense_shard_create(npcg_ctx* ctx, int64_t n, const double* a_block, int64_t lda, int where,
+                               npcg_op** out);
 int npcg_op_gram_shard_create(npcg_ctx* ctx, int64_t m_local, int64_t n, const double* g, int64_t ldg,
-                              int where, int64_t m_total, npcg_exchange_fn fn, void* user, npcg_op** out);
-/* DenseOperator over the column block A[:, rank*nb : rank*nb + nloc] (n x nloc,
- * nb = ceil(n / nranks)) of a symmetric A: A v = all-gather_g A[:, R_g]^T v.
- * (The symmetry check needs the whole matrix and is the caller's.) */
-int npcg_op_dense_shard_create(npcg_ctx* ctx, int64_t n, int64_t nranks, int64_t rank, const double* a_block,
-                               int64_t lda, int where, npcg_exchange_fn fn, void* user, npcg_op** out);
-/* Stored KernelOperator shard: this rank builds the column block K[:, R_g]
- * of the Gaussian kernel on device from all n points (operators.cpp:125-150). */
-int npcg_op_kernel_shard_create(npcg_ctx* ctx, int64_t n, int64_t d, const double* pts, int64_t ldp, double sigma,
-                                int64_t nranks, int64_t rank, int where, npcg_exchange_fn fn, void* user,
-                                npcg_op** out);
-/* Low-rank synthetic operator shard: A[:, R_g] = G diag(lambda) G[R_g, :]^T / r. */
-int npcg_op_lowrank_shard_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g, int64_t ldg,
-                                 const double* lambda, int64_t nranks, int64_t rank, int where, npcg_exchange_fn fn,
-                                 void* user, npcg_op** out);
+                              int where, int64_t m_total, npcg_op** out);
 /* The reference's plug-in point: a user subclass of LinearOperator
  * (operators.hpp:25-47, NVI do_matvec / do_apply_block / do_column) as a
  * device operator every entry point accepts (sketch, power method, PCG,
@@ -167,6 +175,9 @@ int npcg_op_callback_create(npcg_ctx* ctx, int64_t n, npcg_apply_fn apply, npcg_
 int npcg_op_regularize(npcg_op* base, double mu, npcg_op** out);
 int npcg_op_destroy(npcg_op* op);
 int npcg_op_dim(const npcg_op* op, int64_t* n);
+/* This rank's row block [offset, offset + count) of the operator's vectors
+ * (offset 0, count n on an unsharded context). */
+int npcg_op_rows(const npcg_op* op, int64_t* offset, int64_t* count);
 int npcg_op_kind(const npcg_op* op); /* 0 dense, 1 gram, 2 kernel stored, 3 kernel matrix-free, 4 user callback,
                                         5 regularized */
 int npcg_op_has_column_access(const npcg_op* op);
@@ -207,6 +218,8 @@ int npcg_nys_from_factors(npcg_ctx* ctx, int64_t n, int64_t ell, const double* u
                           const double* lambda, double shift_used, int where, npcg_nys** out);
 int npcg_nys_info(const npcg_nys* nys, int64_t* n, int64_t* sketch_cols, int64_t* ell_factored,
                   double* shift_used);
+/* This rank's rows [offset, offset + count) of Omega, Y and U. */
+int npcg_nys_rows(const npcg_nys* nys, int64_t* offset, int64_t* count);
 /* lambda (ell), U (n x ell, nullable) of the factored approximation. */
 int npcg_nys_get(npcg_nys* nys, double* lambda, double* u, int64_t ldu, int where);
 /* The cached sketch pair (omega, y: n x size), nullable outputs. */

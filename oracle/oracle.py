@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import shutil
 import subprocess
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -35,8 +36,9 @@ def _cpu_has_avx512() -> bool:
 
 
 def build(force: bool = False) -> Path:
-    """Compile the oracle with its Makefile (g++ + bundled OpenBLAS)."""
-    if force or not LIB_PATH.exists():
+    """Compile the oracle with its Makefile (g++ + bundled OpenBLAS); make
+    rebuilds only when a source changed."""
+    if force or not LIB_PATH.exists() or shutil.which("make"):
         subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
     return LIB_PATH
 

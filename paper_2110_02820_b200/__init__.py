@@ -145,13 +145,46 @@ def _f64(a):
 
 # ------------------------------------------------------------------ context
 class Context:
-    """npcg_ctx: one B200, one stream."""
+    """npcg_ctx: one B200, one stream. ``Context.sharded(...)`` /
+    ``Context.exchange(...)`` make a row-sharded context (one process per GPU,
+    include/npcg_capi.h): every n-vector argument is then this rank's row
+    block (``LinearOperator.rows()``)."""
 
-    def __init__(self, device: int = 0):
-        h = _vp()
-        _check(lib().npcg_ctx_create(C.c_int(device), C.byref(h)))
-        self.h = h.value
+    def __init__(self, device: int = 0, _handle=None):
+        if _handle is None:
+            h = _vp()
+            _check(lib().npcg_ctx_create(C.c_int(device), C.byref(h)))
+            _handle = h.value
+        self.h = _handle
         self.device = device
+        self._keep = None
+
+    @classmethod
+    def sharded(cls, device: int, rank: int, world: int, nccl_id: bytes) -> "Context":
+        """NCCL data plane created inside the library (ncclCommInitRank)."""
+        if len(nccl_id) != 128:
+            raise InvalidArgument("Context.sharded: the NCCL unique id is 128 bytes")
+        h = _vp()
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        _check(lib().npcg_ctx_create_sharded(C.c_int(device), C.c_int(rank), C.c_int(world), idbuf, C.byref(h)))
+        return cls(device, h.value)
+
+    @classmethod
+    def exchange(cls, device: int, rank: int, world: int, exchange) -> "Context":
+        """Host-callback data plane (``exchange.cfn`` an npcg_exchange_fn, e.g.
+        dist.TorchExchange); the exchange object is kept alive with the context."""
+        h = _vp()
+        _check(lib().npcg_ctx_create_exchange(C.c_int(device), C.c_int(rank), C.c_int(world), exchange.cfn, None,
+                                              C.byref(h)))
+        ctx = cls(device, h.value)
+        ctx._keep = exchange
+        return ctx
+
+    def layout(self, n: int) -> tuple[int, int, int, int]:
+        """(rank, world, offset, count) of dimension n's row blocks."""
+        r, w, off, cnt = C.c_int(), C.c_int(), _i64(), _i64()
+        _check(lib().npcg_ctx_layout(_vp(self.h), _i64(n), C.byref(r), C.byref(w), C.byref(off), C.byref(cnt)))
+        return r.value, w.value, off.value, cnt.value
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
@@ -192,6 +225,13 @@ class Context:
 
 
 _default_ctx = None
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for Context.sharded (rank 0 creates, the host distributes)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().npcg_nccl_unique_id(buf))
+    return buf.raw
 
 
 def default_context() -> Context:
@@ -316,6 +356,15 @@ class LinearOperator:
         _check(lib().npcg_op_dim(_vp(self.h), C.byref(n)))
         return n.value
 
+    def rows(self) -> tuple[int, int]:
+        """(offset, count) of this rank's row block of every n-vector ((0, n) unsharded)."""
+        off, cnt = _i64(), _i64()
+        _check(lib().npcg_op_rows(_vp(self.h), C.byref(off), C.byref(cnt)))
+        return off.value, cnt.value
+
+    def local_dim(self) -> int:
+        return self.rows()[1]
+
     @property
     def kind(self) -> int:
         return lib().npcg_op_kind(_vp(self.h))
@@ -325,7 +374,7 @@ class LinearOperator:
 
     def matvec(self, v) -> np.ndarray:
         v = _f64(v).ravel(order="F")
-        out = np.empty(self.dim())
+        out = np.empty(self.local_dim())
         _check(lib().npcg_op_apply(_vp(self.h), _i64(v.size), _i64(1), _ptr(v), _i64(max(v.size, 1)), _ptr(out),
                                    _i64(max(out.size, 1)), HOST))
         return out
@@ -335,17 +384,14 @@ class LinearOperator:
         if V.ndim == 1:
             V = V.reshape(-1, 1, order="F")
         rows, k = V.shape
-        out = np.empty((self.dim(), k), order="F")
-        if k == 1:  # keep apply_block semantics (its messages) for one column
-            _check(lib().npcg_op_apply(_vp(self.h), _i64(rows), _i64(1), _ptr(V), _i64(max(rows, 1)), _ptr(out),
-                                       _i64(max(self.dim(), 1)), HOST))
-            return out
+        nl = self.local_dim()
+        out = np.empty((nl, k), order="F")
         _check(lib().npcg_op_apply(_vp(self.h), _i64(rows), _i64(k), _ptr(V), _i64(max(rows, 1)), _ptr(out),
-                                   _i64(max(self.dim(), 1)), HOST))
+                                   _i64(max(nl, 1)), HOST))
         return out
 
     def column(self, j: int) -> np.ndarray:
-        out = np.empty(self.dim())
+        out = np.empty(self.local_dim())
         _check(lib().npcg_op_column(_vp(self.h), _i64(j), _ptr(out), HOST))
         return out
 
@@ -546,6 +592,9 @@ class RegularizedOperator(LinearOperator):
     def dim(self) -> int:
         return self.base.dim()
 
+    def local_dim(self) -> int:
+        return super().local_dim() if self.h else self.base.dim()
+
     def has_column_access(self) -> bool:
         return False
 
@@ -639,6 +688,12 @@ def _clone(nys: "_Nys", factors_only: bool) -> "_Nys":
     return _Nys(h.value)
 
 
+def _nys_rows(nys: "_Nys") -> int:
+    off, cnt = _i64(), _i64()
+    _check(lib().npcg_nys_rows(_vp(nys.h), C.byref(off), C.byref(cnt)))
+    return cnt.value
+
+
 def _approx_from(nys: _Nys) -> NystromApproximation:
     """The factored approximation of `nys` as an independent value: a
     factors-only handle (later extends / refactors of the pair leave it
@@ -648,7 +703,7 @@ def _approx_from(nys: _Nys) -> NystromApproximation:
     e = max(ell.value, 0)
     lam = np.empty(e)
     _check(lib().npcg_nys_get(_vp(nys.h), _ptr(lam), None, _i64(max(n.value, 1)), HOST))
-    return NystromApproximation(None, lam, shift.value, _clone(nys, True), n.value)
+    return NystromApproximation(None, lam, shift.value, _clone(nys, True), _nys_rows(nys))
 
 
 class SketchPair:
@@ -667,7 +722,7 @@ class SketchPair:
         return size.value
 
     def arrays(self, n=None):
-        n = n or self.op.dim()
+        n = _nys_rows(self._nys)  # this rank's rows (all n unsharded)
         k = self.size()
         om = np.empty((n, k), order="F")
         y = np.empty((n, k), order="F")
@@ -778,15 +833,17 @@ def randomized_nystrom(op: LinearOperator, ell: int, rng: Rng) -> NystromApproxi
     return nystrom_from_sketch(pair)
 
 
-def make_approximation(u, lam, shift_used=0.0, ctx: Context | None = None) -> NystromApproximation:
+def make_approximation(u, lam, shift_used=0.0, ctx: Context | None = None, n: int | None = None) -> NystromApproximation:
+    """An approximation from its factors; on a sharded context `u` is this
+    rank's row block and `n` the full dimension."""
     ctx = ctx or default_context()
     u = _f64(u)
     lam = _f64(lam).ravel()
-    n, ell = u.shape[0], lam.size
+    n, ell = (u.shape[0] if n is None else int(n)), lam.size
     h = _vp()
     _check(lib().npcg_nys_from_factors(_vp(ctx.h), _i64(n), _i64(ell), _ptr(u) if ell else None, _i64(max(n, 1)),
                                        _ptr(lam) if ell else None, C.c_double(shift_used), HOST, C.byref(h)))
-    return NystromApproximation(u.reshape(n, ell), lam, shift_used, _Nys(h.value), n)
+    return NystromApproximation(u.reshape(u.shape[0], ell), lam, shift_used, _Nys(h.value), u.shape[0])
 
 
 # ------------------------------------------------------------------ preconditioner
@@ -850,7 +907,7 @@ def _pcg(op, pre, mu, B, eta, max_iter, relative, record_iterates, x0):
     if single:
         B = B.reshape(-1, 1, order="F")
     n, s = B.shape
-    if n != op.dim():
+    if n != (op.local_dim() if isinstance(op, LinearOperator) else op.dim()):
         raise InvalidArgument("nystrom_pcg: right-hand side length mismatch")
     if x0 is not None:
         x0 = _f64(x0).reshape(n, s, order="F")

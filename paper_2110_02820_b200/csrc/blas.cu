@@ -397,6 +397,17 @@ double sum_squares(Ctx& ctx, const double* p, i64 rows, i64 cols, i64 ld) {
   return h;
 }
 
+bool all_finite_rows(Ctx& ctx, const double* p, i64 rows, i64 cols, i64 ld) {
+  const bool ok = all_finite(ctx, p, rows, cols, ld);
+  return rows_allreduce_host(ctx, ok ? 0.0 : 1.0, true) == 0.0;
+}
+double sum_squares_rows(Ctx& ctx, const double* p, i64 rows, i64 cols, i64 ld) {
+  return rows_allreduce_host(ctx, sum_squares(ctx, p, rows, cols, ld), false);
+}
+double max_abs_rows(Ctx& ctx, const double* p, i64 rows, i64 cols, i64 ld) {
+  return rows_allreduce_host(ctx, max_abs(ctx, p, rows, cols, ld), true);
+}
+
 void symmetry_stats(Ctx& ctx, const double* a, i64 n, i64 ld, double* asym, double* amax) {
   DBuf<unsigned long long> out(2, ctx.stream);
   out.zero();

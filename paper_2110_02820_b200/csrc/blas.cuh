@@ -17,6 +17,12 @@ void download(Ctx& ctx, const double* src, i64 lds, i64 rows, i64 cols, double* 
 bool all_finite(Ctx& ctx, const double* p, i64 rows, i64 cols, i64 ld);
 /// sum of squares of a rows x cols block, deterministic (synchronises).
 double sum_squares(Ctx& ctx, const double* p, i64 rows, i64 cols, i64 ld);
+/// Row-sharded reductions: the same over this rank's row block, combined over
+/// every rank of a sharded context (collective: every rank must call, also
+/// with zero local rows). Identical to the plain ones unsharded.
+bool all_finite_rows(Ctx& ctx, const double* p, i64 rows, i64 cols, i64 ld);
+double sum_squares_rows(Ctx& ctx, const double* p, i64 rows, i64 cols, i64 ld);
+double max_abs_rows(Ctx& ctx, const double* p, i64 rows, i64 cols, i64 ld);
 /// max |a_ij - a_ji| and max |a_ij| of a square matrix (synchronises).
 void symmetry_stats(Ctx& ctx, const double* a, i64 n, i64 ld, double* asym, double* amax);
 /// Y = X + a * Y  elementwise on rows x cols (ld shared).

@@ -228,13 +228,15 @@ __global__ void small_solve_kernel(const double* A, i64 lda, int k, const double
   }
 }
 
+// squared column norms (the square root is taken on the host after the
+// row-sharded all-reduce; sqrt is correctly rounded on both sides)
 __global__ void colnorms_kernel(const double* A, i64 lda, i64 n, int s, double* out) {
   __shared__ double sh[32];
   const int c = blockIdx.x;
   double acc = 0.0;
   for (i64 r = threadIdx.x; r < n; r += blockDim.x) acc += A[r + c * lda] * A[r + c * lda];
   acc = block_sum(acc, sh);
-  if (threadIdx.x == 0) out[c] = sqrt(acc);
+  if (threadIdx.x == 0) out[c] = acc;
 }
 
 __global__ void negate_kernel(const double* a, i64 lda, int rows, int cols, double* out, i64 ldo) {
@@ -248,33 +250,41 @@ BlockPcgResult block_pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 s, con
                                const PcgOptions& opt, double* X, i64 ldx) {
   using Clock = std::chrono::steady_clock;
   const auto t0 = Clock::now();
-  const i64 n = op.n;
+  // Sharded: B, X and every n x k block are this rank's rows; the k x k Grams
+  // and column norms are all-reduced, and the one upfront QR of B runs
+  // replicated on the all-gathered B (s is a handful of columns).
+  const i64 n = op.nloc, nfull = op.n;
   BlockPcgResult res;
   res.converged.assign(static_cast<size_t>(s), false);
   res.history.assign(static_cast<size_t>(s), {});
   if (s > KMAX) fail(NPCG_EINVAL, "block_nystrom_pcg: at most 32 right-hand sides per block");
-  if (!all_finite(ctx, B, n, s, ldb)) invalid("block_nystrom_pcg: right-hand side has non-finite entries");
+  if (!all_finite_rows(ctx, B, n, s, ldb)) invalid("block_nystrom_pcg: right-hand side has non-finite entries");
   std::vector<double> thr(static_cast<size_t>(s));
   DBuf<double> nrm(s, ctx.stream);
-  NPCG_LAUNCH(ctx, colnorms_kernel, static_cast<unsigned>(s), 256, 0, B, ldb, n, static_cast<int>(s), nrm.p);
+  auto colnorms = [&](const double* A, i64 lda, std::vector<double>& outv) {
+    NPCG_LAUNCH(ctx, colnorms_kernel, static_cast<unsigned>(s), 256, 0, A, lda, n, static_cast<int>(s), nrm.p);
+    rows_allreduce(ctx, nrm.p, s);
+    NPCG_CUDA(cudaMemcpyAsync(outv.data(), nrm.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    for (auto& v : outv) v = std::sqrt(v);
+  };
   std::vector<double> bnorm(static_cast<size_t>(s));
-  NPCG_CUDA(cudaMemcpyAsync(bnorm.data(), nrm.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx.stream));
-  ctx.sync();
+  colnorms(B, ldb, bnorm);
   for (i64 j = 0; j < s; ++j) thr[j] = opt.relative ? opt.eta * bnorm[j] : opt.eta;
   res.eta_used = opt.eta;
 
   // ---- column-pivoted QR of B
   DMat Aq;
-  Aq.alloc(n, s, ctx.stream, false);
-  copy2d(ctx, n, s, B, ldb, Aq.p(), Aq.ld);
+  Aq.alloc(nfull, s, ctx.stream, false);
+  rows_allgather(ctx, ctx.split(nfull), B, ldb, s, Aq.p(), Aq.ld);
   DBuf<double> tau(s, ctx.stream);
   DBuf<int> jp(s, ctx.stream);
-  NPCG_LAUNCH(ctx, colpiv_qr_kernel, 1, 1024, 0, Aq.p(), Aq.ld, n, static_cast<int>(s), tau.p, jp.p);
+  NPCG_LAUNCH(ctx, colpiv_qr_kernel, 1, 1024, 0, Aq.p(), Aq.ld, nfull, static_cast<int>(s), tau.p, jp.p);
   std::vector<double> hq(static_cast<size_t>(s * s));
   std::vector<int> jpvt(static_cast<size_t>(s));
-  download(ctx, Aq.p(), Aq.ld, std::min<i64>(n, s), s, hq.data(), s, NPCG_HOST);
+  download(ctx, Aq.p(), Aq.ld, std::min<i64>(nfull, s), s, hq.data(), s, NPCG_HOST);
   NPCG_CUDA(cudaMemcpy(jpvt.data(), jp.p, sizeof(int) * s, cudaMemcpyDeviceToHost));
-  const i64 kmin = std::min<i64>(n, s);
+  const i64 kmin = std::min<i64>(nfull, s);
   const double pivot_max = std::abs(hq[0]);
   i64 rank = 0;
   for (i64 i = 0; i < kmin; ++i)
@@ -292,9 +302,15 @@ BlockPcgResult block_pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 s, con
     return res;
   }
   DMat Qr, mix, negmix, defl;
-  Qr.alloc(n, rank, ctx.stream, false);
-  NPCG_LAUNCH(ctx, form_q_kernel, static_cast<unsigned>(rank), 256, 0, Aq.p(), Aq.ld, n, static_cast<int>(rank),
-              tau.p, Qr.p(), Qr.ld);
+  {
+    DMat Qf;  // Q_r over all n rows (replicated), then this rank's rows
+    Qf.alloc(nfull, rank, ctx.stream, false);
+    NPCG_LAUNCH(ctx, form_q_kernel, static_cast<unsigned>(rank), 256, 0, Aq.p(), Aq.ld, nfull, static_cast<int>(rank),
+                tau.p, Qf.p(), Qf.ld);
+    Qr.alloc(n, rank, ctx.stream, false);
+    copy2d(ctx, n, rank, Qf.p() + op.off, Qf.ld, Qr.p(), Qr.ld);
+    ctx.sync();
+  }
   std::vector<double> hmix(static_cast<size_t>(rank * s), 0.0);  // R[0:rank, :] P^T (solvers.cpp:203-208)
   for (i64 k = 0; k < s; ++k)
     for (i64 i = 0; i < rank && i <= k; ++i) hmix[i + jpvt[k] * rank] = hq[i + k * s];
@@ -328,6 +344,7 @@ BlockPcgResult block_pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 s, con
   };
   auto gram = [&](const double* a, i64 lda, const double* b, i64 ldbb, double* out, i64 ldo) {  // a^T b
     gemm(ctx, k, k, n, 1.0, Operand{a, lda, true}, Operand{b, ldbb, true}, 0.0, out, ldo);
+    rows_allreduce(ctx, out, ldo * k);
   };
   auto solve = [&](const DMat& A, const DMat& rhs, DMat& out) {
     NPCG_LAUNCH(ctx, small_solve_kernel, 1, 32, 0, A.p(), A.ld, k, rhs.p(), rhs.ld, k, out.p(), out.ld, fb.p);
@@ -339,10 +356,7 @@ BlockPcgResult block_pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 s, con
   std::vector<double> hres(static_cast<size_t>(s));
   auto record = [&]() -> bool {  // solvers.cpp:225-237
     rowdot(ctx, R.p(), R.ld, n, k, mix.p(), mix.ld, static_cast<int>(s), defl.p(), defl.ld, orig.p(), orig.ld);
-    NPCG_LAUNCH(ctx, colnorms_kernel, static_cast<unsigned>(s), 256, 0, orig.p(), orig.ld, n, static_cast<int>(s),
-                nrm.p);
-    NPCG_CUDA(cudaMemcpyAsync(hres.data(), nrm.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx.stream));
-    ctx.sync();
+    colnorms(orig.p(), orig.ld, hres);
     bool all = true;
     for (i64 j = 0; j < s; ++j) {
       if (!std::isfinite(hres[j])) fail(NPCG_ERUNTIME, "block_nystrom_pcg: non-finite residual");

@@ -70,6 +70,11 @@ int guard(F&& f) {
   }
 }
 
+/// Re-raise the status of a nested C-ABI call inside guard().
+void guard_rethrow(int rc) {
+  if (rc != NPCG_OK) fail(rc, g_err);
+}
+
 void need(const void* p, const char* what) {
   if (!p) invalid(std::string(what) + ": null handle or pointer");
 }
@@ -158,6 +163,40 @@ int npcg_ctx_create(int device, npcg_ctx** out) {
     auto c = std::make_unique<npcg_ctx>();
     c->c = std::make_unique<Ctx>(device);
     *out = c.release();
+  });
+}
+int npcg_nccl_unique_id(void* out128) {
+  return guard([&] {
+    need(out128, "npcg_nccl_unique_id");
+    nccl_unique_id(out128);
+  });
+}
+int npcg_ctx_create_sharded(int device, int rank, int world, const void* nccl_id128, npcg_ctx** out) {
+  return guard([&] {
+    need(out, "npcg_ctx_create_sharded");
+    auto c = std::make_unique<npcg_ctx>();
+    c->c = std::make_unique<Ctx>(device);
+    c->c->comm = make_nccl_comm(device, rank, world, nccl_id128);
+    *out = c.release();
+  });
+}
+int npcg_ctx_create_exchange(int device, int rank, int world, npcg_exchange_fn fn, void* user, npcg_ctx** out) {
+  return guard([&] {
+    need(out, "npcg_ctx_create_exchange");
+    auto c = std::make_unique<npcg_ctx>();
+    c->c = std::make_unique<Ctx>(device);
+    c->c->comm = make_callback_comm(rank, world, fn, user);
+    *out = c.release();
+  });
+}
+int npcg_ctx_layout(const npcg_ctx* ctx, int64_t n, int* rank, int* world, int64_t* offset, int64_t* count) {
+  return guard([&] {
+    need(ctx, "npcg_ctx_layout");
+    const Ctx& c = *ctx->c;
+    if (rank) *rank = c.rank();
+    if (world) *world = c.world();
+    if (offset) *offset = c.row_offset(n);
+    if (count) *count = c.local_rows(n);
   });
 }
 int npcg_ctx_destroy(npcg_ctx* ctx) {
@@ -287,14 +326,43 @@ double npcg_ulp_spacing(double x) { return ulp_spacing_host(x); }
 
 // ============================== operators ===================================
 namespace {
-npcg_op* make_dense(npcg_ctx* ctx, DMat&& a, i64 n, int kind) {
-  auto op = std::make_unique<DenseOp>();
-  op->ctx = ctx->c.get();
-  op->n = n;
+/// The handle for a finished operator. On a sharded context `local` is the
+/// rank's share (column block / row block of X / kernel work share) working on
+/// full-length inputs and is wrapped in a ShardOp; otherwise it is the operator.
+npcg_op* finish_op(npcg_ctx* ctx, std::unique_ptr<Op> local, i64 n, int kind) {
+  Ctx& c = *ctx->c;
+  if (c.sharded() && n < c.world()) invalid("sharded operator: dimension smaller than the number of ranks");
+  local->set_dim(c, n);
+  local->kind = kind;
+  if (!c.sharded()) return new npcg_op{ctx, std::move(local)};
+  auto op = std::make_unique<ShardOp>();
+  op->set_dim(c, n);
   op->kind = kind;
-  op->a = std::move(a);
-  auto h = new npcg_op{ctx, std::move(op)};
-  return h;
+  op->local = std::move(local);
+  return new npcg_op{ctx, std::move(op)};
+}
+
+npcg_op* make_dense(npcg_ctx* ctx, DMat&& a, i64 n, int kind) {
+  Ctx& c = *ctx->c;
+  if (!c.sharded()) {
+    auto op = std::make_unique<DenseOp>();
+    op->a = std::move(a);
+    return finish_op(ctx, std::move(op), n, kind);
+  }
+  // keep this rank's column block A[:, R_g] (= rows R_g, A symmetric)
+  auto blk = std::make_unique<DenseColBlockOp>();
+  blk->set_dim(c, n);
+  blk->a.alloc(n, blk->nloc, c.stream, false);
+  copy2d(c, n, blk->nloc, a.col(blk->off), a.ld, blk->a.p(), blk->a.ld);
+  c.sync();
+  a.buf.release();
+  return finish_op(ctx, std::move(blk), n, kind);
+}
+
+npcg_op* make_colblock(npcg_ctx* ctx, DMat&& block, i64 n, int kind) {
+  auto blk = std::make_unique<DenseColBlockOp>();
+  blk->a = std::move(block);
+  return finish_op(ctx, std::move(blk), n, kind);
 }
 }  // namespace
 
@@ -319,11 +387,18 @@ int npcg_op_gram_create(npcg_ctx* ctx, int64_t m, int64_t n, const double* g, in
     auto op = std::make_unique<GramOp>();
     op->ctx = &c;
     op->n = n;
-    op->m = m;
     op->div = static_cast<double>(m);
-    op->kind = kGram;
-    gram_upload(c, *op, g, ldg, where);
-    *out = new npcg_op{ctx, std::move(op)};
+    if (c.sharded()) {  // this rank's rows of X (the m rows split like any dimension)
+      const RowSplit sp = c.split(m);
+      op->m = sp.count(c.rank());
+      if (op->m < 1) invalid("GramRidgeOperator shard: more ranks than design rows");
+      op->shard_partial = true;
+      gram_upload(c, *op, g + sp.offset(c.rank()), ldg, where);
+    } else {
+      op->m = m;
+      gram_upload(c, *op, g, ldg, where);
+    }
+    *out = finish_op(ctx, std::move(op), n, kGram);
   });
 }
 
@@ -333,143 +408,46 @@ int npcg_op_gram_create_streamed(npcg_ctx* ctx, int64_t m, int64_t n, const doub
     Ctx& c = C(ctx);
     if (m < 1 || n < 1) invalid("GramRidgeOperator: design matrix must be nonempty");  // operators.cpp:106-107
     if (ldg < m) invalid("leading dimension smaller than the row count");
+    if (c.sharded()) {  // sharded: the synchronous upload of this rank's rows
+      guard_rethrow(npcg_op_gram_create(ctx, m, n, g, ldg, NPCG_HOST, out));
+      return;
+    }
     auto op = std::make_unique<GramOp>();
     op->ctx = &c;
     op->n = n;
     op->m = m;
     op->div = static_cast<double>(m);
-    op->kind = kGram;
     gram_upload_streamed(c, *op, g, ldg);
-    *out = new npcg_op{ctx, std::move(op)};
+    *out = finish_op(ctx, std::move(op), n, kGram);
   });
 }
 
 int npcg_op_gram_shard_create(npcg_ctx* ctx, int64_t m_local, int64_t n, const double* g, int64_t ldg, int where,
-                              int64_t m_total, npcg_exchange_fn fn, void* user, npcg_op** out) {
+                              int64_t m_total, npcg_op** out) {
   return guard([&] {
     Ctx& c = C(ctx);
     if (m_local < 1 || n < 1 || m_total < m_local) invalid("GramRidgeOperator shard: bad block dimensions");
-    if (!fn) invalid("sharded operator: exchange callback required");
     auto local = std::make_unique<GramOp>();
     local->ctx = &c;
     local->n = n;
     local->m = m_local;
     local->div = static_cast<double>(m_total);
-    local->kind = kGram;
+    local->shard_partial = c.sharded();
     gram_upload(c, *local, g, ldg, where);
-    auto op = std::make_unique<ShardOp>();
-    op->ctx = &c;
-    op->n = n;
-    op->kind = kGram;
-    op->mode = 0;
-    op->local = std::move(local);
-    op->fn = fn;
-    op->user = user;
-    *out = new npcg_op{ctx, std::move(op)};
+    *out = finish_op(ctx, std::move(local), n, kGram);
   });
 }
 
-int npcg_op_dense_shard_create(npcg_ctx* ctx, int64_t n, int64_t nranks, int64_t rank, const double* a_block,
-                               int64_t lda, int where, npcg_exchange_fn fn, void* user, npcg_op** out) {
+int npcg_op_dense_shard_create(npcg_ctx* ctx, int64_t n, const double* a_block, int64_t lda, int where,
+                               npcg_op** out) {
   return guard([&] {
     Ctx& c = C(ctx);
-    if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks) invalid("DenseOperator shard: bad rank layout");
-    if (!fn) invalid("sharded operator: exchange callback required");
-    const i64 nmax = cdiv(n, nranks), off = rank * nmax, nloc = std::min<i64>(nmax, n - off);
-    if (nloc < 1) invalid("DenseOperator shard: more ranks than rows");
-    auto local = std::make_unique<DenseColBlockOp>();
-    local->ctx = &c;
-    local->n = n;
-    local->nloc = nloc;
-    local->kind = kDense;
-    upload(c, local->a, n, nloc, a_block, lda, where);
-    if (!all_finite(c, local->a.p(), n, nloc, local->a.ld))
-      invalid("DenseOperator: matrix has non-finite entries");
-    auto op = std::make_unique<ShardOp>();
-    op->ctx = &c;
-    op->n = n;
-    op->kind = kDense;
-    op->mode = 1;
-    op->nranks = nranks;
-    op->rank = rank;
-    op->nmax = nmax;
-    op->local = std::move(local);
-    op->fn = fn;
-    op->user = user;
-    *out = new npcg_op{ctx, std::move(op)};
-  });
-}
-
-namespace {
-npcg_op* make_colblock_shard(npcg_ctx* ctx, DMat&& block, i64 n, i64 nranks, i64 rank, int kind,
-                             npcg_exchange_fn fn, void* user) {
-  Ctx& c = C(ctx);
-  const i64 nmax = cdiv(n, nranks), nloc = std::min<i64>(nmax, n - rank * nmax);
-  auto local = std::make_unique<DenseColBlockOp>();
-  local->ctx = &c;
-  local->n = n;
-  local->nloc = nloc;
-  local->kind = kind;
-  local->a = std::move(block);
-  auto op = std::make_unique<ShardOp>();
-  op->ctx = &c;
-  op->n = n;
-  op->kind = kind;
-  op->mode = 1;
-  op->nranks = nranks;
-  op->rank = rank;
-  op->nmax = nmax;
-  op->local = std::move(local);
-  op->fn = fn;
-  op->user = user;
-  return new npcg_op{ctx, std::move(op)};
-}
-void check_shard(i64 n, i64 nranks, i64 rank, npcg_exchange_fn fn) {
-  if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks) invalid("sharded operator: bad rank layout");
-  if (!fn) invalid("sharded operator: exchange callback required");
-  if (n - rank * cdiv(n, nranks) < 1) invalid("sharded operator: more ranks than rows");
-}
-}  // namespace
-
-int npcg_op_kernel_shard_create(npcg_ctx* ctx, int64_t n, int64_t d, const double* pts, int64_t ldp, double sigma,
-                                int64_t nranks, int64_t rank, int where, npcg_exchange_fn fn, void* user,
-                                npcg_op** out) {
-  return guard([&] {
-    Ctx& c = C(ctx);
-    if (n < 1) invalid("KernelOperator: need at least one point");   // operators.cpp:143
-    if (!(sigma > 0.0)) invalid("KernelOperator: sigma must be > 0");  // :144
-    check_shard(n, nranks, rank, fn);
-    DMat P;
-    upload(c, P, n, d, pts, ldp, where);
-    if (!all_finite(c, P.p(), n, d, P.ld)) invalid("KernelOperator: points have non-finite entries");
-    const i64 nmax = cdiv(n, nranks), off = rank * nmax, nloc = std::min<i64>(nmax, n - off);
-    DMat K;
-    build_kernel_colblock(c, P, n, d, sigma, off, nloc, K);
-    *out = make_colblock_shard(ctx, std::move(K), n, nranks, rank, kKernelStored, fn, user);
-  });
-}
-
-int npcg_op_lowrank_shard_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g, int64_t ldg,
-                                 const double* lambda, int64_t nranks, int64_t rank, int where, npcg_exchange_fn fn,
-                                 void* user, npcg_op** out) {
-  return guard([&] {
-    Ctx& c = C(ctx);
-    if (n < 1 || r < 1) invalid("lowrank operator: need n >= 1 and r >= 1");
-    check_shard(n, nranks, rank, fn);
-    DMat G, GD;
-    upload(c, G, n, r, g, ldg, where);
-    GD.alloc(n, r, c.stream, false);
-    copy2d(c, n, r, G.p(), G.ld, GD.p(), GD.ld);
-    DBuf<double> lam(r, c.stream);
-    NPCG_CUDA(cudaMemcpyAsync(lam.p, lambda, sizeof(double) * r, cudaMemcpyHostToDevice, c.stream));
-    scale_cols(c, GD.p(), n, r, GD.ld, lam.p);
-    const i64 nmax = cdiv(n, nranks), off = rank * nmax, nloc = std::min<i64>(nmax, n - off);
-    DMat A;  // A[:, R_g] = G diag(lambda) G[R_g, :]^T / r
-    A.alloc(n, nloc, c.stream, false);
-    gemm(c, n, nloc, r, 1.0, Operand{GD.p(), GD.ld, false}, Operand{G.p() + off, G.ld, false}, 0.0, A.p(), A.ld);
-    divide(c, n, nloc, A.p(), A.ld, static_cast<double>(r));
-    c.sync();
-    *out = make_colblock_shard(ctx, std::move(A), n, nranks, rank, kDense, fn, user);
+    if (n < 1) invalid("DenseOperator: matrix must be square");
+    const i64 nloc = c.local_rows(n);
+    DMat blk;
+    upload(c, blk, n, nloc, a_block, lda, where);
+    if (!all_finite(c, blk.p(), n, nloc, blk.ld)) invalid("DenseOperator: matrix has non-finite entries");
+    *out = c.sharded() ? make_colblock(ctx, std::move(blk), n, kDense) : make_dense(ctx, std::move(blk), n, kDense);
   });
 }
 
@@ -484,18 +462,26 @@ int npcg_op_kernel_create(npcg_ctx* ctx, int64_t n, int64_t d, const double* pts
     if (!all_finite(c, P.p(), n, d, P.ld)) invalid("KernelOperator: points have non-finite entries");
     if (n <= dense_cap) {  // :148-149
       DMat K;
-      build_kernel_matrix(c, P, n, d, sigma, K);
-      *out = make_dense(ctx, std::move(K), n, kKernelStored);
+      if (c.sharded()) {  // this rank's column block K[:, R_g], built from all points
+        build_kernel_colblock(c, P, n, d, sigma, c.row_offset(n), c.local_rows(n), K);
+        *out = make_colblock(ctx, std::move(K), n, kKernelStored);
+      } else {
+        build_kernel_matrix(c, P, n, d, sigma, K);
+        *out = make_dense(ctx, std::move(K), n, kKernelStored);
+      }
     } else {
       auto op = std::make_unique<KernelFreeOp>();
       op->ctx = &c;
       op->n = n;
       op->d = d;
       op->sigma = sigma;
-      op->kind = kKernelFree;
       op->pts = std::move(P);
+      op->shard_rank = c.rank();
+      op->shard_world = c.world();
+      op->shard_off = c.row_offset(n);
+      op->shard_rows = c.local_rows(n);
       prepare_kernel_free(c, *op);
-      *out = new npcg_op{ctx, std::move(op)};
+      *out = finish_op(ctx, std::move(op), n, kKernelFree);
     }
   });
 }
@@ -510,14 +496,16 @@ int npcg_op_synthesize(npcg_ctx* ctx, int64_t n, const double* lambda, uint64_t 
         invalid("SpectrumProfile: eigenvalues must be finite and >= 0");
       if (i > 0 && lambda[i] > lambda[i - 1]) invalid("SpectrumProfile: eigenvalues must be nonincreasing");
     }
-    // operators.cpp:211-219: Q from a seeded n x n Gaussian; A = Q diag(l) Q^T; (A + A^T)/2
+    // operators.cpp:211-219: Q from a seeded n x n Gaussian; A = Q diag(l) Q^T; (A + A^T)/2.
+    // (A sharded context builds the whole A on every rank -- an O(n^3) input
+    // generator -- and keeps its column block.)
     HostRng rng(seed);
     std::vector<double> g(static_cast<size_t>(n * n));
     rng.gaussian(n, n, g.data());
     DMat G, Q, A, S;
     upload(c, G, n, n, g.data(), n, NPCG_HOST);
     Q.alloc(n, n, c.stream, false);
-    orthonormalize(c, G.p(), G.ld, n, n, Q.p(), Q.ld);
+    orthonormalize(c, G.p(), G.ld, n, n, Q.p(), Q.ld);  // replicated (not row-sharded) on every rank
     DBuf<double> lam(n, c.stream);
     NPCG_CUDA(cudaMemcpyAsync(lam.p, lambda, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
     copy2d(c, n, n, Q.p(), Q.ld, G.p(), G.ld);  // G <- Q diag(lambda)
@@ -543,6 +531,15 @@ int npcg_op_lowrank_create(npcg_ctx* ctx, int64_t n, int64_t r, const double* g,
     DBuf<double> lam(r, c.stream);
     NPCG_CUDA(cudaMemcpyAsync(lam.p, lambda, sizeof(double) * r, cudaMemcpyHostToDevice, c.stream));
     scale_cols(c, GD.p(), n, r, GD.ld, lam.p);
+    if (c.sharded()) {  // A[:, R_g] = G diag(lambda) G[R_g, :]^T / r
+      const i64 off = c.row_offset(n), nloc = c.local_rows(n);
+      A.alloc(n, nloc, c.stream, false);
+      gemm(c, n, nloc, r, 1.0, Operand{GD.p(), GD.ld, false}, Operand{G.p() + off, G.ld, false}, 0.0, A.p(), A.ld);
+      divide(c, n, nloc, A.p(), A.ld, static_cast<double>(r));
+      c.sync();
+      *out = make_colblock(ctx, std::move(A), n, kDense);
+      return;
+    }
     A.alloc(n, n, c.stream, false);
     gemm(c, n, n, r, 1.0, Operand{GD.p(), GD.ld, false}, Operand{G.p(), G.ld, false}, 0.0, A.p(), A.ld);
     divide(c, n, n, A.p(), A.ld, static_cast<double>(r));
@@ -561,8 +558,7 @@ int npcg_op_callback_create(npcg_ctx* ctx, int64_t n, npcg_apply_fn apply, npcg_
     if (n < 1) invalid("LinearOperator: dimension must be positive");
     if (where != NPCG_HOST && where != NPCG_DEVICE) invalid("npcg_op_callback_create: where must be host or device");
     auto op = std::make_unique<CallbackOp>();
-    op->ctx = &c;
-    op->n = n;
+    op->set_dim(c, n);  // on a sharded context the callback sees this rank's row blocks
     op->kind = kCallback;
     op->fn = apply;
     op->col = column;
@@ -579,8 +575,7 @@ int npcg_op_regularize(npcg_op* base, double mu, npcg_op** out) {
     Ctx& c = C(base->ctx);
     if (!(mu >= 0.0)) invalid("RegularizedOperator: mu must be >= 0");  // operators.cpp:86
     auto op = std::make_unique<RegOp>();
-    op->ctx = &c;
-    op->n = base->op->n;
+    op->set_dim(c, base->op->n);
     op->kind = kRegularized;
     op->base = base->op.get();
     op->mu = mu;
@@ -603,6 +598,13 @@ int npcg_op_dim(const npcg_op* op, int64_t* n) {
     *n = op->op->n;
   });
 }
+int npcg_op_rows(const npcg_op* op, int64_t* offset, int64_t* count) {
+  return guard([&] {
+    need(op, "npcg_op_rows");
+    if (offset) *offset = op->op->off;
+    if (count) *count = op->op->nloc;
+  });
+}
 int npcg_op_kind(const npcg_op* op) { return op ? op->op->kind : -1; }
 int npcg_op_has_column_access(const npcg_op* op) { return op && op->op->has_column() ? 1 : 0; }
 
@@ -611,7 +613,7 @@ int npcg_op_apply(npcg_op* op, int64_t rows, int64_t k, const double* v, int64_t
   return guard([&] {
     need(op, "npcg_op_apply");
     Ctx& c = C(op->ctx);
-    const i64 n = op->op->n;
+    const i64 n = op->op->nloc;  // this rank's rows (all of them unsharded)
     const bool single = k == 1;
     if (rows != n) {  // operators.cpp:14-19, 33-34
       if (single)
@@ -621,7 +623,7 @@ int npcg_op_apply(npcg_op* op, int64_t rows, int64_t k, const double* v, int64_t
     }
     if (k <= 0) return;
     View in = view_in(c, v, n, k, ldv, where);
-    if (!all_finite(c, in.p, n, k, in.ld))
+    if (!all_finite_rows(c, in.p, n, k, in.ld))
       invalid(single ? "LinearOperator - matvec: input has non-finite entries"
                      : "LinearOperator - apply_block: input has non-finite entries");
     DMat o;
@@ -638,10 +640,11 @@ int npcg_op_column(npcg_op* op, int64_t j, double* out, int where) {
     Ctx& c = C(op->ctx);
     if (!op->op->has_column()) fail(NPCG_ERUNTIME, "LinearOperator - column: operator has no column access");
     if (j < 0 || j >= op->op->n) invalid("LinearOperator - column: index out of range");
+    const i64 nl = op->op->nloc;  // sharded: this rank's rows of the column
     DMat o;
-    o.alloc(op->op->n, 1, c.stream, false);
+    o.alloc(nl, 1, c.stream, false);
     op->op->column(j, o.p());
-    download(c, o.p(), o.ld, op->op->n, 1, out, op->op->n, where);
+    download(c, o.p(), o.ld, nl, 1, out, nl, where);
     c.sync();
   });
 }
@@ -657,6 +660,8 @@ int npcg_nys_create(npcg_op* op, npcg_nys** out) {
     h->s.ctx = &c;
     h->s.op = op->op.get();
     h->s.n = op->op->n;
+    h->s.nloc = op->op->nloc;
+    h->s.off = op->op->off;
     *out = h.release();
   });
 }
@@ -683,9 +688,10 @@ int npcg_nys_extend_rng(npcg_nys* nys, int64_t extra, npcg_rng* rng) {
     // nystrom.cpp:36-45: validate, then draw the n x extra Gaussian block.
     if (extra < 1) invalid("extend_sketch: extra must be >= 1");
     if (nys->s.size + extra > nys->s.n) invalid("extend_sketch: sketch size would exceed dimension");
+    // the whole block is drawn (the reference's stream on every rank); this rank keeps its rows
     std::vector<double> raw(static_cast<size_t>(nys->s.n * extra));
     rng->r.gaussian(nys->s.n, extra, raw.data());
-    nys_extend(nys->s, raw.data(), nys->s.n, extra, NPCG_HOST);
+    nys_extend(nys->s, raw.data() + nys->s.off, nys->s.n, extra, NPCG_HOST);
     nys->ctx->c->sync();
   });
 }
@@ -769,6 +775,8 @@ int npcg_column_sampling_nystrom(npcg_op* op, int64_t ell, const int64_t* indice
     h->s.ctx = &c;
     h->s.op = op->op.get();
     h->s.n = n;
+    h->s.nloc = op->op->nloc;
+    h->s.off = op->op->off;
     nys_extend_columns(h->s, idx);
     h->s.used = idx;
     nys_factor(h->s);
@@ -792,11 +800,13 @@ int npcg_nys_from_factors(npcg_ctx* ctx, int64_t n, int64_t ell, const double* u
     Nys& s = h->s;
     s.ctx = &c;
     s.n = n;
+    s.nloc = c.local_rows(n);  // sharded: u holds this rank's rows
+    s.off = c.row_offset(n);
     auto f = std::make_shared<Factors>();
     f->ell = ell;
     f->shift = shift_used;
     if (ell > 0) {
-      upload(c, f->u, n, ell, u, ldu, where);
+      upload(c, f->u, s.nloc, ell, u, ldu, where);
       f->lambda.alloc(ell, c.stream);
       NPCG_CUDA(cudaMemcpyAsync(f->lambda.p, lambda, sizeof(double) * ell,
                                 where == NPCG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c.stream));
@@ -804,7 +814,7 @@ int npcg_nys_from_factors(npcg_ctx* ctx, int64_t n, int64_t ell, const double* u
       NPCG_CUDA(cudaMemcpyAsync(f->lambda_host.data(), f->lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToHost,
                                 c.stream));
     } else {
-      f->u.alloc(n, 0, c.stream, false);
+      f->u.alloc(s.nloc, 0, c.stream, false);
     }
     c.sync();
     s.fac = std::move(f);
@@ -820,6 +830,13 @@ int npcg_nys_info(const npcg_nys* nys, int64_t* n, int64_t* sketch_cols, int64_t
     if (shift) *shift = nys->s.factored() ? nys->s.fac->shift : 0.0;
   });
 }
+int npcg_nys_rows(const npcg_nys* nys, int64_t* offset, int64_t* count) {
+  return guard([&] {
+    need(nys, "npcg_nys_rows");
+    if (offset) *offset = nys->s.off;
+    if (count) *count = nys->s.nloc;
+  });
+}
 int npcg_nys_get(npcg_nys* nys, double* lambda, double* u, int64_t ldu, int where) {
   return guard([&] {
     need(nys, "npcg_nys_get");
@@ -831,7 +848,7 @@ int npcg_nys_get(npcg_nys* nys, double* lambda, double* u, int64_t ldu, int wher
       if (where == NPCG_HOST) std::memcpy(lambda, f.lambda_host.data(), sizeof(double) * ell);
       else NPCG_CUDA(cudaMemcpyAsync(lambda, f.lambda.p, sizeof(double) * ell, cudaMemcpyDeviceToDevice, c.stream));
     }
-    if (u && ell > 0) download(c, f.u.p(), f.u.ld, nys->s.n, ell, u, ldu, where);
+    if (u && ell > 0) download(c, f.u.p(), f.u.ld, nys->s.nloc, ell, u, ldu, where);
     c.sync();
   });
 }
@@ -840,8 +857,8 @@ int npcg_nys_get_sketch(npcg_nys* nys, double* omega, double* y, int64_t ld, int
     need(nys, "npcg_nys_get_sketch");
     Ctx& c = C(nys->ctx);
     if (nys->s.size == 0) return;
-    if (omega) download(c, nys->s.omega().p(), nys->s.omega().ld, nys->s.n, nys->s.size, omega, ld, where);
-    if (y) download(c, nys->s.y().p(), nys->s.y().ld, nys->s.n, nys->s.size, y, ld, where);
+    if (omega) download(c, nys->s.omega().p(), nys->s.omega().ld, nys->s.nloc, nys->s.size, omega, ld, where);
+    if (y) download(c, nys->s.y().p(), nys->s.y().ld, nys->s.nloc, nys->s.size, y, ld, where);
     c.sync();
   });
 }
@@ -853,6 +870,8 @@ int npcg_nys_clone(const npcg_nys* nys, int factors_only, npcg_nys** out) {
     h->ctx = nys->ctx;
     h->s.ctx = nys->s.ctx;
     h->s.n = nys->s.n;
+    h->s.nloc = nys->s.nloc;
+    h->s.off = nys->s.off;
     h->s.fac = nys->s.fac;
     if (!factors_only) {  // shares the sketch store; the first append by either handle past the other copies
       h->s.op = nys->s.op;
@@ -891,7 +910,7 @@ int pre_apply_common(npcg_pre* pre, int64_t s, const double* r, int64_t ldr, dou
     need(pre, "npcg_pre_apply");
     Ctx& c = C(pre->ctx);
     if (s <= 0) return;
-    const i64 n = pre->p.n;
+    const i64 n = pre->p.nloc;
     View in = view_in(c, r, n, s, ldr, where);
     DMat o;
     o.alloc(n, s, c.stream, false);
@@ -935,14 +954,14 @@ int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, 
     }
     if (!(opts->eta > 0.0)) invalid(std::string(context) + ": eta must be > 0");  // solvers.cpp:27-31
     if (opts->max_iter < 0) invalid(std::string(context) + ": max_iter must be >= 0");
-    const i64 n = op->op->n;
+    const i64 n = op->op->nloc;  // this rank's rows of b, x0, x (all of them unsharded)
     if (s <= 0) return;
     PcgOptions po{opts->eta, opts->max_iter, opts->relative != 0, opts->record_iterates != 0};
     View B = view_in(c, b, n, s, ldb, where);
     View X0;
     if (x0) {
       X0 = view_in(c, x0, n, s, ldx0, where);
-      if (!all_finite(c, X0.p, n, s, X0.ld)) invalid("LinearOperator - matvec: input has non-finite entries");
+      if (!all_finite_rows(c, X0.p, n, s, X0.ld)) invalid("LinearOperator - matvec: input has non-finite entries");
     }
     DMat X;
     X.alloc(n, s, c.stream, false);
@@ -999,13 +1018,13 @@ int npcg_block_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const doubl
     need(op, "npcg_block_pcg");
     need(opts, "npcg_block_pcg options");
     Ctx& c = C(op->ctx);
-    const i64 n = op->op->n;
+    const i64 n = op->op->nloc;
     // solvers.cpp:156-165
     if (s < 1) invalid("block_nystrom_pcg: need at least one column");
     if (s > 32) invalid("block_nystrom_pcg: at most 32 right-hand sides per block in this build");
     if (!(opts->eta > 0.0)) invalid("block_nystrom_pcg: eta must be > 0");
     if (!(mu >= 0.0)) invalid("block_nystrom_pcg: mu must be >= 0");
-    if (pre && pre->p.ell > 0 && pre->p.n != n) invalid("block_nystrom_pcg: preconditioner dimension mismatch");
+    if (pre && pre->p.ell > 0 && pre->p.n != op->op->n) invalid("block_nystrom_pcg: preconditioner dimension mismatch");
     View B = view_in(c, b, n, s, ldb, where);
     DMat X;
     X.alloc(n, s, c.stream, false);
@@ -1047,23 +1066,25 @@ int npcg_iteration_bound(double kappa, double epsilon, int64_t* out) {
 // =============================== adaptive ===================================
 namespace {
 double dot_dev(Ctx& c, const double* a, const double* b, i64 n) {
-  // v.w through the coldot kernel (one column dotted with one vector)
+  // v.w through the coldot kernel (one column dotted with one vector); summed over the ranks when sharded
   DBuf<double> o(1, c.stream);
   coldot(c, a, dev_ld(n), n, 1, b, dev_ld(n), 1, o.p, 1);
+  rows_allreduce(c, o.p, 1);
   double h = 0.0;
   NPCG_CUDA(cudaMemcpyAsync(&h, o.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
   return h;
 }
 
-// estimate_error_power (adaptive.cpp:83-109) from the raw start vector g.
+// estimate_error_power (adaptive.cpp:83-109) from the raw start vector g
+// (this rank's rows when sharded; norms, dots and U^T v are all-reduced).
 double power_estimate(Ctx& c, Op& op, const Nys& s, i64 q, const double* g_dev) {
-  const i64 n = op.n, ell = s.factored() ? s.fac->ell : 0;
+  const i64 n = op.nloc, ell = s.factored() ? s.fac->ell : 0;
   DMat v, w, t;
   v.alloc(n, 1, c.stream, true);
   w.alloc(n, 1, c.stream, true);
   copy2d(c, n, 1, g_dev, n, v.p(), v.ld);
-  const double v0 = std::sqrt(sum_squares(c, v.p(), n, 1, v.ld));
+  const double v0 = std::sqrt(sum_squares_rows(c, v.p(), n, 1, v.ld));
   if (v0 == 0.0) return 0.0;
   divide(c, n, 1, v.p(), v.ld, v0);
   double estimate = 0.0;
@@ -1072,12 +1093,13 @@ double power_estimate(Ctx& c, Op& op, const Nys& s, i64 q, const double* g_dev) 
     op.apply(v.p(), v.ld, 1, w.p(), w.ld);
     if (ell > 0) {  // w -= U (lambda .* (U^T v))
       coldot(c, s.fac->u.p(), s.fac->u.ld, n, ell, v.p(), v.ld, 1, t.p(), t.ld);
+      rows_allreduce(c, t.p(), ell);
       scale_cols(c, t.p(), 1, ell, 1, s.fac->lambda.p);  // t_j *= lambda_j (as a 1 x ell row)
       axpby(c, ell, 1, 0.0, t.p(), -1.0, t.p(), t.ld);  // t = -t (exact)
       rowdot(c, s.fac->u.p(), s.fac->u.ld, n, ell, t.p(), t.ld, 1, w.p(), w.ld, w.p(), w.ld);
     }
     estimate = dot_dev(c, v.p(), w.p(), n);
-    const double nrm = std::sqrt(sum_squares(c, w.p(), n, 1, w.ld));
+    const double nrm = std::sqrt(sum_squares_rows(c, w.p(), n, 1, w.ld));
     if (nrm == 0.0) return 0.0;
     copy2d(c, n, 1, w.p(), w.ld, v.p(), v.ld);
     divide(c, n, 1, v.p(), v.ld, nrm);
@@ -1094,7 +1116,7 @@ int npcg_power_estimate(npcg_op* op, npcg_nys* nys, int64_t q, const double* g_r
     if (q < 1) invalid("estimate_error_power: q must be >= 1");  // adaptive.cpp:86
     if (nys->s.factored() && nys->s.fac->ell > 0 && nys->s.n != op->op->n)
       invalid("estimate_error_power: factor shape mismatch");
-    View g = view_in(c, g_raw, op->op->n, 1, op->op->n, where);
+    View g = view_in(c, g_raw, op->op->nloc, 1, op->op->nloc, where);
     *est = power_estimate(c, *op->op, nys->s, q, g.p);
   });
 }
@@ -1107,8 +1129,8 @@ int npcg_power_estimate_rng(npcg_op* op, npcg_nys* nys, int64_t q, npcg_rng* rng
     if (nys->s.factored() && nys->s.fac->ell > 0 && nys->s.n != op->op->n)
       invalid("estimate_error_power: factor shape mismatch");
     std::vector<double> g(static_cast<size_t>(op->op->n));
-    rng->r.gaussian(op->op->n, 1, g.data());  // gaussian_vector (adaptive.cpp:90)
-    View gv = view_in(c, g.data(), op->op->n, 1, op->op->n, NPCG_HOST);
+    rng->r.gaussian(op->op->n, 1, g.data());  // gaussian_vector (adaptive.cpp:90); this rank keeps its rows
+    View gv = view_in(c, g.data() + op->op->off, op->op->nloc, 1, op->op->nloc, NPCG_HOST);
     *est = power_estimate(c, *op->op, nys->s, q, gv.p);
   });
 }
@@ -1148,6 +1170,8 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
     s.ctx = &c;
     s.op = op->op.get();
     s.n = n;
+    s.nloc = op->op->nloc;  // sharded: every draw is the whole block; this rank keeps its rows
+    s.off = op->op->off;
     // Draw-ahead (error strategy, Gaussian sketch): the stream after an Omega
     // block is always the power vector g, then -- if the loop continues -- the
     // next block, whose size the doubling rule fixes in advance. A host thread
@@ -1208,7 +1232,7 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
         rng->r.gaussian(n, extra, raw.data());
       }
       start_ahead(s.size + extra);
-      nys_extend(s, raw.data(), n, extra, NPCG_HOST);
+      nys_extend(s, raw.data() + s.off, n, extra, NPCG_HOST);
     };
     auto estimate = [&]() {
       std::vector<double> g;
@@ -1221,7 +1245,7 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
         g.resize(static_cast<size_t>(n));
         rng->r.gaussian(n, 1, g.data());
       }
-      View gv = view_in(c, g.data(), n, 1, n, NPCG_HOST);
+      View gv = view_in(c, g.data() + s.off, s.nloc, 1, s.nloc, NPCG_HOST);
       return power_estimate(c, *op->op, s, cfg->q, gv.p);
     };
     std::optional<double> err;

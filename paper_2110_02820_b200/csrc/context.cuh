@@ -6,10 +6,12 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
 
+#include "comm.cuh"
 #include "common.cuh"
 
 namespace npcg {
@@ -46,6 +48,16 @@ struct Ctx {
   std::atomic<int64_t> launches{0};
   EncodeTiledFn encode_tiled = nullptr;
   std::mutex mu;  // serialises public calls sharing this context
+  // Row-sharded contexts (one process per GPU): the communicator every
+  // operator dimension is split over (null = unsharded, one GPU).
+  std::shared_ptr<Comm> comm;
+  bool sharded() const { return comm && comm->world > 1; }
+  int rank() const { return comm ? comm->rank : 0; }
+  int world() const { return comm ? comm->world : 1; }
+  /// The local row block of an n-dimensional operator / vector on this rank.
+  RowSplit split(i64 n) const { return RowSplit(n, world()); }
+  i64 local_rows(i64 n) const { return split(n).count(rank()); }
+  i64 row_offset(i64 n) const { return split(n).offset(rank()); }
   bool prof = false;
   std::vector<ProfRec> prof_recs;
 

@@ -410,9 +410,10 @@ void trsm_right_lt(Ctx& ctx, i64 m, i64 n, double* Y, i64 ldy, const double* L, 
 namespace {
 // One CholeskyQR pass: Q = Y L^{-T} with L L^T = Y^T Y (+ shift I). `Y` is
 // consumed. Returns false on Cholesky breakdown. L is left in `Lm`.
-bool cholqr_pass(Ctx& ctx, double* Y, i64 ldy, i64 m, i64 n, double shift, DMat& Lm, double* Q, i64 ldq) {
+bool cholqr_pass(Ctx& ctx, double* Y, i64 ldy, i64 m, i64 n, double shift, DMat& Lm, double* Q, i64 ldq, bool dist) {
   Lm.alloc(n, n, ctx.stream, false);
   gemm(ctx, n, n, m, 1.0, Operand{Y, ldy, true}, Operand{Y, ldy, true}, 0.0, Lm.p(), Lm.ld);
+  if (dist) rows_allreduce(ctx, Lm.p(), Lm.ld * n);  // Y^T Y over all row blocks
   if (shift > 0.0) NPCG_LAUNCH(ctx, add_diag_kernel, static_cast<unsigned>(cdiv(n, 256)), 256, 0, Lm.p(), n, Lm.ld, shift);
   CholFactor f;
   if (!cholesky(ctx, Lm.p(), n, Lm.ld, f)) return false;
@@ -421,12 +422,14 @@ bool cholqr_pass(Ctx& ctx, double* Y, i64 ldy, i64 m, i64 n, double shift, DMat&
 }
 }  // namespace
 
-void orthonormalize(Ctx& ctx, const double* G_in, i64 ldg_in, i64 m, i64 n, double* Q, i64 ldq, double* Rt, i64 ldr) {
+void orthonormalize(Ctx& ctx, const double* G_in, i64 ldg_in, i64 m, i64 n, double* Q, i64 ldq, double* Rt, i64 ldr,
+                    bool dist) {
   if (n <= 0) return;
+  dist = dist && ctx.sharded();
   // Scale by an exact power of two so max|G| ~ 1: the Gram G^T G neither
   // underflows (e.g. the nu-shifted zero matrix, whose B ~ sqrt(nu) ~ 1e-162)
   // nor overflows. Q is scale-invariant; R^T is scaled back exactly.
-  const double amax = max_abs(ctx, G_in, m, n, ldg_in);
+  const double amax = dist ? max_abs_rows(ctx, G_in, m, n, ldg_in) : max_abs(ctx, G_in, m, n, ldg_in);
   int e2 = 0;
   if (amax > 0.0 && std::isfinite(amax)) std::frexp(amax, &e2);
   DMat scaled;
@@ -444,12 +447,13 @@ void orthonormalize(Ctx& ctx, const double* G_in, i64 ldg_in, i64 m, i64 n, doub
   copy2d(ctx, m, n, G, ldg, work.p(), work.ld);
   std::vector<DMat> Ls(1);
   bool shifted = false;
-  if (!cholqr_pass(ctx, work.p(), work.ld, m, n, 0.0, Ls[0], Q, ldq)) {
+  if (!cholqr_pass(ctx, work.p(), work.ld, m, n, 0.0, Ls[0], Q, ldq, dist)) {
     // Shifted CholeskyQR (Fukaya et al.): s = 11 (m n + n(n+1)) u ||G||_F^2.
-    const double fro2 = sum_squares(ctx, G, m, n, ldg);
-    const double s = 11.0 * (static_cast<double>(m) * n + static_cast<double>(n) * (n + 1)) * 2.220446049250313e-16 * fro2;
+    const double fro2 = dist ? sum_squares_rows(ctx, G, m, n, ldg) : sum_squares(ctx, G, m, n, ldg);
+    const double mt = dist ? rows_allreduce_host(ctx, static_cast<double>(m), false) : static_cast<double>(m);
+    const double s = 11.0 * (mt * n + static_cast<double>(n) * (n + 1)) * 2.220446049250313e-16 * fro2;
     copy2d(ctx, m, n, G, ldg, work.p(), work.ld);
-    if (!cholqr_pass(ctx, work.p(), work.ld, m, n, s, Ls[0], Q, ldq))
+    if (!cholqr_pass(ctx, work.p(), work.ld, m, n, s, Ls[0], Q, ldq, dist))
       fail(NPCG_ERUNTIME, "orthonormal_columns: shifted CholeskyQR broke down (rank-deficient input)");
     shifted = true;
   }
@@ -460,8 +464,11 @@ void orthonormalize(Ctx& ctx, const double* G_in, i64 ldg_in, i64 m, i64 n, doub
     DMat L;
     L.alloc(n, n, ctx.stream, false);
     gemm(ctx, n, n, m, 1.0, Operand{Q, ldq, true}, Operand{Q, ldq, true}, 0.0, L.p(), L.ld);
+    if (dist) rows_allreduce(ctx, L.p(), L.ld * n);
     if (!shifted || more > 0) {
-      const double tol = std::max(1e-14, 4.0 * std::sqrt(static_cast<double>(m)) * 2.220446049250313e-16);
+      // (sharded: m is the local row count; ~world x m rows in all)
+      const double tol = std::max(1e-14, 4.0 * std::sqrt(static_cast<double>(m) * (dist ? ctx.world() : 1)) *
+                                             2.220446049250313e-16);
       if (identity_deviation(ctx, L.p(), L.ld, n) <= tol) break;
     }
     CholFactor f;
@@ -561,14 +568,15 @@ void jacobi_svd_small(Ctx& ctx, double* W, i64 ldw, i64 n, double* Vs, i64 ldv, 
               sigma);
 }
 
-void thin_svd(Ctx& ctx, const double* B, i64 ldb, i64 m, i64 n, double* U, i64 ldu, double* sigma) {
-  if (m < n) invalid("thin_svd: expected a tall (m >= n) matrix");
+void thin_svd(Ctx& ctx, const double* B, i64 ldb, i64 m, i64 n, double* U, i64 ldu, double* sigma, bool dist) {
+  dist = dist && ctx.sharded();
+  if (!dist && m < n) invalid("thin_svd: expected a tall (m >= n) matrix");
   if (n <= 0) return;
   DMat Q, Rt, Vs;
   Q.alloc(m, n, ctx.stream, false);
   Rt.alloc(n, n, ctx.stream, false);
   Vs.alloc(n, n, ctx.stream, false);
-  orthonormalize(ctx, B, ldb, m, n, Q.p(), Q.ld, Rt.p(), Rt.ld);
+  orthonormalize(ctx, B, ldb, m, n, Q.p(), Q.ld, Rt.p(), Rt.ld, dist);
   const char* mode = std::getenv("NPCG_SVD");
   if (mode && std::string(mode) == "jacobi") {
     jacobi_svd_small(ctx, Rt.p(), Rt.ld, n, Vs.p(), Vs.ld, sigma);

@@ -39,8 +39,10 @@ void trsm_right_lt(Ctx& ctx, i64 m, i64 n, double* Y, i64 ldy, const double* L, 
 /// Orthonormal basis Q (m x n) of range(G) (m >= n, full column rank),
 /// by CholeskyQR2 with a shifted CholeskyQR3 fallback. If R != nullptr the
 /// upper-triangular factor (G = Q R) is written there (n x n, ld ldr).
+/// `dist`: G's rows are this rank's block of a row-sharded matrix (the Grams
+/// and norms are all-reduced; R is replicated, Q keeps the local rows).
 void orthonormalize(Ctx& ctx, const double* G, i64 ldg, i64 m, i64 n, double* Q, i64 ldq,
-                    double* R = nullptr, i64 ldr = 0);
+                    double* R = nullptr, i64 ldr = 0, bool dist = false);
 
 /// max_ij |G_ij - delta_ij| of an n x n matrix (synchronises the stream).
 double identity_deviation(Ctx& ctx, const double* G, i64 ldg, i64 n);
@@ -50,7 +52,8 @@ bool try_orthonormalize(Ctx& ctx, const double* G, i64 ldg, i64 m, i64 n, double
 
 /// Thin SVD of a tall matrix (dgesdd('S') equivalent up to column signs):
 /// U (m x n) left singular vectors, sigma (n) descending, on device.
-void thin_svd(Ctx& ctx, const double* B, i64 ldb, i64 m, i64 n, double* U, i64 ldu, double* sigma);
+void thin_svd(Ctx& ctx, const double* B, i64 ldb, i64 m, i64 n, double* U, i64 ldu, double* sigma,
+              bool dist = false);
 
 /// One-sided Jacobi on the n x n matrix W (ld ldw, overwritten): finds an
 /// orthogonal V with W V orthogonal columns. sigma(j) = ||(W V)(:,j)||,

@@ -447,8 +447,8 @@ __device__ __forceinline__ void kf_col_flush(const double* CRED, int h, i64 J, i
 template <int S, int DP, bool CLAMP>
 __global__ void __launch_bounds__(KF_THREADS, 2)
     kfree_sym_kernel(const double* __restrict__ pts, i64 ldp, i64 n, int d, int dp_rt, const double* __restrict__ norms,
-                     double c, const double* __restrict__ V, i64 ldv, i64 npairs, double* __restrict__ part,
-                     const int* __restrict__ gate) {
+                     double c, const double* __restrict__ V, i64 ldv, i64 pair0, i64 npairs,
+                     double* __restrict__ part, const int* __restrict__ gate) {
   if (gate && *gate == 0) return;
   extern __shared__ double kfs[];
   const int dp = DP ? DP : dp_rt;
@@ -465,7 +465,8 @@ __global__ void __launch_bounds__(KF_THREADS, 2)
   const i64 nb = (n + KF_BM - 1) / KF_BM;
   double* mypart = part + static_cast<i64>(blockIdx.x) * S * n;
 
-  const i64 u0 = npairs * blockIdx.x / gridDim.x, u1 = npairs * (blockIdx.x + 1) / gridDim.x;
+  // this CTA's contiguous share of the pairs [pair0, pair0 + npairs) (a rank's share when sharded)
+  const i64 u0 = pair0 + npairs * blockIdx.x / gridDim.x, u1 = pair0 + npairs * (blockIdx.x + 1) / gridDim.x;
   if (u0 >= u1) return;
   // pair u -> (I, J): rows I' < I hold I*nb - I(I-1)/2 pairs
   auto row_off = [&](i64 I) { return I * nb - I * (I - 1) / 2; };
@@ -782,8 +783,8 @@ void kernel_block(Ctx& ctx, const KernelFreeOp& op, i64 row0, i64 rows, i64 col0
 }
 
 template <int S, int DP, bool CLAMP>
-void kfree_sym_launch(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, i64 smem, i64 npairs, double c,
-                      double* part, const int* gate, i64& grid) {
+void kfree_sym_launch(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, i64 smem, i64 pair0, i64 npairs,
+                      double c, double* part, const int* gate, i64& grid) {
   static int per_sm = 0;
   static i64 per_sm_smem = -1;
   if (per_sm_smem != smem) {
@@ -794,11 +795,11 @@ void kfree_sym_launch(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv
     per_sm = std::max(per_sm, 1);
     per_sm_smem = smem;
   }
-  grid = std::min<i64>(static_cast<i64>(per_sm) * ctx.sm_count, npairs);
+  grid = std::max<i64>(1, std::min<i64>(static_cast<i64>(per_sm) * ctx.sm_count, npairs));
   if (!part) return;  // sizing call
   const int d = static_cast<int>(op.d);
   NPCG_LAUNCH(ctx, (kfree_sym_kernel<S, DP, CLAMP>), static_cast<unsigned>(grid), KF_THREADS, static_cast<int>(smem),
-              op.pts_s.p(), op.pts_s.ld, op.n, d, (d + 3) / 4 * 4, op.norms_s.p, c, V, ldv, npairs, part, gate);
+              op.pts_s.p(), op.pts_s.ld, op.n, d, (d + 3) / 4 * 4, op.norms_s.p, c, V, ldv, pair0, npairs, part, gate);
 }
 
 template <int S>
@@ -811,11 +812,19 @@ void kfree_sym(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, doubl
   const double c = -1.0 / (2.0 * op.sigma * op.sigma);
   // |exponent| <= |c| max ||x_i - x_j||^2 <= |c| 4 max ||x||^2: below 700 no clamp is needed
   const bool clamp = !(std::fabs(c) * 4.0 * op.max_norm < 690.0);
-  const i64 nb = cdiv(op.n, KF_BM), npairs = nb * (nb + 1) / 2;
+  const i64 nb = cdiv(op.n, KF_BM), all_pairs = nb * (nb + 1) / 2;
+  // a sharded operator evaluates an equal contiguous share of the pairs; its
+  // output is then a full-length partial (reduce-scattered by the ShardOp)
+  const i64 pair0 = all_pairs * op.shard_rank / op.shard_world;
+  const i64 npairs = all_pairs * (op.shard_rank + 1) / op.shard_world - pair0;
+  if (npairs <= 0) {
+    NPCG_CUDA(cudaMemset2DAsync(out, sizeof(double) * ldo, 0, sizeof(double) * op.n, S, ctx.stream));
+    return;
+  }
   auto launch = [&](double* part, i64& grid) {
-    if (dp == 32 && !clamp) kfree_sym_launch<S, 32, false>(ctx, op, V, ldv, smem, npairs, c, part, gate, grid);
-    else if (dp == 32) kfree_sym_launch<S, 32, true>(ctx, op, V, ldv, smem, npairs, c, part, gate, grid);
-    else kfree_sym_launch<S, 0, true>(ctx, op, V, ldv, smem, npairs, c, part, gate, grid);
+    if (dp == 32 && !clamp) kfree_sym_launch<S, 32, false>(ctx, op, V, ldv, smem, pair0, npairs, c, part, gate, grid);
+    else if (dp == 32) kfree_sym_launch<S, 32, true>(ctx, op, V, ldv, smem, pair0, npairs, c, part, gate, grid);
+    else kfree_sym_launch<S, 0, true>(ctx, op, V, ldv, smem, pair0, npairs, c, part, gate, grid);
   };
   i64 grid = 0;
   launch(nullptr, grid);
@@ -823,7 +832,7 @@ void kfree_sym(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, doubl
   NPCG_CUDA(cudaMemsetAsync(part.p, 0, sizeof(double) * grid * S * op.n, ctx.stream));
   launch(part.p, grid);
   // reference work (every entry of K): the kernel evaluates the upper blocks only
-  ctx.prof_work(static_cast<double>(op.n) * op.n * (2.0 * d + 2.0 * S), 8.0 * op.n * (d + 2 * S));
+  ctx.prof_work(static_cast<double>(op.n) * op.n * (2.0 * d + 2.0 * S) / op.shard_world, 8.0 * op.n * (d + 2 * S));
   NPCG_LAUNCH(ctx, kfree_reduce_kernel, static_cast<unsigned>(cdiv(op.n * S, 256)), 256, 0, part.p,
               static_cast<int>(grid), op.n, S, out, ldo, gate);
 }
@@ -877,12 +886,24 @@ void prepare_kernel_free(Ctx& ctx, KernelFreeOp& op) {
               op.pts.p(), op.pts.ld, op.n, op.d, op.pts_rm.p(), op.pts_rm.ld);
 }
 
+// Which sharded paths produce a full-length partial (see kernel_apply_free):
+// the symmetric pair kernel (k <= 2) and the column-block sketch path (k > 8).
+bool KernelFreeOp::partial_output(i64 k) const {
+  if (shard_world <= 1) return false;
+  static const char* mode = std::getenv("NPCG_KFREE");
+  const bool blocked = mode && std::string(mode) == "blocked";
+  if (blocked) return false;
+  return (k <= 2 && d <= 64) || k > 8;
+}
+
 void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ldv, i64 k, double* out, i64 ldo,
                        const int* gate) {
   static const char* mode = std::getenv("NPCG_KFREE");  // diagnostics: "blocked" / "scalar"
   const bool force_blocked = mode && std::string(mode) == "blocked";
   const bool force_scalar = mode && std::string(mode) == "scalar";
   const bool rowwise = mode && std::string(mode) == "rowwise";  // diagnostics: non-symmetric fused kernel
+  const bool sharded = op.shard_world > 1;
+  if (sharded && (force_scalar || rowwise)) fail(NPCG_ERUNTIME, "KernelOperator shard: NPCG_KFREE diagnostics modes are unsharded only");
   if (k <= 2 && op.d <= 64 && !force_blocked && !force_scalar) {
     if (rowwise) {
       if (k == 1) kfree_fused<1>(ctx, op, V, ldv, out, ldo, gate);
@@ -914,7 +935,11 @@ void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ld
     DMat Kt;
     Kt.alloc(n, R, ctx.stream, false);
     NPCG_CUDA(cudaMemset2DAsync(out, sizeof(double) * ldo, 0, sizeof(double) * n, k, ctx.stream));
-    for (i64 r0 = 0; r0 < n; r0 += R) {
+    for (i64 r0 = 0, blk = 0; r0 < n; r0 += R, ++blk) {
+      // sharded: the column blocks are dealt round-robin over the ranks (the
+      // work of block r0 falls with n - r0, so round-robin keeps it balanced)
+      // and `out` is this rank's full-length partial
+      if (blk % op.shard_world != op.shard_rank) continue;
       const i64 rb = std::min(R, n - r0), L = n - r0;
       if (op.d <= 64) {  // one fused pass (DMMA dots + exp + store)
         kernel_block(ctx, op, r0, L, r0, rb, Kt.p(), Kt.ld);
@@ -944,17 +969,20 @@ void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ld
     const i64 R = std::min<i64>(n, std::max<i64>(128, budget / (8 * std::max<i64>(n, 1)) / 128 * 128));
     DMat Kt;  // K[:, r0 : r0+R] = (K_R)^T, n x R: its columns are contiguous
     Kt.alloc(n, R, ctx.stream, false);
-    for (i64 r0 = 0; r0 < n; r0 += R) {
-      const i64 rb = std::min(R, n - r0);
+    // sharded: only this rank's rows [shard_off, shard_off + shard_rows), written to out's local rows
+    const i64 row_lo = sharded ? op.shard_off : 0, row_hi = sharded ? op.shard_off + op.shard_rows : n;
+    for (i64 r0 = row_lo; r0 < row_hi; r0 += R) {
+      const i64 rb = std::min(R, row_hi - r0);
       gemm(ctx, n, rb, op.d, -2.0, Operand{op.pts.p(), op.pts.ld, false}, Operand{op.pts.p() + r0, op.pts.ld, false},
            0.0, Kt.p(), Kt.ld);
       NPCG_LAUNCH(ctx, kernel_colblock_epilogue_kernel,
                   static_cast<unsigned>(std::min<i64>(cdiv(rb * n, 256), ctx.sm_count * 16)), 256, 0, Kt.p(), Kt.ld, n,
                   rb, r0, op.norms.p, c);
+      double* o = out + (r0 - row_lo);
       if (k <= 8) {  // few vectors: out_R = (K_R^T)^T V as column dots (HBM-bound on the block)
-        coldot(ctx, Kt.p(), Kt.ld, n, rb, V, ldv, static_cast<int>(k), out + r0, ldo, 0.0, nullptr, 0, gate);
+        coldot(ctx, Kt.p(), Kt.ld, n, rb, V, ldv, static_cast<int>(k), o, ldo, 0.0, nullptr, 0, gate);
       } else {
-        gemm(ctx, rb, k, n, 1.0, Operand{Kt.p(), Kt.ld, true}, Operand{V, ldv, true}, 0.0, out + r0, ldo);
+        gemm(ctx, rb, k, n, 1.0, Operand{Kt.p(), Kt.ld, true}, Operand{V, ldv, true}, 0.0, o, ldo);
       }
     }
     return;

@@ -21,9 +21,9 @@ void Op::apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i6
   // out = A p; out += mu p.
   apply(P, ldp, S, out, ldo, gate);
   if (ldp == ldo) {
-    axpby(*ctx, n, S, mu, P, 1.0, out, ldo);
+    axpby(*ctx, nloc, S, mu, P, 1.0, out, ldo);
   } else {
-    for (int s = 0; s < S; ++s) axpby(*ctx, n, 1, mu, P + s * ldp, 1.0, out + s * ldo, ldo);
+    for (int s = 0; s < S; ++s) axpby(*ctx, nloc, 1, mu, P + s * ldp, 1.0, out + s * ldo, ldo);
   }
 }
 
@@ -43,9 +43,11 @@ __global__ void gather_cols_kernel2(const double* __restrict__ a, i64 lda, i64 n
     out[i + c * ldo] = a[i + idx[c] * lda];
   }
 }
-__global__ void unit_cols_kernel(double* __restrict__ om, i64 ldo, const i64* __restrict__ idx, i64 k) {
+// omega(:, c) = e_idx[c], restricted to this rank's rows [off, off + nloc)
+__global__ void unit_cols_kernel(double* __restrict__ om, i64 ldo, const i64* __restrict__ idx, i64 k, i64 off,
+                                 i64 nloc) {
   const i64 c = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c < k) om[idx[c] + c * ldo] = 1.0;
+  if (c < k && idx[c] >= off && idx[c] < off + nloc) om[idx[c] - off + c * ldo] = 1.0;
 }
 }  // namespace
 
@@ -133,13 +135,13 @@ void RegOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const i
     base->apply_shift(V, ldv, static_cast<int>(k), mu, out, ldo, gate);
   } else {
     base->apply(V, ldv, k, out, ldo, gate);
-    for (i64 s = 0; s < k; ++s) axpby(*ctx, n, 1, mu, V + s * ldv, 1.0, out + s * ldo, ldo);
+    for (i64 s = 0; s < k; ++s) axpby(*ctx, nloc, 1, mu, V + s * ldv, 1.0, out + s * ldo, ldo);
   }
 }
 void RegOp::apply_shift(const double* P, i64 ldp, int S, double mu2, double* out, i64 ldo, const int* gate) {
   apply(P, ldp, S, out, ldo, gate);
   if (mu2 != 0.0) {  // (A_mu p) += mu2 p (nystrom_pcg on a regularized operator, solvers.cpp:137-141)
-    for (int s = 0; s < S; ++s) axpby(*ctx, n, 1, mu2, P + s * ldp, 1.0, out + s * ldo, ldo);
+    for (int s = 0; s < S; ++s) axpby(*ctx, nloc, 1, mu2, P + s * ldp, 1.0, out + s * ldo, ldo);
   }
 }
 
@@ -153,24 +155,27 @@ void ensure_capacity(Nys& s, i64 cols) {
   const i64 have = s.sk ? s.sk->omega.cols : 0;
   const i64 cap = std::min<i64>(s.n, std::max<i64>(cols, 2 * have));
   auto st = std::make_shared<SketchStore>();
-  st->omega.alloc(s.n, cap, s.ctx->stream, true);
-  st->y.alloc(s.n, cap, s.ctx->stream, true);
+  st->omega.alloc(s.nloc, cap, s.ctx->stream, true);
+  st->y.alloc(s.nloc, cap, s.ctx->stream, true);
   if (s.size > 0) {
-    copy2d(*s.ctx, s.n, s.size, s.sk->omega.p(), s.sk->omega.ld, st->omega.p(), st->omega.ld);
-    copy2d(*s.ctx, s.n, s.size, s.sk->y.p(), s.sk->y.ld, st->y.p(), st->y.ld);
+    copy2d(*s.ctx, s.nloc, s.size, s.sk->omega.p(), s.sk->omega.ld, st->omega.p(), st->omega.ld);
+    copy2d(*s.ctx, s.nloc, s.size, s.sk->y.p(), s.sk->y.ld, st->y.p(), st->y.ld);
   }
   st->filled = s.size;
   s.sk = std::move(st);
 }
 }  // namespace
 
-// extend_sketch (nystrom.cpp:36-58) after the Gaussian draw.
+// extend_sketch (nystrom.cpp:36-58) after the Gaussian draw. `raw` is this
+// rank's row block of the n x extra Gaussian (all of it unsharded). On a
+// sharded context the Gram-Schmidt projections and the CholeskyQR Grams are
+// all-reduced (l_old x extra, extra x extra) and Y_new = A Q_new all-gathers Q.
 void nys_extend(Nys& s, const double* raw, i64 ld, i64 extra, int where) {
   Ctx& ctx = *s.ctx;
   if (!s.op) fail(NPCG_ERUNTIME, "extend_sketch: approximation has no operator");
   if (extra < 1) invalid("extend_sketch: extra must be >= 1");
   if (s.size + extra > s.n) invalid("extend_sketch: sketch size would exceed dimension");
-  const i64 n = s.n, old = s.size;
+  const i64 n = s.nloc, old = s.size;
   DMat fresh;
   upload(ctx, fresh, n, extra, raw, ld, where);
   ensure_capacity(s, old + extra);
@@ -182,12 +187,13 @@ void nys_extend(Nys& s, const double* raw, i64 ld, i64 extra, int where) {
     for (int pass = 0; pass < 2; ++pass) {
       gemm(ctx, old, extra, n, 1.0, Operand{st.omega.p(), st.omega.ld, true}, Operand{fresh.p(), fresh.ld, true}, 0.0,
            coef.p(), coef.ld);
+      rows_allreduce(ctx, coef.p(), coef.ld * extra);  // Omega^T fresh over all row blocks
       gemm(ctx, n, extra, old, -1.0, Operand{st.omega.p(), st.omega.ld, false}, Operand{coef.p(), coef.ld, true}, 1.0,
            fresh.p(), fresh.ld);
     }
   }
   double* q_new = st.omega.col(old);
-  orthonormalize(ctx, fresh.p(), fresh.ld, n, extra, q_new, st.omega.ld);
+  orthonormalize(ctx, fresh.p(), fresh.ld, n, extra, q_new, st.omega.ld, nullptr, 0, /*dist=*/true);
   s.op->apply(q_new, st.omega.ld, extra, st.y.col(old), st.y.ld);
   s.size = st.filled = old + extra;
   s.fac.reset();  // the handle now holds an unfactored, larger sketch
@@ -200,11 +206,11 @@ void nys_extend_columns(Nys& s, const std::vector<i64>& idx) {
   ensure_capacity(s, old + extra);
   SketchStore& st = *s.sk;
   // omega columns: e_j (fresh capacity is zero; reused capacity is cleared first)
-  NPCG_CUDA(cudaMemset2DAsync(st.omega.col(old), st.omega.ld * 8, 0, s.n * 8, extra, ctx.stream));
+  NPCG_CUDA(cudaMemset2DAsync(st.omega.col(old), st.omega.ld * 8, 0, s.nloc * 8, extra, ctx.stream));
   DBuf<i64> d(extra, ctx.stream);
   NPCG_CUDA(cudaMemcpyAsync(d.p, idx.data(), sizeof(i64) * extra, cudaMemcpyHostToDevice, ctx.stream));
   NPCG_LAUNCH(ctx, unit_cols_kernel, static_cast<unsigned>(cdiv(extra, 256)), 256, 0, st.omega.col(old), st.omega.ld,
-              d.p, extra);
+              d.p, extra, s.off, s.nloc);
   s.op->columns(idx.data(), extra, st.y.col(old), st.y.ld);
   ctx.sync();
   s.size = st.filled = old + extra;
@@ -223,10 +229,13 @@ double ulp_spacing(double x) {
 }  // namespace
 
 // nystrom_from_sketch (nystrom.cpp:96-140). The result is built in a fresh
-// Factors and published only after every check passed.
+// Factors and published only after every check passed. Sharded: ||Y||_F, the
+// finiteness checks and the core Omega^T Y_nu are all-reduced, so every rank
+// takes the same shift / Cholesky branch on bitwise-identical l x l data;
+// B = Y_nu L^-T and U keep the local rows.
 void nys_factor(Nys& s) {
   Ctx& ctx = *s.ctx;
-  const i64 n = s.n, ell = s.size;
+  const i64 n = s.nloc, ell = s.size;
   auto f = std::make_shared<Factors>();
   f->ell = ell;
   if (ell == 0) {
@@ -236,9 +245,9 @@ void nys_factor(Nys& s) {
   }
   const DMat& om = s.omega();
   const DMat& y = s.y();
-  if (!all_finite(ctx, y.p(), n, ell, y.ld))
+  if (!all_finite_rows(ctx, y.p(), n, ell, y.ld))
     fail(NPCG_ERUNTIME, "nystrom_from_sketch: sketch has non-finite entries");
-  const double ynorm = std::sqrt(sum_squares(ctx, y.p(), n, ell, y.ld));
+  const double ynorm = std::sqrt(sum_squares_rows(ctx, y.p(), n, ell, y.ld));
   const double nu0 = ulp_spacing(ynorm);
   double nu = nu0;
   DMat ynu, core, b;
@@ -250,10 +259,11 @@ void nys_factor(Nys& s) {
     add_scaled(ctx, n, ell, y.p(), nu, om.p(), ynu.p(), ynu.ld);  // Y + nu Omega (shared ld)
     gemm(ctx, ell, ell, n, 1.0, Operand{om.p(), om.ld, true}, Operand{ynu.p(), ynu.ld, true}, 0.0,
          core.p(), core.ld);
+    rows_allreduce(ctx, core.p(), core.ld * ell);  // Omega^T Y_nu over all row blocks
     CholFactor cf;
     if (!cholesky(ctx, core.p(), ell, core.ld, cf)) continue;
     trsm_right_lt(ctx, n, ell, ynu.p(), ynu.ld, core.p(), core.ld, cf, b.p(), b.ld);
-    if (!all_finite(ctx, b.p(), n, ell, b.ld)) continue;
+    if (!all_finite_rows(ctx, b.p(), n, ell, b.ld)) continue;
     f->shift = nu;
     factored = true;
     break;
@@ -261,7 +271,7 @@ void nys_factor(Nys& s) {
   if (!factored) {
     std::ostringstream msg;
     msg << "nystrom_from_sketch: Cholesky failed after 3 shift escalations"
-        << " (n = " << n << ", ell = " << ell << ", initial shift = " << nu0 << ", final shift = " << nu / 10.0
+        << " (n = " << s.n << ", ell = " << ell << ", initial shift = " << nu0 << ", final shift = " << nu / 10.0
         << ", ||Y||_F = " << ynorm << ")";
     fail(NPCG_ERUNTIME, msg.str());
   }
@@ -269,7 +279,7 @@ void nys_factor(Nys& s) {
   core.buf.release();
   f->u.alloc(n, ell, ctx.stream, false);
   DBuf<double> sigma(ell, ctx.stream);
-  thin_svd(ctx, b.p(), b.ld, n, ell, f->u.p(), f->u.ld, sigma.p);
+  thin_svd(ctx, b.p(), b.ld, n, ell, f->u.p(), f->u.ld, sigma.p, /*dist=*/true);
   f->lambda.alloc(ell, ctx.stream);
   NPCG_LAUNCH(ctx, clamp_lambda_kernel, static_cast<unsigned>(cdiv(ell, 256)), 256, 0, sigma.p, ell, f->shift,
               f->lambda.p);
@@ -307,6 +317,7 @@ void pre_build(Pre& p, const Nys& s, double mu) {
   p.ctx = s.ctx;
   p.fac = s.fac;
   p.n = s.n;
+  p.nloc = s.nloc;
   p.ell = s.fac->ell;
   p.mu = mu;
   p.lambda_ell = s.fac->lambda_min();
@@ -319,31 +330,34 @@ void pre_build(Pre& p, const Nys& s, double mu) {
 }
 
 namespace {
-// out = V + U diag(g) U^T V   (preconditioner.cpp:17-45 shapes)
+// out = V + U diag(g) U^T V   (preconditioner.cpp:17-45 shapes). Sharded: U
+// and V are this rank's rows; T = U^T V is all-reduced (l x S).
 void lowrank_update(Pre& p, const double* g, const double* V, i64 ldv, i64 S, double* out, i64 ldo,
                     const int* gate) {
   Ctx& ctx = *p.ctx;
+  const i64 n = p.nloc;
   if (p.ell == 0) {
-    copy2d(ctx, p.n, S, V, ldv, out, ldo);
+    copy2d(ctx, n, S, V, ldv, out, ldo);
     return;
   }
   const Factors& s = *p.fac;
   DMat T;
   T.alloc(p.ell, S, ctx.stream, false);
   if (S <= 8) {
-    coldot(ctx, s.u.p(), s.u.ld, p.n, p.ell, V, ldv, static_cast<int>(S), T.p(), T.ld, 0.0, nullptr, 0, gate);
+    coldot(ctx, s.u.p(), s.u.ld, n, p.ell, V, ldv, static_cast<int>(S), T.p(), T.ld, 0.0, nullptr, 0, gate);
   } else {
-    gemm(ctx, p.ell, S, p.n, 1.0, Operand{s.u.p(), s.u.ld, true}, Operand{V, ldv, true}, 0.0, T.p(), T.ld);
+    gemm(ctx, p.ell, S, n, 1.0, Operand{s.u.p(), s.u.ld, true}, Operand{V, ldv, true}, 0.0, T.p(), T.ld);
   }
+  rows_allreduce(ctx, T.p(), T.ld * S);
   NPCG_LAUNCH(ctx, scale_rows_kernel, static_cast<unsigned>(cdiv(p.ell * S, 256)), 256, 0, T.p(), p.ell, S, T.ld, g,
               gate);
   if (S <= 8) {
-    rowdot(ctx, s.u.p(), s.u.ld, p.n, p.ell, T.p(), T.ld, static_cast<int>(S), V, ldv, out, ldo, gate);
+    rowdot(ctx, s.u.p(), s.u.ld, n, p.ell, T.p(), T.ld, static_cast<int>(S), V, ldv, out, ldo, gate);
   } else {
     DMat us;
-    us.alloc(p.n, S, ctx.stream, false);
-    gemm(ctx, p.n, S, p.ell, 1.0, Operand{s.u.p(), s.u.ld, false}, Operand{T.p(), T.ld, true}, 0.0, us.p(), us.ld);
-    add2d(ctx, p.n, S, V, ldv, us.p(), us.ld, out, ldo);  // r + (U scaled)
+    us.alloc(n, S, ctx.stream, false);
+    gemm(ctx, n, S, p.ell, 1.0, Operand{s.u.p(), s.u.ld, false}, Operand{T.p(), T.ld, true}, 0.0, us.p(), us.ld);
+    add2d(ctx, n, S, V, ldv, us.p(), us.ld, out, ldo);  // r + (U scaled)
   }
 }
 }  // namespace

@@ -15,10 +15,19 @@ enum OpKind { kDense = 0, kGram = 1, kKernelStored = 2, kKernelFree = 3, kCallba
 /// do_apply_block(); the C-ABI layer does the reference's dim/finite checks.
 struct Op {
   Ctx* ctx = nullptr;
-  i64 n = 0;
+  i64 n = 0;              // operator dimension
+  i64 nloc = 0, off = 0;  // this rank's row block of every n-vector (nloc = n, off = 0 unsharded)
   int kind = kDense;
+  /// Set n and the local row block from the context's layout.
+  void set_dim(Ctx& c, i64 n_) {
+    ctx = &c;
+    n = n_;
+    nloc = c.local_rows(n_);
+    off = c.row_offset(n_);
+  }
   virtual ~Op() = default;
-  /// out (n x k) = A V  (device pointers).
+  /// out (n x k) = A V  (device pointers; on a sharded context V and out are
+  /// this rank's row blocks, nloc x k).
   virtual void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate = nullptr) = 0;
   /// out = A P + mu P with the reference's rounding order (out = A p; out += mu p).
   virtual void apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate);
@@ -27,6 +36,10 @@ struct Op {
   /// A product costs far more than a host round trip (matrix-free kernel):
   /// the PCG driver then keeps one iteration in flight instead of several.
   virtual bool costly() const { return false; }
+  /// For the local operator of a ShardOp: apply() on a full-length input
+  /// yields a full-length partial (reduce-scattered by the ShardOp) rather
+  /// than this rank's rows.
+  virtual bool partial_output(i64 /*k*/) const { return false; }
   /// out(:, c) = A(:, idx[c]) for c < k (host indices; ld ldo). Default: column() per index.
   virtual void columns(const i64* idx, i64 k, double* out, i64 ldo);
 };
@@ -60,6 +73,8 @@ struct GramOp : Op {  // GramRidgeOperator (operators.cpp:105-121): (1/m) G^T (G
   /// (the caller's host buffer is free afterwards) and raise the constructor's
   /// non-finite error (operators.cpp:108-109) if the flag is set.
   void settle();
+  bool shard_partial = false;  // local operator of a ShardOp over a row block of X: full-length partial output
+  bool partial_output(i64) const override { return shard_partial; }
   ~GramOp() override;
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
   void apply_shift(const double* P, i64 ldp, int S, double mu, double* out, i64 ldo, const int* gate) override;
@@ -86,6 +101,12 @@ struct KernelFreeOp : Op {  // KernelOperator beyond dense_cap (operators.cpp:15
   void column(i64 j, double* out) override;
   void columns(const i64* idx, i64 k, double* out, i64 ldo) override;
   bool costly() const override { return true; }
+  bool partial_output(i64 k) const override;
+  // Row-sharded use (the local operator of a ShardOp): this rank's share of
+  // the work -- a range of the symmetric block pairs (k <= 2), of the column
+  // blocks (k > 8), or its own row block (3..8 vectors).
+  int shard_rank = 0, shard_world = 1;
+  i64 shard_off = 0, shard_rows = 0;
 };
 
 /// A user operator behind C callbacks (npcg_op_callback_create): the
@@ -110,31 +131,29 @@ struct RegOp : Op {
   bool costly() const override { return base->costly(); }
 };
 
-/// Exchange callback of a sharded operator (npcg_exchange_fn in the C-ABI):
-/// kind 0 = in-place sum all-reduce of `count` doubles (send == recv);
-/// kind 1 = all-gather of `count` doubles per rank into recv (rank-major).
-/// Enqueued on `stream`; returns 0 on success.
-using ExchangeFn = int (*)(void* user, int kind, double* send, double* recv, int64_t count, void* stream);
-
-/// Column block A[:, off : off+nloc] of a symmetric A held by one rank; its
-/// apply gives rows off.. of A V (A^T V restricted to the block).
+/// Column block A[:, off : off+nloc] of a symmetric A held by one rank; on a
+/// full-length input V its apply gives rows off.. of A V (A^T V restricted to
+/// the block).
 struct DenseColBlockOp : Op {
-  DMat a;   // n x nloc
-  i64 nloc = 0;
+  DMat a;  // n x nloc
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
+  bool has_column() const override { return true; }
+  /// Local rows of A(:, j) = row j of the block (A symmetric).
+  void column(i64 j, double* out) override;
 };
 
-/// Row-sharded operator for one-process-per-GPU runs: `local` computes this
-/// rank's share, `fn` completes it (mode 0: all-reduce of partial products --
-/// Gram over a row block of X; mode 1: all-gather of row blocks -- dense
-/// column block). Vectors are replicated on every rank.
+/// Row-sharded operator (sharded context, one process per GPU): apply()
+/// takes and returns this rank's row blocks. It all-gathers the input over
+/// the ranks (NCCL), runs `local` on the full-length block and keeps the local
+/// rows `local` produced (column block A[:, R_g]: the stored dense / kernel /
+/// low-rank operators) or reduce-scatters the full-length partial it produced
+/// (Gram ridge over a row block of X, the symmetric matrix-free kernel).
 struct ShardOp : Op {
-  std::unique_ptr<Op> local;
-  int mode = 0;
-  i64 nranks = 1, rank = 0, nmax = 0;  // mode 1: equal blocks of nmax rows (last one short)
-  ExchangeFn fn = nullptr;
-  void* user = nullptr;
+  std::unique_ptr<Op> local;  // works on full-length inputs
   void apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) override;
+  bool has_column() const override { return local->has_column(); }
+  void column(i64 j, double* out) override;
+  bool costly() const override { return local->costly(); }
 };
 
 /// Build the stored Gaussian kernel matrix (operators.cpp:125-150) on device.
@@ -161,7 +180,7 @@ struct SketchStore {
 /// from it share it, so extending or refactoring the handle later never
 /// changes an existing preconditioner (the reference's value semantics).
 struct Factors {
-  DMat u;                         // n x ell
+  DMat u;                         // n x ell (this rank's rows on a sharded context)
   DBuf<double> lambda;            // ell, nonincreasing
   std::vector<double> lambda_host;
   i64 ell = 0;
@@ -173,7 +192,8 @@ struct Factors {
 struct Nys {
   Ctx* ctx = nullptr;
   Op* op = nullptr;  // not owned; nullptr for from_factors
-  i64 n = 0;
+  i64 n = 0;              // dimension
+  i64 nloc = 0, off = 0;  // this rank's rows of Omega, Y, U (nloc = n unsharded)
   std::shared_ptr<SketchStore> sk;  // first `size` columns are this handle's pair
   i64 size = 0;
   std::shared_ptr<const Factors> fac;  // null until factored; replaced only by a successful nys_factor
@@ -196,6 +216,7 @@ struct Pre {
   Ctx* ctx = nullptr;
   std::shared_ptr<const Factors> fac;  // U, lambda (device)
   i64 n = 0, ell = 0;
+  i64 nloc = 0;  // local rows of U and of the vectors it is applied to
   double mu = 0.0, lambda_ell = 0.0;
   DBuf<double> gain_inv;  // (lambda_ell + mu)/(lambda + mu) - 1
   DBuf<double> gain_fwd;  // (lambda + mu)/(lambda_ell + mu) - 1

@@ -219,6 +219,17 @@ __global__ void record_kernel(i64 n, int S, const double* __restrict__ X, i64 ld
   }
 }
 
+// Row-sharded contexts: this rank's sum of the per-block partials (fixed
+// order), all-reduced over the ranks before the fin_* kernel reads it as a
+// single block.
+__global__ void rank_partials_kernel(const double* __restrict__ part, int nblk, int stride, double* __restrict__ out) {
+  const int idx = threadIdx.x;
+  if (idx >= stride) return;
+  double v = 0.0;
+  for (int b = 0; b < nblk; ++b) v += part[b * stride + idx];
+  out[idx] = v;
+}
+
 __global__ void snapshot_running_kernel(const State* __restrict__ st, int S, int* __restrict__ flags) {
   const int s = threadIdx.x;
   if (s < S) flags[s] = st->c[s].status == 0 ? 1 : 0;
@@ -1046,7 +1057,7 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
   using Clock = std::chrono::steady_clock;
   const auto t0 = Clock::now();
   if (S < 1 || S > kMaxS) fail(NPCG_EINVAL, "pcg_solve: 1..8 right-hand sides per batch");
-  const i64 n = op.n;
+  const i64 n = op.nloc;  // this rank's rows of every vector (all of them unsharded)
   const int nblk = static_cast<int>(std::max<i64>(1, std::min<i64>(cdiv(n, 2048), 2 * ctx.sm_count)));
   const i64 hstride = opt.max_iter + 1;
   DMat R, Z, P, V;
@@ -1062,6 +1073,16 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
   DBuf<double> part(static_cast<i64>(nblk) * 2 * S, ctx.stream);
   DBuf<double> hist(S * hstride, ctx.stream);
   int* gate = &st.p->any_running;
+  // Sharded: every dot / norm is this rank's partial; combine() sums the
+  // block partials per rank and all-reduces them (bitwise-identical scalars on
+  // every rank, so all ranks take the same convergence branch).
+  DBuf<double> rsum(2 * S, ctx.stream);
+  auto combine = [&](int stride) -> std::pair<const double*, int> {
+    if (!ctx.sharded()) return {part.p, nblk};
+    NPCG_LAUNCH(ctx, rank_partials_kernel, 1, 32, 0, part.p, nblk, stride, rsum.p);
+    rows_allreduce(ctx, rsum.p, stride);
+    return {rsum.p, 1};
+  };
 
   // x = x0 (or 0); r = b - A_mu x0 (solvers.cpp:52-53; A 0 = 0 is elided, matvec_count keeps the +1)
   if (X0) {
@@ -1073,8 +1094,11 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
     NPCG_LAUNCH(ctx, resid0_kernel, nblk, 256, 0, n, static_cast<int>(S), B, ldb, static_cast<const double*>(nullptr),
                 0, R.p(), R.ld, part.p);
   }
-  NPCG_LAUNCH(ctx, fin0_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, opt.eta, opt.relative ? 1 : 0,
-              hist.p, hstride);
+  {
+    const auto [pp, nb] = combine(2 * static_cast<int>(S));
+    NPCG_LAUNCH(ctx, fin0_kernel, 1, 256, 0, st.p, static_cast<int>(S), pp, nb, opt.eta, opt.relative ? 1 : 0,
+                hist.p, hstride);
+  }
   DBuf<int> run_flags;
   // iterate record: room for iteration t (doubling growth, zero-filled)
   auto reserve_iterate = [&](i64 t) -> double* {
@@ -1098,7 +1122,10 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
   // z = P^{-1} r; p = z; rz = r.z
   if (!identity) pre_apply_inverse(*pre, R.p(), R.ld, S, Z.p(), Z.ld, gate);
   NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), R.p(), R.ld, Zp, ldz, P.p(), P.ld, st.p, part.p);
-  NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, 0, 0);
+  {
+    const auto [pp, nb] = combine(static_cast<int>(S));
+    NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), pp, nb, 0, 0);
+  }
 
   if (!iterates && persistent_eligible(ctx, op, S) && !(std::getenv("NPCG_PCG") && std::string(std::getenv("NPCG_PCG")) == "classic")) {
     run_persistent(ctx, op, pre, mu, S, X, ldx, R, Z, P, V, st.p, hist.p, hstride, opt.max_iter);
@@ -1135,18 +1162,27 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
       op.apply_shift(P.p(), P.ld, static_cast<int>(S), mu, V.p(), V.ld, gate);
       NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), P.p(), P.ld, V.p(), V.ld,
                   static_cast<double*>(nullptr), 0, st.p, part.p);
-      NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, 1, static_cast<int>(t));
+      {
+        const auto [pp, nb] = combine(static_cast<int>(S));
+        NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), pp, nb, 1, static_cast<int>(t));
+      }
       NPCG_LAUNCH(ctx, update_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, P.p(), P.ld, V.p(), V.ld, R.p(),
                   R.ld, st.p, part.p);
-      NPCG_LAUNCH(ctx, fin_res_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, static_cast<int>(t),
-                  opt.max_iter, hist.p, hstride);
+      {
+        const auto [pp, nb] = combine(static_cast<int>(S));
+        NPCG_LAUNCH(ctx, fin_res_kernel, 1, 256, 0, st.p, static_cast<int>(S), pp, nb, static_cast<int>(t),
+                    opt.max_iter, hist.p, hstride);
+      }
       if (iterates)
         NPCG_LAUNCH(ctx, record_kernel, nblk, 256, 0, n, static_cast<int>(S), X, ldx, reserve_iterate(t), st.p,
                     run_flags.p);
       if (!identity) pre_apply_inverse(*pre, R.p(), R.ld, S, Z.p(), Z.ld, gate);
       NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), R.p(), R.ld, Zp, ldz,
                   static_cast<double*>(nullptr), 0, st.p, part.p);
-      NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), part.p, nblk, 2, static_cast<int>(t));
+      {
+        const auto [pp, nb] = combine(static_cast<int>(S));
+        NPCG_LAUNCH(ctx, fin_dot_kernel, 1, 256, 0, st.p, static_cast<int>(S), pp, nb, 2, static_cast<int>(t));
+      }
       NPCG_LAUNCH(ctx, pupdate_kernel, nblk, 256, 0, n, static_cast<int>(S), P.p(), P.ld, Zp, ldz, st.p);
       enqueue_snapshot(t);
       const i64 depth = op.costly() ? 1 : kDepth;  // no overshoot products when one product is expensive

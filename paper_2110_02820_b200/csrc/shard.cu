@@ -1,48 +1,33 @@
-// Row-sharded operators for multi-GPU runs: one process per GPU,
-// vectors replicated, the operator split by rows.
+// Row-sharded operators for one-process-per-GPU runs.
 //
-//   Gram (ridge, cfg 2): rank g holds the row block X_g of the design; its
-//     local product X_g^T (X_g v) / m is a partial n-vector and one in-place
-//     all-reduce (n doubles per RHS) completes A v.
-//   Dense / stored kernel (cfgs 1, 3, 5): rank g holds the column block
-//     A[:, R_g] (= rows R_g, A symmetric); its local product is rows R_g of
-//     A v and one all-gather (ceil(n/G) doubles per rank per RHS) completes it.
-//
-// The exchange is a callback enqueued on the library stream (the host binds
-// it to NCCL through torch.distributed), so the PCG loop, the sketch and the
-// power iterations run unchanged on a ShardOp: everything downstream of the
-// operator (factorisation, preconditioner, vector updates) is replicated and
-// deterministic, hence identical on every rank.
+// Every n-vector is split into balanced contiguous row blocks R_g (comm.cuh).
+// A product V -> A V on a sharded context:
+//   1. all-gather V's row blocks into the full n x k block (NCCL all-gather;
+//      the PCG's search direction p, a sketch block Q);
+//   2. the local operator on the full block:
+//        stored A (dense, stored kernel, low-rank; cfgs 1, 3, 5): rank g holds
+//          the column block A[:, R_g] = rows R_g (A symmetric) and produces its
+//          rows of A V directly;
+//        Gram ridge (cfg 2): rank g holds the row block X_g of the design and
+//          produces the full-length partial X_g^T (X_g V) / m;
+//        matrix-free kernel (cfg 4): rank g evaluates its share of the
+//          symmetric 128 x 128 block pairs (or of the sketch's column blocks)
+//          and produces a full-length partial;
+//   3. partial outputs are reduce-scattered (NCCL) into the row blocks.
+// Everything downstream (factorisation, preconditioner, PCG vector updates)
+// works on the local row blocks with all-reduced row reductions.
 #include "blas.cuh"
 #include "gemm.cuh"
 #include "ops.cuh"
 
 namespace npcg {
 namespace {
-
-// send (nmax x k, contiguous) <- local block (nloc x k, ld)
-__global__ void pack_block_kernel(const double* __restrict__ src, i64 lds, i64 nloc, i64 nmax, i64 k,
-                                  double* __restrict__ dst) {
-  const i64 total = nmax * k;
-  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 i = idx % nmax, s = idx / nmax;
-    dst[idx] = i < nloc ? src[i + s * lds] : 0.0;
-  }
+// out (cols) <- row j of the n x cols block (ld)
+__global__ void block_row_kernel(const double* __restrict__ a, i64 lda, i64 j, i64 cols, double* __restrict__ out) {
+  for (i64 c = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; c < cols;
+       c += static_cast<i64>(gridDim.x) * blockDim.x)
+    out[c] = a[j + c * lda];
 }
-
-// out (n x k, ldo) <- gathered blocks recv[r][s][i] (rank-major, nmax x k each)
-__global__ void unpack_gather_kernel(const double* __restrict__ recv, i64 nranks, i64 nmax, i64 k, i64 n,
-                                     double* __restrict__ out, i64 ldo) {
-  const i64 total = n * k;
-  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 row = idx % n, s = idx / n;
-    const i64 r = row / nmax, i = row % nmax;
-    out[row + s * ldo] = recv[(r * k + s) * nmax + i];
-  }
-}
-
 }  // namespace
 
 void DenseColBlockOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
@@ -53,25 +38,37 @@ void DenseColBlockOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ld
   }
 }
 
+void DenseColBlockOp::column(i64 j, double* out) {
+  NPCG_LAUNCH(*ctx, block_row_kernel, static_cast<unsigned>(std::max<i64>(1, std::min<i64>(cdiv(nloc, 256), 1024))),
+              256, 0, a.p(), a.ld, j, nloc, out);
+}
+
 void ShardOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
   Ctx& c = *ctx;
-  if (mode == 0) {
-    local->apply(V, ldv, k, out, ldo, gate);
-    const i64 count = ldo * (k - 1) + n;  // one contiguous span (column pads ride along)
-    if (fn(user, 0, out, out, count, c.stream) != 0) fail(NPCG_ECUDA, "sharded operator: all-reduce failed");
+  const RowSplit sp = c.split(n);
+  DMat full;
+  full.alloc(n, k, c.stream, false);
+  rows_allgather(c, sp, V, ldv, k, full.p(), full.ld);
+  if (local->partial_output(k)) {
+    DMat part;
+    part.alloc(n, k, c.stream, false);
+    local->apply(full.p(), full.ld, k, part.p(), part.ld, gate);
+    rows_reduce_scatter(c, sp, part.p(), part.ld, k, out, ldo);
+  } else {
+    local->apply(full.p(), full.ld, k, out, ldo, gate);
+  }
+}
+
+void ShardOp::column(i64 j, double* out) {
+  if (auto* blk = dynamic_cast<DenseColBlockOp*>(local.get())) {
+    blk->column(j, out);
     return;
   }
-  // mode 1: local rows -> padded send block -> all-gather -> scatter into out
-  DMat loc;
-  loc.alloc(nmax, k, c.stream, false);
-  local->apply(V, ldv, k, loc.p(), loc.ld, gate);
-  DBuf<double> send(nmax * k, c.stream), recv(nranks * nmax * k, c.stream);
-  const i64 nloc = static_cast<DenseColBlockOp*>(local.get())->nloc;
-  NPCG_LAUNCH(c, pack_block_kernel, static_cast<unsigned>(std::min<i64>(cdiv(nmax * k, 256), 4096)), 256, 0,
-              loc.p(), loc.ld, nloc, nmax, k, send.p);
-  if (fn(user, 1, send.p, recv.p, nmax * k, c.stream) != 0) fail(NPCG_ECUDA, "sharded operator: all-gather failed");
-  NPCG_LAUNCH(c, unpack_gather_kernel, static_cast<unsigned>(std::min<i64>(cdiv(n * k, 256), 4096)), 256, 0,
-              recv.p, nranks, nmax, k, n, out, ldo);
+  // full column on every rank, keep the local rows
+  DBuf<double> full(n, ctx->stream);
+  local->column(j, full.p);
+  NPCG_CUDA(cudaMemcpyAsync(out, full.p + off, sizeof(double) * nloc, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->sync();
 }
 
 }  // namespace npcg

@@ -1,19 +1,23 @@
-"""Multi-GPU plumbing for the row-sharded operators.
+"""Multi-GPU plumbing: row-sharded contexts, one process per GPU.
 
-One process per GPU. The operator is split by rows and every vector (p, r,
-x, Ω, Y, U) stays replicated, so the only communication of a solve is the
-exchange that completes each operator product:
+On a sharded context (include/npcg_capi.h) every dimension n is split into
+balanced contiguous row blocks R_g and every n-length object of the path --
+Omega, Y, U, x, r, z, p, the right-hand sides -- lives on its owner as the local
+row block. The library itself issues the exchanges from C++ on its stream:
 
-* Gram (ridge): rank g holds the row block X_g; A v = Σ_g X_gᵀ(X_g v)/m is an
-  in-place all-reduce of n doubles per right-hand side.
-* Dense / stored kernel: rank g holds the column block A[:, R_g] (= rows R_g,
-  A symmetric); A v is an all-gather of ceil(n/G) doubles per rank.
+* all-gather of p before each operator product (and of each sketch block);
+* sum all-reduce of the row reductions: Omega^T Y_nu and the CholeskyQR /
+  Gram-Schmidt Grams (l x l), ||Y||_F, U^T r (l), the PCG dots;
+* reduce-scatter of full-length partial products (Gram ridge over a row
+  block of X; the symmetric matrix-free kernel's share of block pairs).
 
-The library enqueues the exchange through a C callback on its own stream
-(``npcg_exchange_fn`` in include/npcg_capi.h); :class:`TorchExchange` binds it
-to ``torch.distributed`` — NCCL over NVLink on B200s, gloo in the CPU tests.
-Factorisation and preconditioner are replicated and deterministic, so every
-rank holds bitwise-identical scalars and takes the same convergence branch.
+Production: :func:`nccl_context` -- NCCL inside the library (the unique id
+travels over torch.distributed once; no Python on the per-iteration path).
+Tests: :func:`exchange_context` with :class:`TorchExchange` -- a host-staged
+callback transport over torch.distributed (gloo): the library synchronises its
+stream, the callback copies the block to the host, runs the collective on CPU
+tensors and copies the result back, so ranks sharing one GPU never wait on
+each other inside a kernel.
 """
 from __future__ import annotations
 
@@ -23,52 +27,41 @@ import numpy as np
 
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
-ALLREDUCE, ALLGATHER = 0, 1
-
-
-def block_size(total: int, nranks: int) -> int:
-    """Rows per rank: equal blocks of ceil(total / nranks), the last one short
-    (the layout npcg_op_dense_shard_create assumes)."""
-    return -(-total // nranks)
+ALLREDUCE, ALLGATHER, REDUCE_SCATTER = 0, 1, 2
 
 
 def shard_rows(total: int, nranks: int, rank: int) -> tuple[int, int]:
-    """(offset, count) of `rank`'s contiguous row block."""
+    """(offset, count) of `rank`'s balanced contiguous row block (comm.cuh RowSplit):
+    floor(total / nranks) rows, one more for the first total % nranks ranks."""
     if not 0 <= rank < nranks:
         raise ValueError("shard_rows: rank out of range")
-    nb = block_size(total, nranks)
-    off = min(total, rank * nb)
-    return off, max(0, min(nb, total - off))
+    q, r = divmod(total, nranks)
+    return rank * q + min(rank, r), q + (1 if rank < r else 0)
 
 
-def unpack_gathered(recv: np.ndarray, n: int, nranks: int, k: int) -> np.ndarray:
-    """Host restatement of the library's unpack_gather_kernel: rank-major
-    blocks of nb x k (col-major) -> n x k."""
-    nb = block_size(n, nranks)
-    blocks = recv.reshape(nranks, k, nb)
-    out = np.empty((n, k), order="F")
-    for r in range(nranks):
-        off, cnt = shard_rows(n, nranks, r)
-        out[off:off + cnt, :] = blocks[r, :, :cnt].T
-    return out
+def nccl_context(device: int, group=None):
+    """A row-sharded npcg Context over NCCL for this process's rank of the
+    torch.distributed group (rank 0 creates the NCCL unique id)."""
+    import torch.distributed as dist
+    import paper_2110_02820_b200 as npcg
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [npcg.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return npcg.Context.sharded(device, rank, world, obj[0])
 
 
-class _DevView:
-    """__cuda_array_interface__ over a raw device pointer (no copy)."""
-
-    def __init__(self, ptr: int, count: int):
-        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
-                                         "version": 3, "strides": None, "stream": None}
+def exchange_context(device: int, group=None):
+    """A row-sharded npcg Context whose exchanges run through TorchExchange."""
+    import paper_2110_02820_b200 as npcg
+    ex = TorchExchange(group)
+    return npcg.Context.exchange(device, ex.rank, ex.world, ex)
 
 
 class TorchExchange:
-    """Completes sharded operator products with torch.distributed collectives.
-
-    ``exchange()`` works on torch tensors (CPU tensors + gloo in the tests);
-    ``cfn`` is the C callback the library calls with device pointers and its
-    stream: the collective is enqueued with that stream as torch's current
-    stream, so it is ordered with the library's kernels and no host sync occurs.
-    """
+    """npcg_exchange_fn over torch.distributed with host staging (any backend
+    that handles CPU tensors, e.g. gloo): kind 0 sum all-reduce in place,
+    1 all-gather rank-major, 2 reduce-scatter (all-reduce, keep this rank's
+    block)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -81,22 +74,36 @@ class TorchExchange:
         self.cfn = EXCHANGE_FN(self._call)
 
     def exchange(self, kind: int, send, recv) -> None:
+        """The collective on host tensors (send: count doubles; recv as documented)."""
         if kind == ALLREDUCE:
             self.dist.all_reduce(send, group=self.group)
         elif kind == ALLGATHER:
             count = send.numel()
             self.dist.all_gather(list(recv.view(self.world, count).unbind(0)), send, group=self.group)
+        elif kind == REDUCE_SCATTER:
+            count = recv.numel()
+            full = send.clone()
+            self.dist.all_reduce(full, group=self.group)
+            recv.copy_(full[self.rank * count:(self.rank + 1) * count])
         else:
             raise ValueError(f"unknown exchange kind {kind}")
 
     def _call(self, user, kind, send, recv, count, stream) -> int:
         try:
             import torch
-            s = torch.cuda.ExternalStream(stream)
-            with torch.cuda.stream(s):
-                st = torch.as_tensor(_DevView(send, count), device="cuda")
-                rt = st if kind == ALLREDUCE else torch.as_tensor(_DevView(recv, count * self.world), device="cuda")
-                self.exchange(kind, st, rt)
+            nsend = count * (self.world if kind == REDUCE_SCATTER else 1)
+            nrecv = count * (self.world if kind == ALLGATHER else 1)
+            torch.cuda.ExternalStream(stream).synchronize()  # the library's producers are done
+            dsend = torch.as_tensor(_DevView(send, nsend), device="cuda")
+            hs = dsend.cpu()
+            if kind == ALLREDUCE:
+                self.exchange(kind, hs, hs)
+                dsend.copy_(hs)
+            else:
+                hr = torch.empty(nrecv, dtype=torch.float64)
+                self.exchange(kind, hs, hr)
+                torch.as_tensor(_DevView(recv, nrecv), device="cuda").copy_(hr)
+            torch.cuda.synchronize()  # the copies land before the library's consumers
             self.calls += 1
             return 0
         except BaseException as e:  # noqa: BLE001 - reported through the library's status code
@@ -104,72 +111,15 @@ class TorchExchange:
             return 1
 
 
-def ShardedGramOperator(x_local, m_total: int, exchange: TorchExchange, ctx=None, where=None, ld=None):
-    """GramRidgeOperator over this rank's row block X_g (m_local x n) of a
-    design with m_total rows (npcg_op_gram_shard_create). `x_local` is a host
-    array, or a device pointer with `where=DEVICE`, `ld` and shape given by
-    (m_local, n) in `x_local` as a tuple (ptr, m_local, n)."""
-    from . import DEVICE, HOST, _check, _f64, _i64, _ptr, _vp, default_context, lib, LinearOperator
-    ctx = ctx or default_context()
-    h = _vp()
-    if where == DEVICE:
-        ptr, m_local, n = x_local
-        _check(lib().npcg_op_gram_shard_create(_vp(ctx.h), _i64(m_local), _i64(n), _vp(ptr), _i64(ld), DEVICE,
-                                               _i64(m_total), exchange.cfn, None, C.byref(h)))
-    else:
-        x = _f64(x_local)
-        _check(lib().npcg_op_gram_shard_create(_vp(ctx.h), _i64(x.shape[0]), _i64(x.shape[1]), _ptr(x),
-                                               _i64(max(x.shape[0], 1)), HOST, _i64(m_total), exchange.cfn, None,
-                                               C.byref(h)))
-    op = LinearOperator(h.value, ctx)
-    op._exchange = exchange  # keep the callback alive with the handle
-    return op
+class _DevView:
+    """__cuda_array_interface__ over a raw device pointer (no copy)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None, "stream": None}
 
 
-def ShardedDenseOperator(a_block, n: int, exchange: TorchExchange, ctx=None):
-    """DenseOperator over this rank's column block A[:, R_g] (n x nloc) of a
-    symmetric n x n A (npcg_op_dense_shard_create)."""
-    from . import HOST, _check, _f64, _i64, _ptr, _vp, default_context, lib, LinearOperator
-    ctx = ctx or default_context()
-    a = _f64(a_block)
-    off, cnt = shard_rows(n, exchange.world, exchange.rank)
-    if a.shape != (n, cnt):
-        raise ValueError(f"ShardedDenseOperator: expected the {n} x {cnt} column block at {off}")
-    h = _vp()
-    _check(lib().npcg_op_dense_shard_create(_vp(ctx.h), _i64(n), _i64(exchange.world), _i64(exchange.rank),
-                                            _ptr(a), _i64(max(n, 1)), HOST, exchange.cfn, None, C.byref(h)))
-    op = LinearOperator(h.value, ctx)
-    op._exchange = exchange
-    return op
-
-
-def ShardedKernelOperator(points, sigma: float, exchange: TorchExchange, ctx=None):
-    """Stored Gaussian KernelOperator over this rank's column block K[:, R_g],
-    built on device from all n points (npcg_op_kernel_shard_create)."""
-    from . import HOST, _check, _f64, _i64, _ptr, _vp, default_context, lib, LinearOperator
-    ctx = ctx or default_context()
-    p = _f64(points)
-    n, d = p.shape
-    h = _vp()
-    _check(lib().npcg_op_kernel_shard_create(_vp(ctx.h), _i64(n), _i64(d), _ptr(p), _i64(max(n, 1)),
-                                             C.c_double(sigma), _i64(exchange.world), _i64(exchange.rank), HOST,
-                                             exchange.cfn, None, C.byref(h)))
-    op = LinearOperator(h.value, ctx)
-    op._exchange = exchange
-    return op
-
-
-def ShardedLowRankOperator(g, lam, exchange: TorchExchange, ctx=None):
-    """A = G diag(lam) G^T / r over this rank's column block (npcg_op_lowrank_shard_create)."""
-    from . import HOST, _check, _f64, _i64, _ptr, _vp, default_context, lib, LinearOperator
-    ctx = ctx or default_context()
-    g = _f64(g)
-    lam = np.ascontiguousarray(lam, dtype=np.float64)
-    n, r = g.shape
-    h = _vp()
-    _check(lib().npcg_op_lowrank_shard_create(_vp(ctx.h), _i64(n), _i64(r), _ptr(g), _i64(max(n, 1)), _ptr(lam),
-                                              _i64(exchange.world), _i64(exchange.rank), HOST, exchange.cfn, None,
-                                              C.byref(h)))
-    op = LinearOperator(h.value, ctx)
-    op._exchange = exchange
-    return op
+def local_rows(a: np.ndarray, n: int, rank: int, world: int) -> np.ndarray:
+    """Rows R_rank of an n-row array (Fortran order kept)."""
+    off, cnt = shard_rows(n, world, rank)
+    return np.asfortranarray(a[off:off + cnt])

@@ -119,24 +119,13 @@ def make(name: str, Rng, splitmix64, **kw) -> Workload:
     return CONFIGS[name](Rng, splitmix64, **kw)
 
 
-def build_operator(npcg, w: Workload, ctx=None, exchange=None, streamed=False):
-    """The product operator for a workload (device-resident). With a
-    dist.TorchExchange of world > 1 the ridge design is row-sharded: this rank
-    uploads only its block of X and the products are completed by all-reduce;
-    the stored kernel / low-rank operators are built per column block and
-    completed by all-gather. `streamed` overlaps the upload of a ridge design
-    with the sketch (npcg_op_gram_create_streamed)."""
-    if exchange is not None:
-        from . import dist as pd
-        if w.kind == "gram":
-            x = w.data["x"]
-            off, cnt = pd.shard_rows(x.shape[0], exchange.world, exchange.rank)
-            return pd.ShardedGramOperator(x[off:off + cnt, :], x.shape[0], exchange, ctx=ctx)
-        if w.kind == "kernel" and w.n <= w.data["dense_cap"]:
-            return pd.ShardedKernelOperator(w.data["points"], w.data["sigma"], exchange, ctx=ctx)
-        if w.kind == "lowrank":
-            return pd.ShardedLowRankOperator(w.data["g"], w.data["lambda"], exchange, ctx=ctx)
-        raise ValueError(f"row sharding is not wired for the {w.kind} workload")
+def build_operator(npcg, w: Workload, ctx=None, streamed=False):
+    """The product operator for a workload (device-resident). On a row-sharded
+    context (dist.nccl_context / dist.exchange_context) the same constructors
+    keep this rank's share: the column block A[:, R_g] of the dense / stored
+    kernel / low-rank operators, the rows of X for the ridge Gram operator, a
+    share of the matrix-free kernel work. `streamed` overlaps the upload of a
+    ridge design with the sketch (npcg_op_gram_create_streamed)."""
     if w.kind == "synth":
         return npcg.synthesize_operator(w.data["lambda"], w.data["seed"], ctx=ctx)
     if w.kind == "dense":
