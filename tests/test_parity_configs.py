@@ -78,6 +78,33 @@ def compare_solve(rp, ro):
     return err
 
 
+def compare_solve_floor(rp, ro, orc, oop, b, mu, opre, eta):
+    """SURVEY Appendix A.2 for iteration counts that differ by more than one.
+    At the small-mu end of config 5's path the residual is not monotone near
+    eta (it dips, rises ~100x and falls again -- the oracle's own history shows
+    it), so the stopping iteration is decided by whether the dip crosses eta.
+    Then: (1) the product's residual history equals the oracle's (continued
+    past its stop) to rounding drift while the residual is far above eta; (2)
+    the earlier stop is a near-tie -- both residuals at that iteration lie
+    within 25 % of eta ||b||; (3) the product's solution equals the oracle's
+    iterate at the same iteration (record_iterates) to 1e-8."""
+    if abs(rp.iterations - ro.iterations) <= 1:
+        return compare_solve(rp, ro)
+    t_end = max(rp.iterations, ro.iterations)
+    rc = orc.nystrom_pcg(oop, b, mu, opre, eta=eta * 1e-4, relative=True, max_iter=t_end, record_iterates=True)
+    thr = eta * np.linalg.norm(b)
+    hg, ho = np.asarray(rp.residual_history), np.asarray(rc.residual_history)
+    t0 = min(rp.iterations, ro.iterations)
+    far = ho[:t0 + 1] > 1e3 * thr
+    drift = np.abs(hg[:t0 + 1] - ho[:t0 + 1])[far] / ho[:t0 + 1][far]
+    assert drift.max() <= 1e-6, drift.max()
+    assert abs(hg[t0] - thr) <= 0.25 * thr and abs(ho[t0] - thr) <= 0.25 * thr, (hg[t0], ho[t0], thr)
+    xo = np.asarray(rc.iterates[rp.iterations])
+    err = np.linalg.norm(rp.x - xo) / np.linalg.norm(xo)
+    assert err <= X_RTOL, f"x rel err vs the oracle iterate at t = {rp.iterations}: {err:.3e}"
+    return err
+
+
 def run_fixed(npcg, orc, w):
     op, oop = operators(npcg, orc, w)
     pair = npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, w.omega)
@@ -159,7 +186,7 @@ def test_cfg5_lowrank_operator_matches_oracle_build(npcg, orc):
     assert np.abs(a_gpu - a_cpu).max() <= 1e-13 * np.abs(a_cpu).max()
 
 
-def run_regpath(npcg, orc, w):
+def run_regpath(npcg, orc, w, floor_check=False):
     op, oop = operators(npcg, orc, w)
     pair = npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, w.omega)
     ap = npcg.nystrom_from_sketch(pair)
@@ -170,7 +197,10 @@ def run_regpath(npcg, orc, w):
         reps = npcg.nystrom_pcg(op, w.b, mu, pre, eta=w.eta, relative=True)  # 4 RHS share each pass over A
         for j, rp in enumerate(reps):
             ro = orc.nystrom_pcg(oop, w.b[:, j], mu, opre, eta=w.eta, relative=True)
-            compare_solve(rp, ro)
+            if floor_check:
+                compare_solve_floor(rp, ro, orc, oop, b=w.b[:, j], mu=mu, opre=opre, eta=w.eta)
+            else:
+                compare_solve(rp, ro)
 
 
 def test_cfg5_regularization_path_reduced(npcg, orc):
@@ -181,7 +211,7 @@ def test_cfg5_regularization_path_reduced(npcg, orc):
 def test_cfg5_regularization_path_n20000(npcg, orc):
     """config 5 at n = 20 000 (r = 1000, ell = 400), the same
     construction; four mu of the path (10^-6 .. 10^-1, all 4 RHS each)."""
-    run_regpath(npcg, orc, shared_inputs(npcg, orc, "cfg5", n=20000, r=1000, ell=400, nmu=4))
+    run_regpath(npcg, orc, shared_inputs(npcg, orc, "cfg5", n=20000, r=1000, ell=400, nmu=4), floor_check=True)
 
 
 @pytest.mark.slow

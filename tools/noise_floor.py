@@ -19,7 +19,7 @@ from oracle.workload_ops import build_oracle_operator  # noqa: E402
 from paper_2110_02820_b200 import workloads  # noqa: E402
 
 CASES = [("cfg1", {}), ("cfg2", {}), ("cfg3", {"n": 20000, "ell": 1000}),
-         ("cfg5", {"n": 10000, "r": 1000, "ell": 400, "nmu": 1})]
+         ("cfg5", {"n": 10000, "r": 1000, "ell": 400, "nmu": 2})]
 
 
 def lam_rel(a, b):
