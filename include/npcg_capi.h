@@ -106,6 +106,15 @@ int npcg_rng_sample(npcg_rng* rng, int64_t n, int64_t k, int64_t* out); /* rando
 /* count successive Rng::uniform() draws (random.cpp:20) into dst. */
 int npcg_rng_uniform_fill(npcg_rng* rng, int64_t count, double* dst);
 uint64_t npcg_splitmix64(uint64_t seed);                       /* bench.cpp:180-185 */
+/* The reference generator continued on the GPU: the same
+ * mt19937_64 word stream as the host calls above (bitwise), produced by a
+ * device kernel from the engine's state; the Rng advances exactly as the host
+ * draw would. npcg_rng_gaussian_device fills dst (device, col-major rows x
+ * cols, ld) like npcg_rng_gaussian, with the Box-Muller transform on the GPU
+ * (CUDA log/cos: deviates within a few ulp of libm's). On a row-sharded ctx
+ * only this rank's rows land in dst (ld >= its row count). */
+int npcg_rng_words_device(npcg_ctx* ctx, npcg_rng* rng, int64_t count, uint64_t* dst);
+int npcg_rng_gaussian_device(npcg_ctx* ctx, npcg_rng* rng, int64_t rows, int64_t cols, double* dst, int64_t ld);
 
 /* ---- operators (operators.hpp:25-168) ----------------------------------- */
 /* DenseOperator(Matrix a), operators.cpp:64-70 (square + symmetry check). */

@@ -287,6 +287,36 @@ class Rng:
     def gaussian_vector(self, n: int) -> np.ndarray:
         return self.gaussian_matrix(n, 1)[:, 0].copy()
 
+    def _device_buffer(self, ctx, nbytes):
+        p = _vp()
+        _check(lib().npcg_dev_alloc(_vp(ctx.h), _i64(nbytes), C.byref(p)))
+        return p
+
+    def words_device(self, count: int, ctx: "Context | None" = None) -> np.ndarray:
+        """`count` engine words generated on the GPU (npcg_rng_words_device), copied to the host."""
+        ctx = ctx or default_context()
+        buf = self._device_buffer(ctx, 8 * max(count, 1))
+        try:
+            _check(lib().npcg_rng_words_device(_vp(ctx.h), _vp(self.h), _i64(count), buf))
+            out = np.empty(count, dtype=np.uint64)
+            _check(lib().npcg_memcpy(_vp(ctx.h), out.ctypes.data_as(_vp), HOST, buf, DEVICE, _i64(8 * count)))
+        finally:
+            lib().npcg_dev_free(_vp(ctx.h), buf)
+        return out
+
+    def gaussian_matrix_device(self, rows: int, cols: int, ctx: "Context | None" = None) -> np.ndarray:
+        """gaussian_matrix drawn on the GPU (npcg_rng_gaussian_device), copied to the host."""
+        ctx = ctx or default_context()
+        buf = self._device_buffer(ctx, 8 * max(rows * cols, 1))
+        try:
+            _check(lib().npcg_rng_gaussian_device(_vp(ctx.h), _vp(self.h), _i64(rows), _i64(cols), buf,
+                                                  _i64(max(rows, 1))))
+            out = np.empty((rows, cols), order="F")
+            _check(lib().npcg_memcpy(_vp(ctx.h), _ptr(out), HOST, buf, DEVICE, _i64(8 * rows * cols)))
+        finally:
+            lib().npcg_dev_free(_vp(ctx.h), buf)
+        return out
+
     def uniform_fill(self, count: int) -> np.ndarray:
         out = np.empty(count)
         _check(lib().npcg_rng_uniform_fill(_vp(self.h), _i64(count), _ptr(out)))

@@ -104,6 +104,15 @@ double ulp_spacing_host(double x) {
   return std::nextafter(ax, std::numeric_limits<double>::infinity()) - ax;
 }
 
+/// Draw Omega blocks / power vectors with the GPU generator (rng_gpu.cu):
+/// always on a row-sharded context (every rank walks the whole stream, on its
+/// GPU instead of its host), and on request (NPCG_DEVICE_RNG=1) otherwise.
+/// Engine words are bitwise the reference's; deviates differ by a few ulp.
+bool use_device_rng(const Ctx& c) {
+  static const bool env = std::getenv("NPCG_DEVICE_RNG") && std::string(std::getenv("NPCG_DEVICE_RNG")) == "1";
+  return env || c.sharded();
+}
+
 Ctx& C(npcg_ctx* c) {
   need(c, "context");
   c->c->activate();
@@ -314,6 +323,22 @@ int npcg_rng_sample(npcg_rng* rng, int64_t n, int64_t k, int64_t* out) {
       std::swap(pool[static_cast<size_t>(i)], pool[static_cast<size_t>(j)]);
     }
     std::copy(pool.begin(), pool.begin() + k, out);
+  });
+}
+int npcg_rng_words_device(npcg_ctx* ctx, npcg_rng* rng, int64_t count, uint64_t* dst) {
+  return guard([&] {
+    need(rng, "npcg_rng_words_device");
+    Ctx& c = C(ctx);
+    device_words(c, rng->r.engine, count, reinterpret_cast<unsigned long long*>(dst));
+  });
+}
+int npcg_rng_gaussian_device(npcg_ctx* ctx, npcg_rng* rng, int64_t rows, int64_t cols, double* dst, int64_t ld) {
+  return guard([&] {
+    need(rng, "npcg_rng_gaussian_device");
+    Ctx& c = C(ctx);
+    if (rows < 0 || cols < 0) invalid("gaussian_matrix: dimensions must be >= 0");
+    device_gaussian(c, rng->r.engine, rows, cols, c.row_offset(rows), c.local_rows(rows), dst, ld);
+    c.sync();
   });
 }
 uint64_t npcg_splitmix64(uint64_t seed) {  // bench.cpp:180-185
@@ -689,9 +714,17 @@ int npcg_nys_extend_rng(npcg_nys* nys, int64_t extra, npcg_rng* rng) {
     if (extra < 1) invalid("extend_sketch: extra must be >= 1");
     if (nys->s.size + extra > nys->s.n) invalid("extend_sketch: sketch size would exceed dimension");
     // the whole block is drawn (the reference's stream on every rank); this rank keeps its rows
-    std::vector<double> raw(static_cast<size_t>(nys->s.n * extra));
-    rng->r.gaussian(nys->s.n, extra, raw.data());
-    nys_extend(nys->s, raw.data() + nys->s.off, nys->s.n, extra, NPCG_HOST);
+    Ctx& c = *nys->ctx->c;
+    if (use_device_rng(c)) {
+      DMat raw;
+      raw.alloc(nys->s.nloc, extra, c.stream, false);
+      device_gaussian(c, rng->r.engine, nys->s.n, extra, nys->s.off, nys->s.nloc, raw.p(), raw.ld);
+      nys_extend(nys->s, raw.p(), raw.ld, extra, NPCG_DEVICE);
+    } else {
+      std::vector<double> raw(static_cast<size_t>(nys->s.n * extra));
+      rng->r.gaussian(nys->s.n, extra, raw.data());
+      nys_extend(nys->s, raw.data() + nys->s.off, nys->s.n, extra, NPCG_HOST);
+    }
     nys->ctx->c->sync();
   });
 }
@@ -1183,7 +1216,7 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
       std::promise<void> g_ready;
       std::future<void> g_fut;
       std::vector<double> g, raw;
-      std::mt19937_64 after_g, after_raw;
+      Mt64 after_g, after_raw;
       i64 extra = 0;
       bool active = false, g_taken = false;
       void finish() {
@@ -1192,7 +1225,9 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
       }
       ~DrawAhead() { finish(); }
     } ahead;
-    const bool draw_ahead = cfg->tol_mode == 0 && cfg->sketch == 0 && std::getenv("NPCG_NO_DRAW_AHEAD") == nullptr;
+    const bool dev_rng = use_device_rng(c);
+    const bool draw_ahead =
+        !dev_rng && cfg->tol_mode == 0 && cfg->sketch == 0 && std::getenv("NPCG_NO_DRAW_AHEAD") == nullptr;
     auto start_ahead = [&](i64 size_after) {
       if (!draw_ahead) return;
       const i64 ex = size_after >= cfg->ell_max ? 0
@@ -1219,6 +1254,13 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
         extend_columns_rng(s, extra, rng->r);
         return;
       }
+      if (dev_rng) {  // the GPU generator continues the caller's engine
+        DMat raw;
+        raw.alloc(s.nloc, extra, c.stream, false);
+        device_gaussian(c, rng->r.engine, n, extra, s.off, s.nloc, raw.p(), raw.ld);
+        nys_extend(s, raw.p(), raw.ld, extra, NPCG_DEVICE);
+        return;
+      }
       std::vector<double> raw;
       if (ahead.active) {
         ahead.finish();
@@ -1235,6 +1277,12 @@ int npcg_adaptive(npcg_op* op, const npcg_adaptive_cfg* cfg, npcg_rng* rng, npcg
       nys_extend(s, raw.data() + s.off, n, extra, NPCG_HOST);
     };
     auto estimate = [&]() {
+      if (dev_rng) {
+        DMat gd;
+        gd.alloc(s.nloc, 1, c.stream, false);
+        device_gaussian(c, rng->r.engine, n, 1, s.off, s.nloc, gd.p(), gd.ld);
+        return power_estimate(c, *op->op, s, cfg->q, gd.p());
+      }
       std::vector<double> g;
       if (ahead.active && !ahead.g_taken) {
         ahead.g_fut.wait();

@@ -102,3 +102,31 @@ def test_ulp_spacing(impl):  # :158-164
 def test_splitmix64_seed_derivation(impl):  # bench.cpp:180-185
     # splitmix64 reference vector (first output for state 0): 0xe220a8397b1dcdaf
     assert impl.splitmix64(0) == 0xE220A8397B1DCDAF
+
+
+# ---- the generator on the GPU ---------------------------
+@pytest.mark.gpu
+def test_device_engine_words_are_the_reference_stream(orc):
+    import paper_2110_02820_b200 as npcg
+    for seed, skip in ((0, 0), (5, 1), (42, 311), (7, 100001)):
+        r, o = npcg.Rng(seed), orc.Rng(seed)
+        for _ in range(skip):  # arbitrary stream positions, including mid-block
+            assert r.word() == o.word()
+        w = r.words_device(3 * 312 + 17)
+        ref = np.array([o.word() for _ in range(w.size)], dtype=np.uint64)
+        assert np.array_equal(w, ref)
+        assert r.word() == o.word()  # the host engine continues exactly after the device draw
+
+
+@pytest.mark.gpu
+def test_device_gaussian_matches_host_draw(orc):
+    import paper_2110_02820_b200 as npcg
+    r, o = npcg.Rng(9), orc.Rng(9)
+    r.gaussian_vector(77)
+    o.gaussian_vector(77)  # odd word offset into a block
+    g = r.gaussian_matrix_device(1000, 37)
+    h = o.gaussian_matrix(1000, 37)
+    ulp = np.abs(g - h) / np.spacing(np.maximum(np.abs(h), 1e-300))
+    assert np.max(ulp) <= 4, np.max(ulp)  # CUDA log/cos vs libm
+    assert np.median(ulp) == 0
+    assert r.word() == o.word()
