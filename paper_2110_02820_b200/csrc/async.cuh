@@ -29,6 +29,9 @@ __device__ __forceinline__ void mbarrier_wait_parity(uint64_t* bar, uint32_t par
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbarrier_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // global -> shared bulk copy of `bytes` (multiple of 16, both addresses 16-byte
 // aligned), completion counted on `bar` (complete_tx).
 __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -527,15 +527,21 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
                 pr[s][k] = make_double2(i < n ? pcur[i + s * a.ldw] : 0.0, i + 1 < n ? pcur[i + 1 + s * a.ldw] : 0.0);
               }
           }
-          // column dots of the previous step: 16 warp partials summed in fixed order
+          // column dots of the previous step: the 16 warp partials of each of
+          // the 2S dots reduced by a fixed shuffle tree over 16 lanes, on the
+          // last four warps (warp 0 issues the ring's bulk copies; a serial sum
+          // there made it the laggard at every step's barrier)
+          static_assert(PT / 32 == 16 && 2 * S * 16 <= 128, "flush layout");
           auto flush_dots = [&](i64 jp, int buf) {
-            if (tid < 2 * S) {
-              const int e = tid / S, s = tid % S;
-              if (jp + e < cb1) {
-                double v = 0.0;
-                for (int w = 0; w < PT / 32; ++w) v += wdot[buf][w][e * S + s];
+            const int loc = tid - (PT - 128);
+            if (loc >= 0) {
+              const int slot = loc >> 4, w = loc & 15;
+              double v = slot < 2 * S ? wdot[buf][w][slot] : 0.0;
+#pragma unroll
+              for (int m = 8; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+              const int e = slot / S, s = slot % S;
+              if (w == 0 && slot < 2 * S && jp + e < cb1)
                 a.colpart[(static_cast<i64>(rb) * S + s) * a.pstride + jp + e] = v;
-              }
             }
           };
           i64 jprev = -1;
