@@ -59,4 +59,20 @@ inline NystromPreconditioner build_preconditioner(const NystromApproximation& ap
   return p;
 }
 
+/// woodbury_inverse_apply(u, lambda, mu, b) (preconditioner.cpp:104-114) on the
+/// approximation's device factors: (U diag(lambda) U^T + mu I)^-1 b.
+inline Vector woodbury_inverse_apply(const NystromApproximation& approx, double mu, const Vector& b) {
+  if (b.size() != approx.dim()) throw std::invalid_argument("woodbury_inverse_apply: shape mismatch");
+  Vector x(b.size());
+  check_status(npcg_woodbury_inverse_apply(approx.device.get(), mu, 1, b.data(), std::max<Index>(b.size(), 1),
+                                           x.data(), std::max<Index>(x.size(), 1), NPCG_HOST));
+  return x;
+}
+
+/// sketch_and_solve(op, b, mu, ell, rng) (preconditioner.cpp:116-121).
+inline Vector sketch_and_solve(const LinearOperator& op, const Vector& b, double mu, Index ell, Rng& rng) {
+  if (!(mu > 0.0)) throw std::invalid_argument("sketch_and_solve: mu must be > 0");
+  return woodbury_inverse_apply(randomized_nystrom(op, ell, rng), mu, b);
+}
+
 }  // namespace npcg

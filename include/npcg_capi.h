@@ -256,6 +256,11 @@ int npcg_pre_apply_inverse(npcg_pre* pre, int64_t s, const double* r, int64_t ld
 int npcg_pre_apply(npcg_pre* pre, int64_t s, const double* v, int64_t ldv, double* out,
                    int64_t ldo, int where);
 int npcg_pre_destroy(npcg_pre* pre);
+/* woodbury_inverse_apply(approx.u, approx.lambda, mu, B) (preconditioner.cpp:104-114):
+ * X = (U diag(lambda) U^T + mu I)^-1 B for B n x s, mu > 0. sketch_and_solve
+ * (:116-121) = randomized_nystrom + this (C++/Python facades). */
+int npcg_woodbury_inverse_apply(npcg_nys* nys, double mu, int64_t s, const double* b, int64_t ldb, double* x,
+                                int64_t ldx, int where);
 
 /* ---- solvers (solvers.hpp:20-93) ----------------------------------------- */
 typedef struct {
@@ -285,6 +290,18 @@ typedef struct {
 int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, int64_t ldb,
              const double* x0, int64_t ldx0, const npcg_solve_opts* opts, double* x, int64_t ldx,
              npcg_solve_report* reports, double* history, double* iterates, int where);
+
+/* Regularisation path (the paper's protocol):
+ * one Nystrom approximation `nys` reused for every mu; for k = 0..nmu-1 the
+ * preconditioner is rebuilt for mus[k] (only its l gains change) and the s
+ * right-hand sides are solved together (npcg_pcg). warm_start != 0 starts mu_k
+ * from the solutions of mu_{k-1} (the paper goes from the largest mu down),
+ * otherwise from 0. x: n x s per mu, mu-major (x + k * s * ldx), nullable;
+ * reports: nmu x s, mu-major. A diverged column is reported (status), not
+ * fatal: the path goes on. */
+int npcg_regularization_path(npcg_op* op, npcg_nys* nys, int64_t nmu, const double* mus, int64_t s,
+                             const double* b, int64_t ldb, const npcg_solve_opts* opts, int warm_start,
+                             double* x, int64_t ldx, npcg_solve_report* reports, int where);
 
 /* block_nystrom_pcg (solvers.cpp:150-279), O'Leary block PCG, 1 <= s <= 32
  * (one joint Krylov space; not separable into batches).

@@ -552,6 +552,27 @@ Vector NystromPreconditioner::apply(const Vector& v) const {  // preconditioner.
   for (size_t i = 0; i < v.size(); ++i) out[i] = v[i] + us[i];
   return out;
 }
+// preconditioner.cpp:104-114: (U diag(lambda) U^T + mu I)^-1 b
+Vector woodbury_inverse_apply(const Matrix& u, const Vector& lambda, double mu, const Vector& b) {
+  if (!(mu > 0.0)) throw std::invalid_argument("woodbury_inverse_apply: mu must be > 0");
+  if (u.rows != static_cast<Index>(b.size()) || u.cols != static_cast<Index>(lambda.size()))
+    throw std::invalid_argument("woodbury_inverse_apply: shape mismatch");
+  Vector out(b.size());
+  if (u.cols == 0) {
+    for (size_t i = 0; i < b.size(); ++i) out[i] = b[i] / mu;
+    return out;
+  }
+  Vector t(static_cast<size_t>(u.cols));
+  gemv(true, u.rows, u.cols, 1.0, u.data(), u.rows, b.data(), 0.0, t.data());
+  Vector core(t.size());
+  for (size_t j = 0; j < t.size(); ++j) core[j] = (1.0 / (lambda[j] + mu)) * t[j];
+  Vector uc(b.size()), ut(b.size());
+  gemv(false, u.rows, u.cols, 1.0, u.data(), u.rows, core.data(), 0.0, uc.data());
+  gemv(false, u.rows, u.cols, 1.0, u.data(), u.rows, t.data(), 0.0, ut.data());
+  for (size_t i = 0; i < b.size(); ++i) out[i] = uc[i] + (b[i] - ut[i]) / mu;
+  return out;
+}
+
 Vector NystromPreconditioner::apply_inverse(const Vector& r) const {  // preconditioner.cpp:27-36
   if (static_cast<Index>(r.size()) != dim())
     throw std::invalid_argument("NystromPreconditioner - apply_inverse: length mismatch");

@@ -173,6 +173,7 @@ struct NystromPreconditioner {  // preconditioner.hpp:20-37
   Matrix apply_inverse_block(const Matrix& r) const;  // :38-45
 };
 NystromPreconditioner build_preconditioner(const NystromApproximation&, double mu);  // :80-89
+Vector woodbury_inverse_apply(const Matrix& u, const Vector& lambda, double mu, const Vector& b);  // :104-114
 
 // ---- solvers.cpp ------------------------------------------------------------
 struct SolveOptions { double eta = 1e-10; Index max_iter = 500; bool relative = false; bool record_iterates = false; };

@@ -455,6 +455,21 @@ def build_preconditioner(approx: NystromApproximation, mu: float) -> NystromPrec
     return NystromPreconditioner(h.value, approx.u.shape[0], mu)
 
 
+def woodbury_inverse_apply(approx: NystromApproximation, mu: float, b) -> np.ndarray:
+    """preconditioner.cpp:104-114 on the approximation's (U, lambda)."""
+    b = _f64(b).ravel()
+    x = np.empty(b.size)
+    _check(lib().orc_woodbury(C.c_void_p(approx.h.h), C.c_double(mu), _i64(b.size), _ptr(b), _ptr(x)))
+    return x
+
+
+def sketch_and_solve(op, b, mu: float, ell: int, rng: Rng) -> np.ndarray:
+    """preconditioner.cpp:116-121."""
+    if not mu > 0.0:
+        raise InvalidArgument("sketch_and_solve: mu must be > 0")
+    return woodbury_inverse_apply(randomized_nystrom(op, ell, rng), mu, b)
+
+
 # ---------------------------------------------------------------- solvers.cpp
 @dataclass
 class SolveReport:

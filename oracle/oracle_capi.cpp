@@ -273,6 +273,13 @@ int orc_pre_build(void* approx, double mu, void** out) {
   });
 }
 void orc_pre_free(void* p) { delete static_cast<NystromPreconditioner*>(p); }
+int orc_woodbury(void* approx, double mu, int64_t n, const double* b, double* x) {
+  return guard([&] {
+    auto* a = static_cast<NystromApproximation*>(approx);
+    const Vector out = woodbury_inverse_apply(a->u, a->lambda, mu, vec(n, b));
+    std::memcpy(x, out.data(), sizeof(double) * static_cast<size_t>(n));
+  });
+}
 int orc_pre_apply_inverse(void* p, int64_t n, int64_t s, const double* r, double* z) {
   return guard([&] {
     auto* pre = static_cast<NystromPreconditioner*>(p);

@@ -917,6 +917,25 @@ def build_preconditioner(approx: NystromApproximation, mu: float) -> NystromPrec
     return NystromPreconditioner(h.value, approx, mu)
 
 
+def woodbury_inverse_apply(approx: NystromApproximation, mu: float, b) -> np.ndarray:
+    """woodbury_inverse_apply (preconditioner.cpp:104-114) on the device factors:
+    (U diag(lambda) U^T + mu I)^-1 b."""
+    b = _f64(b)
+    single = b.ndim == 1
+    B = b.reshape(-1, 1, order="F") if single else b
+    out = np.empty(B.shape, order="F")
+    _check(lib().npcg_woodbury_inverse_apply(_vp(approx.h.h), C.c_double(mu), _i64(B.shape[1]), _ptr(B),
+                                             _i64(max(B.shape[0], 1)), _ptr(out), _i64(max(B.shape[0], 1)), HOST))
+    return out[:, 0].copy() if single else out
+
+
+def sketch_and_solve(op, b, mu: float, ell: int, rng: "Rng") -> np.ndarray:
+    """sketch_and_solve (preconditioner.cpp:116-121)."""
+    if not mu > 0.0:
+        raise InvalidArgument("sketch_and_solve: mu must be > 0")
+    return woodbury_inverse_apply(randomized_nystrom(op, ell, rng), mu, b)
+
+
 # ------------------------------------------------------------------ solvers
 @dataclass
 class SolveReport:
@@ -1023,6 +1042,36 @@ def block_nystrom_pcg(op, B, mu, precond, eta=1e-10, max_iter=500, relative=Fals
                                     _ptr(fres), _ptr(hist), hlen.ctypes.data_as(_vp), HOST))
     return BlockSolveReport(X, rep.iterations, [bool(c) for c in conv], list(defl[: rep.n_deflated]),
                             rep.fallback_count, fres, [hist[: hlen[j], j].copy() for j in range(s)])
+
+
+def regularization_path(op: LinearOperator, B, mus, approx: NystromApproximation, warm_start: bool = True,
+                        eta=1e-10, max_iter=500, relative=True):
+    """One Nystrom approximation reused along a regularisation path
+    (npcg_regularization_path): for each mu in order the
+    preconditioner is rebuilt and the right-hand sides solved, warm-started
+    from the previous mu's solutions. Returns [(mu, [SolveReport per column])]."""
+    B = _f64(B)
+    if B.ndim == 1:
+        B = B.reshape(-1, 1, order="F")
+    n, s = B.shape
+    mus = np.ascontiguousarray(mus, dtype=np.float64)
+    nmu = mus.size
+    X = np.empty((n, s * nmu), order="F")
+    reps = (_SolveReport * (s * nmu))()
+    opts = _SolveOpts(float(eta), int(max_iter), int(bool(relative)), 0)
+    with _bound(_unwrap(op)) as oh:
+        _check(lib().npcg_regularization_path(_vp(oh), _vp(approx.h.h), _i64(nmu), _ptr(mus), _i64(s), _ptr(B),
+                                              _i64(n), C.byref(opts), C.c_int(int(warm_start)), _ptr(X), _i64(n),
+                                              reps, HOST))
+    out = []
+    for k in range(nmu):
+        cols = []
+        for j in range(s):
+            r = reps[k * s + j]
+            cols.append(SolveReport(X[:, k * s + j].copy(), r.iterations, np.empty(0), bool(r.converged),
+                                    r.matvec_count, r.wall_time, r.eta_used, None, r.status))
+        out.append((float(mus[k]), cols))
+    return out
 
 
 def iteration_bound(kappa: float, eps: float) -> int:

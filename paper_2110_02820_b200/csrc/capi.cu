@@ -960,6 +960,23 @@ int npcg_pre_apply_inverse(npcg_pre* pre, int64_t s, const double* r, int64_t ld
 int npcg_pre_apply(npcg_pre* pre, int64_t s, const double* v, int64_t ldv, double* out, int64_t ldo, int where) {
   return pre_apply_common(pre, s, v, ldv, out, ldo, where, false);
 }
+int npcg_woodbury_inverse_apply(npcg_nys* nys, double mu, int64_t s, const double* b, int64_t ldb, double* x,
+                                int64_t ldx, int where) {
+  return guard([&] {
+    need(nys, "npcg_woodbury_inverse_apply");
+    Ctx& c = C(nys->ctx);
+    if (!(mu > 0.0)) invalid("woodbury_inverse_apply: mu must be > 0");  // preconditioner.cpp:106-107
+    if (!nys->s.factored()) fail(NPCG_ERUNTIME, "woodbury_inverse_apply: approximation not factored");
+    if (s <= 0) return;
+    const i64 n = nys->s.nloc;
+    View B = view_in(c, b, n, s, ldb, where);
+    DMat X;
+    X.alloc(n, s, c.stream, false);
+    woodbury_apply(c, *nys->s.fac, n, mu, B.p, B.ld, s, X.p(), X.ld);
+    download(c, X.p(), X.ld, n, s, x, ldx, where);
+    c.sync();
+  });
+}
 int npcg_pre_destroy(npcg_pre* pre) {
   delete pre;
   return NPCG_OK;
@@ -1042,6 +1059,55 @@ int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, 
     return NPCG_EDIVERGED;
   }
   return rc;
+}
+
+int npcg_regularization_path(npcg_op* op, npcg_nys* nys, int64_t nmu, const double* mus, int64_t s,
+                             const double* b, int64_t ldb, const npcg_solve_opts* opts, int warm_start,
+                             double* x, int64_t ldx, npcg_solve_report* reports, int where) {
+  return guard([&] {
+    need(op, "npcg_regularization_path");
+    need(nys, "npcg_regularization_path approximation");
+    need(opts, "npcg_regularization_path options");
+    Ctx& c = C(op->ctx);
+    if (nmu < 0 || s < 0) invalid("regularization_path: counts must be >= 0");
+    if (!nys->s.factored()) fail(NPCG_ERUNTIME, "build_preconditioner: approximation not factored");
+    if (nys->s.fac->ell > 0 && nys->s.n != op->op->n) invalid("nystrom_pcg: preconditioner dimension mismatch");
+    if (!(opts->eta > 0.0)) invalid("nystrom_pcg: eta must be > 0");
+    if (opts->max_iter < 0) invalid("nystrom_pcg: max_iter must be >= 0");
+    const i64 n = op->op->nloc;
+    if (s == 0 || nmu == 0) return;
+    PcgOptions po{opts->eta, opts->max_iter, opts->relative != 0, false};
+    View B = view_in(c, b, n, s, ldb, where);
+    DMat X, Xprev;
+    X.alloc(n, s, c.stream, false);
+    for (i64 k = 0; k < nmu; ++k) {
+      const double mu = mus[k];
+      Pre p;
+      pre_build(p, nys->s, mu);  // rejects mu <= 0 (preconditioner.cpp:80-89)
+      const bool warm = warm_start != 0 && k > 0;
+      if (warm) copy2d(c, n, s, X.p(), X.ld, Xprev.p(), Xprev.ld);
+      for (i64 s0 = 0; s0 < s; s0 += 8) {
+        const i64 sb = std::min<i64>(8, s - s0);
+        PcgResult r = pcg_solve(c, *op->op, &p, mu, sb, B.p + s0 * B.ld, B.ld,
+                                warm ? Xprev.p() + s0 * Xprev.ld : nullptr, Xprev.ld, po, X.p() + s0 * X.ld, X.ld,
+                                nullptr, "nystrom_pcg");
+        for (i64 j = 0; j < sb; ++j) {
+          const PcgColumnReport& cr = r.cols[static_cast<size_t>(j)];
+          npcg_solve_report& rep = reports[k * s + s0 + j];
+          rep.iterations = cr.iterations;
+          rep.matvec_count = cr.matvec_count;
+          rep.converged = cr.converged ? 1 : 0;
+          rep.status = cr.status;
+          rep.eta_used = cr.eta_used;
+          rep.wall_time = r.wall_time;
+          rep.history_len = static_cast<int64_t>(cr.history.size());
+        }
+      }
+      if (x) download(c, X.p(), X.ld, n, s, x + k * s * ldx, ldx, where);
+      if (k == 0 && warm_start) Xprev.alloc(n, s, c.stream, false);
+    }
+    c.sync();
+  });
 }
 
 int npcg_block_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, int64_t ldb,

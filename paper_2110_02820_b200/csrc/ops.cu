@@ -369,4 +369,51 @@ void pre_apply(Pre& p, const double* V, i64 ldv, i64 S, double* out, i64 ldo) {
   lowrank_update(p, p.gain_fwd.p, V, ldv, S, out, ldo, nullptr);
 }
 
+namespace {
+__global__ void inv_shift_scale_kernel(const double* __restrict__ T, i64 ell, i64 S, i64 ldt,
+                                       const double* __restrict__ lambda, double mu, double* __restrict__ core) {
+  const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= ell * S) return;
+  const i64 j = idx % ell, s = idx / ell;
+  core[j + s * ldt] = __dmul_rn(__ddiv_rn(1.0, __dadd_rn(lambda[j], mu)), T[j + s * ldt]);
+}
+// X = W1 + (B - W2) / mu   (preconditioner.cpp:113, same association)
+__global__ void woodbury_combine_kernel(i64 n, i64 S, const double* __restrict__ W1, i64 ldw,
+                                        const double* __restrict__ W2, const double* __restrict__ B, i64 ldb,
+                                        double mu, double* __restrict__ X, i64 ldx) {
+  const i64 total = n * S;
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = idx % n, s = idx / n;
+    X[i + s * ldx] = __dadd_rn(W1[i + s * ldw], __ddiv_rn(__dsub_rn(B[i + s * ldb], W2[i + s * ldw]), mu));
+  }
+}
+}  // namespace
+
+void woodbury_apply(Ctx& ctx, const Factors& f, i64 n, double mu, const double* B, i64 ldb, i64 S, double* X,
+                    i64 ldx) {
+  if (!(mu > 0.0)) invalid("woodbury_inverse_apply: mu must be > 0");
+  if (S <= 0) return;
+  const i64 ell = f.ell;
+  DMat W1, W2;
+  W1.alloc(n, S, ctx.stream, false);
+  W2.alloc(n, S, ctx.stream, false);
+  if (ell == 0) {  // b / mu
+    NPCG_CUDA(cudaMemset2DAsync(W1.p(), W1.ld * 8, 0, n * 8, S, ctx.stream));
+    NPCG_CUDA(cudaMemset2DAsync(W2.p(), W2.ld * 8, 0, n * 8, S, ctx.stream));
+  } else {
+    DMat T, core;
+    T.alloc(ell, S, ctx.stream, false);
+    core.alloc(ell, S, ctx.stream, false);
+    gemm(ctx, ell, S, n, 1.0, Operand{f.u.p(), f.u.ld, true}, Operand{B, ldb, true}, 0.0, T.p(), T.ld);  // U^T b
+    rows_allreduce(ctx, T.p(), T.ld * S);
+    NPCG_LAUNCH(ctx, inv_shift_scale_kernel, static_cast<unsigned>(cdiv(ell * S, 256)), 256, 0, T.p(), ell, S, T.ld,
+                f.lambda.p, mu, core.p());
+    gemm(ctx, n, S, ell, 1.0, Operand{f.u.p(), f.u.ld, false}, Operand{core.p(), core.ld, true}, 0.0, W1.p(), W1.ld);
+    gemm(ctx, n, S, ell, 1.0, Operand{f.u.p(), f.u.ld, false}, Operand{T.p(), T.ld, true}, 0.0, W2.p(), W2.ld);
+  }
+  NPCG_LAUNCH(ctx, woodbury_combine_kernel, static_cast<unsigned>(std::min<i64>(cdiv(n * S, 256), 4096)), 256, 0, n,
+              S, W1.p(), W1.ld, W2.p(), B, ldb, mu, X, ldx);
+}
+
 }  // namespace npcg

@@ -225,5 +225,9 @@ void pre_build(Pre& p, const Nys& s, double mu);
 /// Z = P^{-1} R (n x S). Z may alias nothing of R.
 void pre_apply_inverse(Pre& p, const double* R, i64 ldr, i64 S, double* Z, i64 ldz, const int* gate = nullptr);
 void pre_apply(Pre& p, const double* V, i64 ldv, i64 S, double* out, i64 ldo);
+/// woodbury_inverse_apply (preconditioner.cpp:104-114): X = (U diag(lambda) U^T + mu I)^-1 B
+/// = U ((lambda + mu)^-1 .* (U^T B)) + (B - U U^T B) / mu, on the factored approximation f.
+void woodbury_apply(Ctx& ctx, const Factors& f, i64 nloc, double mu, const double* B, i64 ldb, i64 S, double* X,
+                    i64 ldx);
 
 }  // namespace npcg

@@ -91,3 +91,54 @@ def test_constant_eigenvalues_reduce_to_identity(impl):  # :136-143
     v = impl.Rng(52).gaussian_vector(6)
     assert np.array_equal(p.apply_inverse(v), v)
     assert np.array_equal(p.apply(v), v)
+
+
+# ---- preconditioner_test.cpp:186-252: woodbury_inverse_apply / sketch_and_solve
+def test_woodbury_worked_example(impl):  # :187-194
+    approx = impl.make_approximation(np.eye(2)[:, :1], np.array([3.0]), 0.0)
+    out = impl.woodbury_inverse_apply(approx, 1.0, np.array([4.0, 2.0]))
+    assert abs(out[0] - 1.0) <= 1e-14 and abs(out[1] - 2.0) <= 1e-14
+
+
+def test_woodbury_empty_divides_by_mu(impl):  # :195-199
+    approx = impl.make_approximation(np.zeros((2, 0)), np.zeros(0), 0.0)
+    assert np.array_equal(impl.woodbury_inverse_apply(approx, 0.5, np.array([4.0, 2.0])), [8.0, 4.0])
+
+
+def test_woodbury_matches_dense_inverse(impl):  # :200-210
+    rng = impl.Rng(71)
+    a = random_psd(impl, rng, 20)
+    approx = impl.randomized_nystrom(impl.DenseOperator(a), 7, rng)
+    mu = 0.2
+    b = rng.gaussian_vector(20)
+    want = np.linalg.solve(approx.materialize() + mu * np.eye(20), b)
+    assert np.linalg.norm(impl.woodbury_inverse_apply(approx, mu, b) - want) < 1e-10 * np.linalg.norm(want)
+    with pytest.raises(ValueError):
+        impl.woodbury_inverse_apply(approx, 0.0, b)
+
+
+def test_sketch_and_solve(impl):  # :213-252
+    rng = impl.Rng(81)
+    g = rng.gaussian_matrix(12, 3)
+    a = g @ g.T
+    a = (a + a.T) / 2
+    b = rng.gaussian_vector(12)
+    x = impl.sketch_and_solve(impl.DenseOperator(a), b, 0.4, 5, rng)
+    want = np.linalg.solve(a + 0.4 * np.eye(12), b)
+    assert np.linalg.norm(x - want) < 1e-8 * np.linalg.norm(want)
+    rng = impl.Rng(82)
+    for trial in range(8):
+        a = random_psd(impl, rng, 30)
+        b = rng.gaussian_vector(30)
+        x = impl.sketch_and_solve(impl.DenseOperator(a), b, 0.5, 6, impl.Rng(1000 + trial))
+        approx = impl.randomized_nystrom(impl.DenseOperator(a), 6, impl.Rng(1000 + trial))
+        err = np.abs(np.linalg.eigvalsh(a - approx.materialize())).max()
+        star = np.linalg.solve(a + 0.5 * np.eye(30), b)
+        assert np.linalg.norm(x - star) / np.linalg.norm(star) <= err / 0.5 + 1e-12
+    d = np.full(10, 1e-6)
+    d[0] = 1.0
+    rng = impl.Rng(83)
+    b = rng.gaussian_vector(10)
+    x = impl.sketch_and_solve(impl.DenseOperator(np.diag(d)), b, 1.0, 3, rng)
+    star = np.linalg.solve(np.diag(d) + np.eye(10), b)
+    assert np.linalg.norm(x - star) / np.linalg.norm(star) <= 1e-5

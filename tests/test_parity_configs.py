@@ -219,3 +219,26 @@ def test_cfg4_kernel_matrix_free_adaptive_n20000(npcg, orc):
     """SURVEY §8(c): config 4 at n = 20 000 (same d, sigma, mu/n, ell0;
     ell_max = n/10 = 2000), matrix-free on both sides."""
     run_adaptive_free(npcg, orc, shared_inputs(npcg, orc, "cfg4", n=20000, ell_max=2000))
+
+
+def test_cfg5_warm_started_regularization_path(npcg, orc):
+    """the paper's path protocol -- largest mu
+    first, each solve warm-started from the previous solution, one sketch --
+    against the oracle run the same way (nystrom_pcg with x0)."""
+    w = shared_inputs(npcg, orc, "cfg5", n=3000, r=300, ell=150, nmu=5)
+    op, oop = operators(npcg, orc, w)
+    ap = npcg.nystrom_from_sketch(npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, w.omega))
+    ao = orc.nystrom_from_sketch(orc.extend_sketch_with(orc.make_empty_sketch(w.n), oop, w.omega))
+    mus = sorted(w.mus, reverse=True)
+    path = npcg.regularization_path(op, w.b, mus, ap, warm_start=True, eta=w.eta, relative=True)
+    cold = npcg.regularization_path(op, w.b, mus, ap, warm_start=False, eta=w.eta, relative=True)
+    prev = [None] * w.b.shape[1]
+    for (mu, reps), (_, creps) in zip(path, cold):
+        opre = orc.build_preconditioner(ao, mu)
+        for j, rp in enumerate(reps):
+            ro = orc.nystrom_pcg(oop, w.b[:, j], mu, opre, eta=w.eta, relative=True, x0=prev[j])
+            compare_solve(rp, ro)
+            prev[j] = ro.x
+            rc = orc.nystrom_pcg(oop, w.b[:, j], mu, opre, eta=w.eta, relative=True)
+            compare_solve(creps[j], rc)
+    assert sum(r.iterations for _, rs in path for r in rs) <= sum(r.iterations for _, rs in cold for r in rs)
