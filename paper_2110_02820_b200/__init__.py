@@ -35,7 +35,7 @@ from pathlib import Path
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libnpcg_b200.so"
+LIB_PATH = Path(os.environ["NPCG_LIB_PATH"]) if os.environ.get("NPCG_LIB_PATH") else PKG / "libnpcg_b200.so"  # override: diagnostics
 
 _i64 = C.c_int64
 _dp = C.POINTER(C.c_double)

@@ -32,6 +32,14 @@ __device__ __forceinline__ void mbarrier_wait_parity(uint64_t* bar, uint32_t par
 __device__ __forceinline__ void mbarrier_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// shared-memory counter add with acquire-release semantics at CTA scope (a
+// warp counts itself in: its prior shared stores are released, the last
+// arriver acquires everyone's)
+__device__ __forceinline__ unsigned atom_add_acq_rel_cta(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
 // global -> shared bulk copy of `bytes` (multiple of 16, both addresses 16-byte
 // aligned), completion counted on `bar` (complete_tx).
 __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

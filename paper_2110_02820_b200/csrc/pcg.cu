@@ -291,6 +291,7 @@ struct PersistArgs {
   const int* cseg;                    // G + 1: first segment of each CTA
   const int* ustart;                  // nrb + 1: first segment of each row block
   double* colpart;
+  double* pil;                        // dense symmetric: p_t column-interleaved, entry (j, s) at j*SP + s
   double *pv_part, *rr_part, *rz_part;  // G x S
   State* st;
   double* hist;
@@ -310,6 +311,13 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   __shared__ int running_sh;
   constexpr int DPV = GRAM ? PV : dense_pv(S), DPW = 2 * PT * DPV, DNST = GRAM ? NST : dense_nst(S);
   __shared__ uint64_t full_bar[DNST];
+  // dense symmetric use: p_t entries of the slots' columns, per-step warp
+  // partials of the 2S column dots (one set per slot pair), arrival counters
+  constexpr int SP = (S + 1) / 2 * 2;  // p entries per column, padded to 16 bytes
+  constexpr bool DEC = !GRAM && S == 1;  // the decoupled symmetric loop (one right-hand side)
+  __shared__ __align__(16) double pring[DEC ? DNST * SP : 2];
+  __shared__ double sdot[DEC ? DNST / 2 : 1][PT / 32][DEC ? 2 * S : 1];
+  __shared__ unsigned pair_cnt[DNST / 2];
   extern __shared__ __align__(128) double ring[];  // DNST x DPW doubles, fed by bulk copies (TMA)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t ring_head = 0, ring_tail = 0;  // segments consumed (all threads) / issued (thread 0)
@@ -317,6 +325,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
     for (int q = 0; q < DNST; ++q) mbarrier_init(&full_bar[q], 1);
     mbarrier_fence_init();
   }
+  if (tid < DNST / 2) pair_cnt[tid] = 0u;
   auto ring_issue = [&](const double* src, i64 count) {  // thread 0 only
     const int slot = static_cast<int>(ring_tail % DNST);
     const uint32_t bytes = static_cast<uint32_t>(round_up(count, 2) * 8);
@@ -374,12 +383,16 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
       };
       // ---- P1
       tick(t, 0);
-      if (!first)
+      if (!first || a.pil)
         for (i64 i = r0 + tid; i < r1; i += PT)
 #pragma unroll
-          for (int s = 0; s < S; ++s) pcur[i + s * a.ldw] = p_at(i, s);
+          for (int s = 0; s < S; ++s) {
+            const double v = p_at(i, s);
+            if (!first) pcur[i + s * a.ldw] = v;
+            if (a.pil) a.pil[i * SP + s] = v;  // column-interleaved copy: the ring's p entries
+          }
       if constexpr (!GRAM) {
-        if (!first) grid.sync();  // dense streams p_t from pcur
+        if (!first || a.pil) grid.sync();  // dense streams p_t from pcur / pil
       }
       if constexpr (GRAM) {
         static_assert(S == 1, "gram persistent path is single right-hand side");
@@ -507,9 +520,6 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
           const i64 rb0 = static_cast<i64>(rb) * DPW, cnt = min(static_cast<i64>(DPW), n - rb0);
           const i64 cb0 = a.sym ? a.unit[3 * kseg + 1] : static_cast<i64>(cb) * a.cpb;
           const i64 cb1 = a.sym ? a.unit[3 * kseg + 2] : min(n, cb0 + a.cpb);
-          const i64 offd = rb0 + DPW;  // first column beyond the diagonal block
-          __shared__ double wdot[2][PT / 32][2 * S];
-          double2 pr[S][DPV];  // p_t on this thread's rows (symmetric dots)
           double2 acc[S][DPV];
           bool ok[DPV];
 #pragma unroll
@@ -518,7 +528,31 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
 #pragma unroll
             for (int s = 0; s < S; ++s) acc[s][k] = make_double2(0.0, 0.0);
           }
-          if (a.sym) {
+          if (DEC && a.sym) {
+            // Symmetric use, one right-hand side, warps decoupled: a step is two columns (two ring
+            // slots, each the column segment plus its S entries of p_t, one
+            // mbarrier). No block barrier per step: every warp takes its slots,
+            // does its axpy and its share of the 2S column dots, posts the dots
+            // and counts itself in on the step's slot pair; the last warp in
+            // sums the 16 warp partials in fixed order, writes the column dots
+            // and refills both slots (DNST/2 steps ahead). A fast warp runs at
+            // most DNST/2 steps ahead of the slowest.
+            const i64 offd = rb0 + DPW;  // first column beyond the diagonal block
+            const i64 ncol = cb1 - cb0, npad = round_up(ncol, 2);
+            const uint32_t base = ring_head;
+            const uint32_t seg_bytes = static_cast<uint32_t>(round_up(cnt, 2) * 8);
+            auto sym_issue = [&](i64 q) {  // one thread: segment column q into its slot
+              const int slot = static_cast<int>((base + static_cast<uint32_t>(q)) % DNST);
+              if (q < ncol) {
+                mbarrier_expect_tx(&full_bar[slot], seg_bytes + SP * 8);
+                bulk_copy_g2s(ring + static_cast<i64>(slot) * DPW, a.A + (cb0 + q) * a.lda + rb0, seg_bytes,
+                              &full_bar[slot]);
+                bulk_copy_g2s(pring + slot * SP, a.pil + (cb0 + q) * SP, SP * 8, &full_bar[slot]);
+              } else {
+                mbarrier_arrive(&full_bar[slot]);  // odd tail: the step's second slot carries nothing
+              }
+            };
+            double2 pr[S][DPV];  // p_t on this thread's rows (column dots)
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -526,59 +560,38 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
                 const i64 i = rb0 + 2 * (tid + static_cast<i64>(PT) * k);
                 pr[s][k] = make_double2(i < n ? pcur[i + s * a.ldw] : 0.0, i + 1 < n ? pcur[i + 1 + s * a.ldw] : 0.0);
               }
-          }
-          // column dots of the previous step: the 16 warp partials of each of
-          // the 2S dots reduced by a fixed shuffle tree over 16 lanes, on the
-          // last four warps (warp 0 issues the ring's bulk copies; a serial sum
-          // there made it the laggard at every step's barrier)
-          static_assert(PT / 32 == 16 && 2 * S * 16 <= 128, "flush layout");
-          auto flush_dots = [&](i64 jp, int buf) {
-            const int loc = tid - (PT - 128);
-            if (loc >= 0) {
-              const int slot = loc >> 4, w = loc & 15;
-              double v = slot < 2 * S ? wdot[buf][w][slot] : 0.0;
+            __syncthreads();  // the previous segment's slots are all released
+            if (tid == 0)
+              for (i64 q = 0; q < min(npad, static_cast<i64>(DNST)); ++q) sym_issue(q);
+            constexpr int NV = 2 * S <= 2 ? 2 : 2 * S <= 4 ? 4 : 8;  // 2S dots padded to a power of two
+            constexpr int LG = NV == 2 ? 1 : NV == 4 ? 2 : 3;
+            constexpr int LPS = 32 / NV, WPL = (PT / 32) / LPS;      // fixed-order reduction: lanes per dot, warps per lane
+            for (i64 q = 0; q < npad; q += 2) {
+              const i64 j = cb0 + q;
+              const bool two = q + 1 < ncol;
+              const uint32_t u0 = base + static_cast<uint32_t>(q);
+              const int sl0 = static_cast<int>(u0 % DNST), sl1 = static_cast<int>((u0 + 1) % DNST);
+              const int pair = sl0 >> 1;
+              mbarrier_wait_parity(&full_bar[sl0], (u0 / DNST) & 1u);
+              mbarrier_wait_parity(&full_bar[sl1], ((u0 + 1) / DNST) & 1u);
+              const double* s0 = ring + static_cast<i64>(sl0) * DPW;
+              const double* s1 = ring + static_cast<i64>(sl1) * DPW;
+              double2 c0[DPV], c1[DPV];
+              double q0[S], q1[S];
 #pragma unroll
-              for (int m = 8; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-              const int e = slot / S, s = slot % S;
-              if (w == 0 && slot < 2 * S && jp + e < cb1)
-                a.colpart[(static_cast<i64>(rb) * S + s) * a.pstride + jp + e] = v;
-            }
-          };
-          i64 jprev = -1;
-          int step = 0;
-          if (tid == 0)
-            for (i64 j = cb0; j < min(cb1, cb0 + DNST); ++j) ring_issue(a.A + j * a.lda + rb0, cnt);
-          // p_t of the whole vector is in pcur (slice owners wrote it before the barrier)
-          auto load_p = [&](i64 j, double* dst) {
+              for (int k = 0; k < DPV; ++k) {
+                c0[k] = ok[k] ? reinterpret_cast<const double2*>(s0)[tid + PT * k] : make_double2(0.0, 0.0);
+                c1[k] = (ok[k] && two) ? reinterpret_cast<const double2*>(s1)[tid + PT * k] : make_double2(0.0, 0.0);
+              }
 #pragma unroll
-            for (int s = 0; s < S; ++s) dst[s] = j < cb1 ? pcur[j + s * a.ldw] : 0.0;
-          };
-          double q0[S], q1[S];
-          for (i64 j = cb0; j < cb1; j += 2) {
-            const bool two = j + 1 < cb1;
-            load_p(j, q0);
-            load_p(j + 1, q1);
-            const double* s0 = ring_wait();
-            const double* s1 = two ? ring_wait() : nullptr;
-            double2 c0[DPV], c1[DPV];
-#pragma unroll
-            for (int k = 0; k < DPV; ++k) {
-              c0[k] = ok[k] ? reinterpret_cast<const double2*>(s0)[tid + PT * k] : make_double2(0.0, 0.0);
-              c1[k] = (ok[k] && two) ? reinterpret_cast<const double2*>(s1)[tid + PT * k] : make_double2(0.0, 0.0);
-            }
-            __syncthreads();  // every thread holds its values: the two slots may be refilled
-            if (tid == 0) {
-              if (j + DNST < cb1) ring_issue(a.A + (j + DNST) * a.lda + rb0, cnt);
-              if (j + DNST + 1 < cb1) ring_issue(a.A + (j + DNST + 1) * a.lda + rb0, cnt);
-            }
-            if (a.sym) {
-              if (jprev >= 0) flush_dots(jprev, (step - 1) & 1);
-              jprev = -1;
-              if (j >= offd) {  // both columns are beyond the diagonal block (offd is even)
-                // the 2S dots (slot e*S + s), padded to a power of two, reduced over
-                // the warp by a transposed butterfly: lane group g ends with slot g
-                constexpr int NV = 2 * S <= 2 ? 2 : 2 * S <= 4 ? 4 : 8;
-                constexpr int LG = NV == 2 ? 1 : NV == 4 ? 2 : 3;
+              for (int s = 0; s < S; ++s) {
+                q0[s] = pring[sl0 * SP + s];
+                q1[s] = two ? pring[sl1 * SP + s] : 0.0;
+              }
+              const bool offdiag = j >= offd;  // both columns beyond the diagonal block (offd and j are even)
+              if (offdiag) {
+                // the 2S dots (slot e*S + s) reduced over the warp by a transposed
+                // butterfly: lane group g ends with slot g
                 double d[NV];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) d[v] = 0.0;
@@ -603,26 +616,166 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
 #pragma unroll
                 for (int m = 16 >> LG; m >= 1; m >>= 1) d[0] += __shfl_xor_sync(0xffffffffu, d[0], m);
                 const int slot = lane >> (5 - LG);
-                if ((lane & ((32 >> LG) - 1)) == 0 && slot < 2 * S) wdot[step & 1][warp][slot] = d[0];
-                jprev = j;
+                if ((lane & ((32 >> LG) - 1)) == 0 && slot < 2 * S) sdot[pair][warp][slot] = d[0];
               }
-              ++step;
-            }
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-              const double p0 = q0[s], p1 = q1[s];
+              for (int s = 0; s < S; ++s) {
+                const double p0 = q0[s], p1 = q1[s];
+#pragma unroll
+                for (int k = 0; k < DPV; ++k) {
+                  acc[s][k].x += c0[k].x * p0;
+                  acc[s][k].y += c0[k].y * p0;
+                  acc[s][k].x += c1[k].x * p1;
+                  acc[s][k].y += c1[k].y * p1;
+                }
+              }
+              // count in on the pair (the slots' values are consumed, the dots posted)
+              __syncwarp();  // the warp's reads and dot stores are ordered before lane 0's release
+              unsigned last = 0;
+              if (lane == 0) last = (atom_add_acq_rel_cta(&pair_cnt[pair], 1u) & (PT / 32 - 1)) == PT / 32 - 1;
+              if (__shfl_sync(0xffffffffu, last, 0)) {  // (the shuffle's warp sync orders lane 0's acquire before the reads)
+                if (offdiag) {
+                  const int slot = lane / LPS, g = lane % LPS;
+                  double v = 0.0;
+                  if (slot < 2 * S) {
+#pragma unroll
+                    for (int w = 0; w < WPL; ++w) v += sdot[pair][g * WPL + w][slot];
+                  }
+#pragma unroll
+                  for (int m = LPS / 2; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+                  const int e = slot / S, s = slot % S;
+                  if (g == 0 && slot < 2 * S && j + e < cb1)
+                    a.colpart[(static_cast<i64>(rb) * S + s) * a.pstride + j + e] = v;
+                }
+                if (lane == 0) {
+                  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
+                  if (q + DNST < npad) {
+                    sym_issue(q + DNST);
+                    sym_issue(q + DNST + 1);
+                  }
+                }
+              }
+            }
+            ring_head = base + static_cast<uint32_t>(npad);
+          } else {
+            // full use (A col-major): CTA (rb, cb) streams rows [rb*DPW, +DPW) of
+            // columns [cb*cpb, +cpb); symmetric use with 2-4 right-hand sides:
+            // the block-upper segments as above, each step's 2S column dots
+            // reduced over the warp by a transposed butterfly and across the
+            // warps at the next step's block barrier (measured: decoupled warps
+            // are slower here, 17.7 vs 11.9 ms per iteration at n = 1e5, S = 4).
+            // Each column segment is one contiguous bulk copy into the ring
+            // (DNST segments in flight); two columns per step, one block barrier
+            // per step frees their slots.
+            const i64 offd = rb0 + DPW;  // first column beyond the diagonal block
+            __shared__ double wdot[2][PT / 32][2 * S];
+            double2 pr[S][DPV];  // p_t on this thread's rows (symmetric dots)
+            if (a.sym) {
+#pragma unroll
+              for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int k = 0; k < DPV; ++k) {
+                  const i64 i = rb0 + 2 * (tid + static_cast<i64>(PT) * k);
+                  pr[s][k] = make_double2(i < n ? pcur[i + s * a.ldw] : 0.0, i + 1 < n ? pcur[i + 1 + s * a.ldw] : 0.0);
+                }
+            }
+            // column dots of the previous step: the 16 warp partials of each of
+            // the 2S dots reduced by a fixed shuffle tree over 16 lanes, on the
+            // last four warps (warp 0 issues the ring's bulk copies; a serial sum
+            // there made it the laggard at every step's barrier)
+            static_assert(PT / 32 == 16 && 2 * S * 16 <= 128, "flush layout");
+            auto flush_dots = [&](i64 jp, int buf) {
+              const int loc = tid - (PT - 128);
+              if (loc >= 0) {
+                const int slot = loc >> 4, w = loc & 15;
+                double v = slot < 2 * S ? wdot[buf][w][slot] : 0.0;
+#pragma unroll
+                for (int m = 8; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+                const int e = slot / S, s = slot % S;
+                if (w == 0 && slot < 2 * S && jp + e < cb1)
+                  a.colpart[(static_cast<i64>(rb) * S + s) * a.pstride + jp + e] = v;
+              }
+            };
+            i64 jprev = -1;
+            int step = 0;
+            if (tid == 0)
+              for (i64 j = cb0; j < min(cb1, cb0 + DNST); ++j) ring_issue(a.A + j * a.lda + rb0, cnt);
+            // p_t of the whole vector is in pcur (slice owners wrote it before the barrier)
+            auto load_p = [&](i64 j, double* dst) {
+#pragma unroll
+              for (int s = 0; s < S; ++s) dst[s] = j < cb1 ? pcur[j + s * a.ldw] : 0.0;
+            };
+            double q0[S], q1[S];
+            for (i64 j = cb0; j < cb1; j += 2) {
+              const bool two = j + 1 < cb1;
+              load_p(j, q0);
+              load_p(j + 1, q1);
+              const double* s0 = ring_wait();
+              const double* s1 = two ? ring_wait() : nullptr;
+              double2 c0[DPV], c1[DPV];
 #pragma unroll
               for (int k = 0; k < DPV; ++k) {
-                acc[s][k].x += c0[k].x * p0;
-                acc[s][k].y += c0[k].y * p0;
-                acc[s][k].x += c1[k].x * p1;
-                acc[s][k].y += c1[k].y * p1;
+                c0[k] = ok[k] ? reinterpret_cast<const double2*>(s0)[tid + PT * k] : make_double2(0.0, 0.0);
+                c1[k] = (ok[k] && two) ? reinterpret_cast<const double2*>(s1)[tid + PT * k] : make_double2(0.0, 0.0);
+              }
+              __syncthreads();  // every thread holds its values: the two slots may be refilled
+              if (tid == 0) {
+                if (j + DNST < cb1) ring_issue(a.A + (j + DNST) * a.lda + rb0, cnt);
+                if (j + DNST + 1 < cb1) ring_issue(a.A + (j + DNST + 1) * a.lda + rb0, cnt);
+              }
+              if (a.sym) {
+                if (jprev >= 0) flush_dots(jprev, (step - 1) & 1);
+                jprev = -1;
+                if (j >= offd) {  // both columns are beyond the diagonal block (offd is even)
+                  // the 2S dots (slot e*S + s), padded to a power of two, reduced over
+                  // the warp by a transposed butterfly: lane group g ends with slot g
+                  constexpr int NV = 2 * S <= 2 ? 2 : 2 * S <= 4 ? 4 : 8;
+                  constexpr int LG = NV == 2 ? 1 : NV == 4 ? 2 : 3;
+                  double d[NV];
+#pragma unroll
+                  for (int v = 0; v < NV; ++v) d[v] = 0.0;
+#pragma unroll
+                  for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int k = 0; k < DPV; ++k) {
+                      d[s] += c0[k].x * pr[s][k].x + c0[k].y * pr[s][k].y;
+                      d[S + s] += c1[k].x * pr[s][k].x + c1[k].y * pr[s][k].y;
+                    }
+#pragma unroll
+                  for (int st = 0; st < LG; ++st) {
+                    const int m = 16 >> st, half = NV >> (st + 1);
+                    const bool hi = lane & m;
+#pragma unroll
+                    for (int v = 0; v < half; ++v) {
+                      const double send = hi ? d[v] : d[v + half];
+                      const double keep = hi ? d[v + half] : d[v];
+                      d[v] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                    }
+                  }
+#pragma unroll
+                  for (int m = 16 >> LG; m >= 1; m >>= 1) d[0] += __shfl_xor_sync(0xffffffffu, d[0], m);
+                  const int slot = lane >> (5 - LG);
+                  if ((lane & ((32 >> LG) - 1)) == 0 && slot < 2 * S) wdot[step & 1][warp][slot] = d[0];
+                  jprev = j;
+                }
+                ++step;
+              }
+#pragma unroll
+              for (int s = 0; s < S; ++s) {
+                const double p0 = q0[s], p1 = q1[s];
+#pragma unroll
+                for (int k = 0; k < DPV; ++k) {
+                  acc[s][k].x += c0[k].x * p0;
+                  acc[s][k].y += c0[k].y * p0;
+                  acc[s][k].x += c1[k].x * p1;
+                  acc[s][k].y += c1[k].y * p1;
+                }
               }
             }
-          }
-          if (a.sym) {
-            __syncthreads();
-            if (jprev >= 0) flush_dots(jprev, (step - 1) & 1);
+            if (a.sym) {
+              __syncthreads();
+              if (jprev >= 0) flush_dots(jprev, (step - 1) & 1);
+            }
           }
 #pragma unroll
           for (int s = 0; s < S; ++s) {
@@ -897,7 +1050,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   DBuf<i64> units;
   DBuf<int> cseg, ustart;
   double sym_entries = 0.0;  // entries of A streamed per iteration in symmetric use
-  DBuf<double> colpart;
+  DBuf<double> colpart, pil;
   int sym = 0;
   if (dense) {
     const i64 dpw = dense_pw(static_cast<int>(S));
@@ -953,6 +1106,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
       NPCG_CUDA(cudaMemcpyAsync(ustart.p, hs.data(), sizeof(int) * hs.size(), cudaMemcpyHostToDevice, ctx.stream));
       part.alloc(static_cast<i64>(nseg) * S * dpw, ctx.stream);
       colpart.alloc(nrb * S * pstride, ctx.stream);
+      if (S == 1) pil.alloc(2 * n, ctx.stream);
       ctx.sync();  // host staging vectors go out of scope
     } else {
       ncb = std::max<i64>(1, G / nrb);
@@ -1002,6 +1156,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   pa.cseg = cseg.p;
   pa.ustart = ustart.p;
   pa.colpart = colpart.p;
+  pa.pil = sym && S == 1 ? pil.p : nullptr;
   pa.pv_part = scal.p;
   pa.rr_part = scal.p + G * S;
   pa.rz_part = scal.p + 2 * G * S;
