@@ -371,6 +371,17 @@ int npcg_gemm(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, cons
               int a_kmajor, const double* b, int64_t ldb, int b_kmajor, double beta, double* c, int64_t ldc,
               int where);
 
+/* The same product with both operands K-major (A stored K x M, B stored
+ * K x N), run on the INT8 tensor cores by digit-plane splitting (ozaki.cuh):
+ * the sketch products Y = A Omega of stored symmetric operators
+ * (nystrom.cpp:56 through operators.cpp:76-78). C = A B. */
+int npcg_gemm_ozaki(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
+                    const double* b, int64_t ldb, double* c, int64_t ldc, int where);
+/* Diagnostics: C32 (m x n col-major int32) = A8 B8^T, A8 m x kp and B8 n x kp
+ * row-major int8 host arrays (kp % 128 == 0), on the tcgen05 INT8 GEMM. */
+int npcg_gemm_i8(npcg_ctx* ctx, int64_t m, int64_t n, int64_t kp, const int8_t* a8, const int8_t* b8,
+                 int32_t* c32);
+
 #ifdef __cplusplus
 }
 #endif

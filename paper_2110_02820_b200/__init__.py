@@ -359,6 +359,34 @@ def gemm(a, b, transa=False, transb=False, alpha=1.0, beta=0.0, c=None, ctx: Con
     return out
 
 
+def gemm_ozaki(a, b, ctx: Context | None = None):
+    """a.T @ b for a (K x M) and b (K x N) on the INT8 tensor cores (digit-plane
+    splitting, FP64 accuracy; npcg_gemm_ozaki)."""
+    ctx = ctx or default_context()
+    a, b = _f64(a), _f64(b)
+    k, m = a.shape
+    kb, n = b.shape
+    if k != kb:
+        raise InvalidArgument("gemm_ozaki: inner dimensions differ")
+    out = np.zeros((m, n), order="F")
+    _check(lib().npcg_gemm_ozaki(_vp(ctx.h), _i64(m), _i64(n), _i64(k), _ptr(a), _i64(max(k, 1)), _ptr(b),
+                                 _i64(max(k, 1)), _ptr(out), _i64(max(m, 1)), HOST))
+    return out
+
+
+def gemm_i8(a8, b8, ctx: Context | None = None):
+    """a8 @ b8.T (int8 in, int32 out) on the tcgen05 INT8 GEMM (diagnostics)."""
+    ctx = ctx or default_context()
+    a8 = np.ascontiguousarray(a8, dtype=np.int8)
+    b8 = np.ascontiguousarray(b8, dtype=np.int8)
+    m, kp = a8.shape
+    n = b8.shape[0]
+    out = np.zeros((n, m), dtype=np.int32)  # col-major m x n
+    _check(lib().npcg_gemm_i8(_vp(ctx.h), _i64(m), _i64(n), _i64(kp), a8.ctypes.data_as(C.c_void_p),
+                              b8.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
+    return out.T
+
+
 def thin_svd(b, ctx: Context | None = None):
     ctx = ctx or default_context()
     b = _f64(b)

@@ -22,6 +22,7 @@
 #include "blas.cuh"
 #include "factor.cuh"
 #include "gemm.cuh"
+#include "ozaki.cuh"
 #include "ops.cuh"
 #include "pcg.cuh"
 #include "rng.hpp"
@@ -1438,6 +1439,36 @@ int npcg_gemm(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, cons
     gemm(cx, m, n, k, alpha, Operand{A.p, A.ld, a_kmajor != 0}, Operand{B.p, B.ld, b_kmajor != 0}, beta,
          const_cast<double*>(Cv.p), Cv.ld);
     if (Cv.owned.p() != nullptr || where == NPCG_HOST) download(cx, Cv.p, Cv.ld, m, n, c, ldc, where);
+    cx.sync();
+  });
+}
+
+int npcg_gemm_ozaki(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
+                    const double* b, int64_t ldb, double* c, int64_t ldc, int where) {
+  return guard([&] {
+    Ctx& cx = C(ctx);
+    if (m < 0 || n < 0 || k < 0) invalid("npcg_gemm_ozaki: negative dimension");
+    if (m == 0 || n == 0) return;
+    View A = view_in(cx, a, k, m, lda, where);
+    View B = view_in(cx, b, k, n, ldb, where);
+    View Cv = view_in(cx, c, m, n, ldc, where);
+    gemm_ozaki(cx, m, n, k, A.p, A.ld, B.p, B.ld, const_cast<double*>(Cv.p), Cv.ld);
+    if (Cv.owned.p() != nullptr || where == NPCG_HOST) download(cx, Cv.p, Cv.ld, m, n, c, ldc, where);
+    cx.sync();
+  });
+}
+
+int npcg_gemm_i8(npcg_ctx* ctx, int64_t m, int64_t n, int64_t kp, const int8_t* a8, const int8_t* b8,
+                 int32_t* c32) {
+  return guard([&] {
+    Ctx& cx = C(ctx);
+    if (m <= 0 || n <= 0 || kp <= 0 || kp % 128 != 0) invalid("npcg_gemm_i8: bad shape");
+    DBuf<int8_t> da(m * kp, cx.stream), db(n * kp, cx.stream);
+    DBuf<int32_t> dc(m * n, cx.stream);
+    NPCG_CUDA(cudaMemcpyAsync(da.p, a8, m * kp, cudaMemcpyHostToDevice, cx.stream));
+    NPCG_CUDA(cudaMemcpyAsync(db.p, b8, n * kp, cudaMemcpyHostToDevice, cx.stream));
+    gemm_i8_raw(cx, static_cast<int>(m), static_cast<int>(n), kp, da.p, db.p, dc.p);
+    NPCG_CUDA(cudaMemcpyAsync(c32, dc.p, sizeof(int32_t) * m * n, cudaMemcpyDeviceToHost, cx.stream));
     cx.sync();
   });
 }

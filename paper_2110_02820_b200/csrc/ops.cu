@@ -3,6 +3,7 @@
 // function below; paths relative to /root/reference/proj/core/src/).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 #include <sstream>
 #include <string>
@@ -12,6 +13,7 @@
 #include "factor.cuh"
 #include "gemm.cuh"
 #include "ops.cuh"
+#include "ozaki.cuh"
 
 namespace npcg {
 
@@ -61,10 +63,21 @@ void DenseOp::columns(const i64* idx, i64 k, double* out, i64 ldo) {
 
 // DenseOperator::do_matvec / do_apply_block (operators.cpp:72-78). A is
 // symmetric, so A V is computed as A^T V: each output entry is a dot of a
-// contiguous column with V (coldot for <= 8 columns; DMMA GEMM beyond).
+// contiguous column with V (coldot for <= 8 columns; DMMA GEMM beyond; the
+// sketch-sized blocks of a large A on the INT8 tensor cores by digit-plane
+// splitting, which costs two passes over A and pays from ~130 columns on).
+bool ozaki_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("NPCG_OZAKI");  // diagnostics: NPCG_OZAKI=0 keeps every product on DMMA
+    return e == nullptr || std::string(e) != "0";
+  }();
+  return on;
+}
 void DenseOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const int* gate) {
   if (k <= 8) {
     coldot(*ctx, a.p(), a.ld, n, n, V, ldv, static_cast<int>(k), out, ldo, 0.0, nullptr, 0, gate);
+  } else if (k >= 192 && n >= 4096 && a.rows == n && a.cols == n && ozaki_enabled()) {
+    gemm_ozaki(*ctx, n, k, n, a.p(), a.ld, V, ldv, out, ldo);
   } else {
     gemm(*ctx, n, k, n, 1.0, Operand{a.p(), a.ld, true}, Operand{V, ldv, true}, 0.0, out, ldo);
   }
