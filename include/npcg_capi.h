@@ -371,11 +371,11 @@ int npcg_gemm(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, cons
               int a_kmajor, const double* b, int64_t ldb, int b_kmajor, double beta, double* c, int64_t ldc,
               int where);
 
-/* The same product with both operands K-major (A stored K x M, B stored
- * K x N), run on the INT8 tensor cores by digit-plane splitting (ozaki.cuh):
- * the sketch products Y = A Omega of stored symmetric operators
- * (nystrom.cpp:56 through operators.cpp:76-78). C = A B. */
-int npcg_gemm_ozaki(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
+/* C = A B run on the INT8 tensor cores by digit-plane splitting (ozaki.cuh):
+ * the sketch products Y = A Omega of stored and matrix-free kernel operators
+ * (nystrom.cpp:56 through operators.cpp:76-78,166-177). A stored K x M
+ * (a_kmajor) or M x K; B stored K x N. */
+int npcg_gemm_ozaki(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int a_kmajor,
                     const double* b, int64_t ldb, double* c, int64_t ldc, int where);
 /* Diagnostics: C32 (m x n col-major int32) = A8 B8^T, A8 m x kp and B8 n x kp
  * row-major int8 host arrays (kp % 128 == 0), on the tcgen05 INT8 GEMM. */

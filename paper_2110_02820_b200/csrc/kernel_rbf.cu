@@ -935,6 +935,10 @@ void kernel_apply_free(Ctx& ctx, const KernelFreeOp& op, const double* V, i64 ld
     DMat Kt;
     Kt.alloc(n, R, ctx.stream, false);
     NPCG_CUDA(cudaMemset2DAsync(out, sizeof(double) * ldo, 0, sizeof(double) * n, k, ctx.stream));
+    // (The INT8 digit-plane GEMM was measured here and rejected: the mirror
+    // product's contraction is one block wide (R = 2048 at n = 1e6), where the
+    // per-plane-sum epilogues cost as much as the products -- 38 TF/s FP64-
+    // equivalent against DMMA's 35, less the two splits of every block.)
     for (i64 r0 = 0, blk = 0; r0 < n; r0 += R, ++blk) {
       // sharded: the column blocks are dealt round-robin over the ranks (the
       // work of block r0 falls with n - r0, so round-robin keeps it balanced)

@@ -77,7 +77,7 @@ void DenseOp::apply(const double* V, i64 ldv, i64 k, double* out, i64 ldo, const
   if (k <= 8) {
     coldot(*ctx, a.p(), a.ld, n, n, V, ldv, static_cast<int>(k), out, ldo, 0.0, nullptr, 0, gate);
   } else if (k >= 192 && n >= 4096 && a.rows == n && a.cols == n && ozaki_enabled()) {
-    gemm_ozaki(*ctx, n, k, n, a.p(), a.ld, V, ldv, out, ldo);
+    gemm_ozaki(*ctx, n, k, n, a.p(), a.ld, true, V, ldv, 0.0, out, ldo);
   } else {
     gemm(*ctx, n, k, n, 1.0, Operand{a.p(), a.ld, true}, Operand{V, ldv, true}, 0.0, out, ldo);
   }

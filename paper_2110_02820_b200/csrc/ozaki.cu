@@ -62,7 +62,7 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
 constexpr int SPLIT_THREADS = 1024;
 __global__ void __launch_bounds__(SPLIT_THREADS, 1)
     ozaki_split_kernel(const double* __restrict__ p, i64 ld, i64 R, i64 K, i64 Kp, i64 plane,
-                       int8_t* __restrict__ D, int* __restrict__ E) {
+                       int8_t* __restrict__ D, int* __restrict__ E, double* __restrict__ S) {
   __shared__ double sh[33];
   const i64 pw = plane / 4;                     // plane stride in 32-bit words
   for (i64 r = blockIdx.x; r < R; r += gridDim.x) {
@@ -79,7 +79,10 @@ __global__ void __launch_bounds__(SPLIT_THREADS, 1)
     const double m = block_max(fmax(m0, m1), sh);
     int e = 0;
     if (m > 0.0) frexp(m, &e);  // m < 2^e
-    if (threadIdx.x == 0) E[r] = e;
+    if (threadIdx.x == 0) {
+      E[r] = e;
+      S[r] = ldexp(1.0, e);
+    }
     // X = round(a 2^(55-e)) (|X| <= 2^55; two factors keep the scale representable
     // for any e); X + OFF = sum_t u_t 128^(7-t) with 7-bit fields u_t (u_0 the
     // top, 8 bits), so the signed digits d_t = u_t - 64 are plain bit fields
@@ -112,6 +115,89 @@ __global__ void __launch_bounds__(SPLIT_THREADS, 1)
       for (int t = 0; t < NS; ++t) out[t * pw + k0 / 4] = w[t];
     }
     __syncthreads();  // sh is reused by the next row's maximum
+  }
+}
+
+// rows of an M-major operand (entry (m, k) at p[m + k*ld]) -> the same K-major
+// planes: 32 rows per CTA, lanes run over m (coalesced), warps over k; digits
+// are transposed through shared memory in 32 x 128 tiles (one 128-byte plane
+// row per store).
+constexpr int SPM_THREADS = 256;
+__global__ void __launch_bounds__(SPM_THREADS)
+    ozaki_split_mmajor_kernel(const double* __restrict__ p, i64 ld, i64 R, i64 K, i64 Kp, i64 plane,
+                              int8_t* __restrict__ D, int* __restrict__ E, double* __restrict__ S) {
+  __shared__ double wmax[SPM_THREADS / 32][32];
+  __shared__ double fsh[2][32];
+  __shared__ uint32_t tile[NS][32][33];  // [plane][row][word of 4 digits] (+1: conflict-free rows)
+  constexpr int NW = SPM_THREADS / 32;
+  constexpr unsigned long long OFF = 0x0102040810204080ull >> 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 m = static_cast<i64>(blockIdx.x) * 32 + lane;
+  const bool ok = m < R;
+  double mx = 0.0;
+  if (ok)
+    for (i64 k = warp; k < K; k += NW) mx = fmax(mx, fabs(p[m + k * ld]));
+  wmax[warp][lane] = mx;
+  __syncthreads();
+  if (warp == 0) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) v = fmax(v, wmax[w][lane]);
+    int e = 0;
+    if (v > 0.0) frexp(v, &e);
+    if (ok) {
+      E[m] = e;
+      S[m] = ldexp(1.0, e);
+    }
+    const int s1 = (55 - e) / 2, s2 = (55 - e) - s1;
+    fsh[0][lane] = ldexp(1.0, s1);
+    fsh[1][lane] = ldexp(1.0, s2);
+  }
+  __syncthreads();
+  const double f1 = fsh[0][lane], f2 = fsh[1][lane];
+  for (i64 k0 = 0; k0 < Kp; k0 += 128) {
+    // warp w: k0 + 16w .. +15 (4 words of 4 digits) for row m = lane
+#pragma unroll
+    for (int wq = 0; wq < 4; ++wq) {
+      uint32_t w[NS];
+#pragma unroll
+      for (int t = 0; t < NS; ++t) w[t] = 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const i64 k = k0 + 16 * warp + 4 * wq + q;
+        const double v = (ok && k < K) ? p[m + k * ld] : 0.0;
+        const unsigned long long X = static_cast<unsigned long long>(__double2ll_rn((v * f1) * f2)) + OFF;
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+          const uint32_t u = static_cast<uint32_t>(X >> (7 * (NS - 1 - t))) & (t == 0 ? 0xffu : 0x7fu);
+          w[t] |= ((u - 64u) & 0xffu) << (8 * q);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < NS; ++t) tile[t][lane][4 * warp + wq] = w[t];
+    }
+    __syncthreads();
+    // plane t, row r: 32 words (128 bytes) at D + t*plane + (m0 + r)*Kp + k0
+    for (int idx = threadIdx.x; idx < NS * 32 * 32; idx += SPM_THREADS) {
+      const int wd = idx & 31, r = (idx >> 5) & 31, t = idx >> 10;
+      const i64 mr = static_cast<i64>(blockIdx.x) * 32 + r;
+      if (mr < R) reinterpret_cast<uint32_t*>(D + t * plane + mr * Kp + k0)[wd] = tile[t][r][wd];
+    }
+    __syncthreads();
+  }
+}
+
+// C = beta C + sum_c part[c] in fixed order (chunked K)
+__global__ void chunk_sum_kernel(const double* __restrict__ part, int nchunk, i64 M, i64 N, double beta,
+                                 double* __restrict__ C, i64 ldc) {
+  const i64 total = M * N;
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s += part[c * total + idx];
+    const i64 i = idx % M, j = idx / M;
+    double* cp = C + i + j * ldc;
+    *cp = beta == 0.0 ? s : *cp + s;
   }
 }
 
@@ -163,13 +249,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 struct I8Args {
   int M, N;
-  int kb0, nkb;     // K blocks [kb0, kb0 + nkb) of every plane pair
-  int t_lo, t_hi;   // A planes t_lo..t_hi (0-based), B plane g - 2 - t
-  int g2;           // g - 2 (0-based plane sum)
-  const int *EA, *EB;
+  int nkb, ckb;     // K blocks of every plane pair; blocks per K chunk (a work unit is (chunk, tile))
+  int nchunk;       // > 1: chunk c writes the partial C + c * cstride (combined afterwards in fixed order)
+  i64 cstride;
+  int kb_off_b;     // B's K block = A's K block + kb_off_b (B planes split once over a longer K)
+  int g2_hi, g2_lo; // plane sums g2 = g2_hi .. g2_lo (g - 2, 0-based) per unit; A plane t in [0, g2], B plane g2 - t
+  const int* EA;    // row exponents of A
+  const double* SB; // column factors 2^F_j of B
   double* C;        // FP64 out (mode 0/1) or int32 out (mode 2)
   i64 ldc;
-  int mode;         // 0: C = v, 1: C += v, 2: raw int32
+  int mode;         // the unit's first plane sum: 0 C = v, 1 C += v, 2 raw int32; later ones add
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -184,7 +273,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint32_t* tmem_base_sh = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = (a.N + BN - 1) / BN, tiles = ((a.M + BM - 1) / BM) * tiles_n;
-  const int npairs = a.t_hi - a.t_lo + 1, kiters = npairs * a.nkb;
+  const int units = tiles * a.nchunk, NG = a.g2_hi - a.g2_lo + 1;  // sub-tiles (unit, plane sum)
+  // unit u: chunk u / tiles (K blocks [c*ckb, min(nkb, (c+1)*ckb))), tile u % tiles (n fastest)
+  auto chunk_kb = [&](int u, int& kb0) {
+    kb0 = (u / tiles) * a.ckb;
+    return min(a.ckb, a.nkb - kb0);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -208,24 +302,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0) {  // ---- TMA producer (the warp waits, one lane issues)
     uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
-      for (int i = 0; i < kiters; ++i, ++it) {
-        const int s = static_cast<int>(it % STAGES);
-        if (it >= STAGES) mbarrier_wait_parity(&empty[s], ((it / STAGES) - 1) & 1u);
-        if (lane == 0) {
-          const int t = a.t_lo + i / a.nkb, u = a.g2 - t, kb = a.kb0 + i % a.nkb;
-          uint8_t* sa = smem + s * STAGE_BYTES;
-          mbarrier_expect_tx(&full[s], STAGE_BYTES);
-          tma3d(sa, &mapA, &full[s], kb * BKB, m0, t);
-          tma3d(sa + A_TILE, &mapB, &full[s], kb * BKB, n0, u);
+    for (int un = blockIdx.x; un < units; un += gridDim.x) {
+      const int tile = un % tiles, m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+      int kb0;
+      const int ck = chunk_kb(un, kb0);
+      for (int g2 = a.g2_hi; g2 >= a.g2_lo; --g2) {
+        const int kiters = (g2 + 1) * ck;
+        for (int i = 0; i < kiters; ++i, ++it) {
+          const int s = static_cast<int>(it % STAGES);
+          if (it >= STAGES) mbarrier_wait_parity(&empty[s], ((it / STAGES) - 1) & 1u);
+          if (lane == 0) {
+            const int t = i / ck, u = g2 - t, kb = kb0 + i % ck;
+            uint8_t* sa = smem + s * STAGE_BYTES;
+            mbarrier_expect_tx(&full[s], STAGE_BYTES);
+            tma3d(sa, &mapA, &full[s], kb * BKB, m0, t);
+            tma3d(sa + A_TILE, &mapB, &full[s], (kb + a.kb_off_b) * BKB, n0, u);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else if (warp == 1) {  // ---- MMA issuer (the warp waits, one lane issues)
     uint32_t it = 0, lt = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++lt) {
+    for (int sub = blockIdx.x * NG; sub < units * NG; sub += (sub % NG == NG - 1) ? (gridDim.x - 1) * NG + 1 : 1, ++lt) {
+      const int un = sub / NG, g2 = a.g2_hi - sub % NG;
+      int kb0;
+      const int kiters = (g2 + 1) * chunk_kb(un, kb0);
       const int buf = static_cast<int>(lt & 1u);
       if (lt >= 2) mbarrier_wait_parity(&tempty[buf], ((lt >> 1) - 1) & 1u);
       tc_fence_after();
@@ -250,29 +352,40 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else {  // ---- epilogue: warps 2..5, TMEM lanes 32*(warp%4)..+31
     const int q = warp & 3;
     uint32_t lt = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++lt) {
+    for (int sub = blockIdx.x * NG; sub < units * NG; sub += (sub % NG == NG - 1) ? (gridDim.x - 1) * NG + 1 : 1, ++lt) {
+      const int un = sub / NG, g2 = a.g2_hi - sub % NG;
+      const int mode = g2 == a.g2_hi ? a.mode : 1;
       const int buf = static_cast<int>(lt & 1u);
-      const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+      const int tile = un % tiles, m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+      double* Cu = a.C + static_cast<i64>(un / tiles) * a.cstride;
       mbarrier_wait_parity(&tfull[buf], (lt >> 1) & 1u);
       tc_fence_after();
       const int row = m0 + 32 * q + lane;
       const bool rok = row < a.M;
-      const int ea = (a.mode != 2 && rok) ? a.EA[row] : 0;
+      // v = P 2^(E_i + F_j - 12 - 7 g2): row factor once per sub-tile, column factor 2^F_j from the split
+      const double sr = (mode != 2 && rok) ? ldexp(1.0, a.EA[row] - 12 - 7 * g2) : 0.0;
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(buf * BN + 32 * c), r);
         if (!rok) continue;
+        const int cb = n0 + 32 * c;
+        if (mode == 2) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (cb + j < a.N) reinterpret_cast<int32_t*>(Cu)[row + static_cast<i64>(cb + j) * a.ldc] = static_cast<int32_t>(r[j]);
+          continue;
+        }
+        double* cp = Cu + row + static_cast<i64>(cb) * a.ldc;  // (L2-resident across a fused unit's plane sums)
+        double o[32];
+        if (mode == 1) {  // all 32 loads in flight before any store (no load-after-store chain)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = cb + j < a.N ? cp[static_cast<i64>(j) * a.ldc] : 0.0;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int col = n0 + 32 * c + j;
-          if (col >= a.N) continue;
-          if (a.mode == 2) {
-            reinterpret_cast<int32_t*>(a.C)[row + static_cast<i64>(col) * a.ldc] = static_cast<int32_t>(r[j]);
-          } else {
-            const double v = ldexp(static_cast<double>(static_cast<int32_t>(r[j])), ea + a.EB[col] - 12 - 7 * a.g2);
-            double* cp = a.C + row + static_cast<i64>(col) * a.ldc;
-            *cp = a.mode == 0 ? v : *cp + v;
-          }
+          if (cb + j >= a.N) continue;
+          const double v = (static_cast<double>(static_cast<int32_t>(r[j])) * a.SB[cb + j]) * sr;
+          cp[static_cast<i64>(j) * a.ldc] = mode == 0 ? v : o[j] + v;
         }
       }
       tc_fence_before();
@@ -305,8 +418,8 @@ void launch_i8(Ctx& ctx, const CUtensorMap& ma, const CUtensorMap& mb, const I8A
   std::call_once(once, [] {
     NPCG_CUDA(cudaFuncSetAttribute(i8_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
   });
-  const int tiles = static_cast<int>(cdiv(args.M, BM) * cdiv(args.N, BN));
-  const int grid = std::min(tiles, ctx.sm_count);
+  const int units = static_cast<int>(cdiv(args.M, BM) * cdiv(args.N, BN)) * args.nchunk;
+  const int grid = std::min(units, ctx.sm_count);
   NPCG_LAUNCH(ctx, i8_gemm_kernel, grid, GEMM_THREADS, GEMM_SMEM, ma, mb, args);
 }
 
@@ -318,73 +431,115 @@ void gemm_i8_raw(Ctx& ctx, int M, int N, i64 Kp, const int8_t* A8, const int8_t*
   I8Args args{};
   args.M = M;
   args.N = N;
-  args.kb0 = 0;
   args.nkb = static_cast<int>(Kp / BKB);
-  args.t_lo = 0;
-  args.t_hi = 0;
-  args.g2 = 0;
+  args.ckb = args.nkb;
+  args.nchunk = 1;
+  args.g2_hi = 0;
+  args.g2_lo = 0;
   args.C = reinterpret_cast<double*>(C32);
   args.ldc = M;
   args.mode = 2;
   launch_i8(ctx, ma, mb, args);
 }
 
-void gemm_ozaki(Ctx& ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, const double* B, i64 ldb, double* C,
-                i64 ldc) {
+void ozaki_split(Ctx& ctx, const double* P, i64 ld, bool kmajor, i64 rows, i64 K, OzakiPlanes& out) {
+  out.rows = rows;
+  out.K = K;
+  out.Kp = round_up(std::max<i64>(K, 1), BKB);
+  out.d.alloc(NS * rows * out.Kp, ctx.stream);
+  out.e.alloc(rows, ctx.stream);
+  out.s.alloc(rows, ctx.stream);
+  if (kmajor)
+    NPCG_LAUNCH(ctx, ozaki_split_kernel, static_cast<unsigned>(ctx.sm_count), SPLIT_THREADS, 0, P, ld, rows, K, out.Kp,
+                rows * out.Kp, out.d.p, out.e.p, out.s.p);
+  else
+    NPCG_LAUNCH(ctx, ozaki_split_mmajor_kernel, static_cast<unsigned>(cdiv(rows, 32)), SPM_THREADS, 0, P, ld, rows, K,
+                out.Kp, rows * out.Kp, out.d.p, out.e.p, out.s.p);
+}
+
+bool ozaki_splittable(const double* P, i64 ld, bool kmajor) {
+  // the K-major splitter reads rows as 16-byte pairs
+  return !kmajor || ((ld & 1) == 0 && (reinterpret_cast<uintptr_t>(P) & 15) == 0);
+}
+
+void gemm_ozaki_planes(Ctx& ctx, const OzakiPlanes& A, const OzakiPlanes& B, i64 k_off_b, double beta, double* C,
+                       i64 ldc) {
+  const i64 M = A.rows, N = B.rows, K = A.K;
   if (M <= 0 || N <= 0) return;
   if (M > INT32_MAX || N > INT32_MAX) invalid("gemm_ozaki: dimension too large");
+  if (beta != 0.0 && beta != 1.0) invalid("gemm_ozaki: beta must be 0 or 1");
+  if (k_off_b % BKB != 0 || k_off_b + K > B.K) invalid("gemm_ozaki: B planes do not cover the K range");
+  const int nkb = static_cast<int>(A.Kp / BKB), ckb = static_cast<int>(KCHUNK / BKB);
+  const int nchunk = (nkb + ckb - 1) / ckb;
+  // K split into int32-safe chunks: each chunk's partial is assembled on its own, then summed in fixed order
+  DBuf<double> part;
+  if (nchunk > 1) part.alloc(static_cast<i64>(nchunk) * M * N, ctx.stream);
+  const CUtensorMap ma = plane_map(ctx, A.d.p, A.Kp, M, NS, BM), mb = plane_map(ctx, B.d.p, B.Kp, N, NS, BN);
+  // Plane sums g = NS + 1 .. 2, smallest first. When B's planes fit in L2 each
+  // unit runs all of them back to back in one launch (its C tile stays in L2
+  // across the additions); otherwise one launch per plane sum, so all CTAs
+  // stream the same B planes at the same time (B tiles are shared through L2).
+  const bool fused = static_cast<double>(NS) * N * B.Kp < 48.0 * (1 << 20) || static_cast<double>(NS) * N * K < 48.0 * (1 << 20);
+  for (int g2 = NS - 1; g2 >= 0; g2 = fused ? -1 : g2 - 1) {
+    I8Args args{};
+    args.M = static_cast<int>(M);
+    args.N = static_cast<int>(N);
+    args.nkb = nkb;
+    args.ckb = ckb;
+    args.nchunk = nchunk;
+    args.kb_off_b = static_cast<int>(k_off_b / BKB);
+    args.g2_hi = g2;
+    args.g2_lo = fused ? 0 : g2;
+    args.EA = A.e.p;
+    args.SB = B.s.p;
+    const bool first = g2 == NS - 1;
+    if (nchunk > 1) {
+      args.C = part.p;
+      args.ldc = M;
+      args.cstride = M * N;
+      args.mode = first ? 0 : 1;
+    } else {
+      args.C = C;
+      args.ldc = ldc;
+      args.mode = (first && beta == 0.0) ? 0 : 1;
+    }
+    launch_i8(ctx, ma, mb, args);
+    if (ctx.prof) ctx.prof_label(fused ? "i8_gemm_kernel[fused]" : "i8_gemm_kernel[per-plane]");
+  }
+  if (nchunk > 1)
+    NPCG_LAUNCH(ctx, chunk_sum_kernel, static_cast<unsigned>(std::min<i64>(cdiv(M * N, 256), 8 * ctx.sm_count)), 256, 0,
+                part.p, nchunk, M, N, beta, C, ldc);
+  ctx.prof_work(2.0 * static_cast<double>(M) * N * K, 8.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N +
+                                                              static_cast<double>(M) * N));
+}
+
+void gemm_ozaki(Ctx& ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, bool a_kmajor, const double* B, i64 ldb,
+                double beta, double* C, i64 ldc) {
+  if (M <= 0 || N <= 0) return;
+  if (beta != 0.0 && beta != 1.0) invalid("gemm_ozaki: beta must be 0 or 1");
   if (K <= 0) {
-    NPCG_CUDA(cudaMemset2DAsync(C, ldc * 8, 0, M * 8, N, ctx.stream));
+    if (beta == 0.0) NPCG_CUDA(cudaMemset2DAsync(C, ldc * 8, 0, M * 8, N, ctx.stream));
     return;
   }
-  if (((lda | ldb) & 1) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
-    // the splitter reads rows as 16-byte pairs: unaligned operands stay on the FP64 DMMA GEMM
-    gemm(ctx, M, N, K, 1.0, Operand{A, lda, true}, Operand{B, ldb, true}, 0.0, C, ldc);
+  if (!ozaki_splittable(A, lda, a_kmajor) || !ozaki_splittable(B, ldb, true)) {
+    gemm(ctx, M, N, K, 1.0, Operand{A, lda, a_kmajor}, Operand{B, ldb, true}, beta, C, ldc);
     return;
   }
-  const i64 Kp = round_up(K, BKB);
   // A in row panels: the planes of one panel (NS bytes per entry) stay within a workspace budget
+  const i64 Kp = round_up(K, BKB);
   size_t free_b = 0, total_b = 0;
   NPCG_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const i64 budget = std::max<i64>(i64(1) << 30, std::min<i64>(i64(24) << 30, static_cast<i64>(free_b / 4)));
   i64 prow = std::max<i64>(BM, budget / (NS * Kp) / BM * BM);
   prow = std::min(prow, round_up(M, BM));
-  DBuf<int8_t> a8(NS * prow * Kp, ctx.stream), b8(NS * N * Kp, ctx.stream);
-  DBuf<int> ea(prow, ctx.stream), eb(N, ctx.stream);
-  const unsigned sgrid = static_cast<unsigned>(ctx.sm_count);
-  NPCG_LAUNCH(ctx, ozaki_split_kernel, sgrid, SPLIT_THREADS, 0, B, ldb, N, K, Kp, N * Kp, b8.p, eb.p);
-  const CUtensorMap mb = plane_map(ctx, b8.p, Kp, N, NS, BN);
-  const int nkb_all = static_cast<int>(Kp / BKB);
+  OzakiPlanes bp;
+  ozaki_split(ctx, B, ldb, true, N, K, bp);
   for (i64 r0 = 0; r0 < M; r0 += prow) {
     const i64 rows = std::min(prow, M - r0);
-    NPCG_LAUNCH(ctx, ozaki_split_kernel, sgrid, SPLIT_THREADS, 0, A + r0 * lda, lda, rows, K, Kp, rows * Kp, a8.p,
-                ea.p);
-    const CUtensorMap ma = plane_map(ctx, a8.p, Kp, rows, NS, BM);
-    bool first = true;
-    for (int kb0 = 0; kb0 < nkb_all; kb0 += static_cast<int>(KCHUNK / BKB)) {
-      const int nkb = std::min(nkb_all - kb0, static_cast<int>(KCHUNK / BKB));
-      // smallest planes first: g = NS + 1 .. 2 (0-based plane sum g2 = NS - 1 .. 0)
-      for (int g2 = NS - 1; g2 >= 0; --g2) {
-        I8Args args{};
-        args.M = static_cast<int>(rows);
-        args.N = static_cast<int>(N);
-        args.kb0 = kb0;
-        args.nkb = nkb;
-        args.t_lo = 0;
-        args.t_hi = g2;
-        args.g2 = g2;
-        args.EA = ea.p;
-        args.EB = eb.p;
-        args.C = C + r0;
-        args.ldc = ldc;
-        args.mode = first ? 0 : 1;
-        first = false;
-        launch_i8(ctx, ma, mb, args);
-      }
-    }
+    OzakiPlanes ap;
+    ozaki_split(ctx, a_kmajor ? A + r0 * lda : A + r0, lda, a_kmajor, rows, K, ap);
+    gemm_ozaki_planes(ctx, ap, bp, 0, beta, C + r0, ldc);
   }
-  ctx.prof_work(2.0 * static_cast<double>(M) * N * K, 8.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N +
-                                                              static_cast<double>(M) * N));
 }
 
 }  // namespace npcg

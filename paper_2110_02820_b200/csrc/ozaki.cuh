@@ -18,11 +18,30 @@
 
 namespace npcg {
 
-/// C (M x N, col-major, ldc) = A B, A K-major (entry (m,k) at A[k + m*lda]),
-/// B K-major (entry (k,n) at B[k + n*ldb]). FP64 in and out; the products run
-/// on the INT8 tensor pipe.
-void gemm_ozaki(Ctx& ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, const double* B, i64 ldb, double* C,
-                i64 ldc);
+/// C (M x N, col-major, ldc) = A B + beta C (beta 0 or 1). A K-major (entry
+/// (m,k) at A[k + m*lda]) or M-major (at A[m + k*lda]); B K-major (entry (k,n)
+/// at B[k + n*ldb]). FP64 in and out; the products run on the INT8 tensor pipe.
+void gemm_ozaki(Ctx& ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, bool a_kmajor, const double* B, i64 ldb,
+                double beta, double* C, i64 ldc);
+
+/// Digit planes of one operand: `rows` rows of K entries (planes [NS][rows][Kp]
+/// int8, K contiguous, zero-padded to Kp), one exponent per row.
+struct OzakiPlanes {
+  DBuf<int8_t> d;
+  DBuf<int> e;     // row exponents (entries < 2^e)
+  DBuf<double> s;  // 2^e
+  i64 rows = 0, K = 0, Kp = 0;
+};
+/// Split rows x K operand P (kmajor: row r at P + r*ld, contiguous; else entry
+/// (r, k) at P[r + k*ld]) into planes.
+void ozaki_split(Ctx& ctx, const double* P, i64 ld, bool kmajor, i64 rows, i64 K, OzakiPlanes& out);
+/// Whether ozaki_split can read P (K-major rows must be 16-byte aligned pairs).
+bool ozaki_splittable(const double* P, i64 ld, bool kmajor);
+/// C (A.rows x B.rows) = A B^T over A's K entries + beta C, B's planes taken from
+/// K offset k_off_b (a multiple of 128): one split of a long operand serves
+/// products over any 128-aligned range of it.
+void gemm_ozaki_planes(Ctx& ctx, const OzakiPlanes& A, const OzakiPlanes& B, i64 k_off_b, double beta, double* C,
+                       i64 ldc);
 
 /// False when NPCG_OZAKI=0 (diagnostics: every product stays on the FP64 DMMA GEMM).
 bool ozaki_enabled();

@@ -49,6 +49,18 @@ def test_ozaki_gemm_fp64_accuracy(npcg, m, n, k, spread):
     assert np.array_equal(got, npcg.gemm_ozaki(a, b))  # deterministic
 
 
+@pytest.mark.parametrize("m,n,k", [(300, 260, 500), (77, 513, 2000), (1000, 300, 70000)])
+def test_ozaki_gemm_m_major_operand(npcg, m, n, k):
+    """A stored M x K (rows of A strided): the transposing splitter."""
+    rng = np.random.default_rng(m * k)
+    a = rng.standard_normal((m, k)) * np.exp(rng.uniform(-3, 3, (m, 1)))
+    b = rng.standard_normal((k, n))
+    ref = a @ b
+    got = npcg.gemm_ozaki(a, b, transa=False)
+    assert np.max(np.abs(got - ref) / scheme_bound(a.T, b)) <= 4 * EPS
+    assert np.array_equal(got, npcg.gemm_ozaki(np.ascontiguousarray(a).copy(order="F"), b, transa=False))
+
+
 def test_ozaki_gemm_zero_and_extreme_rows(npcg):
     rng = np.random.default_rng(3)
     k, m, n = 640, 300, 260
@@ -81,3 +93,24 @@ def test_dense_sketch_uses_int8_path_and_matches_dmma(npcg):
     dm = npcg.gemm(a, v)
     bound = np.abs(a) @ np.abs(v)
     assert np.max(np.abs(got - dm) / bound) <= 16 * EPS
+
+
+def test_matrix_free_kernel_sketch_block_int8(npcg, monkeypatch):
+    """Matrix-free RBF kernel, a sketch-width block (k = 256) over several
+    column blocks of K: both symmetric products (K[r0:n,R]^T V and its mirror
+    K[r0+rb:n,R] V_R) run on the emulated GEMM with V split once. Checked on
+    sampled rows against numpy FP64 (operators.cpp:166-177's entry formula)."""
+    monkeypatch.setenv("NPCG_KBLOCK_BYTES", str(1 << 30))  # 1 GB blocks: R = 3328 columns, 12 blocks at n = 40000
+    rng = np.random.default_rng(21)
+    n, d, k, sigma = 40000, 32, 256, 0.5
+    pts = rng.random((n, d))
+    v = rng.standard_normal((n, k))
+    op = npcg.KernelOperator(pts, sigma, dense_cap=1)
+    y = op.apply_block(v)
+    rows = rng.choice(n, 24, replace=False)
+    sq = ((pts[rows, None, :] - pts[None, :, :]) ** 2).sum(axis=2)
+    kr = np.exp(-sq / (2 * sigma * sigma))
+    kr[np.arange(len(rows)), rows] = 1.0
+    ref = kr @ v
+    bound = np.abs(kr) @ np.abs(v) + np.outer(kr.sum(axis=1), np.abs(v).max(axis=0)) + np.abs(v).sum(axis=0)[None, :]
+    assert np.max(np.abs(y[rows] - ref) / bound) <= 16 * EPS
