@@ -264,9 +264,18 @@ constexpr int RING_BYTES = NST * PW * 8;
 // dense path: row-block width per CTA (3-4 right-hand sides use half-width
 // blocks: 2 double2 slots per thread keep the accumulators in registers) and
 // ring depth (the same bytes in flight)
-constexpr int dense_pv(int S) { return S >= 3 ? 2 : PV; }
+constexpr int dense_pv(int S) { return S >= 3 ? 1 : PV; }  // 3-4 RHS: 1024-row blocks for the DMMA path
+// DMMA symmetric path (3-4 right-hand sides): 24 slots of 1024 rows + a 16-byte pad
+constexpr int MDNST = 24, MSLOT = 1024 + 2;
+constexpr int ring_bytes(bool gram, int S) { return (!gram && S >= 3) ? MDNST * MSLOT * 8 : RING_BYTES; }
 constexpr int dense_pw(int S) { return 2 * PT * dense_pv(S); }
 constexpr int dense_nst(int S) { return RING_BYTES / (dense_pw(S) * 8); }
+
+__device__ __forceinline__ void pcg_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 
 struct PersistArgs {
   i64 n, m;
@@ -305,16 +314,20 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[32];
   __shared__ double red[2][PT / 32], red2[2][PT / 32];
-  __shared__ double zred[PT / 32][32];
+  // P2/P5 cross-warp staging (S x 16 x 32); the DMMA loop's per-step column dots alias it
+  __shared__ double zbuf[(S * (PT / 32) * 32) > (!GRAM && S >= 3 ? 2 * (PT / 32) * 64 : 0)
+                             ? S * (PT / 32) * 32 : 2 * (PT / 32) * 64];
   __shared__ double wred[4 * S * (PT / 32)];  // P4: per-warp partials of up to 4 x S dots
   __shared__ ColState cs[S];
   __shared__ int running_sh;
   constexpr int DPV = GRAM ? PV : dense_pv(S), DPW = 2 * PT * DPV, DNST = GRAM ? NST : dense_nst(S);
-  __shared__ uint64_t full_bar[DNST];
+  __shared__ uint64_t full_bar[DNST > MDNST ? DNST : MDNST];
   // dense symmetric use: p_t entries of the slots' columns, per-step warp
   // partials of the 2S column dots (one set per slot pair), arrival counters
   constexpr int SP = (S + 1) / 2 * 2;  // p entries per column, padded to 16 bytes
   constexpr bool DEC = !GRAM && S == 1;  // the decoupled symmetric loop (one right-hand side)
+  constexpr bool MMA = !GRAM && S >= 3;  // the DMMA symmetric loop (3-4 right-hand sides)
+  auto mdot = [&](int b, int w, int k) -> double& { return zbuf[(b * (PT / 32) + w) * 64 + k]; };
   __shared__ __align__(16) double pring[DEC ? DNST * SP : 2];
   __shared__ double sdot[DEC ? DNST / 2 : 1][PT / 32][DEC ? 2 * S : 1];
   __shared__ unsigned pair_cnt[DNST / 2];
@@ -322,7 +335,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t ring_head = 0, ring_tail = 0;  // segments consumed (all threads) / issued (thread 0)
   if (tid == 0) {
-    for (int q = 0; q < DNST; ++q) mbarrier_init(&full_bar[q], 1);
+    for (int q = 0; q < (DNST > MDNST ? DNST : MDNST); ++q) mbarrier_init(&full_bar[q], 1);
     mbarrier_fence_init();
   }
   if (tid < DNST / 2) pair_cnt[tid] = 0u;
@@ -483,12 +496,12 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             }
             if (b < G) s0 += a.part[static_cast<i64>(b) * PW + j];
           }
-          zred[warp][lane] = s0 + s1;
+          zbuf[warp * 32 + lane] = s0 + s1;
           __syncthreads();
           if (warp == 0 && j < r1) {
             double s = 0.0;
 #pragma unroll
-            for (int w = 0; w < PT / 32; ++w) s += zred[w][lane];  // fixed order
+            for (int w = 0; w < PT / 32; ++w) s += zbuf[w * 32 + lane];  // fixed order
             const double pj = pcur[j];
             double v = s / a.div;  // operators.cpp:115 (division), then out += mu p
             v = __dadd_rn(v, __dmul_rn(a.mu, pj));  // out += mu p, unfused (solvers.cpp:139)
@@ -515,6 +528,130 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         // symmetric: CTA c's equal-byte range of the block-upper work list, as
         // segments kseg in [cseg[c], cseg[c+1]) of (row block, column range)
         const int kbeg = a.sym ? a.cseg[c] : c, kend = a.sym ? a.cseg[c + 1] : (c < nrb * ncb ? c + 1 : c);
+        if (MMA && a.sym) {
+          // Symmetric use, 3-4 right-hand sides, on the FP64 tensor pipe: a step
+          // is 8 columns (8 ring slots of the 1024-row block, 3 steps in flight);
+          // warp w owns rows 64w..64w+63 of the block and issues per step
+          //   16 DMMA  Y[rows, s] += A[rows, cols] P[cols, s]   (8 row tiles x 2 k-halves)
+          //   16 DMMA  D[cols, s] += A[rows, cols]^T P[rows, s] (16 row quads, k = rows)
+          // so the column dots are reduced inside the tensor core instead of by
+          // shuffles; the 16 warp partials of D are summed in fixed order after
+          // the step's block barrier. Row permutations inside the fragments
+          // (rows {0,1,8,9,16,17,24,25}+o for an 8-row tile, {0,1,16,17}+o for a
+          // 4-row quad) with a 16-byte slot pad make every fragment load hit 16
+          // distinct bank pairs (2 wavefronts, the minimum for 256 bytes).
+          static_assert(!MMA || DPW == 1024, "MMA path: 16 warps x 64 rows");
+          constexpr int MS = 8;  // columns per step
+          const int q4 = lane & 3, l4 = lane >> 2;
+          const int wrow = 64 * warp;
+          auto frow_axpy = [&](int t) {  // row (within the warp's 64) of accumulator/A-fragment row l4 of tile t
+            return 2 * (t & 3) + 32 * (t >> 2) + (l4 & 1) + 8 * ((l4 >> 1) & 1) + 16 * (l4 >> 2);
+          };
+          auto frow_dot = [&](int qd) {  // row of the dot's k index q4 in quad qd
+            return 2 * (qd & 7) + 32 * (qd >> 3) + (q4 & 1) + 16 * (q4 >> 1);
+          };
+          for (int kseg = kbeg; kseg < kend; ++kseg) {
+            const int rb = static_cast<int>(a.unit[3 * kseg]);
+            const i64 rb0 = static_cast<i64>(rb) * DPW, cnt = min(static_cast<i64>(DPW), n - rb0);
+            const i64 cb0 = a.unit[3 * kseg + 1], cb1 = a.unit[3 * kseg + 2], offd = rb0 + DPW;
+            const i64 ncol = cb1 - cb0, npad = round_up(ncol, MS);
+            const uint32_t base = ring_head;  // a multiple of MS: a step's 8 slots are consecutive
+            const uint32_t seg_bytes = static_cast<uint32_t>(round_up(cnt, 2) * 8);
+            __syncthreads();  // the previous segment's slots and dot buffers are released
+            if (cnt < DPW) {  // last row block: zero the slot tails once (TMA fills only cnt rows)
+              for (int idx = tid; idx < MDNST * (DPW - static_cast<int>(cnt)); idx += PT) {
+                const int sl = idx / (DPW - static_cast<int>(cnt)), r = idx % (DPW - static_cast<int>(cnt));
+                ring[static_cast<i64>(sl) * MSLOT + cnt + r] = 0.0;
+              }
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncthreads();
+            }
+            auto mma_issue = [&](i64 q) {  // thread 0: segment column q into its slot
+              if (q >= npad) return;
+              const int slot = static_cast<int>((base + static_cast<uint32_t>(q)) % MDNST);
+              if (q >= ncol) {  // padding column of the last step: complete the slot's phase with no bytes
+                mbarrier_arrive(&full_bar[slot]);
+                return;
+              }
+              mbarrier_expect_tx(&full_bar[slot], seg_bytes);
+              bulk_copy_g2s(ring + static_cast<i64>(slot) * MSLOT, a.A + (cb0 + q) * a.lda + rb0, seg_bytes,
+                            &full_bar[slot]);
+            };
+            if (tid == 0)
+              for (i64 q = 0; q < min(npad, static_cast<i64>(MDNST)); ++q) mma_issue(q);
+            // p_t on the warp's rows in the dot's B-fragment layout (k = row, n = rhs)
+            double prow[16];
+#pragma unroll
+            for (int qd = 0; qd < 16; ++qd) {
+              const i64 i = rb0 + wrow + frow_dot(qd);
+              prow[qd] = (l4 < S && i < n) ? pcur[i + l4 * a.ldw] : 0.0;
+            }
+            double yacc[8][2];
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt) yacc[tt][0] = yacc[tt][1] = 0.0;
+            int step = 0;
+            for (i64 q = 0; q < npad; q += MS, ++step) {
+              const i64 j0 = cb0 + q;
+              // the axpy's B fragments: p_t of columns j0 + 4h + q4, rhs l4
+              double pc[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const i64 j = j0 + 4 * h + q4;
+                pc[h] = (l4 < S && j < cb1) ? pcur[j + l4 * a.ldw] : 0.0;
+              }
+              const uint32_t u0 = base + static_cast<uint32_t>(q);
+              const int sl0 = static_cast<int>(u0 % MDNST);  // slots sl0 .. sl0+7
+              for (int cc = 0; cc < MS && q + cc < ncol; ++cc)
+                mbarrier_wait_parity(&full_bar[sl0 + cc], ((u0 + cc) / MDNST) & 1u);
+              const double* sb = ring + static_cast<i64>(sl0) * MSLOT + wrow;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const bool cok = q + 4 * h + q4 < ncol;
+                const double* col = sb + static_cast<i64>(4 * h + q4) * MSLOT;
+#pragma unroll
+                for (int tt = 0; tt < 8; ++tt) {
+                  const double av = cok ? col[frow_axpy(tt)] : 0.0;
+                  pcg_dmma(yacc[tt][0], yacc[tt][1], av, pc[h]);
+                }
+              }
+              if (j0 + MS > offd) {
+                double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // four chains over the 16 row quads
+                const bool cok = q + l4 < ncol;
+                const double* col = sb + static_cast<i64>(l4) * MSLOT;
+#pragma unroll
+                for (int qd = 0; qd < 16; ++qd) {
+                  const double av = cok ? col[frow_dot(qd)] : 0.0;
+                  pcg_dmma(d[qd & 3][0], d[qd & 3][1], av, prow[qd]);
+                }
+                mdot(step & 1, warp, 2 * lane) = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
+                mdot(step & 1, warp, 2 * lane + 1) = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
+              }
+              __syncthreads();  // every warp is done with the step's slots and has posted its dots
+              // the step's column dots: one thread per (column, rhs) on the last warps (warp 0 issues the refills)
+              if (j0 + MS > offd && tid >= PT - MS * S) {
+                const int cc = (tid - (PT - MS * S)) / S, sr = (tid - (PT - MS * S)) % S;
+                const i64 j = j0 + cc;
+                if (j >= offd && j < cb1) {
+                  double sum = 0.0;
+#pragma unroll
+                  for (int w = 0; w < PT / 32; ++w) sum += mdot(step & 1, w, MS * cc + sr);  // fixed order
+                  a.colpart[(static_cast<i64>(rb) * S + sr) * a.pstride + j] = sum;
+                }
+              }
+              if (tid == 0)
+                for (int cc = 0; cc < MS; ++cc) mma_issue(q + MDNST + cc);
+            }
+            ring_head = base + static_cast<uint32_t>(npad);
+            // row partials of the segment: Y[row f, rhs 2 q4 + e]
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int sr = 2 * q4 + e, row = wrow + frow_axpy(tt);
+                if (sr < S && row < cnt) a.part[(static_cast<i64>(kseg) * S + sr) * DPW + row] = yacc[tt][e];
+              }
+          }
+        } else
         for (int kseg = kbeg; kseg < kend; ++kseg) {
           const int rb = a.sym ? static_cast<int>(a.unit[3 * kseg]) : c % nrb, cb = a.sym ? kseg : c / nrb;
           const i64 rb0 = static_cast<i64>(rb) * DPW, cnt = min(static_cast<i64>(DPW), n - rb0);
@@ -659,11 +796,12 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             ring_head = base + static_cast<uint32_t>(npad);
           } else {
             // full use (A col-major): CTA (rb, cb) streams rows [rb*DPW, +DPW) of
-            // columns [cb*cpb, +cpb); symmetric use with 2-4 right-hand sides:
+            // columns [cb*cpb, +cpb); symmetric use with two right-hand sides:
             // the block-upper segments as above, each step's 2S column dots
             // reduced over the warp by a transposed butterfly and across the
-            // warps at the next step's block barrier (measured: decoupled warps
-            // are slower here, 17.7 vs 11.9 ms per iteration at n = 1e5, S = 4).
+            // warps at the next step's block barrier (measured at n = 1e5:
+            // decoupled warps 17.7 vs 11.9 ms per iteration at S = 4; the DMMA
+            // loop 9.1 vs 7.45 ms at S = 2, 9.3 vs 11.7 ms at S = 4).
             // Each column segment is one contiguous bulk copy into the ring
             // (DNST segments in flight); two columns per step, one block barrier
             // per step frees their slots.
@@ -949,40 +1087,57 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
       tick(t, 7);
       grid.sync();
       tick(t, 8);
-      // ---- P5: z = r + U t on the slice (32 rows x 16 column groups), partial r.z
+      // ---- P5: z = r + U t on the slice (32 rows x 16 column groups; U read once
+      // for all S right-hand sides), partial r.z
       auto uat = [&](i64 i, i64 j) { return a.U[i + j * a.ldu]; };
-#pragma unroll
-      for (int s = 0; s < S; ++s) {
-        double rz = 0.0;
+      {
+        double rz = 0.0;  // warp s < S accumulates r.z of right-hand side s
         for (i64 i0 = r0; i0 < r1; i0 += 32) {
           const i64 i = i0 + lane;
-          double acc = 0.0;
+          double acc[S];
+#pragma unroll
+          for (int s = 0; s < S; ++s) acc[s] = 0.0;
           if (i < r1) {
-            double acc1 = 0.0;  // two chains, loads several columns ahead
+            double acc1[S];  // two chains, loads several columns ahead
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc1[s] = 0.0;
             i64 j = warp;
-#pragma unroll 4
+#pragma unroll 2
             for (; j + PT / 32 < a.ell; j += 2 * (PT / 32)) {
-              acc += uat(i, j) * a.T[j + s * a.ell];
-              acc1 += uat(i, j + PT / 32) * a.T[j + PT / 32 + s * a.ell];
+              const double u0 = uat(i, j), u1 = uat(i, j + PT / 32);
+#pragma unroll
+              for (int s = 0; s < S; ++s) {
+                acc[s] += u0 * a.T[j + s * a.ell];
+                acc1[s] += u1 * a.T[j + PT / 32 + s * a.ell];
+              }
             }
-            if (j < a.ell) acc += uat(i, j) * a.T[j + s * a.ell];
-            acc += acc1;
+            if (j < a.ell) {
+              const double u0 = uat(i, j);
+#pragma unroll
+              for (int s = 0; s < S; ++s) acc[s] += u0 * a.T[j + s * a.ell];
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s] += acc1[s];
           }
-          zred[warp][lane] = acc;
+#pragma unroll
+          for (int s = 0; s < S; ++s) zbuf[(s * (PT / 32) + warp) * 32 + lane] = acc[s];
           __syncthreads();
-          if (warp == 0 && i < r1) {
+          if (warp < S && i < r1) {
             double u = 0.0;
 #pragma unroll
-            for (int w = 0; w < PT / 32; ++w) u += zred[w][lane];
-            const double r = a.R[i + s * a.ldw];
+            for (int w = 0; w < PT / 32; ++w) u += zbuf[(warp * (PT / 32) + w) * 32 + lane];
+            const double r = a.R[i + warp * a.ldw];
             const double z = r + u;
-            a.Z[i + s * a.ldw] = z;
+            a.Z[i + warp * a.ldw] = z;
             rz += r * z;
           }
           __syncthreads();
         }
-        rz = block_sum(rz, sh);
-        if (tid == 0) a.rz_part[c * S + s] = rz;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const double tot = block_sum(warp == s ? rz : 0.0, sh);
+          if (tid == 0) a.rz_part[c * S + s] = tot;
+        }
       }
       tick(t, 9);
       grid.sync();
@@ -1023,10 +1178,10 @@ void launch_persistent(Ctx& ctx, PersistArgs& pa, int G, int smem) {
 template <int S, bool GRAM>
 int persistent_grid(const Ctx& ctx) {
   NPCG_CUDA(cudaFuncSetAttribute(pcg_persistent_kernel<S, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 RING_BYTES));
+                                 ring_bytes(GRAM, S)));
   int per_sm = 0;
   NPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_persistent_kernel<S, GRAM>, PT,
-                                                          GRAM ? 0 : RING_BYTES));
+                                                          GRAM ? 0 : ring_bytes(GRAM, S)));
   if (per_sm < 1) fail(NPCG_ECUDA, "pcg_persistent_kernel does not fit on an SM");
   return ctx.sm_count;  // one CTA per SM: cheapest grid barrier, enough bytes in flight
 }
@@ -1173,7 +1328,7 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
     tr.zero();
     pa.trace = tr.p;
   }
-  const int smem = gram ? 0 : RING_BYTES;
+  const int smem = gram ? 0 : ring_bytes(false, static_cast<int>(S));
   if (gram) launch_persistent<1, true>(ctx, pa, G, smem);
   else if (S == 1) launch_persistent<1, false>(ctx, pa, G, smem);
   else if (S == 2) launch_persistent<2, false>(ctx, pa, G, smem);
