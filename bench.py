@@ -7,7 +7,8 @@ K 20 GB, ell = 1000, mu = 0.05, relative tol 1e-10), the largest config whose
 operator fits one GPU and the north star's >= 70 %-of-HBM target. One step =
 one full solve as the reference's run_benchmark times it (bench.cpp:214-275:
 sketch + preconditioner + PCG, the operator already built): Nyström sketch of
-the raw Gaussian Omega (orthonormalise + Y = K Omega on DMMA), on-device
+the raw Gaussian Omega (orthonormalise on DMMA; Y = K Omega as an FP64 GEMM
+emulated on the INT8 tcgen05 tensor cores by digit-plane splitting), on-device
 factorisation (shift, Cholesky, TRSM, thin SVD), preconditioner, PCG to 1e-10.
 `--config cfg1|cfg2|cfg4|cfg5` selects the other BASELINE configs.
 
@@ -284,6 +285,8 @@ ALGO_NOTE = {
     "pcg_persistent_kernel": ("hbm", "per PCG iteration: X once (8*m*n B; dense: the block-upper part of A that "
                                      "the symmetric kernel streams, ~4*n^2 + 4*n*rowblock B, vs the reference's "
                                      "8*n^2), U twice (2*8*n*l B) and ~10 n-vectors (80*n B); x iterations"),
+    "i8_gemm_kernel": ("tensor", "FP64-equivalent 2*M*N*K flops per emulated GEMM (the sketch Y = K Omega: 36 INT8 "
+                                 "digit-plane products on tcgen05; int8 ops = 36x)"),
     "kfree_sym_kernel": ("tensor", "reference count n^2*(2d+2k) flops per launch (the kernel evaluates the upper "
                                    "block pairs only: half of that on the pipe)"),
 }

@@ -5,6 +5,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <future>
@@ -29,22 +30,48 @@
 
 using namespace npcg;
 
+// Handles made on a context (operators, sketches, preconditioners) hold a
+// counted reference to it: npcg_ctx_destroy drops the caller's reference and
+// the context (its stream, its pool) goes when the last handle does, whatever
+// order a garbage collector destroys them in.
 struct npcg_ctx {
   std::unique_ptr<Ctx> c;
+  std::atomic<int> refs{1};
+};
+inline void ctx_release(npcg_ctx* p) {
+  if (p && p->refs.fetch_sub(1) == 1) delete p;
+}
+struct CtxRef {
+  npcg_ctx* p = nullptr;
+  CtxRef() = default;
+  CtxRef(npcg_ctx* c) : p(c) {  // NOLINT: implicit, handles are aggregate-initialised from npcg_ctx*
+    if (p) p->refs.fetch_add(1);
+  }
+  CtxRef(const CtxRef& o) : CtxRef(o.p) {}
+  CtxRef& operator=(const CtxRef& o) {
+    if (o.p) o.p->refs.fetch_add(1);
+    ctx_release(p);
+    p = o.p;
+    return *this;
+  }
+  ~CtxRef() { ctx_release(p); }
+  operator npcg_ctx*() const { return p; }  // NOLINT
+  npcg_ctx* operator->() const { return p; }
 };
 struct npcg_rng {
   HostRng r;
 };
+// (the context reference is the first member: destroyed last, after the device buffers)
 struct npcg_op {
-  npcg_ctx* ctx;
+  CtxRef ctx;
   std::unique_ptr<Op> op;
 };
 struct npcg_nys {
-  npcg_ctx* ctx;
+  CtxRef ctx;
   Nys s;
 };
 struct npcg_pre {
-  npcg_ctx* ctx;
+  CtxRef ctx;
   Pre p;
 };
 
@@ -210,7 +237,7 @@ int npcg_ctx_layout(const npcg_ctx* ctx, int64_t n, int* rank, int* world, int64
   });
 }
 int npcg_ctx_destroy(npcg_ctx* ctx) {
-  return guard([&] { delete ctx; });
+  return guard([&] { ctx_release(ctx); });
 }
 int npcg_ctx_sync(npcg_ctx* ctx) {
   return guard([&] { C(ctx).sync(); });
