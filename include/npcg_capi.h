@@ -373,10 +373,11 @@ int npcg_gemm(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, cons
 
 /* C = A B run on the INT8 tensor cores by digit-plane splitting (ozaki.cuh):
  * the sketch products Y = A Omega of stored and matrix-free kernel operators
- * (nystrom.cpp:56 through operators.cpp:76-78,166-177). A stored K x M
- * (a_kmajor) or M x K; B stored K x N. */
+ * (nystrom.cpp:56 through operators.cpp:76-78) and the factorisation's
+ * Grams / triangular solve / U = Q V (nystrom.cpp:115-122, dense.cpp:81-117).
+ * A stored K x M (a_kmajor) or M x K; B stored K x N (b_kmajor) or N x K. */
 int npcg_gemm_ozaki(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int a_kmajor,
-                    const double* b, int64_t ldb, double* c, int64_t ldc, int where);
+                    const double* b, int64_t ldb, int b_kmajor, double* c, int64_t ldc, int where);
 /* Diagnostics: C32 (m x n col-major int32) = A8 B8^T, A8 m x kp and B8 n x kp
  * row-major int8 host arrays (kp % 128 == 0), on the tcgen05 INT8 GEMM. */
 int npcg_gemm_i8(npcg_ctx* ctx, int64_t m, int64_t n, int64_t kp, const int8_t* a8, const int8_t* b8,

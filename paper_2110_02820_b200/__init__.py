@@ -359,18 +359,20 @@ def gemm(a, b, transa=False, transb=False, alpha=1.0, beta=0.0, c=None, ctx: Con
     return out
 
 
-def gemm_ozaki(a, b, transa=True, ctx: Context | None = None):
-    """op(a) @ b on the INT8 tensor cores (digit-plane splitting, FP64 accuracy;
-    npcg_gemm_ozaki): op(a) = a.T for a (K x M) (K-major), else a (M x K)."""
+def gemm_ozaki(a, b, transa=True, transb=False, ctx: Context | None = None):
+    """op(a) @ op(b) on the INT8 tensor cores (digit-plane splitting, FP64
+    accuracy; npcg_gemm_ozaki): op(a) = a.T for a (K x M) (K-major), else a
+    (M x K); op(b) = b (K x N), or b.T for b (N x K) when transb."""
     ctx = ctx or default_context()
     a, b = _f64(a), _f64(b)
     k, m = a.shape if transa else a.shape[::-1]
-    kb, n = b.shape
+    kb, n = b.shape[::-1] if transb else b.shape
     if k != kb:
         raise InvalidArgument("gemm_ozaki: inner dimensions differ")
     out = np.zeros((m, n), order="F")
     _check(lib().npcg_gemm_ozaki(_vp(ctx.h), _i64(m), _i64(n), _i64(k), _ptr(a), _i64(max(a.shape[0], 1)),
-                                 C.c_int(int(transa)), _ptr(b), _i64(max(k, 1)), _ptr(out), _i64(max(m, 1)), HOST))
+                                 C.c_int(int(transa)), _ptr(b), _i64(max(b.shape[0], 1)), C.c_int(int(not transb)),
+                                 _ptr(out), _i64(max(m, 1)), HOST))
     return out
 
 

@@ -1471,15 +1471,16 @@ int npcg_gemm(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, cons
 }
 
 int npcg_gemm_ozaki(npcg_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int a_kmajor,
-                    const double* b, int64_t ldb, double* c, int64_t ldc, int where) {
+                    const double* b, int64_t ldb, int b_kmajor, double* c, int64_t ldc, int where) {
   return guard([&] {
     Ctx& cx = C(ctx);
     if (m < 0 || n < 0 || k < 0) invalid("npcg_gemm_ozaki: negative dimension");
     if (m == 0 || n == 0) return;
     View A = view_in(cx, a, a_kmajor ? k : m, a_kmajor ? m : k, lda, where);
-    View B = view_in(cx, b, k, n, ldb, where);
+    View B = view_in(cx, b, b_kmajor ? k : n, b_kmajor ? n : k, ldb, where);
     View Cv = view_in(cx, c, m, n, ldc, where);
-    gemm_ozaki(cx, m, n, k, A.p, A.ld, a_kmajor != 0, B.p, B.ld, 0.0, const_cast<double*>(Cv.p), Cv.ld);
+    gemm_ozaki(cx, m, n, k, A.p, A.ld, a_kmajor != 0, B.p, B.ld, 0.0, const_cast<double*>(Cv.p), Cv.ld,
+               b_kmajor != 0);
     if (Cv.owned.p() != nullptr || where == NPCG_HOST) download(cx, Cv.p, Cv.ld, m, n, c, ldc, where);
     cx.sync();
   });

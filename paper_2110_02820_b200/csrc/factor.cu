@@ -25,6 +25,7 @@
 #include "eig.cuh"
 #include "factor.cuh"
 #include "gemm.cuh"
+#include "ozaki.cuh"
 
 namespace cg = cooperative_groups;
 

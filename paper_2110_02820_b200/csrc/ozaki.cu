@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS, 1)
         }
       }
 #pragma unroll
-      for (int t = 0; t < NS; ++t) out[t * pw + k0 / 4] = w[t];
+      for (int t = 0; t < NS; ++t) __stcs(out + t * pw + k0 / 4, w[t]);  // streaming: keep the row in L2 for the digit pass
     }
     __syncthreads();  // sh is reused by the next row's maximum
   }
@@ -469,8 +469,24 @@ void gemm_ozaki_planes(Ctx& ctx, const OzakiPlanes& A, const OzakiPlanes& B, i64
   if (M > INT32_MAX || N > INT32_MAX) invalid("gemm_ozaki: dimension too large");
   if (beta != 0.0 && beta != 1.0) invalid("gemm_ozaki: beta must be 0 or 1");
   if (k_off_b % BKB != 0 || k_off_b + K > B.K) invalid("gemm_ozaki: B planes do not cover the K range");
-  const int nkb = static_cast<int>(A.Kp / BKB), ckb = static_cast<int>(KCHUNK / BKB);
-  const int nchunk = (nkb + ckb - 1) / ckb;
+  // K chunks: int32-safe (<= 511 blocks) and, for few output tiles, enough
+  // (chunk, tile) units to fill the SMs in whole waves
+  const int nkb = static_cast<int>(A.Kp / BKB);
+  const i64 tiles = cdiv(M, BM) * cdiv(N, BN);
+  int nchunk = static_cast<int>(cdiv(nkb, KCHUNK / BKB));
+  if (tiles < 2 * ctx.sm_count) {
+    double best = -1.0;
+    for (int nc = nchunk; nc <= 32 && nc <= std::max(1, nkb / 16); ++nc) {
+      const i64 units = tiles * nc, waves = cdiv(units, ctx.sm_count);
+      const double eff = static_cast<double>(units) / static_cast<double>(waves * ctx.sm_count);
+      if (eff > best + 0.02) {
+        best = eff;
+        nchunk = nc;
+      }
+    }
+  }
+  const int ckb = static_cast<int>(cdiv(nkb, nchunk));
+  nchunk = static_cast<int>(cdiv(nkb, ckb));
   // K split into int32-safe chunks: each chunk's partial is assembled on its own, then summed in fixed order
   DBuf<double> part;
   if (nchunk > 1) part.alloc(static_cast<i64>(nchunk) * M * N, ctx.stream);
@@ -514,15 +530,15 @@ void gemm_ozaki_planes(Ctx& ctx, const OzakiPlanes& A, const OzakiPlanes& B, i64
 }
 
 void gemm_ozaki(Ctx& ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, bool a_kmajor, const double* B, i64 ldb,
-                double beta, double* C, i64 ldc) {
+                double beta, double* C, i64 ldc, bool b_kmajor) {
   if (M <= 0 || N <= 0) return;
   if (beta != 0.0 && beta != 1.0) invalid("gemm_ozaki: beta must be 0 or 1");
   if (K <= 0) {
     if (beta == 0.0) NPCG_CUDA(cudaMemset2DAsync(C, ldc * 8, 0, M * 8, N, ctx.stream));
     return;
   }
-  if (!ozaki_splittable(A, lda, a_kmajor) || !ozaki_splittable(B, ldb, true)) {
-    gemm(ctx, M, N, K, 1.0, Operand{A, lda, a_kmajor}, Operand{B, ldb, true}, beta, C, ldc);
+  if (!ozaki_splittable(A, lda, a_kmajor) || !ozaki_splittable(B, ldb, b_kmajor)) {
+    gemm(ctx, M, N, K, 1.0, Operand{A, lda, a_kmajor}, Operand{B, ldb, b_kmajor}, beta, C, ldc);
     return;
   }
   // A in row panels: the planes of one panel (NS bytes per entry) stay within a workspace budget
@@ -533,7 +549,7 @@ void gemm_ozaki(Ctx& ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, bool a_
   i64 prow = std::max<i64>(BM, budget / (NS * Kp) / BM * BM);
   prow = std::min(prow, round_up(M, BM));
   OzakiPlanes bp;
-  ozaki_split(ctx, B, ldb, true, N, K, bp);
+  ozaki_split(ctx, B, ldb, b_kmajor, N, K, bp);
   for (i64 r0 = 0; r0 < M; r0 += prow) {
     const i64 rows = std::min(prow, M - r0);
     OzakiPlanes ap;

@@ -15,6 +15,7 @@
 #pragma once
 
 #include "context.cuh"
+#include "gemm.cuh"
 
 namespace npcg {
 
@@ -22,7 +23,8 @@ namespace npcg {
 /// (m,k) at A[k + m*lda]) or M-major (at A[m + k*lda]); B K-major (entry (k,n)
 /// at B[k + n*ldb]). FP64 in and out; the products run on the INT8 tensor pipe.
 void gemm_ozaki(Ctx& ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, bool a_kmajor, const double* B, i64 ldb,
-                double beta, double* C, i64 ldc);
+                double beta, double* C, i64 ldc, bool b_kmajor = true);
+
 
 /// Digit planes of one operand: `rows` rows of K entries (planes [NS][rows][Kp]
 /// int8, K contiguous, zero-padded to Kp), one exponent per row.

@@ -61,6 +61,21 @@ def test_ozaki_gemm_m_major_operand(npcg, m, n, k):
     assert np.array_equal(got, npcg.gemm_ozaki(np.ascontiguousarray(a).copy(order="F"), b, transa=False))
 
 
+@pytest.mark.parametrize("m,n,k", [(1000, 1000, 50000), (3000, 520, 1000)])
+def test_ozaki_gemm_factorisation_shapes(npcg, m, n, k):
+    """The factorisation's shapes: a Gram (few output tiles: K split into
+    parallel chunks) and Y L^-T with an N-major B (transposing splits of both)."""
+    rng = np.random.default_rng(m + n)
+    a = rng.standard_normal((k, m)) if m == n else rng.standard_normal((m, k))
+    b = rng.standard_normal((k, n)) if m == n else rng.standard_normal((n, k))
+    transa, transb = (True, False) if m == n else (False, True)
+    ref = (a.T if transa else a) @ (b.T if transb else b)
+    got = npcg.gemm_ozaki(a, b, transa=transa, transb=transb)
+    aa = a if transa else a.T
+    bb = b.T if transb else b
+    assert np.max(np.abs(got - ref) / scheme_bound(aa, bb)) <= 4 * EPS
+
+
 def test_ozaki_gemm_zero_and_extreme_rows(npcg):
     rng = np.random.default_rng(3)
     k, m, n = 640, 300, 260

@@ -34,7 +34,7 @@ def run(f):
     torch.cuda.synchronize(); t = time.perf_counter(); f(); ctx.sync(); torch.cuda.synchronize(); return time.perf_counter() - t
 dmma = lambda: L.npcg_gemm(vp(ctx.h), i64(M), i64(ell), i64(M), C.c_double(1.0), vp(A.data_ptr()), i64(M), C.c_int(1),
                            vp(Om.data_ptr()), i64(M), C.c_int(1), C.c_double(0.0), vp(Y1.data_ptr()), i64(M), npcg.DEVICE)
-oz = lambda: L.npcg_gemm_ozaki(vp(ctx.h), i64(M), i64(ell), i64(M), vp(A.data_ptr()), i64(M), C.c_int(1), vp(Om.data_ptr()), i64(M),
+oz = lambda: L.npcg_gemm_ozaki(vp(ctx.h), i64(M), i64(ell), i64(M), vp(A.data_ptr()), i64(M), C.c_int(1), vp(Om.data_ptr()), i64(M), C.c_int(1),
                                vp(Y2.data_ptr()), i64(M), npcg.DEVICE)
 for f, name in ((dmma, "dmma"), (oz, "ozaki")):
     run(f)

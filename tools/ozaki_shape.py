@@ -14,6 +14,6 @@ L = npcg.lib(); vp = C.c_void_p; i64 = C.c_int64
 for r in range(reps):
     ctx.sync(); t = time.perf_counter()
     npcg._check(L.npcg_gemm_ozaki(vp(ctx.h), i64(M), i64(N), i64(K), vp(A.data_ptr()), i64(K if ak else M), C.c_int(ak),
-                                  vp(B.data_ptr()), i64(K), vp(Cm.data_ptr()), i64(M), npcg.DEVICE))
+                                  vp(B.data_ptr()), i64(K), C.c_int(1), vp(Cm.data_ptr()), i64(M), npcg.DEVICE))
     ctx.sync(); dt = time.perf_counter() - t
     print("M=%d N=%d K=%d kmajor=%d: %.2f ms, %.1f TF/s fp64-eq" % (M, N, K, ak, dt * 1e3, 2.0 * M * N * K / dt / 1e12), flush=True)
