@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "blas.cuh"
@@ -353,6 +354,55 @@ void copy2d(Ctx& ctx, i64 rows, i64 cols, const double* src, i64 lds, double* ds
   NPCG_CUDA(cudaMemcpy2DAsync(dst, ldd * 8, src, lds * 8, rows * 8, cols, cudaMemcpyDeviceToDevice, ctx.stream));
 }
 
+namespace {
+// Host (pageable) -> device copy of a rows x cols column-major block through the
+// context's pinned ring: chunks of whole columns (or row pieces of one column)
+// are packed into a 32 MB pinned slot by several host threads, then copied
+// asynchronously on the context stream; the next chunk is packed while the
+// previous one crosses PCIe. (A plain cudaMemcpy from pageable memory runs at
+// ~12 GB/s here; the PCIe 5 x16 link carries ~54 GB/s.)
+void h2d_pinned(Ctx& ctx, double* dst, i64 ldd, const double* src, i64 lds, i64 rows, i64 cols) {
+  constexpr int NS = Ctx::kPinSlots;
+  const i64 slot_doubles = Ctx::kPinSlotBytes / 8;
+  if (!ctx.pin) {
+    NPCG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx.pin), Ctx::kPinSlotBytes * NS, cudaHostAllocDefault));
+    for (auto& ev : ctx.pin_free) NPCG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (auto& ev : ctx.pin_free) NPCG_CUDA(cudaEventRecord(ev, ctx.stream));
+  }
+  const i64 rpc = std::min(rows, slot_doubles);                       // rows per piece
+  const i64 cpc = rpc == rows ? std::max<i64>(1, slot_doubles / rows) : 1;  // columns per chunk
+  const int nthr = static_cast<int>(std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2)));
+  int q = 0;
+  for (i64 c0 = 0; c0 < cols; c0 += cpc) {
+    const i64 nc = std::min(cpc, cols - c0);
+    for (i64 r0 = 0; r0 < rows; r0 += rpc, q = (q + 1) % NS) {
+      const i64 nr = std::min(rpc, rows - r0);
+      double* slot = reinterpret_cast<double*>(ctx.pin + q * Ctx::kPinSlotBytes);
+      NPCG_CUDA(cudaEventSynchronize(ctx.pin_free[q]));  // the slot's previous copy has landed
+      auto pack = [&](int t) {  // thread t: an equal share of the chunk's bytes
+        const i64 total = nr * nc, a = total * t / nthr, b = total * (t + 1) / nthr;
+        for (i64 e = a; e < b;) {
+          const i64 c = e / nr, r = e % nr, len = std::min(nr - r, b - e);
+          std::memcpy(slot + c * nr + r, src + (c0 + c) * lds + r0 + r, len * 8);
+          e += len;
+        }
+      };
+      if (nr * nc * 8 < (i64{4} << 20) || nthr == 1) {
+        for (int t = 0; t < nthr; ++t) pack(t);
+      } else {
+        std::vector<std::thread> th;
+        for (int t = 1; t < nthr; ++t) th.emplace_back(pack, t);
+        pack(0);
+        for (auto& x : th) x.join();
+      }
+      NPCG_CUDA(cudaMemcpy2DAsync(dst + r0 + c0 * ldd, ldd * 8, slot, nr * 8, nr * 8, nc, cudaMemcpyHostToDevice,
+                                  ctx.stream));
+      NPCG_CUDA(cudaEventRecord(ctx.pin_free[q], ctx.stream));
+    }
+  }
+}
+}  // namespace
+
 void upload(Ctx& ctx, DMat& dst, i64 rows, i64 cols, const double* src, i64 lds, int where) {
   if (rows <= 0 || cols <= 0) {
     dst.alloc(rows, cols, ctx.stream, true);
@@ -362,6 +412,10 @@ void upload(Ctx& ctx, DMat& dst, i64 rows, i64 cols, const double* src, i64 lds,
   dst.alloc(rows, cols, ctx.stream, false);
   if (dst.ld > rows)  // only the column pads need zeroing; the copy fills the rest
     NPCG_CUDA(cudaMemset2DAsync(dst.p() + rows, dst.ld * 8, 0, (dst.ld - rows) * 8, cols, ctx.stream));
+  if (where == NPCG_HOST && rows * cols * 8 >= (i64{16} << 20)) {
+    h2d_pinned(ctx, dst.p(), dst.ld, src, lds, rows, cols);
+    return;
+  }
   NPCG_CUDA(cudaMemcpy2DAsync(dst.p(), dst.ld * 8, src, lds * 8, rows * 8, cols,
                               where == NPCG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx.stream));
 }

@@ -182,6 +182,10 @@ Ctx::~Ctx() {
   if (stage) cudaFree(stage);
   for (cudaEvent_t ev : stage_free)
     if (ev) cudaEventDestroy(ev);
+  if (stream) cudaStreamSynchronize(stream);  // the pinned ring's last copies
+  if (pin) cudaFreeHost(pin);
+  for (cudaEvent_t ev : pin_free)
+    if (ev) cudaEventDestroy(ev);
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);

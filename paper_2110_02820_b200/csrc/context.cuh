@@ -45,6 +45,12 @@ struct Ctx {
   double* stage = nullptr;
   i64 stage_slot = 0;  // doubles per slot
   cudaEvent_t stage_free[kStageSlots] = {};
+  // Pinned host ring of large uploads from pageable memory (created on first
+  // use): host threads fill one slot while the previous one crosses PCIe.
+  static constexpr int kPinSlots = 3;
+  static constexpr i64 kPinSlotBytes = i64{32} << 20;
+  char* pin = nullptr;
+  cudaEvent_t pin_free[kPinSlots] = {};
   std::atomic<int64_t> launches{0};
   EncodeTiledFn encode_tiled = nullptr;
   std::mutex mu;  // serialises public calls sharing this context

@@ -87,7 +87,7 @@ template <class T, bool AK, bool BKM>
 __global__ void __launch_bounds__(T::THREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                      int M, int N, int ktiles, int ktiles_per_split, double alpha, double beta,
-                     double* __restrict__ C, i64 ldc, double* __restrict__ partial) {
+                     double* __restrict__ C, i64 ldc, double* __restrict__ partial, const GemmEpi epi) {
   constexpr int BM = T::BM, BN = T::BN, NCW = T::NCW, TM = T::TM, TN = T::TN, FM = T::FM, FN = T::FN;
   constexpr int A_BYTES = T::A_BYTES, STAGE_BYTES = T::STAGE_BYTES, STAGES = T::STAGES;
   static_assert(BKM || T::TN % 16 == 0, "N-major B reads n fragments in pairs");
@@ -224,6 +224,11 @@ __global__ void __launch_bounds__(T::THREADS, 1)
         if (gn >= N) continue;
         if (partial) {
           partial[(static_cast<i64>(split) * N + gn) * M + gm] = acc[f][j][e];
+        } else if (epi.norms) {  // Gaussian kernel entry from -2 x_i.x_j: (-2 x.x + n_i) + n_j, the reference's order
+          double v = alpha * acc[f][j][e];
+          v = v + epi.norms[gm];
+          v = v + epi.norms[gn];
+          C[gm + static_cast<i64>(gn) * ldc] = gm == gn ? 1.0 : exp(fmax(v, 0.0) * epi.c);
         } else {
           double* cp = C + gm + static_cast<i64>(gn) * ldc;
           *cp = beta == 0.0 ? alpha * acc[f][j][e] : alpha * acc[f][j][e] + beta * *cp;
@@ -264,7 +269,7 @@ CUtensorMap make_map(Ctx& ctx, const double* p, i64 inner, i64 outer, i64 ld, in
 
 template <class T, bool AK, bool BKM>
 void launch(Ctx& ctx, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int ktiles, int kps,
-            int splits, double alpha, double beta, double* C, i64 ldc, double* partial) {
+            int splits, double alpha, double beta, double* C, i64 ldc, double* partial, GemmEpi epi) {
   static std::once_flag once;
   std::call_once(once, [] {
     NPCG_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<T, AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -274,7 +279,7 @@ void launch(Ctx& ctx, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N
   dim3 grid(static_cast<unsigned>(cdiv(N, T::BN)), static_cast<unsigned>(cdiv(M, T::BM)),
             static_cast<unsigned>(splits));
   NPCG_LAUNCH(ctx, (gemm_dmma_kernel<T, AK, BKM>), grid, T::THREADS, T::SMEM_BYTES, ma, mb, M, N, ktiles, kps,
-              alpha, beta, C, ldc, partial);
+              alpha, beta, C, ldc, partial, epi);
 }
 
 // Tile shape + split-K count minimising a wave model of the launch: every CTA
@@ -322,25 +327,26 @@ Plan plan_gemm(const Ctx& ctx, i64 M, i64 N, i64 K, bool b_kmajor) {
 
 template <class T>
 void dispatch(Ctx& ctx, Operand A, Operand B, int m, int n, i64 K, int ktiles, int kps, int splits, double alpha,
-              double beta, double* C, i64 ldc, double* pp) {
+              double beta, double* C, i64 ldc, double* pp, GemmEpi epi) {
   const CUtensorMap ma = A.kmajor ? make_map(ctx, A.p, K, m, A.ld, T::BM) : make_map(ctx, A.p, m, K, A.ld, 16);
   const CUtensorMap mb = B.kmajor ? make_map(ctx, B.p, K, n, B.ld, T::BN) : make_map(ctx, B.p, n, K, B.ld, 16);
   if constexpr (T::TN % 16 == 0) {
-    if (A.kmajor && B.kmajor) launch<T, true, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-    else if (A.kmajor) launch<T, true, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-    else if (B.kmajor) launch<T, false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-    else launch<T, false, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+    if (A.kmajor && B.kmajor) launch<T, true, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp, epi);
+    else if (A.kmajor) launch<T, true, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp, epi);
+    else if (B.kmajor) launch<T, false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp, epi);
+    else launch<T, false, false>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp, epi);
   } else {
     if (!B.kmajor) fail(NPCG_ERUNTIME, "gemm: tile needs a K-major B operand");
-    if (A.kmajor) launch<T, true, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-    else launch<T, false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+    if (A.kmajor) launch<T, true, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp, epi);
+    else launch<T, false, true>(ctx, ma, mb, m, n, ktiles, kps, splits, alpha, beta, C, ldc, pp, epi);
   }
 }
 
 }  // namespace
 
 void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, double beta, double* C,
-          i64 ldc) {
+          i64 ldc, GemmEpi epi) {
+  if (epi.norms && (beta != 0.0 || K <= 0)) invalid("gemm: the kernel epilogue needs beta = 0 and K > 0");
   if (M <= 0 || N <= 0) return;
   if (M > INT32_MAX || N > INT32_MAX) invalid("gemm: dimension too large");
   if (K <= 0) {  // C = beta C
@@ -353,7 +359,11 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
     return;
   }
   const int ktiles = static_cast<int>(cdiv(K, BK));
-  const Plan plan = plan_gemm(ctx, M, N, K, B.kmajor);
+  Plan plan = plan_gemm(ctx, M, N, K, B.kmajor);
+  if (epi.norms) {  // the kernel epilogue runs on whole dot products: no split-K
+    plan.splits = 1;
+    plan.kps = ktiles;
+  }
   const int splits = plan.splits, kps = plan.kps;
   DBuf<double> part;
   double* pp = nullptr;
@@ -362,9 +372,9 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
     pp = part.p;
   }
   const int m = static_cast<int>(M), n = static_cast<int>(N);
-  if (plan.tile == kNarrow) dispatch<TileNarrow>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-  else if (plan.tile == kTall) dispatch<TileTall>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp);
-  else dispatch<TileWide>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp);
+  if (plan.tile == kNarrow) dispatch<TileNarrow>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp, epi);
+  else if (plan.tile == kTall) dispatch<TileTall>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp, epi);
+  else dispatch<TileWide>(ctx, A, B, m, n, K, ktiles, kps, splits, alpha, beta, C, ldc, pp, epi);
   ctx.prof_work(2.0 * static_cast<double>(M) * N * K, 8.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N +
                                                               static_cast<double>(M) * N));
   if (ctx.prof) {

@@ -18,10 +18,18 @@ struct Operand {
   bool kmajor;
 };
 
+/// Optional epilogue: the Gaussian kernel entry K_ij = exp(max(0, (alpha AB_ij
+/// + norms_i) + norms_j) * c), K_ii = 1 (operators.cpp:125-137), applied to the
+/// tile in registers instead of a second pass over C (beta must be 0).
+struct GemmEpi {
+  const double* norms = nullptr;
+  double c = 0.0;
+};
+
 /// C (M x N, col-major, ldc) = alpha * A B + beta * C. Deterministic (split-K
 /// partials are reduced in fixed order). All leading dimensions must be
 /// multiples of 2 and pointers 16-byte aligned (dev_ld() matrices are).
 void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, double beta,
-          double* C, i64 ldc);
+          double* C, i64 ldc, GemmEpi epi = GemmEpi{});
 
 }  // namespace npcg

@@ -32,19 +32,6 @@ __global__ void row_norms_kernel(const double* __restrict__ pts, i64 ld, i64 n, 
   norms[i] = s;
 }
 
-__global__ void kernel_epilogue_kernel(double* __restrict__ K, i64 ldk, i64 n, const double* __restrict__ norms,
-                                       double c) {
-  const i64 total = n * n;
-  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 i = idx % n, j = idx / n;
-    double* p = K + i + j * ldk;
-    double s = *p + norms[i];
-    s = s + norms[j];
-    *p = i == j ? 1.0 : exp(fmax(s, 0.0) * c);
-  }
-}
-
 // Column block [r0, r0+cols) of K (= row block, K symmetric) from the DMMA
 // product -2 X X_R^T (n x cols, in place): entry (j, i) is K(r0+i, j) with the
 // reference rounding order (-2 x.x + ||x_{r0+i}||^2) + ||x_j||^2.
@@ -843,11 +830,11 @@ void build_kernel_matrix(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma, 
   DBuf<double> norms(n, ctx.stream);
   NPCG_LAUNCH(ctx, row_norms_kernel, static_cast<unsigned>(cdiv(n, 256)), 256, 0, pts.p(), pts.ld, n, d, norms.p);
   K.alloc(n, n, ctx.stream, false);
-  // K = -2 X X^T  (A = X M-major, B = X^T N-major)
-  gemm(ctx, n, n, d, -2.0, Operand{pts.p(), pts.ld, false}, Operand{pts.p(), pts.ld, false}, 0.0, K.p(), K.ld);
+  // K = kernel(-2 X X^T + norms) in one pass: the DMMA GEMM (A = X M-major,
+  // B = X^T N-major) with the entry formula in its epilogue
   const double c = -1.0 / (2.0 * sigma * sigma);
-  NPCG_LAUNCH(ctx, kernel_epilogue_kernel, static_cast<unsigned>(std::min<i64>(cdiv(n * n, 256), ctx.sm_count * 16)),
-              256, 0, K.p(), K.ld, n, norms.p, c);
+  gemm(ctx, n, n, d, -2.0, Operand{pts.p(), pts.ld, false}, Operand{pts.p(), pts.ld, false}, 0.0, K.p(), K.ld,
+       GemmEpi{norms.p, c});
 }
 
 void build_kernel_colblock(Ctx& ctx, const DMat& pts, i64 n, i64 d, double sigma, i64 r0, i64 cols, DMat& K) {
