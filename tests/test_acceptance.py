@@ -1,4 +1,4 @@
-"""Acceptance criteria c1, c2, c7, c12, c14 of the reference
+"""Acceptance criteria c1, c2, c7, c9, c10, c12, c13, c14 of the reference
 (/root/reference/proj/tests/acceptance/acceptance.cpp), same trials, same
 seeds, same pass thresholds. On the CPU suite they pin the oracle; on the GPU
 suite they run through the B200 library (c7, the costly one, on the GPU only).
@@ -9,8 +9,9 @@ import math
 import numpy as np
 import pytest
 
-from support import (exact_condition_number, geo_spectrum, min_eigenvalue, nystrom_definitional, poly_spectrum,
-                     preconditioner_matrix, psd_from_spectrum, recommended_sketch_size, rel_diff, sym_eigenvalues)
+from support import (effective_dimension, exact_condition_number, geo_spectrum, min_eigenvalue, nystrom_definitional,
+                     poly_spectrum, preconditioner_matrix, psd_from_spectrum, random_psd, recommended_sketch_size,
+                     rel_diff, spectral_norm, sym_eigenvalues)
 
 
 def nystrom_trials(impl):  # acceptance.cpp:57-86
@@ -164,3 +165,99 @@ def test_c14_krr_column_sampling_ratio(impl):  # acceptance.cpp:565-604
         cg_iters = 500
     assert pcg.converged and pcg.iterations <= 60 and 4 * pcg.iterations <= cg_iters, \
         (out.ell_final, pcg.iterations, cg_iters)
+
+
+def random_features(impl, x, m_rf, sigma, rng):  # bench.cpp:395-407, draws through impl's Rng
+    w = rng.gaussian_matrix(x.shape[1], m_rf) / sigma
+    phase = np.array([2.0 * math.pi * rng.uniform() for _ in range(m_rf)])
+    return np.asfortranarray(math.sqrt(2.0 / m_rf) * np.cos(x @ w + phase[None, :]))
+
+
+def test_c9_sketch_and_solve_bound_and_pcg_vs_cg(impl):  # acceptance.cpp:355-414
+    n_pts, m_rf, ell, sigma = 500, 2000, 200, 1.0
+    for seed in (1, 2):
+        rng = impl.Rng(seed)
+        centers = 2.5 * rng.gaussian_matrix(20, 3)
+        x = np.empty((n_pts, 3))
+        for i in range(n_pts):  # component index drawn before the offset
+            c = rng.integer(20)
+            x[i, :] = centers[c] + 0.2 * rng.gaussian_vector(3)
+        z = random_features(impl, x, m_rf, sigma, rng)
+        op = impl.GramRidgeOperator(z)
+        a = z.T @ z / n_pts
+        w, v = np.linalg.eigh((a + a.T) / 2)
+        approx = impl.randomized_nystrom(op, ell, rng)
+        err_norm = spectral_norm(a - approx.materialize())
+        b = rng.gaussian_vector(m_rf)
+        b = b / np.linalg.norm(b)
+        prev_rel = -1.0
+        for mu in (1e-2, 1e-4, 1e-6):
+            x_star = v @ ((v.T @ b) / (w + mu))
+            x_hat = impl.woodbury_inverse_apply(approx, mu, b)
+            rel = np.linalg.norm(x_hat - x_star) / np.linalg.norm(x_star)
+            assert rel > prev_rel, (seed, mu, rel, prev_rel)  # grows as mu decreases
+            assert rel <= err_norm / mu * (1.0 + 1e-9), (seed, mu, rel, err_norm)
+            prev_rel = rel
+            pcg = impl.nystrom_pcg(op, b, mu, impl.build_preconditioner(approx, mu), eta=1e-10, max_iter=500)
+            assert pcg.converged, (seed, mu, pcg.iterations)
+            if mu == 1e-6:
+                raw = impl.cg(impl.regularize(op, mu), b, eta=1e-10, max_iter=500)
+                assert not raw.converged, (seed, raw.iterations)  # CG must fail at this scale
+
+
+def test_c10_adaptive_doublings_size_and_iterations(impl):  # acceptance.cpp:416-471
+    n, mu, tau, delta = 500, 1e-3, 44.0, 0.25
+    lam = geo_spectrum(n, 0.7)
+    op = impl.DenseOperator(np.asfortranarray(np.diag(lam)))
+    a_mu_diag = lam + mu
+    deff = effective_dimension(lam, delta * tau * mu / 11.0)
+    ell_tilde = 2 * int(math.ceil(2.0 * deff)) + 1
+    allowed_doublings = int(math.ceil(math.log2(ell_tilde / 10.0)))
+    size_cap = 4 * int(math.ceil(2.0 * deff)) + 2
+    iter_cap = impl.iteration_bound(1.0 + 12.0 * tau / 11.0, 1e-6)
+    ok_doublings = ok_size = ok_iters = 0
+    trials = 40
+    rng = impl.Rng(1010)
+    for _ in range(trials):
+        out = impl.adaptive(op, rng, mode="error", ell0=10, ell_max=n, mu=mu, tau=tau)
+        ok_doublings += out.doublings <= allowed_doublings
+        ok_size += out.ell_final <= size_cap
+        if out.hit_cap:
+            continue
+        p = impl.build_preconditioner(out.approximation, mu)
+        x_star = rng.gaussian_vector(n)
+        b = a_mu_diag * x_star
+        run = impl.nystrom_pcg(op, b, mu, p, eta=1e-10, relative=True, max_iter=200, record_iterates=True)
+        den = math.sqrt(x_star @ (a_mu_diag * x_star))
+        for it, xt in enumerate(run.iterates):
+            e = xt - x_star
+            if math.sqrt(e @ (a_mu_diag * e)) / den <= 1e-6:  # diag_energy_error, acceptance.cpp:45-49
+                ok_iters += it <= iter_cap
+                break
+    need = trials * 3 // 4
+    assert ok_doublings >= need and ok_size >= need and ok_iters >= need, (ok_doublings, ok_size, ok_iters)
+
+
+def test_c13_power_estimate_lower_bound_and_sharpness(impl):  # acceptance.cpp:529-563
+    rng = impl.Rng(1313)
+    violations = 0
+    for _ in range(100):
+        n = 20 + rng.integer(61)
+        cond = 10.0 ** (1.0 + 3.0 * rng.uniform())
+        a = random_psd(impl, rng, n, cond)
+        ell = 1 + rng.integer(n // 2)
+        q = 1 + rng.integer(8)
+        approx = impl.randomized_nystrom(impl.DenseOperator(a), ell, rng)
+        estimate = impl.estimate_error_power(impl.DenseOperator(a), approx, q, rng)
+        exact = spectral_norm(a - approx.materialize())
+        violations += estimate > exact + 1e-12 * np.linalg.norm(a)
+    worst_ratio = 1.0
+    for _ in range(20):
+        n = 40
+        lam = geo_spectrum(n, 0.45)
+        ell = 3 + rng.integer(10)
+        approx = impl.make_approximation(np.asfortranarray(np.eye(n)[:, :ell]), lam[:ell].copy())
+        op = impl.DenseOperator(np.asfortranarray(np.diag(lam)))
+        estimate = impl.estimate_error_power(op, approx, 20, rng)
+        worst_ratio = min(worst_ratio, estimate / lam[ell])
+    assert violations == 0 and worst_ratio >= 0.99, (violations, worst_ratio)
