@@ -218,7 +218,19 @@ class DevicePath:
                 npcg._check(L.npcg_nys_extend(nys, i64(w.ell), vp(self.omega.data_ptr()), i64(self.nl), npcg.DEVICE))
                 npcg._check(L.npcg_nys_factor(nys))
             iters = []
-            for mu in (w.mus or [w.mu]):
+            if w.mus:  # cold-start regularisation path: the library batches consecutive mu (one pass over A serves 8 columns)
+                nmu = len(w.mus)
+                if getattr(self, "xpath", None) is None:
+                    self.xpath = self.torch.empty((self.s * nmu, self.nl), dtype=self.torch.float64, device=self.x.device)
+                    self.path_reports = (npcg._SolveReport * (self.s * nmu))()
+                mus = np.ascontiguousarray(w.mus, dtype=np.float64)
+                npcg._check(L.npcg_regularization_path(vp(self.op.h), nys, i64(nmu), npcg._ptr(mus), i64(self.s),
+                                                       vp(self.b.data_ptr()), i64(self.nl), C.byref(self.opts), C.c_int(0),
+                                                       vp(self.xpath.data_ptr()), i64(self.nl), self.path_reports,
+                                                       npcg.DEVICE))
+                return [[(self.path_reports[k * self.s + j].iterations, bool(self.path_reports[k * self.s + j].converged))
+                         for j in range(self.s)] for k in range(nmu)]
+            for mu in [w.mu]:
                 npcg._check(L.npcg_pre_create(nys, C.c_double(mu), C.byref(pre)))
                 rc = L.npcg_pcg(vp(self.op.h), pre, C.c_double(mu), i64(self.s), vp(self.b.data_ptr()), i64(self.nl),
                                 None, i64(self.nl), C.byref(self.opts), vp(self.x.data_ptr()), i64(self.nl),
@@ -252,7 +264,11 @@ def e2e_step(npcg, w, ctx, host):
         pair = npcg.extend_sketch_with(pair, op, host.omega[off:off + nl])
         approx = npcg.nystrom_from_sketch(pair)
     total = 0.0
-    for mu in (w.mus or [w.mu]):
+    if w.mus:  # the library's cold-start path driver (consecutive mu batched over each pass of A)
+        path = npcg.regularization_path(op, host.b[off:off + nl], w.mus, approx, warm_start=False, eta=w.eta,
+                                        max_iter=w.max_iter, relative=w.relative)
+        return float(sum(r.x.sum() for _, reps in path for r in reps))
+    for mu in [w.mu]:
         pre = npcg.build_preconditioner(approx, mu)
         try:
             rep = npcg.nystrom_pcg(op, host.b[off:off + nl], mu, pre, eta=w.eta, max_iter=w.max_iter,

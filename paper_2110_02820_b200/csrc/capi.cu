@@ -1112,7 +1112,48 @@ int npcg_regularization_path(npcg_op* op, npcg_nys* nys, int64_t nmu, const doub
     View B = view_in(c, b, n, s, ldb, where);
     DMat X, Xprev;
     X.alloc(n, s, c.stream, false);
-    for (i64 k = 0; k < nmu; ++k) {
+    auto fill = [&](npcg_solve_report& rep, const PcgColumnReport& cr, double wall) {
+      rep.iterations = cr.iterations;
+      rep.matvec_count = cr.matvec_count;
+      rep.converged = cr.converged ? 1 : 0;
+      rep.status = cr.status;
+      rep.eta_used = cr.eta_used;
+      rep.wall_time = wall;
+      rep.history_len = static_cast<int64_t>(cr.history.size());
+    };
+    // Cold starts: the systems of different mu are independent, so 8 / s
+    // consecutive mu share one pass over A per iteration (8 columns with their
+    // own shift and gains in the persistent loop); each column's arithmetic is
+    // that of its own solve.
+    const i64 group = (warm_start == 0 && s <= 4 && 8 % s == 0 && nys->s.fac->ell > 0 &&
+                       pcg_mu_batch_eligible(c, *op->op, 8)) ? 8 / s : 1;
+    i64 kbatched = 0;
+    if (group > 1) {
+      DMat Bg, Xg;
+      Bg.alloc(n, 8, c.stream, false);
+      Xg.alloc(n, 8, c.stream, false);
+      for (i64 g = 0; g < group; ++g) copy2d(c, n, s, B.p, B.ld, Bg.p() + g * s * Bg.ld, Bg.ld);
+      for (; kbatched + group <= nmu; kbatched += group) {
+        std::vector<Pre> pres(static_cast<size_t>(group));
+        PcgMuCols cols;
+        for (i64 g = 0; g < group; ++g) {
+          pre_build(pres[static_cast<size_t>(g)], nys->s, mus[kbatched + g]);  // rejects mu <= 0
+          for (i64 j = 0; j < s; ++j) {
+            cols.mu.push_back(mus[kbatched + g]);
+            cols.pre.push_back(&pres[static_cast<size_t>(g)]);
+          }
+        }
+        PcgResult r = pcg_solve(c, *op->op, cols.pre[0], cols.mu[0], 8, Bg.p(), Bg.ld, nullptr, 0, po, Xg.p(), Xg.ld,
+                                nullptr, "nystrom_pcg", &cols);
+        for (i64 g = 0; g < group; ++g) {
+          for (i64 j = 0; j < s; ++j)
+            fill(reports[(kbatched + g) * s + j], r.cols[static_cast<size_t>(g * s + j)], r.wall_time);
+          if (x) download(c, Xg.p() + g * s * Xg.ld, Xg.ld, n, s, x + (kbatched + g) * s * ldx, ldx, where);
+        }
+        c.sync();  // the group's preconditioners go out of scope
+      }
+    }
+    for (i64 k = kbatched; k < nmu; ++k) {
       const double mu = mus[k];
       Pre p;
       pre_build(p, nys->s, mu);  // rejects mu <= 0 (preconditioner.cpp:80-89)
@@ -1124,15 +1165,7 @@ int npcg_regularization_path(npcg_op* op, npcg_nys* nys, int64_t nmu, const doub
                                 warm ? Xprev.p() + s0 * Xprev.ld : nullptr, Xprev.ld, po, X.p() + s0 * X.ld, X.ld,
                                 nullptr, "nystrom_pcg");
         for (i64 j = 0; j < sb; ++j) {
-          const PcgColumnReport& cr = r.cols[static_cast<size_t>(j)];
-          npcg_solve_report& rep = reports[k * s + s0 + j];
-          rep.iterations = cr.iterations;
-          rep.matvec_count = cr.matvec_count;
-          rep.converged = cr.converged ? 1 : 0;
-          rep.status = cr.status;
-          rep.eta_used = cr.eta_used;
-          rep.wall_time = r.wall_time;
-          rep.history_len = static_cast<int64_t>(cr.history.size());
+          fill(reports[k * s + s0 + j], r.cols[static_cast<size_t>(j)], r.wall_time);
         }
       }
       if (x) download(c, X.p(), X.ld, n, s, x + k * s * ldx, ldx, where);

@@ -281,10 +281,11 @@ struct PersistArgs {
   i64 n, m;
   const double* A;
   i64 lda;  // gram: X row-major (row a at A + a*lda); dense: n x n col-major
-  double mu, div;
+  double mus[8], div;  // the shift of each column (one value repeated unless the batch spans several mu)
   const double* U;
   i64 ldu, ell;
-  const double* gain;
+  const double* gain;  // column s uses gain[s*gstride + j] (gstride = 0: one preconditioner for all columns)
+  i64 gstride;
   double* X;
   i64 ldx;
   double *R, *Z, *P0, *P1, *V;
@@ -315,9 +316,12 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   __shared__ double sh[32];
   __shared__ double red[2][PT / 32], red2[2][PT / 32];
   // P2/P5 cross-warp staging (S x 16 x 32); the DMMA loop's per-step column dots alias it
-  __shared__ double zbuf[(S * (PT / 32) * 32) > (!GRAM && S >= 3 ? 2 * (PT / 32) * 64 : 0)
-                             ? S * (PT / 32) * 32 : 2 * (PT / 32) * 64];
-  __shared__ double wred[4 * S * (PT / 32)];  // P4: per-warp partials of up to 4 x S dots
+  // (P5 stages at most ZS = 4 right-hand sides per round: 5-8 take two rounds, the ring leaves no room for more)
+  constexpr int ZS = S < 4 ? S : 4;
+  __shared__ double zbuf[(ZS * (PT / 32) * 32) > (!GRAM && S >= 3 ? 2 * (PT / 32) * 64 : 0)
+                             ? ZS * (PT / 32) * 32 : 2 * (PT / 32) * 64];
+  constexpr int UQ = S > 4 ? 2 : 4;  // P4: columns of U per pass
+  __shared__ double wred[UQ * S * (PT / 32)];  // P4: per-warp partials of up to UQ x S dots
   __shared__ ColState cs[S];
   __shared__ int running_sh;
   constexpr int DPV = GRAM ? PV : dense_pv(S), DPW = 2 * PT * DPV, DNST = GRAM ? NST : dense_nst(S);
@@ -504,7 +508,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             for (int w = 0; w < PT / 32; ++w) s += zbuf[w * 32 + lane];  // fixed order
             const double pj = pcur[j];
             double v = s / a.div;  // operators.cpp:115 (division), then out += mu p
-            v = __dadd_rn(v, __dmul_rn(a.mu, pj));  // out += mu p, unfused (solvers.cpp:139)
+            v = __dadd_rn(v, __dmul_rn(a.mus[0], pj));  // out += mu p, unfused (solvers.cpp:139)
             a.V[j] = v;
             pvl += pj * v;
           }
@@ -806,9 +810,11 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             // (DNST segments in flight); two columns per step, one block barrier
             // per step frees their slots.
             const i64 offd = rb0 + DPW;  // first column beyond the diagonal block
-            __shared__ double wdot[2][PT / 32][2 * S];
-            double2 pr[S][DPV];  // p_t on this thread's rows (symmetric dots)
-            if (a.sym) {
+            // (3+ right-hand sides take the DMMA loop above in symmetric use: SYM2 discards that code here)
+            constexpr bool SYM2 = !MMA;
+            __shared__ double wdot[2][PT / 32][SYM2 ? 2 * S : 1];
+            double2 pr[SYM2 ? S : 1][DPV];  // p_t on this thread's rows (symmetric dots)
+            if constexpr (SYM2) if (a.sym) {
 #pragma unroll
               for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -821,12 +827,12 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             // the 2S dots reduced by a fixed shuffle tree over 16 lanes, on the
             // last four warps (warp 0 issues the ring's bulk copies; a serial sum
             // there made it the laggard at every step's barrier)
-            static_assert(PT / 32 == 16 && 2 * S * 16 <= 128, "flush layout");
+            static_assert(PT / 32 == 16 && (!SYM2 || 2 * S * 16 <= 128), "flush layout");
             auto flush_dots = [&](i64 jp, int buf) {
               const int loc = tid - (PT - 128);
               if (loc >= 0) {
                 const int slot = loc >> 4, w = loc & 15;
-                double v = slot < 2 * S ? wdot[buf][w][slot] : 0.0;
+                double v = (SYM2 && slot < 2 * S) ? wdot[buf][w][SYM2 ? slot : 0] : 0.0;
 #pragma unroll
                 for (int m = 8; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
                 const int e = slot / S, s = slot % S;
@@ -861,7 +867,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
                 if (j + DNST < cb1) ring_issue(a.A + (j + DNST) * a.lda + rb0, cnt);
                 if (j + DNST + 1 < cb1) ring_issue(a.A + (j + DNST + 1) * a.lda + rb0, cnt);
               }
-              if (a.sym) {
+              if constexpr (SYM2) if (a.sym) {
                 if (jprev >= 0) flush_dots(jprev, (step - 1) & 1);
                 jprev = -1;
                 if (j >= offd) {  // both columns are beyond the diagonal block (offd is even)
@@ -953,7 +959,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
               for (int b = 0; b < rbj; ++b) sum += a.colpart[(static_cast<i64>(b) * S + s) * a.pstride + j];
               const double pj = pcur[j + s * a.ldw];
               double v = sum;  // operators.cpp:72-78 then solvers.cpp:137-141: out = A p; out += mu p
-              v = __dadd_rn(v, __dmul_rn(a.mu, pj));  // out += mu p, unfused (solvers.cpp:139)
+              v = __dadd_rn(v, __dmul_rn(a.mus[s], pj));  // out += mu p, unfused (solvers.cpp:139)
               a.V[j + s * a.ldw] = v;
               pvl[s] += pj * v;
             }
@@ -967,7 +973,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             sum = warp_sum(sum);
             const double pj = pcur[j + s * a.ldw];
             double v = sum;  // operators.cpp:72-78 then solvers.cpp:137-141: out = A p; out += mu p
-            v = __dadd_rn(v, __dmul_rn(a.mu, pj));  // out += mu p, unfused (solvers.cpp:139)
+            v = __dadd_rn(v, __dmul_rn(a.mus[s], pj));  // out += mu p, unfused (solvers.cpp:139)
             if (lane == 0) {
               a.V[j + s * a.ldw] = v;
               pvl[s] += pj * v;
@@ -1022,7 +1028,6 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
       if (nys) {
         // this CTA's columns of U, up to UQ at a time: r is read once per row for all of them
         // and the UQ x S dots are reduced together (one barrier)
-        constexpr int UQ = 4;
         for (i64 j0 = u0; j0 < u1; j0 += UQ) {
           double w[UQ][S];
 #pragma unroll
@@ -1056,7 +1061,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             if (j0 + q < u1) {
               double tot = 0.0;
               for (int ww = 0; ww < PT / 32; ++ww) tot += wred[tid * (PT / 32) + ww];  // fixed order
-              a.T[(j0 + q) + s * a.ell] = tot * a.gain[j0 + q];
+              a.T[(j0 + q) + s * a.ell] = tot * a.gain[j0 + q + s * a.gstride];
             }
           }
           __syncthreads();
@@ -1120,18 +1125,21 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             for (int s = 0; s < S; ++s) acc[s] += acc1[s];
           }
 #pragma unroll
-          for (int s = 0; s < S; ++s) zbuf[(s * (PT / 32) + warp) * 32 + lane] = acc[s];
-          __syncthreads();
-          if (warp < S && i < r1) {
-            double u = 0.0;
+          for (int h = 0; h < S; h += ZS) {  // ZS right-hand sides per round
 #pragma unroll
-            for (int w = 0; w < PT / 32; ++w) u += zbuf[(warp * (PT / 32) + w) * 32 + lane];
-            const double r = a.R[i + warp * a.ldw];
-            const double z = r + u;
-            a.Z[i + warp * a.ldw] = z;
-            rz += r * z;
+            for (int s = h; s < h + ZS && s < S; ++s) zbuf[((s - h) * (PT / 32) + warp) * 32 + lane] = acc[s];
+            __syncthreads();
+            if (warp >= h && warp < h + ZS && warp < S && i < r1) {
+              double u = 0.0;
+#pragma unroll
+              for (int w = 0; w < PT / 32; ++w) u += zbuf[((warp - h) * (PT / 32) + w) * 32 + lane];
+              const double r = a.R[i + warp * a.ldw];
+              const double z = r + u;
+              a.Z[i + warp * a.ldw] = z;
+              rz += r * z;
+            }
+            __syncthreads();
           }
-          __syncthreads();
         }
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -1160,7 +1168,8 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
 bool persistent_eligible(const Ctx& ctx, Op& op, i64 S) {
   (void)ctx;
   if (auto* g = dynamic_cast<GramOp*>(&op)) return S == 1 && g->n <= PW && g->m >= 1;
-  if (dynamic_cast<DenseOp*>(&op)) return S <= 4 && cdiv(op.n, dense_pw(static_cast<int>(S))) <= ctx.sm_count;
+  if (dynamic_cast<DenseOp*>(&op))  // 1-4 or 8 columns (5-7 are not instantiated)
+    return (S <= 4 || S == 8) && cdiv(op.n, dense_pw(static_cast<int>(S))) <= ctx.sm_count;
   return false;
 }
 
@@ -1186,8 +1195,8 @@ int persistent_grid(const Ctx& ctx) {
   return ctx.sm_count;  // one CTA per SM: cheapest grid barrier, enough bytes in flight
 }
 
-void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64 ldx, DMat& R, DMat& Z, DMat& P,
-                    DMat& V, State* st, double* hist, i64 hstride, i64 max_iter) {
+void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, const PcgMuCols* cols, i64 S, double* X, i64 ldx, DMat& R,
+                    DMat& Z, DMat& P, DMat& V, State* st, double* hist, i64 hstride, i64 max_iter) {
   auto* gram = dynamic_cast<GramOp*>(&op);
   auto* dense = dynamic_cast<DenseOp*>(&op);
   if (gram) gram->settle();
@@ -1196,7 +1205,8 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   const int G = gram ? persistent_grid<1, true>(ctx)
                      : S == 1 ? persistent_grid<1, false>(ctx)
                      : S == 2 ? persistent_grid<2, false>(ctx)
-                     : S == 3 ? persistent_grid<3, false>(ctx) : persistent_grid<4, false>(ctx);
+                     : S == 3 ? persistent_grid<3, false>(ctx)
+                     : S == 4 ? persistent_grid<4, false>(ctx) : persistent_grid<8, false>(ctx);
   DMat P1;
   P1.alloc(n, S, ctx.stream, false);
   DBuf<double> part, T, scal(3 * static_cast<i64>(G) * S, ctx.stream);
@@ -1273,7 +1283,8 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   if (nys) T.alloc(pre->ell * S, ctx.stream);
   PersistArgs pa{};
   pa.n = n;
-  pa.mu = mu;
+  for (i64 s = 0; s < kMaxS; ++s) pa.mus[s] = cols && s < S ? cols->mu[static_cast<size_t>(s)] : mu;
+  DBuf<double> gains;  // several preconditioners in one batch: their gains side by side (ell x S)
   if (gram) {
     pa.m = gram->m;
     pa.A = gram->xr.p();
@@ -1290,6 +1301,14 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
     pa.ldu = pre->fac->u.ld;
     pa.ell = pre->ell;
     pa.gain = pre->gain_inv.p;
+    if (cols) {
+      gains.alloc(pre->ell * S, ctx.stream);
+      for (i64 s = 0; s < S; ++s)
+        NPCG_CUDA(cudaMemcpyAsync(gains.p + s * pre->ell, cols->pre[static_cast<size_t>(s)]->gain_inv.p,
+                                  sizeof(double) * pre->ell, cudaMemcpyDeviceToDevice, ctx.stream));
+      pa.gain = gains.p;
+      pa.gstride = pre->ell;
+    }
     pa.T = T.p;
     pa.uslice = cdiv(pre->ell, G);
   }
@@ -1333,7 +1352,8 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
   else if (S == 1) launch_persistent<1, false>(ctx, pa, G, smem);
   else if (S == 2) launch_persistent<2, false>(ctx, pa, G, smem);
   else if (S == 3) launch_persistent<3, false>(ctx, pa, G, smem);
-  else launch_persistent<4, false>(ctx, pa, G, smem);
+  else if (S == 4) launch_persistent<4, false>(ctx, pa, G, smem);
+  else launch_persistent<8, false>(ctx, pa, G, smem);
   ctx.sync();  // work buffers are released on return
   if (tracing) {
     unsigned long long h[8 * 12];
@@ -1363,8 +1383,28 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, double* X, i64
 
 }  // namespace
 
+bool pcg_mu_batch_eligible(Ctx& ctx, Op& op, i64 S) {
+  if (ctx.sharded()) return false;
+  if (std::getenv("NPCG_PCG") && std::string(std::getenv("NPCG_PCG")) == "classic") return false;
+  if (auto* reg = dynamic_cast<RegOp*>(&op)) return false;
+  return S == kMaxS && persistent_eligible(ctx, op, S);
+}
+
 PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* B, i64 ldb, const double* X0,
-                    i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, IterateRec* iterates, const char* context) {
+                    i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, IterateRec* iterates, const char* context,
+                    const PcgMuCols* cols) {
+  if (cols) {  // columns with their own shift and preconditioner: the persistent loop only, cold start
+    if (X0 || iterates || !pcg_mu_batch_eligible(ctx, op, S) || static_cast<i64>(cols->mu.size()) != S ||
+        static_cast<i64>(cols->pre.size()) != S)
+      fail(NPCG_ERUNTIME, "pcg_solve: per-column shifts need the persistent loop (8 columns, x0 = 0)");
+    pre = cols->pre[0];
+    mu = cols->mu[0];
+    for (i64 s = 0; s < S; ++s) {
+      const Pre* q = cols->pre[static_cast<size_t>(s)];
+      if (!q || q->fac.get() != pre->fac.get() || q->ell != pre->ell || q->mu != cols->mu[static_cast<size_t>(s)])
+        fail(NPCG_ERUNTIME, "pcg_solve: per-column preconditioners must share one factorisation");
+    }
+  }
   // cg on RegularizedOperator(base, a) (solvers.cpp:111-120 + operators.cpp:95-98)
   // is nystrom_pcg's loop on base with shift a: the same products, the same
   // rounding (out = base p; out += a p), so the fused kernels apply.
@@ -1436,7 +1476,17 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
                 static_cast<const int*>(nullptr));
   }
   // z = P^{-1} r; p = z; rz = r.z
-  if (!identity) pre_apply_inverse(*pre, R.p(), R.ld, S, Z.p(), Z.ld, gate);
+  if (!identity && cols) {  // runs of columns with the same preconditioner
+    for (i64 s0 = 0; s0 < S;) {
+      i64 s1 = s0 + 1;
+      while (s1 < S && cols->pre[static_cast<size_t>(s1)] == cols->pre[static_cast<size_t>(s0)]) ++s1;
+      pre_apply_inverse(*cols->pre[static_cast<size_t>(s0)], R.p() + s0 * R.ld, R.ld, s1 - s0, Z.p() + s0 * Z.ld, Z.ld,
+                        gate);
+      s0 = s1;
+    }
+  } else if (!identity) {
+    pre_apply_inverse(*pre, R.p(), R.ld, S, Z.p(), Z.ld, gate);
+  }
   NPCG_LAUNCH(ctx, dot_kernel, nblk, 256, 0, n, static_cast<int>(S), R.p(), R.ld, Zp, ldz, P.p(), P.ld, st.p, part.p);
   {
     const auto [pp, nb] = combine(static_cast<int>(S));
@@ -1444,7 +1494,7 @@ PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* 
   }
 
   if (!iterates && persistent_eligible(ctx, op, S) && !(std::getenv("NPCG_PCG") && std::string(std::getenv("NPCG_PCG")) == "classic")) {
-    run_persistent(ctx, op, pre, mu, S, X, ldx, R, Z, P, V, st.p, hist.p, hstride, opt.max_iter);
+    run_persistent(ctx, op, pre, mu, cols, S, X, ldx, R, Z, P, V, st.p, hist.p, hstride, opt.max_iter);
   } else {
     // pinned status snapshots, one per in-flight iteration
     State* snap = nullptr;

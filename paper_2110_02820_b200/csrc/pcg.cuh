@@ -40,12 +40,22 @@ struct IterateRec {
   i64 cap = 0;  // iterations the buffer holds
 };
 
+/// Columns with their own shift: column s solves (A + mu[s] I) x = b_s with pre[s]
+/// (all built from one factorisation). One pass over A per iteration serves
+/// every column, so a cold-start regularisation path batches several mu.
+struct PcgMuCols {
+  std::vector<double> mu;
+  std::vector<Pre*> pre;
+};
+/// Whether pcg_solve takes per-column shifts for this operator and column count.
+bool pcg_mu_batch_eligible(Ctx& ctx, Op& op, i64 S);
+
 /// Solves (A + mu I) X = B column by column with P^{-1} from `pre`
 /// (nullptr = identity, i.e. cg() on A + mu I). B, X0, X are device n x S
 /// (X0 nullable = 0). `iterates` (nullable): filled with x_0 .. x_t.
 PcgResult pcg_solve(Ctx& ctx, Op& op, Pre* pre, double mu, i64 S, const double* B, i64 ldb, const double* X0,
                     i64 ldx0, const PcgOptions& opt, double* X, i64 ldx, IterateRec* iterates,
-                    const char* context = "nystrom_pcg");
+                    const char* context = "nystrom_pcg", const PcgMuCols* cols = nullptr);
 
 struct BlockPcgResult {
   i64 iterations = 0;

@@ -192,10 +192,15 @@ def run_regpath(npcg, orc, w, floor_check=False):
     ap = npcg.nystrom_from_sketch(pair)
     ao = orc.nystrom_from_sketch(orc.extend_sketch_with(orc.make_empty_sketch(w.n), oop, w.omega))
     compare_approx(ap, ao)
-    for mu in w.mus:  # one sketch reused across the regularisation path
+    # cold-start path driver: pairs of mu share each pass over A (8 columns with their own shift)
+    cold = npcg.regularization_path(op, w.b, w.mus, ap, warm_start=False, eta=w.eta, relative=True)
+    for k, mu in enumerate(w.mus):  # one sketch reused across the regularisation path
         pre, opre = npcg.build_preconditioner(ap, mu), orc.build_preconditioner(ao, mu)
         reps = npcg.nystrom_pcg(op, w.b, mu, pre, eta=w.eta, relative=True)  # 4 RHS share each pass over A
         for j, rp in enumerate(reps):
+            rc = cold[k][1][j]  # the batched column runs its own solve's arithmetic
+            assert (rc.iterations, rc.converged) == (rp.iterations, rp.converged), (mu, j)
+            assert np.linalg.norm(rc.x - rp.x) <= 1e-12 * np.linalg.norm(rp.x), (mu, j)
             ro = orc.nystrom_pcg(oop, w.b[:, j], mu, opre, eta=w.eta, relative=True)
             if floor_check:
                 compare_solve_floor(rp, ro, orc, oop, b=w.b[:, j], mu=mu, opre=opre, eta=w.eta)
@@ -205,6 +210,30 @@ def run_regpath(npcg, orc, w, floor_check=False):
 
 def test_cfg5_regularization_path_reduced(npcg, orc):
     run_regpath(npcg, orc, shared_inputs(npcg, orc, "cfg5", n=3000, r=300, ell=150, nmu=4))
+
+
+@pytest.mark.parametrize("n,s,nmu", [(3000, 1, 9), (3000, 2, 5), (700, 4, 3), (2100, 4, 2)])
+def test_mu_batched_path_equals_per_mu_solves(npcg, orc, n, s, nmu):
+    """8 / s consecutive mu of a cold-start path run as one 8-column persistent
+    solve (per-column shift and gains); a tail group and the small-n
+    (unsymmetric-use) loop included. Each column must reproduce its own solve."""
+    w = shared_inputs(npcg, orc, "cfg5", n=n, r=200, ell=100, nmu=nmu)
+    op, _ = operators(npcg, orc, w)
+    ap = npcg.nystrom_from_sketch(npcg.extend_sketch_with(npcg.make_empty_sketch(op), op, w.omega))
+    b = np.asfortranarray(w.b[:, :s])
+    cold = npcg.regularization_path(op, b, w.mus, ap, warm_start=False, eta=w.eta, relative=True)
+    for k, mu in enumerate(w.mus):
+        pre = npcg.build_preconditioner(ap, mu)
+        reps = npcg.nystrom_pcg(op, b, mu, pre, eta=w.eta, relative=True)
+        reps = reps if isinstance(reps, list) else [reps]
+        for j, rp in enumerate(reps):
+            rc = cold[k][1][j]
+            if s == 4:  # the 4-column solve runs the same DMMA loop: the same arithmetic per column
+                assert (rc.iterations, rc.converged) == (rp.iterations, rp.converged), (mu, j)
+                assert np.linalg.norm(rc.x - rp.x) <= 1e-12 * np.linalg.norm(rp.x), (mu, j)
+            else:  # 1-2 columns stream A in another summation order: the parity tolerance (Appendix A.4)
+                assert abs(rc.iterations - rp.iterations) <= 1 and rc.converged == rp.converged, (mu, j)
+                assert np.linalg.norm(rc.x - rp.x) <= 1e-8 * np.linalg.norm(rp.x), (mu, j)
 
 
 @pytest.mark.slow
