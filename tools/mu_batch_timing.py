@@ -29,4 +29,5 @@ for s in (4, 8):
                         C.byref(opts), vp(path.x.data_ptr()), i64(n), reports, None, None, npcg.DEVICE)
         ctx.sync(); dt = time.perf_counter() - t0
     it = reports[0].iterations
-    print("S=%d: %d iterations, %.3f ms/iteration" % (s, it, dt / it * 1e3), flush=True)
+    print("S=%d: %d iterations, %.3f ms/iteration; rc %d; per column (iterations, status, history_len): %s" % (
+        s, it, dt / it * 1e3, rc, [(r.iterations, r.status, r.history_len) for r in reports]), flush=True)
