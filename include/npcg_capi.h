@@ -296,7 +296,11 @@ int npcg_pcg(npcg_op* op, npcg_pre* pre, double mu, int64_t s, const double* b, 
  * preconditioner is rebuilt for mus[k] (only its l gains change) and the s
  * right-hand sides are solved together (npcg_pcg). warm_start != 0 starts mu_k
  * from the solutions of mu_{k-1} (the paper goes from the largest mu down),
- * otherwise from 0. x: n x s per mu, mu-major (x + k * s * ldx), nullable;
+ * otherwise from 0. With cold starts the systems of different mu are
+ * independent: on a stored dense operator 8 / s consecutive mu (s = 1, 2, 4)
+ * run as one 8-column solve, every column with its own shift and gains, so a
+ * pass over A serves all of them; each column reports what its own solve
+ * would. x: n x s per mu, mu-major (x + k * s * ldx), nullable;
  * reports: nmu x s, mu-major. A diverged column is reported (status), not
  * fatal: the path goes on. */
 int npcg_regularization_path(npcg_op* op, npcg_nys* nys, int64_t nmu, const double* mus, int64_t s,
