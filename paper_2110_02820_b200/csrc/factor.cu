@@ -413,7 +413,9 @@ namespace {
 // consumed. Returns false on Cholesky breakdown. L is left in `Lm`.
 bool cholqr_pass(Ctx& ctx, double* Y, i64 ldy, i64 m, i64 n, double shift, DMat& Lm, double* Q, i64 ldq, bool dist) {
   Lm.alloc(n, n, ctx.stream, false);
-  gemm(ctx, n, n, m, 1.0, Operand{Y, ldy, true}, Operand{Y, ldy, true}, 0.0, Lm.p(), Lm.ld);
+  GemmEpi gram;
+  gram.sym = true;  // Y^T Y: upper tiles + mirror
+  gemm(ctx, n, n, m, 1.0, Operand{Y, ldy, true}, Operand{Y, ldy, true}, 0.0, Lm.p(), Lm.ld, gram);
   if (dist) rows_allreduce(ctx, Lm.p(), Lm.ld * n);  // Y^T Y over all row blocks
   if (shift > 0.0) NPCG_LAUNCH(ctx, add_diag_kernel, static_cast<unsigned>(cdiv(n, 256)), 256, 0, Lm.p(), n, Lm.ld, shift);
   CholFactor f;
@@ -464,7 +466,9 @@ void orthonormalize(Ctx& ctx, const double* G_in, i64 ldg_in, i64 m, i64 n, doub
   for (int more = 0; more < (shifted ? 2 : 1); ++more) {
     DMat L;
     L.alloc(n, n, ctx.stream, false);
-    gemm(ctx, n, n, m, 1.0, Operand{Q, ldq, true}, Operand{Q, ldq, true}, 0.0, L.p(), L.ld);
+    GemmEpi gram;
+    gram.sym = true;
+    gemm(ctx, n, n, m, 1.0, Operand{Q, ldq, true}, Operand{Q, ldq, true}, 0.0, L.p(), L.ld, gram);
     if (dist) rows_allreduce(ctx, L.p(), L.ld * n);
     if (!shifted || more > 0) {
       // (sharded: m is the local row count; ~world x m rows in all)

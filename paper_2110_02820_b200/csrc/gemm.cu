@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(T::THREADS, 1)
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN, split = blockIdx.z;
   const int kt0 = split * ktiles_per_split;
   const int nk = max(0, min(kt0 + ktiles_per_split, ktiles) - kt0);
+  if (epi.sym && n0 + BN <= m0) return;  // Gram product: a tile strictly below the diagonal is mirrored later
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -249,6 +250,14 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ partial, int spl
   *cp = beta == 0.0 ? alpha * s : alpha * s + beta * *cp;
 }
 
+// Gram product: strict lower triangle from the upper one
+__global__ void mirror_upper_kernel(double* __restrict__ C, int n, i64 ldc) {
+  const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<i64>(n) * n) return;
+  const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
+  if (i > j) C[i + static_cast<i64>(j) * ldc] = C[j + static_cast<i64>(i) * ldc];
+}
+
 // 2D FP64 tensor map: inner dimension `inner` (contiguous), outer `outer`,
 // row pitch ld doubles, box (16 x box_outer), 128-byte swizzle, OOB -> 0.
 CUtensorMap make_map(Ctx& ctx, const double* p, i64 inner, i64 outer, i64 ld, int box_outer) {
@@ -291,7 +300,7 @@ struct Plan {
   TileKind tile;
   int splits, kps;
 };
-Plan plan_gemm(const Ctx& ctx, i64 M, i64 N, i64 K, bool b_kmajor) {
+Plan plan_gemm(const Ctx& ctx, i64 M, i64 N, i64 K, bool b_kmajor, bool sym) {
   const int ktiles = static_cast<int>(cdiv(K, BK));
   const double sm_rate = 36e12 / 148.0;  // measured DMMA flop/s per SM (wide tile, 8192^3)
   Plan best{kWide, 1, ktiles};
@@ -301,7 +310,12 @@ Plan plan_gemm(const Ctx& ctx, i64 M, i64 N, i64 K, bool b_kmajor) {
     const int bm = tk == kWide ? TileWide::BM : tk == kNarrow ? TileNarrow::BM : TileTall::BM;
     const int bn = tk == kWide ? TileWide::BN : tk == kNarrow ? TileNarrow::BN : TileTall::BN;
     const double eff = tk == kNarrow ? 0.83 : 1.0;  // measured at 8192^3: 30.1 vs 36.1 TF/s
-    const i64 tiles = cdiv(M, bm) * cdiv(N, bn);
+    i64 tiles = cdiv(M, bm) * cdiv(N, bn);
+    if (sym) {  // tiles that reach the diagonal or lie above it
+      tiles = 0;
+      for (i64 tm = 0; tm < cdiv(M, bm); ++tm)
+        for (i64 tn = 0; tn < cdiv(N, bn); ++tn) tiles += (tn + 1) * bn > tm * bm;
+    }
     const int max_split = std::max(1, std::min(64, ktiles / 4));
     for (int s = 1; s <= max_split; ++s) {
       const int kps = static_cast<int>(cdiv(ktiles, s));
@@ -359,7 +373,8 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
     return;
   }
   const int ktiles = static_cast<int>(cdiv(K, BK));
-  Plan plan = plan_gemm(ctx, M, N, K, B.kmajor);
+  if (epi.sym && (M != N || beta != 0.0 || epi.norms)) invalid("gemm: the Gram form needs M = N, beta = 0 and no kernel epilogue");
+  Plan plan = plan_gemm(ctx, M, N, K, B.kmajor, epi.sym);
   if (epi.norms) {  // the kernel epilogue runs on whole dot products: no split-K
     plan.splits = 1;
     plan.kps = ktiles;
@@ -388,6 +403,8 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
     NPCG_LAUNCH(ctx, splitk_reduce_kernel, static_cast<unsigned>(cdiv(total, 256)), 256, 0, pp, splits, m, n,
                 alpha, beta, C, ldc);
   }
+  if (epi.sym)
+    NPCG_LAUNCH(ctx, mirror_upper_kernel, static_cast<unsigned>(cdiv(M * N, 256)), 256, 0, C, m, ldc);
 }
 
 }  // namespace npcg

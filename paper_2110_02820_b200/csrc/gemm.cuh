@@ -24,6 +24,10 @@ struct Operand {
 struct GemmEpi {
   const double* norms = nullptr;
   double c = 0.0;
+  /// Gram product (B = A^T, M = N, beta = 0): C is symmetric, so only the tiles
+  /// that reach the diagonal or lie above it are computed (36 of 64 at n =
+  /// 1000) and the strict lower triangle is mirrored from the upper one.
+  bool sym = false;
 };
 
 /// C (M x N, col-major, ldc) = alpha * A B + beta * C. Deterministic (split-K
