@@ -392,7 +392,9 @@ bool cholesky(Ctx& ctx, double* a, i64 n, i64 lda, CholFactor& f) {
 void trsm_right_lt(Ctx& ctx, i64 m, i64 n, double* Y, i64 ldy, const double* L, i64 ldl, const CholFactor& f,
                    double* X, i64 ldx) {
   if (f.linv.p()) {  // X = Y L^{-T}: one DMMA GEMM with the explicit inverse
-    gemm(ctx, m, n, n, 1.0, Operand{Y, ldy, false}, Operand{f.linv.p(), f.linv.ld, false}, 0.0, X, ldx);
+    GemmEpi tri;
+    tri.tri = true;  // L^{-T} is upper triangular: an n-tile's K loop stops at its last column
+    gemm(ctx, m, n, n, 1.0, Operand{Y, ldy, false}, Operand{f.linv.p(), f.linv.ld, false}, 0.0, X, ldx, tri);
     return;
   }
   const i64 nb = f.nb;

@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(T::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN, split = blockIdx.z;
   const int kt0 = split * ktiles_per_split;
-  const int nk = max(0, min(kt0 + ktiles_per_split, ktiles) - kt0);
+  const int klim = epi.tri ? min(ktiles, (n0 + BN + BK - 1) / BK) : ktiles;  // triangular B: rows k <= last column
+  const int nk = max(0, min(kt0 + ktiles_per_split, klim) - kt0);
   if (epi.sym && n0 + BN <= m0) return;  // Gram product: a tile strictly below the diagonal is mirrored later
 
   if (threadIdx.x == 0) {
@@ -375,7 +376,7 @@ void gemm(Ctx& ctx, i64 M, i64 N, i64 K, double alpha, Operand A, Operand B, dou
   const int ktiles = static_cast<int>(cdiv(K, BK));
   if (epi.sym && (M != N || beta != 0.0 || epi.norms)) invalid("gemm: the Gram form needs M = N, beta = 0 and no kernel epilogue");
   Plan plan = plan_gemm(ctx, M, N, K, B.kmajor, epi.sym);
-  if (epi.norms) {  // the kernel epilogue runs on whole dot products: no split-K
+  if (epi.norms || epi.tri) {  // the kernel epilogue runs on whole dot products, the triangular K range is per tile: no split-K
     plan.splits = 1;
     plan.kps = ktiles;
   }

@@ -28,6 +28,9 @@ struct GemmEpi {
   /// that reach the diagonal or lie above it are computed (36 of 64 at n =
   /// 1000) and the strict lower triangle is mirrored from the upper one.
   bool sym = false;
+  /// Triangular B (logical K x N with B[k, n] = 0 for k > n, e.g. L^{-T}):
+  /// the K loop of an n-tile stops at the tile's last column.
+  bool tri = false;
 };
 
 /// C (M x N, col-major, ldc) = alpha * A B + beta * C. Deterministic (split-K
