@@ -1067,6 +1067,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
             asm volatile("fence.proxy.async.global;" ::: "memory");
             for (i64 k = 0; k < UNCH; ++k) issue(k);
           }
+          __syncwarp();  // warp 0 reconverges before its lanes spin on the first chunk's barrier
           double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
           for (i64 k = 0; k < nch; ++k) {
             const uint32_t sq = seq0 + static_cast<uint32_t>(k);
@@ -1199,6 +1200,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
           };
           if (tid == 0)
             for (i64 g = 0; g < UNCH; ++g) issue(g);
+          __syncwarp();  // warp 0 reconverges before its lanes spin on the first slot's barrier
           double yacc[4][2];
 #pragma unroll
           for (int tt = 0; tt < 4; ++tt) yacc[tt][0] = yacc[tt][1] = 0.0;

@@ -20,7 +20,7 @@ npcg._check(L.npcg_nys_extend(nys, i64(ell), vp(path.omega.data_ptr()), i64(n), 
 npcg._check(L.npcg_nys_factor(nys))
 mu = 1e-3
 npcg._check(L.npcg_pre_create(nys, C.c_double(mu), C.byref(pre)))
-for s in (4, 8):
+for s in ([int(v) for v in sys.argv[3].split(',')] if len(sys.argv) > 3 else (4, 8)):
     reports = (npcg._SolveReport * s)()
     opts = npcg._SolveOpts(1e-300, 30, 0, 0)
     for rep in range(2):
