@@ -310,13 +310,39 @@ struct PersistArgs {
   State* st;
   double* hist;
   i64 hstride, max_iter, rows_per_cta, slice, uslice;
+  unsigned* gbar;             // grid barrier counter (zero at launch)
   unsigned long long* trace;  // diagnostics (NPCG_PCG_TRACE): CTA 0 phase timestamps of iterations 2..9
 };
 
 template <int S, bool GRAM>
 __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs a) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
+  // Grid barrier (the launch is cooperative: all CTAs are resident): thread 0
+  // counts the CTA in on a monotone global counter and spins until the
+  // barrier's generation is complete; the warp reconverges before the closing
+  // block barrier, so warp 0 arrives there once, as a whole.
+  unsigned grid_gen = 0;
+  struct GridBarrier {
+    unsigned* counter;
+    unsigned& gen;
+    unsigned ctas;
+    __device__ __forceinline__ void sync() {
+      __syncwarp();
+      __syncthreads();
+      ++gen;
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(counter, 1u);
+        const unsigned target = gen * ctas;
+        unsigned seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+        } while (seen < target);
+        __threadfence();
+      }
+      __syncwarp();
+      __syncthreads();
+    }
+  } grid{a.gbar, grid_gen, gridDim.x};
   __shared__ double sh[32];
   __shared__ double red[2][PT / 32], red2[2][PT / 32];
   // P2/P5 cross-warp staging (S x 16 x 32); the DMMA loop's per-step column dots alias it
@@ -1498,6 +1524,9 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, const PcgMuCols* cols
   pa.slice = cdiv(n, G);
   if (dense && S >= 3) pa.slice = round_up(pa.slice, 8);  // the DMMA path bulk-copies U on the slice's rows (16-byte aligned)
   if (P.ld != R.ld || V.ld != R.ld || P1.ld != R.ld || (nys && Z.ld != R.ld)) fail(NPCG_ERUNTIME, "pcg: work layout");
+  DBuf<unsigned> gbar(1, ctx.stream);
+  gbar.zero();
+  pa.gbar = gbar.p;
   static const bool tracing = std::getenv("NPCG_PCG_TRACE") != nullptr;  // diagnostics
   DBuf<unsigned long long> tr;
   if (tracing) {
