@@ -104,6 +104,43 @@ inline SolveReport nystrom_pcg(const LinearOperator& op, const Vector& b, const 
   return detail::pcg_call(op, precond.device.get(), mu, b, &x0, opt);
 }
 
+/// Regularisation path (extension; the paper's protocol):
+/// nystrom_pcg for every mu of `mus` on one approximation, the preconditioner
+/// rebuilt per mu. warm_start starts mu_k from the solutions of mu_{k-1};
+/// with cold starts consecutive mu share each pass over a stored dense A
+/// (npcg_regularization_path). Returns reports[k][j] for mu k, column j of b.
+inline std::vector<std::vector<SolveReport>> regularization_path(const LinearOperator& op, const Matrix& b,
+                                                                 const std::vector<double>& mus,
+                                                                 const NystromApproximation& approx,
+                                                                 bool warm_start = true,
+                                                                 const SolveOptions& opt = {}) {
+  const Index n = op.dim(), s = b.cols();
+  const Index nmu = static_cast<Index>(mus.size());
+  if (b.rows() != n) throw std::invalid_argument("regularization_path: right-hand side row mismatch");
+  if (!approx.device) throw std::runtime_error("build_preconditioner: approximation not factored");
+  npcg_solve_opts o{opt.eta, static_cast<std::int64_t>(opt.max_iter), opt.relative ? 1 : 0, 0};
+  std::vector<npcg_solve_report> reps(static_cast<size_t>(std::max<Index>(nmu * s, 1)));
+  std::vector<double> x(static_cast<size_t>(std::max<Index>(n * s * nmu, 1)));
+  const OpRef ref = device_handle(op);
+  ref.check(npcg_regularization_path(ref, approx.device.get(), nmu, mus.data(), s, b.data(), std::max<Index>(n, 1), &o,
+                                     warm_start ? 1 : 0, x.data(), std::max<Index>(n, 1), reps.data(), NPCG_HOST));
+  std::vector<std::vector<SolveReport>> out(static_cast<size_t>(nmu));
+  for (Index k = 0; k < nmu; ++k)
+    for (Index j = 0; j < s; ++j) {
+      const npcg_solve_report& r = reps[static_cast<size_t>(k * s + j)];
+      SolveReport rep;
+      rep.x = Vector(n);
+      std::copy(x.begin() + (k * s + j) * n, x.begin() + (k * s + j + 1) * n, rep.x.data());
+      rep.iterations = r.iterations;
+      rep.matvec_count = r.matvec_count;
+      rep.converged = r.converged != 0;
+      rep.eta_used = r.eta_used;
+      rep.wall_time = r.wall_time;
+      out[static_cast<size_t>(k)].push_back(std::move(rep));
+    }
+  return out;
+}
+
 /// block_nystrom_pcg (solvers.cpp:150-279).
 inline BlockSolveReport block_nystrom_pcg(const LinearOperator& op, const Matrix& b, double mu,
                                           const NystromPreconditioner& precond, const SolveOptions& opt = {}) {

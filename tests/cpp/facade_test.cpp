@@ -141,6 +141,39 @@ int main(int argc, char** argv) {
     CHECK(out.ell_final >= 4 && out.ell_final <= 32);
     CHECK(out.error_estimate.has_value());
   }
+  // regularisation path: cold starts batch the mu over each pass of A;
+  // every column must reproduce its own nystrom_pcg call
+  {
+    const Index n = 1500;
+    Vector lam(n);
+    for (Index j = 0; j < n; ++j) lam(j) = std::pow(j + 1.0, -1.5);
+    const DenseOperator A = synthesize_operator(SpectrumProfile(lam), 11);
+    Rng rng(11);
+    const Matrix B = gaussian_matrix(rng, n, 4);
+    const NystromApproximation ap = randomized_nystrom(A, 40, rng);
+    const std::vector<double> mus{1e-4, 1e-3, 1e-2};
+    SolveOptions opt;
+    opt.relative = true;
+    const auto path = regularization_path(A, B, mus, ap, /*warm_start=*/false, opt);
+    CHECK(path.size() == 3 && path[0].size() == 4);
+    for (size_t k = 0; k < mus.size(); ++k) {
+      const NystromPreconditioner pre = build_preconditioner(ap, mus[k]);
+      for (Index j = 0; j < 4; ++j) {
+        Vector bj(n);
+        for (Index i = 0; i < n; ++i) bj(i) = B(i, j);
+        const SolveReport one = nystrom_pcg(A, bj, mus[k], pre, opt);
+        const SolveReport& got = path[k][static_cast<size_t>(j)];
+        CHECK(got.converged && one.converged);
+        CHECK(std::abs(static_cast<long>(got.iterations) - static_cast<long>(one.iterations)) <= 1);
+        double err = 0.0, nrm = 0.0;
+        for (Index i = 0; i < n; ++i) {
+          err += (got.x(i) - one.x(i)) * (got.x(i) - one.x(i));
+          nrm += one.x(i) * one.x(i);
+        }
+        CHECK(std::sqrt(err / nrm) < 1e-8);
+      }
+    }
+  }
   // solvers_test.cpp:76-90 — breakdown raises SolveDivergenceError with its report
   {
     Matrix ind = Matrix::Identity(2, 2);
