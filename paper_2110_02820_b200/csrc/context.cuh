@@ -47,7 +47,7 @@ struct Ctx {
   cudaEvent_t stage_free[kStageSlots] = {};
   // Pinned host ring of large uploads from pageable memory (created on first
   // use): host threads fill one slot while the previous one crosses PCIe.
-  static constexpr int kPinSlots = 3;
+  static constexpr int kPinSlots = 8;  // 256 MB: the host packs ahead while earlier device work (e.g. the kernel-matrix build) still holds the stream
   static constexpr i64 kPinSlotBytes = i64{32} << 20;
   char* pin = nullptr;
   cudaEvent_t pin_free[kPinSlots] = {};
