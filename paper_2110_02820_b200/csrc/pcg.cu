@@ -270,7 +270,9 @@ constexpr int MDNST = 24, MSLOT = 1024 + 2;
 // preconditioner passes of the DMMA path (P4 / P5): 3 chunk slots of 16 column segments of up to 512 rows
 constexpr int UCH = 512, USEG = UCH + 2, UNSEG = 16, UNCH = 3;
 constexpr int ring_bytes(bool gram, int S) {
-  return (!gram && S >= 3) ? (MDNST * MSLOT > UNCH * UNSEG * USEG ? MDNST * MSLOT : UNCH * UNSEG * USEG) * 8 : RING_BYTES;
+  const int chunk = UNCH * UNSEG * USEG * 8;  // P4 / P5 chunk slots (every dense instance)
+  const int p1 = (!gram && S >= 3) ? MDNST * MSLOT * 8 : RING_BYTES;
+  return gram ? RING_BYTES : (p1 > chunk ? p1 : chunk);
 }
 constexpr int dense_pw(int S) { return 2 * PT * dense_pv(S); }
 constexpr int dense_nst(int S) { return RING_BYTES / (dense_pw(S) * 8); }
@@ -311,6 +313,7 @@ struct PersistArgs {
   double* hist;
   i64 hstride, max_iter, rows_per_cta, slice, uslice;
   unsigned* gbar;             // grid barrier counter (zero at launch)
+  int pre_dmma;               // dense: P4 / P5 on the DMMA pipe from bulk-copied chunk slots (3+ columns, or large n x ell)
   unsigned long long* trace;  // diagnostics (NPCG_PCG_TRACE): CTA 0 phase timestamps of iterations 2..9
 };
 
@@ -348,8 +351,8 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
   // P2/P5 cross-warp staging (S x 16 x 32); the DMMA loop's per-step column dots alias it
   // (P5 stages at most ZS = 4 right-hand sides per round: 5-8 take two rounds, the ring leaves no room for more)
   constexpr int ZS = S < 4 ? S : 4;
-  __shared__ double zbuf[(ZS * (PT / 32) * 32) > (!GRAM && S >= 3 ? 2 * (PT / 32) * 64 : 0)
-                             ? ZS * (PT / 32) * 32 : 2 * (PT / 32) * 64];
+  __shared__ double zbuf[(ZS * (PT / 32) * 32) > (!GRAM ? (S >= 3 ? 2 : 1) * (PT / 32) * 64 : 0)
+                             ? ZS * (PT / 32) * 32 : (S >= 3 ? 2 : 1) * (PT / 32) * 64];
   constexpr int UQ = S > 4 ? 2 : 4;  // P4: columns of U per pass (4 x 8 accumulators measured slower: 1035 vs 835 us at n = 1e5, ell = 2000)
   __shared__ double wred[UQ * S * (PT / 32)];  // P4: per-warp partials of up to UQ x S dots
   __shared__ ColState cs[S];
@@ -1058,7 +1061,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
         rr = block_sum(rr, sh);
         if (tid == 0) a.rr_part[c * S + s] = rr;
       }
-      if constexpr (MMA) asm volatile("fence.proxy.async.global;" ::: "memory");  // P4 bulk-copies r
+      if constexpr (!GRAM) asm volatile("fence.proxy.async.global;" ::: "memory");  // P4 bulk-copies r
       tick(t, 5);
       grid.sync();
       tick(t, 6);
@@ -1067,7 +1070,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
       double rr_pre[S];  // this thread's entry of the residual partials, loaded ahead of the U pass
 #pragma unroll
       for (int s = 0; s < S; ++s) rr_pre[s] = tid < G ? a.rr_part[tid * S + s] : 0.0;
-      if (MMA && nys) {
+      if (!GRAM && nys && a.pre_dmma) {
         // DMMA path: T[cols, s] = U[:, cols]^T R[:, s] for this CTA's columns of U, 8 at a
         // time. A chunk slot holds 512 rows of r (S segments) and of the 8 columns
         // (bulk copies, 3 chunks in flight); warp w owns rows 32w..32w+31 of the
@@ -1199,7 +1202,7 @@ __global__ void __launch_bounds__(PT, 1) pcg_persistent_kernel(const PersistArgs
       // ---- P5: z = r + U t on the slice (32 rows x 16 column groups; U read once
       // for all S right-hand sides), partial r.z
       auto uat = [&](i64 i, i64 j) { return a.U[i + j * a.ldu]; };
-      if constexpr (MMA) {
+      if (!GRAM && a.pre_dmma) {
         // DMMA path: Z[rows, s] = R + U[rows, :] T[:, s] on the slice, in row chunks of
         // up to 512 rows; a chunk slot holds 16 columns of U on those rows (bulk
         // copies, 3 slots in flight); warp w owns rows 32w..32w+31: 4 row tiles x
@@ -1522,7 +1525,10 @@ void run_persistent(Ctx& ctx, Op& op, Pre* pre, double mu, const PcgMuCols* cols
   pa.hstride = hstride;
   pa.max_iter = max_iter;
   pa.slice = cdiv(n, G);
-  if (dense && S >= 3) pa.slice = round_up(pa.slice, 8);  // the DMMA path bulk-copies U on the slice's rows (16-byte aligned)
+  // 1-2 columns: the scalar passes win while U is small (latency); the bulk-copied DMMA passes once it streams from HBM
+  pa.pre_dmma = dense && nys && (S >= 3 || static_cast<double>(n) * static_cast<double>(pre->ell) >= 8e6) ? 1 : 0;
+  if (const char* f = std::getenv("NPCG_PCG_PRE")) pa.pre_dmma = dense && nys && (S >= 3 || f[0] == 'd') ? 1 : 0;  // diagnostics
+  if (dense && pa.pre_dmma) pa.slice = round_up(pa.slice, 8);  // the DMMA path bulk-copies U on the slice's rows (16-byte aligned)
   if (P.ld != R.ld || V.ld != R.ld || P1.ld != R.ld || (nys && Z.ld != R.ld)) fail(NPCG_ERUNTIME, "pcg: work layout");
   DBuf<unsigned> gbar(1, ctx.stream);
   gbar.zero();
